@@ -1,0 +1,80 @@
+"""Pins for oracle O9 (analytic backward): central finite differences of the oracle's own forward
+(a different computation from the analytic chain rule), plus closed-form special cases
+(SPEC.md:216-217)."""
+import math
+
+import numpy as np
+
+from conftest import random_coords
+import oracle as O
+
+KW = dict(h_kv=2, T=2, m_cmp=2, m_slc=4, m_win=4, m_q=4)
+
+
+def _problem(rng, n=30, G=8, batch=2, H=4, h_kv=2, d=3):
+    c = random_coords(rng, n, G, batch)
+    N = len(c)
+    return (c, rng.standard_normal((N, H, d)), rng.standard_normal((N, h_kv, d)),
+            rng.standard_normal((N, h_kv, d)), rng.uniform(0.1, 0.9, (N, H, 3)), rng.standard_normal((N, H, d)))
+
+
+def test_finite_differences_all_inputs(rng):
+    c, q, k, v, gates, dout = _problem(rng)
+    f0 = O.ssa_forward(c, (8, 8, 8), 2, q, k, v, gates, **KW)
+    I = f0.I                                   # hard routing: indices frozen (READING R15)
+    dq, dk, dv, dg = O.ssa_backward(f0, q, k, v, gates, dout, h_kv=2)
+
+    def loss(q_, k_, v_, g_):
+        f = O.ssa_forward(c, (8, 8, 8), 2, q_, k_, v_, g_, I_override=I, plan=f0.plan, **KW)
+        return float((f.out * dout).sum())
+
+    h = 1e-5
+    sel = np.random.Generator(np.random.PCG64(7))
+    for name, arr, grad in (("q", q, dq), ("k", k, dk), ("v", v, dv), ("gates", gates, dg)):
+        flat = arr.reshape(-1)
+        gflat = grad.reshape(-1)
+        for idx in sel.choice(flat.size, size=min(25, flat.size), replace=False):
+            orig = flat[idx]
+            flat[idx] = orig + h
+            lp = loss(q, k, v, gates)
+            flat[idx] = orig - h
+            lm = loss(q, k, v, gates)
+            flat[idx] = orig
+            fd = (lp - lm) / (2 * h)
+            assert abs(fd - gflat[idx]) <= 1e-5 * max(1.0, abs(fd)), (name, idx, fd, gflat[idx])
+
+
+def test_zero_dout_and_single_token(rng):
+    c, q, k, v, gates, dout = _problem(rng)
+    f = O.ssa_forward(c, (8, 8, 8), 2, q, k, v, gates, **KW)
+    for g in O.ssa_backward(f, q, k, v, gates, np.zeros_like(dout), h_kv=2):
+        assert np.all(g == 0)
+    # N = 1: softmax constant -> dq = dk = 0, dv = (sum_c w_c) dO summed over the group's heads
+    c1 = np.array([[0, 1, 2, 3]])
+    f = O.ssa_forward(c1, (8, 8, 8), 1, q[:1], k[:1], v[:1], gates[:1], **KW)
+    dq, dk, dv, dg = O.ssa_backward(f, q[:1], k[:1], v[:1], gates[:1], dout[:1], h_kv=2)
+    assert np.allclose(dq, 0, atol=1e-15) and np.allclose(dk, 0, atol=1e-15)
+    w = gates[0].sum(axis=1)
+    want = np.stack([(w[2 * g:2 * g + 2, None] * dout[0, 2 * g:2 * g + 2]).sum(axis=0) for g in range(2)])
+    assert np.allclose(dv[0], want, atol=1e-14)
+
+
+def test_gradient_sparsity(rng):
+    """A token that is in no selected block, whose window holds only itself... gets k/v gradient only
+    through its own window and the compression pool: here we check that with gates
+    (0, 1, 0) a token outside every selected block gets exactly zero dk/dv."""
+    c, q, k, v, gates, dout = _problem(rng, n=60)
+    g010 = np.broadcast_to([0.0, 1.0, 0.0], gates.shape).copy()
+    kw = dict(KW, T=1)
+    f = O.ssa_forward(c, (8, 8, 8), 2, q, k, v, g010, **kw)
+    _, dk, dv, _ = O.ssa_backward(f, q, k, v, g010, dout, h_kv=2)
+    plan = f.plan
+    C = plan.offsets["slc"]
+    for g in range(2):
+        used = set()
+        for b in f.I[:, g].reshape(-1):
+            if b >= 0:
+                used.update(plan.perm[C[b]:C[b + 1]].tolist())
+        for t in range(len(c)):
+            if t not in used:
+                assert np.all(dk[t, g] == 0) and np.all(dv[t, g] == 0)
