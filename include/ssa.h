@@ -1,0 +1,198 @@
+/*
+ * ssa.h — C ABI of the B200-native Spatial Sparse Attention library (libssa_b200.so).
+ *
+ * Spatial Sparse Attention (SSA) is the attention of Direct3D-S2 (arXiv 2505.17412, §4.1,
+ * /root/reference/PAPER.md lines 129-226): sparse voxel tokens are grouped into m^3 spatial blocks
+ * (P:143), each compression block's K/V are pooled into one block token (Eq. 7), the
+ * compression attention scores pick the top-k selection blocks per query block (Eq. 8),
+ * flash-style attention runs over the selected blocks (Algorithm 1) and over a local
+ * m_win^3 window, and the three branch outputs are summed with gates (Eq. 6).
+ *
+ * Conventions shared by every entry point
+ *   - Every tensor pointer is a DEVICE pointer (CUDA global memory) owned by the caller. The library
+ *     never allocates device memory: sizes are queried first (ssa_*_size) and the caller passes the
+ *     buffers. The host-side ssa_plan handle is the only host allocation (malloc, freed by
+ *     ssa_plan_destroy).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). All device work is
+ *     enqueued on it. ssa_build_blocks synchronises the stream once (to read block counts and the
+ *     validation flags); ssa_forward / ssa_backward are fully asynchronous: a device-side fault
+ *     surfaces at the caller's next synchronisation.
+ *   - Errors: no exceptions, no abort across the ABI. Host argument errors return immediately
+ *     without enqueuing work. ssa_last_error() returns a thread-local text for the last failure.
+ *   - Layouts are row-major, innermost index last. Token order is the CALLER's order unless
+ *     SSA_INPUT_SORTED is set (then tensors are in the plan's block-sorted order).
+ *   - Head layout (GQA, Alg. 1 signature P:182): q, out, dout, dq: [N, H, d] with
+ *     H = h_kv * h_s; query head h = g*h_s + s uses kv head g; k, v, dk, dv: [N, h_kv, d];
+ *     gates, dgates: [N, H, 3] with branch order (cmp, slc, win) of Eq. 6, values post-sigmoid.
+ *   - Element type of q/k/v/gates/out/dout/dq/dk/dv/dgates: cfg->dtype (SSA_F32 or SSA_BF16). All
+ *     accumulation, softmax statistics and scores are fp32.
+ */
+#ifndef SSA_B200_H
+#define SSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SSA_OK = 0,
+  SSA_ERR_ARG = 1,          /* invalid host argument (null pointer, bad size, bad config)         */
+  SSA_ERR_DUP_COORD = 2,    /* two tokens share a voxel                             */
+  SSA_ERR_COORD_RANGE = 3,  /* coordinate outside [0,grid) or batch index outside [0,batch)        */
+  SSA_ERR_HIERARCHY = 4,    /* block sizes do not form a divisibility chain / m_cmp !| m_slc*/
+  SSA_ERR_BAD_STATE = 5,    /* plan / saved state mismatch                                        */
+  SSA_ERR_WORKSPACE = 6,    /* caller buffer smaller than the queried size                        */
+  SSA_ERR_UNSUPPORTED = 7,  /* configuration outside this build's kernels (reported in last_error) */
+  SSA_ERR_CUDA = 8          /* CUDA runtime error (text in ssa_last_error)                        */
+} ssa_status;
+
+typedef enum { SSA_F32 = 0, SSA_BF16 = 1 } ssa_dtype;
+
+/* Block levels of a plan. */
+typedef enum { SSA_LEVEL_CMP = 0, SSA_LEVEL_SLC = 1, SSA_LEVEL_WIN = 2, SSA_LEVEL_Q = 3 } ssa_level;
+
+typedef struct ssa_plan_s* ssa_plan;
+
+/* ------------------------------------------------------------------------------------------------
+ * ssa_build_blocks — spatial block partition + sort + start offsets C.
+ * PAPER.md:143 ("divide the 3D space into subgrids of size m^3 ... grouped into one block")
+ * ("first sort the input tokens based on their block indices, then compute the starting index C of
+ * each block"), Alg. 1 line 2. Four levels are built at once: compression (m_cmp),
+ * selection (m_slc), window (m_win) and query block (m_q; m_q = 1 is the paper's per-token query).
+ * Sort order: hierarchical-lexicographic over the distinct sizes (coarse to fine), then voxel
+ * order inside the finest block, within batch item b (reading R1). Every level is
+ * contiguous in that order; empty blocks are not materialised.
+ *
+ *   coords      device int32 [n,4] rows (b,x,y,z), 0 <= b < batch, 0 <= x < grid[0] ...
+ *   grid        HOST int32[3] grid extent per axis (latent resolution, e.g. 128 at 1024^3)
+ *   m_*         block edge lengths; the distinct values must form a divisibility chain and
+ *               m_cmp | m_slc (relaxed to >=, reading R2)
+ *   plan_buf    device buffer of ssa_build_blocks_size(...).plan_bytes, owned by the caller; it
+ *               must stay alive and unmodified while the plan is used
+ *   ws          device scratch of ws_bytes (may be reused after the call returns)
+ *   out         receives a host handle (free with ssa_plan_destroy; does not free plan_buf)
+ * Synchronises `stream` once. Errors: SSA_ERR_DUP_COORD, SSA_ERR_COORD_RANGE, SSA_ERR_HIERARCHY,
+ * SSA_ERR_ARG, SSA_ERR_WORKSPACE, SSA_ERR_UNSUPPORTED (key space > 2^34 cells), SSA_ERR_CUDA.
+ * ----------------------------------------------------------------------------------------------*/
+ssa_status ssa_build_blocks_size(int64_t n, int32_t batch, const int32_t grid[3], int32_t m_cmp,
+                                 int32_t m_slc, int32_t m_win, int32_t m_q, size_t* plan_bytes,
+                                 size_t* ws_bytes);
+ssa_status ssa_build_blocks(const int32_t* coords, int64_t n, int32_t batch, const int32_t grid[3],
+                            int32_t m_cmp, int32_t m_slc, int32_t m_win, int32_t m_q, void* plan_buf,
+                            size_t plan_bytes, void* ws, size_t ws_bytes, void* stream, ssa_plan* out);
+void ssa_plan_destroy(ssa_plan plan);
+
+/* Host-readable plan summary + device pointers into plan_buf (all int32, valid while plan_buf is).
+ *   perm[n]        sorted position -> caller token index;  inv_perm[n] the inverse
+ *   offsets[l]     [n_blocks[l]+1] token start of every block of level l (the paper's C)
+ *   block_coords[l][n_blocks[l]*4] (b, x/m, y/m, z/m) of every block
+ *   batch_blocks[l][batch+1] first block of every batch item;  batch_tokens[batch+1]
+ *   cmp_to_slc[n_blocks[CMP]] enclosing selection block of every compression block          */
+typedef struct {
+  int64_t n;
+  int32_t batch;
+  int32_t grid[3];
+  int32_t m[4];
+  int32_t n_blocks[4];
+  int32_t max_fill[4];            /* largest block (tokens) per level                          */
+  int32_t max_blocks_per_batch[4];
+  const int32_t* perm;
+  const int32_t* inv_perm;
+  const int32_t* sorted_coords;  /* [n,4] */
+  const int32_t* offsets[4];
+  const int32_t* block_coords[4];
+  const int32_t* batch_blocks[4];
+  const int32_t* batch_tokens;
+  const int32_t* cmp_to_slc;
+} ssa_plan_info;
+ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
+
+/* ------------------------------------------------------------------------------------------------
+ * Attention configuration.
+ *   h_q, h_kv, d : heads (h_q multiple of h_kv), head dim. top_k : T, the number of selected
+ *   blocks (clamped per batch item to N_slc(b), padded slots hold -1, reading R9).
+ *   scale        : softmax scale; <= 0 means 1/sqrt(d) (Eq. 5).
+ *   dtype        : SSA_F32 (SIMT fp32 kernels) or SSA_BF16 (tcgen05 tensor-core kernels when
+ *                  d == 64 and SSA_FORCE_SIMT is not set; SIMT otherwise).
+ *   pe_k, pe_v   : optional device [m_cmp^3, h_kv, d] (dtype) intra-block PE tables added before
+ *                  pooling (Eq. 7, reading R4); NULL = off. Not differentiated.
+ *   flags        : SSA_INPUT_SORTED — tensors are already in plan order (no internal permute);
+ *                  SSA_FORCE_SIMT   — use the SIMT kernels even where tcgen05 kernels exist;
+ *                  SSA_SAVE_SCORES  — keep the fp32 selection scores in the saved state.
+ * ----------------------------------------------------------------------------------------------*/
+#define SSA_INPUT_SORTED 1u
+#define SSA_FORCE_SIMT 2u
+#define SSA_SAVE_SCORES 4u
+
+typedef struct {
+  int32_t h_q, h_kv, d, top_k;
+  float scale;
+  int32_t dtype;
+  uint32_t flags;
+  const void* pe_k;
+  const void* pe_v;
+} ssa_attn_cfg;
+
+/* ------------------------------------------------------------------------------------------------
+ * ssa_forward — one SSA forward (Eq. 6): pool (Eq. 7) -> compression attention + Eq. 8 block
+ * scores + top-k -> selection attention (Alg. 1, query-block granular) + window
+ * attention -> gated sum (Eq. 6).
+ *   q [n,h_q,d], k/v [n,h_kv,d], gates [n,h_q,3] (dtype, device) -> out [n,h_q,d] (dtype, device)
+ *   saved      device buffer of saved_bytes; filled here, consumed by ssa_backward and the parity
+ *              hooks below. Must not be modified between forward and backward.
+ *   ws         device scratch of ws_bytes (forward-only lifetime).
+ * Errors: SSA_ERR_ARG (bad cfg / null), SSA_ERR_BAD_STATE (plan null), SSA_ERR_WORKSPACE,
+ * SSA_ERR_UNSUPPORTED, SSA_ERR_CUDA (launch failure).
+ * ----------------------------------------------------------------------------------------------*/
+ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, size_t* ws_bytes, size_t* saved_bytes);
+ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, const void* k,
+                       const void* v, const void* gates, void* out, void* saved, size_t saved_bytes,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * ssa_backward — gradients of ssa_forward with the block structure and the selected indices held
+ * constant (hard routing, reading R15; the paper reports only the backward's speed,
+ * P:391). Recomputes probabilities from the saved LSEs (flash-style).
+ *   dout [n,h_q,d] -> dq [n,h_q,d], dk/dv [n,h_kv,d], dgates [n,h_q,3] (all dtype, device).
+ *   q,k,v,gates must be the tensors given to the forward that filled `saved`.
+ * ----------------------------------------------------------------------------------------------*/
+ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, size_t* ws_bytes);
+ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, const void* k,
+                        const void* v, const void* gates, const void* saved, size_t saved_bytes,
+                        const void* dout, void* dq, void* dk, void* dv, void* dgates, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * Parity hooks into a filled saved state (device pointers, valid while `saved` is):
+ *   idx      int32 [n_blocks[Q], h_kv, top_k]  selected selection-block ids (global), -1 padded
+ *   scores   fp32 [n_blocks[Q], h_kv, max_blocks_per_batch[SLC]] (NULL unless SSA_SAVE_SCORES);
+ *            row (Q,g) holds the Eq. 8 score of the selection blocks of Q's batch item (local index)
+ *   o_branch, lse_branch: branch outputs / fp32 LSEs, internal layout [h_kv][n][h_s][d] / [h_kv][n][h_s]
+ *            in plan (sorted) order, branch 0=cmp 1=slc 2=win.
+ * ----------------------------------------------------------------------------------------------*/
+typedef struct {
+  const int32_t* idx;
+  const float* scores;
+  const void* o_branch[3];
+  const float* lse_branch[3];
+  const void* k_cmp;   /* [h_kv][n_blocks[CMP]][d] dtype */
+  const void* v_cmp;
+  int32_t used_tcgen05;  /* 1 if the forward ran the tcgen05 kernels */
+} ssa_saved_view;
+ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,
+                           ssa_saved_view* out);
+
+const char* ssa_status_str(ssa_status s);
+const char* ssa_last_error(void);
+/* Kernels launched by this thread since the last reset (host counter; used by bench.py). */
+int64_t ssa_launch_count(void);
+void ssa_reset_launch_count(void);
+const char* ssa_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSA_B200_H */

@@ -1,0 +1,286 @@
+// api.cu — the C ABI of libssa_b200 (include/ssa.h): size queries, caller-buffer carving and the
+// forward / backward orchestration. Every step of the path runs in this library's kernels.
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+#include "tc.h"
+
+namespace ssa {
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+}  // namespace
+
+void set_error(const std::string& s) { g_err = s; }
+void count_launch(int n) { g_launches += n; }
+ssa_status cuda_status(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return SSA_ERR_CUDA;
+}
+
+namespace {
+
+struct Dims {
+  int64_t N;
+  int H, h_kv, h_s, D, T;
+  size_t esz;
+  int n_cmp, n_slc, n_win, n_q, max_slc_b;
+};
+
+ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
+  if (!p) { set_error("null plan"); return SSA_ERR_BAD_STATE; }
+  if (!cfg) { set_error("null cfg"); return SSA_ERR_ARG; }
+  if (cfg->h_kv < 1 || cfg->h_q < 1 || cfg->h_q % cfg->h_kv) { set_error("h_q must be a positive multiple of h_kv"); return SSA_ERR_ARG; }
+  if (cfg->d < 1) { set_error("d must be >= 1"); return SSA_ERR_ARG; }
+  if (cfg->top_k < 1 || cfg->top_k > 64) { set_error("top_k must be in [1, 64]"); return SSA_ERR_ARG; }
+  if (cfg->dtype != SSA_F32 && cfg->dtype != SSA_BF16) { set_error("dtype must be SSA_F32 or SSA_BF16"); return SSA_ERR_ARG; }
+  if (cfg->d != 16 && cfg->d != 32 && cfg->d != 64) { set_error("head dim must be 16, 32 or 64"); return SSA_ERR_UNSUPPORTED; }
+  d->N = p->info.n;
+  d->H = cfg->h_q;
+  d->h_kv = cfg->h_kv;
+  d->h_s = cfg->h_q / cfg->h_kv;
+  d->D = cfg->d;
+  d->T = cfg->top_k;
+  d->esz = cfg->dtype == SSA_BF16 ? 2 : 4;
+  d->n_cmp = p->info.n_blocks[SSA_LEVEL_CMP];
+  d->n_slc = p->info.n_blocks[SSA_LEVEL_SLC];
+  d->n_win = p->info.n_blocks[SSA_LEVEL_WIN];
+  d->n_q = p->info.n_blocks[SSA_LEVEL_Q];
+  d->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
+  return SSA_OK;
+}
+
+bool use_tc(const Dims& d, const ssa_attn_cfg* cfg) {
+  return tc_available() && cfg->dtype == SSA_BF16 && d.D == 64 && !(cfg->flags & SSA_FORCE_SIMT);
+}
+
+// saved state: kc, vc, o[3], lse[3], I, scores
+void carve_saved(Carve& c, const Dims& d, const ssa_attn_cfg* cfg, Ctx* x) {
+  const int64_t rows = d.N * d.H;
+  x->kc = c.take<char>(size_t(d.h_kv) * d.n_cmp * d.D * d.esz);
+  x->vc = c.take<char>(size_t(d.h_kv) * d.n_cmp * d.D * d.esz);
+  for (int b = 0; b < 3; ++b) x->o[b] = c.take<char>(size_t(rows) * d.D * d.esz);
+  for (int b = 0; b < 3; ++b) x->lse[b] = c.take<float>(rows);
+  x->I = c.take<int32_t>(size_t(d.n_q) * d.h_kv * d.T);
+  x->scores = (cfg->flags & SSA_SAVE_SCORES) ? c.take<float>(size_t(d.n_q) * d.h_kv * std::max(d.max_slc_b, 1)) : nullptr;
+}
+
+void carve_inputs(Carve& c, const Dims& d, Ctx* x, bool with_dout) {
+  const int64_t rows = d.N * d.H, keys = d.N * d.h_kv;
+  x->qs = c.take<char>(size_t(rows) * d.D * d.esz);
+  x->ks = c.take<char>(size_t(keys) * d.D * d.esz);
+  x->vs = c.take<char>(size_t(keys) * d.D * d.esz);
+  x->gs = c.take<float>(size_t(rows) * 3);
+  x->dos = with_dout ? c.take<char>(size_t(rows) * d.D * d.esz) : nullptr;
+}
+
+int pick_chunks(const Plan* p, int h_kv) {
+  int tiles = std::max(1, p->n_cmp_tiles * h_kv);
+  int n = (4 * 148 + tiles - 1) / tiles;
+  return std::min(64, std::max(1, n));
+}
+
+void carve_bwd(Carve& c, const Dims& d, const Plan* p, Ctx* x) {
+  const int64_t rows = d.N * d.H, keys = d.N * d.h_kv;
+  for (int b = 0; b < 3; ++b) x->Dd[b] = c.take<float>(rows);
+  x->dq_acc = c.take<float>(size_t(rows) * d.D);
+  x->dk_acc = c.take<float>(size_t(keys) * d.D);
+  x->dv_acc = c.take<float>(size_t(keys) * d.D);
+  x->dkc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
+  x->dvc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
+  x->n_chunk = pick_chunks(p, d.h_kv);
+  x->dkc_part = c.take<float>(size_t(x->n_chunk) * d.h_kv * d.n_cmp * d.D);
+  x->dvc_part = c.take<float>(size_t(x->n_chunk) * d.h_kv * d.n_cmp * d.D);
+  const int64_t nkeys = int64_t(d.n_slc) * d.h_kv;
+  x->inv_cnt = c.take<int32_t>(nkeys);
+  x->inv_off = c.take<int32_t>(nkeys + 1);
+  x->inv_list = c.take<int32_t>(size_t(d.n_q) * d.h_kv * d.T);
+}
+
+void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
+  x->N = int32_t(d.N);
+  x->H = d.H;
+  x->h_kv = d.h_kv;
+  x->h_s = d.h_s;
+  x->D = d.D;
+  x->T = d.T;
+  x->batch = p->info.batch;
+  x->m_cmp = p->info.m[SSA_LEVEL_CMP];
+  for (int l = 0; l < kLevels; ++l) {
+    x->n_blk[l] = p->info.n_blocks[l];
+    x->max_fill[l] = p->info.max_fill[l];
+    x->off[l] = p->offsets[l];
+    x->tok_block[l] = p->tok_block[l];
+    x->bb[l] = p->batch_blocks[l];
+  }
+  x->max_cmp_b = p->info.max_blocks_per_batch[SSA_LEVEL_CMP];
+  x->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
+  x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.D));
+  x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
+  x->save_scores = (cfg->flags & SSA_SAVE_SCORES) ? 1 : 0;
+  x->perm = p->perm;
+  x->inv_perm = p->inv_perm;
+  x->sorted_coords = p->sorted_coords;
+  x->batch_tokens = p->batch_tokens;
+  x->slc_cmp_begin = p->slc_cmp_begin;
+  x->cmp_to_slc = p->cmp_to_slc;
+  x->q_order = p->q_order;
+  x->q_batch = p->q_batch;
+  x->cmp_tiles = p->cmp_tiles;
+  x->n_cmp_tiles = p->n_cmp_tiles;
+  x->pe_k = cfg->pe_k;
+  x->pe_v = cfg->pe_v;
+}
+}  // namespace
+}  // namespace ssa
+
+using namespace ssa;
+
+extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, size_t* ws_bytes, size_t* saved_bytes) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!ws_bytes || !saved_bytes) { set_error("null size pointer"); return SSA_ERR_ARG; }
+  Ctx x{};
+  Carve cs(nullptr, 0);
+  carve_saved(cs, d, cfg, &x);
+  *saved_bytes = cs.used + 256;
+  Carve cw(nullptr, 0);
+  carve_inputs(cw, d, &x, false);
+  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + 512;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, const void* k, const void* v,
+                                  const void* gates, void* out, void* saved, size_t saved_bytes, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!q || !k || !v || !gates || !out || !saved || !ws) { set_error("null tensor pointer"); return SSA_ERR_ARG; }
+  size_t need_ws, need_saved;
+  s = ssa_forward_size(plan, cfg, &need_ws, &need_saved);
+  if (s != SSA_OK) return s;
+  if (ws_bytes < need_ws || saved_bytes < need_saved) { set_error("ws/saved buffer too small"); return SSA_ERR_WORKSPACE; }
+  if (d.max_slc_b > 0 && p->info.max_blocks_per_batch[SSA_LEVEL_SLC] < 1) { set_error("empty plan"); return SSA_ERR_BAD_STATE; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Ctx x{};
+  fill_common(&x, p, d, cfg);
+  x.q = q; x.k = k; x.v = v; x.gates = gates; x.out = out;
+  Carve cs(saved, saved_bytes);
+  carve_saved(cs, d, cfg, &x);
+  Carve cw(ws, ws_bytes);
+  carve_inputs(cw, d, &x, false);
+  void* tc_ws = cw.take<char>(tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
+  const bool bf16 = cfg->dtype == SSA_BF16;
+  if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
+  if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
+  if (use_tc(d, cfg)) {
+    if ((s = tc_forward(x, tc_ws, st)) != SSA_OK) return s;
+  } else {
+    if ((s = simt_forward(x, bf16, st, false)) != SSA_OK) return s;
+    if ((s = combine_forward(x, bf16, st)) != SSA_OK) return s;
+  }
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, size_t* ws_bytes) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!ws_bytes) { set_error("null size pointer"); return SSA_ERR_ARG; }
+  Ctx x{};
+  Carve cw(nullptr, 0);
+  carve_inputs(cw, d, &x, true);
+  carve_bwd(cw, d, p, &x);
+  size_t scan = scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1);
+  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + 1024;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, const void* k, const void* v,
+                                   const void* gates, const void* saved, size_t saved_bytes, const void* dout,
+                                   void* dq, void* dk, void* dv, void* dgates, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!q || !k || !v || !gates || !saved || !dout || !dq || !dk || !dv || !dgates || !ws) {
+    set_error("null tensor pointer");
+    return SSA_ERR_ARG;
+  }
+  size_t need_ws, need_ws_f, need_saved;
+  if ((s = ssa_backward_size(plan, cfg, &need_ws)) != SSA_OK) return s;
+  if ((s = ssa_forward_size(plan, cfg, &need_ws_f, &need_saved)) != SSA_OK) return s;
+  if (saved_bytes < need_saved) { set_error("saved buffer smaller than this cfg's saved state"); return SSA_ERR_BAD_STATE; }
+  if (ws_bytes < need_ws) { set_error("ws buffer too small"); return SSA_ERR_WORKSPACE; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Ctx x{};
+  fill_common(&x, p, d, cfg);
+  x.q = q; x.k = k; x.v = v; x.gates = gates; x.dout = dout;
+  x.dq = dq; x.dk = dk; x.dv = dv; x.dgates = dgates;
+  Carve cs(const_cast<void*>(saved), saved_bytes);
+  carve_saved(cs, d, cfg, &x);
+  Carve cw(ws, ws_bytes);
+  carve_inputs(cw, d, &x, true);
+  carve_bwd(cw, d, p, &x);
+  void* scan_ws = cw.take<char>(scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1));
+  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
+  const bool bf16 = cfg->dtype == SSA_BF16;
+  if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;
+  if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
+  if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
+  if (use_tc(d, cfg)) {
+    if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
+  } else {
+    if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
+  }
+  return bwd_epilogue(x, bf16, st);
+}
+
+extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,
+                                      ssa_saved_view* out) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!saved || !out) { set_error("null saved/out"); return SSA_ERR_ARG; }
+  Ctx x{};
+  Carve cs(const_cast<void*>(saved), saved_bytes);
+  carve_saved(cs, d, cfg, &x);
+  if (!cs.ok()) { set_error("saved buffer too small"); return SSA_ERR_BAD_STATE; }
+  out->idx = x.I;
+  out->scores = x.scores;
+  for (int b = 0; b < 3; ++b) { out->o_branch[b] = x.o[b]; out->lse_branch[b] = x.lse[b]; }
+  out->k_cmp = x.kc;
+  out->v_cmp = x.vc;
+  out->used_tcgen05 = use_tc(d, cfg) ? 1 : 0;
+  return SSA_OK;
+}
+
+extern "C" const char* ssa_status_str(ssa_status s) {
+  switch (s) {
+    case SSA_OK: return "SSA_OK";
+    case SSA_ERR_ARG: return "SSA_ERR_ARG";
+    case SSA_ERR_DUP_COORD: return "SSA_ERR_DUP_COORD";
+    case SSA_ERR_COORD_RANGE: return "SSA_ERR_COORD_RANGE";
+    case SSA_ERR_HIERARCHY: return "SSA_ERR_HIERARCHY";
+    case SSA_ERR_BAD_STATE: return "SSA_ERR_BAD_STATE";
+    case SSA_ERR_WORKSPACE: return "SSA_ERR_WORKSPACE";
+    case SSA_ERR_UNSUPPORTED: return "SSA_ERR_UNSUPPORTED";
+    case SSA_ERR_CUDA: return "SSA_ERR_CUDA";
+  }
+  return "SSA_ERR_UNKNOWN";
+}
+extern "C" const char* ssa_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t ssa_launch_count(void) { return g_launches; }
+extern "C" void ssa_reset_launch_count(void) { g_launches = 0; }
+extern "C" const char* ssa_build_info(void) {
+  return tc_available() ? "libssa_b200 sm_100a: SIMT fp32 kernels + tcgen05/TMEM bf16 kernels"
+                        : "libssa_b200 sm_100a: SIMT kernels only";
+}

@@ -1,0 +1,122 @@
+// internal.h — shared host-side declarations of libssa_b200 (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/ssa.h"
+
+namespace ssa {
+
+constexpr int kLevels = 4;  // cmp, slc, win, q
+
+// Host handle behind ssa_plan. Device arrays live in the caller's plan_buf.
+struct Plan {
+  ssa_plan_info info;
+  int32_t* perm = nullptr;
+  int32_t* inv_perm = nullptr;
+  int32_t* sorted_coords = nullptr;
+  int32_t* offsets[kLevels] = {};
+  int32_t* block_coords[kLevels] = {};
+  int32_t* tok_block[kLevels] = {};
+  int32_t* batch_blocks[kLevels] = {};
+  int32_t* batch_tokens = nullptr;
+  int32_t* cmp_to_slc = nullptr;
+  int32_t* slc_cmp_begin = nullptr;   // [n_slc+1] first compression block of each selection block
+  int32_t* q_order = nullptr;         // [n_q] query blocks, largest first (LPT work order)
+  int32_t* q_batch = nullptr;         // [n_q] batch item of each query block
+  int32_t* cmp_tiles = nullptr;       // [n_cmp_tiles][2] (batch item, first cmp block), 64-key tiles
+  int32_t n_cmp_tiles = 0;
+  std::vector<int32_t> h_batch_blocks[kLevels];
+  std::vector<int32_t> h_batch_tokens;
+};
+
+// Everything a forward/backward kernel needs, by value (kernel parameter space).
+struct Ctx {
+  // problem
+  int32_t N, H, h_kv, h_s, D, T, batch, m_cmp;
+  int32_t n_blk[kLevels];
+  int32_t max_cmp_b, max_slc_b;   // max compression / selection blocks of one batch item
+  int32_t max_fill[kLevels];
+  float scale;                    // softmax scale (natural)
+  int32_t sorted_input;
+  int32_t save_scores;
+  // plan (device)
+  const int32_t *perm, *inv_perm, *sorted_coords;
+  const int32_t *off[kLevels], *tok_block[kLevels], *bb[kLevels];
+  const int32_t *batch_tokens, *slc_cmp_begin, *cmp_to_slc, *q_order, *q_batch;
+  // caller tensors
+  const void *q, *k, *v, *gates, *pe_k, *pe_v, *dout;
+  void *out, *dq, *dk, *dv, *dgates;
+  // internal tensors: layouts [h_kv][N][h_s][D] (rows), [h_kv][N][D] (keys)
+  void *qs, *ks, *vs, *dos;
+  float* gs;                      // [h_kv][N][h_s][3]
+  void *kc, *vc;                  // [h_kv][n_cmp][D]
+  void* o[3];                     // branch outputs (rows layout, dtype)
+  float* lse[3];                  // [h_kv][N][h_s]
+  int32_t* I;                     // [n_q][h_kv][T]
+  float* scores;                  // [n_q][h_kv][max_slc_b] or null
+  // backward scratch
+  float* Dd[3];                   // [h_kv][N][h_s]  D_c = omega_c <dO, O_c>
+  float *dq_acc, *dk_acc, *dv_acc;  // fp32 [rows] / [keys]
+  float *dkc, *dvc;               // fp32 [h_kv][n_cmp][D]
+  float *dkc_part, *dvc_part;     // fp32 [n_chunk][h_kv][n_cmp][D]
+  int32_t n_chunk;
+  int32_t *inv_off, *inv_list, *inv_cnt;   // inverse selection CSR over (slc block, g)
+  int32_t *cmp_tiles;             // [n_cmp_tiles][2] (batch item, first cmp block) for the KV-outer cmp kernels
+  int32_t n_cmp_tiles;
+};
+
+// SIMT kernels (simt.cu). Return SSA_OK or a launch error.
+ssa_status simt_forward(const Ctx& c, bool bf16, cudaStream_t st, bool attention_only);
+ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout);
+ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st);
+ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st);
+
+// thread-local error text + launch counter (api.cu)
+void set_error(const std::string& s);
+void count_launch(int n = 1);
+ssa_status cuda_status(cudaError_t e, const char* where);
+
+#define SSA_CUDA_TRY(expr)                                              \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) return ::ssa::cuda_status(_e, #expr);        \
+  } while (0)
+
+#define SSA_LAUNCH_CHECK(name)                                          \
+  do {                                                                  \
+    ::ssa::count_launch();                                              \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return ::ssa::cuda_status(_e, name);         \
+  } while (0)
+
+// Simple bump allocator over a caller buffer (device). Alignment 256 B.
+struct Carve {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  Carve(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t off = (used + 255) & ~size_t(255);
+    used = off + count * sizeof(T);
+    return base ? reinterpret_cast<T*>(base + off) : nullptr;
+  }
+  bool ok() const { return used <= cap; }
+};
+
+// ---- scan (scan.cu) ---------------------------------------------------------------------------
+size_t scan_ws_bytes(int64_t n);
+// exclusive prefix sum of int32 in[n] -> out[n]; *total (device) = sum. In-place allowed.
+ssa_status exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* total, void* ws,
+                          cudaStream_t st);
+
+}  // namespace ssa

@@ -1,0 +1,919 @@
+// simt.cu — CUDA-core kernels of the SSA path: input permutation (a2), compression pool (a3, Eq. 7),
+// gated combine (a8, Eq. 6), backward prologue/epilogue, inverse selection CSR, and the SIMT fp32
+// attention kernels (a4-a7, a9). The SIMT attention kernels are the fp32 mode (SSA_F32; tolerance
+// 1e-4 rules out TF32 tensor cores) and the SSA_FORCE_SIMT path; bf16 with d = 64 runs the tcgen05
+// kernels in tc_fwd.cu / tc_bwd.cu.
+//
+// Internal layouts (plan-sorted token order p): rows  [h_kv][N][h_s][D]  (row = (p, s) of group g),
+// keys [h_kv][N][D], compressed keys [h_kv][n_cmp][D], per-row fp32 stats [h_kv][N][h_s].
+#include <cfloat>
+
+#include "internal.h"
+
+namespace ssa {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ld(const float* p) { return *p; }
+__device__ __forceinline__ float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void st(float* p, float v) { *p = v; }
+__device__ __forceinline__ void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------------------------
+// a2: gather caller tensors into the internal block-sorted layouts.
+// ---------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ dst) {
+  // one thread per (p, h, element); src [N][H][D] caller order -> dst [h_kv][N][h_s][D]
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.H * c.D;
+  if (i >= total) return;
+  int e = int(i % c.D);
+  int h = int((i / c.D) % c.H);
+  int p = int(i / (int64_t(c.D) * c.H));
+  int src_p = c.sorted_input ? p : c.perm[p];
+  int g = h / c.h_s, s = h % c.h_s;
+  dst[((int64_t(g) * c.N + p) * c.h_s + s) * c.D + e] = src[(int64_t(src_p) * c.H + h) * c.D + e];
+}
+
+template <class T>
+__global__ void k_gather_keys(Ctx c, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ ks,
+                              T* __restrict__ vs) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.h_kv * c.D;
+  if (i >= total) return;
+  int e = int(i % c.D);
+  int g = int((i / c.D) % c.h_kv);
+  int p = int(i / (int64_t(c.D) * c.h_kv));
+  int src_p = c.sorted_input ? p : c.perm[p];
+  int64_t si = (int64_t(src_p) * c.h_kv + g) * c.D + e;
+  int64_t di = (int64_t(g) * c.N + p) * c.D + e;
+  ks[di] = k[si];
+  vs[di] = v[si];
+}
+
+template <class T>
+__global__ void k_gather_gates(Ctx c, const T* __restrict__ gates, float* __restrict__ gs) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.H * 3;
+  if (i >= total) return;
+  int br = int(i % 3);
+  int h = int((i / 3) % c.H);
+  int p = int(i / (3 * int64_t(c.H)));
+  int src_p = c.sorted_input ? p : c.perm[p];
+  int g = h / c.h_s, s = h % c.h_s;
+  gs[((int64_t(g) * c.N + p) * c.h_s + s) * 3 + br] = ld(gates + (int64_t(src_p) * c.H + h) * 3 + br);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a3: compression pool, Eq. 7 with delta = masked mean (reading R4), optional intra-block PE.
+// grid (n_cmp, h_kv), block D threads.
+// ---------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_pool(Ctx c) {
+  const int j = blockIdx.x, g = blockIdx.y, e = threadIdx.x;
+  const int t0 = c.off[SSA_LEVEL_CMP][j], t1 = c.off[SSA_LEVEL_CMP][j + 1];
+  const T* ks = static_cast<const T*>(c.ks);
+  const T* vs = static_cast<const T*>(c.vs);
+  const T* pek = static_cast<const T*>(c.pe_k);
+  const T* pev = static_cast<const T*>(c.pe_v);
+  const int m = c.m_cmp;
+  float sk = 0.f, sv = 0.f;
+  for (int p = t0; p < t1; ++p) {
+    int64_t idx = (int64_t(g) * c.N + p) * c.D + e;
+    float kk = ld(ks + idx), vv = ld(vs + idx);
+    if (pek || pev) {
+      const int4 cc = reinterpret_cast<const int4*>(c.sorted_coords)[p];
+      int loc = ((cc.y % m) * m + (cc.z % m)) * m + (cc.w % m);
+      int64_t pi = (int64_t(loc) * c.h_kv + g) * c.D + e;
+      if (pek) kk += ld(pek + pi);
+      if (pev) vv += ld(pev + pi);
+    }
+    sk += kk;
+    sv += vv;
+  }
+  const float inv = 1.f / float(t1 - t0);
+  int64_t o = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
+  st(static_cast<T*>(c.kc) + o, sk * inv);
+  st(static_cast<T*>(c.vc) + o, sv * inv);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a4 + a5 (SIMT): compression attention (two passes) + Eq. 8 block scores + top-k, one CTA per
+// (query block, kv group), query blocks in LPT order. Thread = row (t, s).
+// ---------------------------------------------------------------------------------------------
+constexpr int kRows = 128;
+constexpr int kKT = 32;   // keys per smem tile
+
+template <class T, int D>
+__global__ void __launch_bounds__(kRows) k_cmp_fwd(Ctx c) {
+  extern __shared__ float sm[];
+  float* Kt = sm;                       // [kKT][D]
+  float* Vt = Kt + kKT * D;             // [kKT][D]
+  float* Pt = Vt + kKT * D;             // [kRows][kKT+1]
+  float* red = Pt + kRows * (kKT + 1);  // [4][kKT]
+  float* sc_cmp = red + 4 * kKT;        // [max_cmp_b]
+  float* sc_slc = sc_cmp + c.max_cmp_b; // [max_slc_b]
+  __shared__ float bv[kRows / 32];
+  __shared__ int bi[kRows / 32];
+  __shared__ int chosen[64];
+
+  const int Q = c.q_order[blockIdx.x], g = blockIdx.y, tid = threadIdx.x;
+  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int b = c.q_batch[Q];
+  const int c0 = c.bb[SSA_LEVEL_CMP][b], c1 = c.bb[SSA_LEVEL_CMP][b + 1], nk = c1 - c0;
+  const int s0 = c.bb[SSA_LEVEL_SLC][b], s1 = c.bb[SSA_LEVEL_SLC][b + 1], ns = s1 - s0;
+  const int rows = (t1 - t0) * c.h_s;
+  const T* qs = static_cast<const T*>(c.qs);
+  const T* kc = static_cast<const T*>(c.kc);
+  const T* vc = static_cast<const T*>(c.vc);
+  const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
+  const float qscale = c.scale * kLog2e;
+  for (int i = tid; i < nk; i += kRows) sc_cmp[i] = 0.f;
+  const int64_t row_base = (int64_t(g) * c.N + t0) * c.h_s;
+
+  for (int r0 = 0; r0 < rows; r0 += kRows) {
+    const int r = r0 + tid;
+    const bool valid = r < rows;
+    float q[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) q[e] = valid ? ld(qs + (row_base + r) * D + e) * qscale : 0.f;
+    // pass 1: log2-domain LSE over all compressed keys of the batch item
+    float m = -FLT_MAX, l = 0.f;
+    for (int k0 = 0; k0 < nk; k0 += kKT) {
+      const int nt = min(kKT, nk - k0);
+      __syncthreads();
+      for (int i = tid; i < nt * D; i += kRows)
+        Kt[i] = ld(kc + (int64_t(g) * n_cmp + c0 + k0) * D + i);
+      __syncthreads();
+      for (int j = 0; j < nt; ++j) {
+        float x = 0.f;
+#pragma unroll
+        for (int e = 0; e < D; ++e) x += q[e] * Kt[j * D + e];
+        float mn = fmaxf(m, x);
+        l = l * exp2f(m - mn) + exp2f(x - mn);
+        m = mn;
+      }
+    }
+    const float lse2 = m + log2f(l);
+    // pass 2: P = exp(S - LSE), O = P V, column sums of P into sc_cmp
+    float o[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) o[e] = 0.f;
+    for (int k0 = 0; k0 < nk; k0 += kKT) {
+      const int nt = min(kKT, nk - k0);
+      __syncthreads();
+      for (int i = tid; i < nt * D; i += kRows) {
+        Kt[i] = ld(kc + (int64_t(g) * n_cmp + c0 + k0) * D + i);
+        Vt[i] = ld(vc + (int64_t(g) * n_cmp + c0 + k0) * D + i);
+      }
+      __syncthreads();
+      for (int j = 0; j < kKT; ++j) {
+        float p = 0.f;
+        if (j < nt) {
+          float x = 0.f;
+#pragma unroll
+          for (int e = 0; e < D; ++e) x += q[e] * Kt[j * D + e];
+          p = valid ? exp2f(x - lse2) : 0.f;
+#pragma unroll
+          for (int e = 0; e < D; ++e) o[e] += p * Vt[j * D + e];
+        }
+        Pt[tid * (kKT + 1) + j] = p;
+      }
+      __syncthreads();
+      {
+        const int col = tid & (kKT - 1), part = tid / kKT;
+        float s = 0.f;
+        for (int i = part * 32; i < part * 32 + 32; ++i) s += Pt[i * (kKT + 1) + col];
+        red[part * kKT + col] = s;
+      }
+      __syncthreads();
+      if (tid < nt) sc_cmp[k0 + tid] += (red[tid] + red[kKT + tid]) + (red[2 * kKT + tid] + red[3 * kKT + tid]);
+    }
+    if (valid) {
+      T* oc = static_cast<T*>(c.o[0]);
+#pragma unroll
+      for (int e = 0; e < D; ++e) st(oc + (row_base + r) * D + e, o[e]);
+      c.lse[0][row_base + r] = lse2 * kLn2;
+    }
+  }
+  __syncthreads();
+  // Eq. 8: selection-block score = sum over its compression blocks (contiguous range)
+  for (int B = tid; B < ns; B += kRows) {
+    float s = 0.f;
+    for (int i = c.slc_cmp_begin[s0 + B]; i < c.slc_cmp_begin[s0 + B + 1]; ++i) s += sc_cmp[i - c0];
+    sc_slc[B] = s;
+    if (c.save_scores) c.scores[(int64_t(Q) * c.h_kv + g) * c.max_slc_b + B] = s;
+  }
+  __syncthreads();
+  // top-k: T rounds of block argmax (value desc, index asc); scores >= 0 so -1 marks "taken"
+  const int Teff = min(c.T, ns);
+  for (int it = 0; it < Teff; ++it) {
+    float best = -2.f;
+    int bidx = 0x7fffffff;
+    for (int B = tid; B < ns; B += kRows) {
+      float v = sc_slc[B];
+      if (v > best) { best = v; bidx = B; }   // strided ascending scan keeps the lowest index on ties
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if ((tid & 31) == 0) { bv[tid >> 5] = best; bi[tid >> 5] = bidx; }
+    __syncthreads();
+    if (tid == 0) {
+      float bb = bv[0];
+      int ii = bi[0];
+      for (int w = 1; w < kRows / 32; ++w)
+        if (bv[w] > bb || (bv[w] == bb && bi[w] < ii)) { bb = bv[w]; ii = bi[w]; }
+      chosen[it] = ii;
+      sc_slc[ii] = -1.f;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int i = 1; i < Teff; ++i) {   // ascending block index
+      int v = chosen[i], j = i - 1;
+      while (j >= 0 && chosen[j] > v) { chosen[j + 1] = chosen[j]; --j; }
+      chosen[j + 1] = v;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < c.T; j += kRows)
+    c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + chosen[j] : -1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a6 / a7 (SIMT): single-pass online-softmax attention over a list of key segments.
+// mode 1 = selection (CTA per (query block, g), segments = selected blocks I, Alg. 1),
+// mode 2 = window    (CTA per (window, g), one segment = the window itself).
+// ---------------------------------------------------------------------------------------------
+template <class T, int D>
+__global__ void __launch_bounds__(kRows) k_attn_fwd(Ctx c, int mode) {
+  __shared__ float Kt[kKT * D];
+  __shared__ float Vt[kKT * D];
+  __shared__ int seg_s[64], seg_e[64];
+  __shared__ int nseg;
+  const int g = blockIdx.y, tid = threadIdx.x;
+  int t0, t1;
+  if (mode == 1) {
+    const int Q = c.q_order[blockIdx.x];
+    t0 = c.off[SSA_LEVEL_Q][Q];
+    t1 = c.off[SSA_LEVEL_Q][Q + 1];
+    if (tid == 0) {
+      int n = 0;
+      for (int j = 0; j < c.T; ++j) {
+        int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+        if (B >= 0) { seg_s[n] = c.off[SSA_LEVEL_SLC][B]; seg_e[n] = c.off[SSA_LEVEL_SLC][B + 1]; ++n; }
+      }
+      nseg = n;
+    }
+  } else {
+    const int W = blockIdx.x;
+    t0 = c.off[SSA_LEVEL_WIN][W];
+    t1 = c.off[SSA_LEVEL_WIN][W + 1];
+    if (tid == 0) { seg_s[0] = t0; seg_e[0] = t1; nseg = 1; }
+  }
+  __syncthreads();
+  const int rows = (t1 - t0) * c.h_s;
+  const T* qs = static_cast<const T*>(c.qs);
+  const T* ks = static_cast<const T*>(c.ks);
+  const T* vs = static_cast<const T*>(c.vs);
+  const float qscale = c.scale * kLog2e;
+  const int64_t row_base = (int64_t(g) * c.N + t0) * c.h_s;
+  const int br = mode;  // branch index: 1 = slc, 2 = win
+  for (int r0 = 0; r0 < rows; r0 += kRows) {
+    const int r = r0 + tid;
+    const bool valid = r < rows;
+    float q[D], o[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+      q[e] = valid ? ld(qs + (row_base + r) * D + e) * qscale : 0.f;
+      o[e] = 0.f;
+    }
+    float m = -FLT_MAX, l = 0.f;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      for (int k0 = seg_s[sgi]; k0 < seg_e[sgi]; k0 += kKT) {
+        const int nt = min(kKT, seg_e[sgi] - k0);
+        __syncthreads();
+        for (int i = tid; i < nt * D; i += kRows) {
+          Kt[i] = ld(ks + (int64_t(g) * c.N + k0) * D + i);
+          Vt[i] = ld(vs + (int64_t(g) * c.N + k0) * D + i);
+        }
+        __syncthreads();
+        for (int j = 0; j < nt; ++j) {
+          float x = 0.f;
+#pragma unroll
+          for (int e = 0; e < D; ++e) x += q[e] * Kt[j * D + e];
+          float mn = fmaxf(m, x);
+          float a = exp2f(m - mn), p = exp2f(x - mn);
+          l = l * a + p;
+#pragma unroll
+          for (int e = 0; e < D; ++e) o[e] = o[e] * a + p * Vt[j * D + e];
+          m = mn;
+        }
+      }
+    }
+    if (valid) {
+      const float inv = 1.f / l;
+      T* ob = static_cast<T*>(c.o[br]);
+#pragma unroll
+      for (int e = 0; e < D; ++e) st(ob + (row_base + r) * D + e, o[e] * inv);
+      c.lse[br][row_base + r] = (m + log2f(l)) * kLn2;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a8: gated sum (Eq. 6) + scatter to caller order. Thread per (p, h, e).
+// ---------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_combine(Ctx c) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.H * c.D;
+  if (i >= total) return;
+  int e = int(i % c.D);
+  int h = int((i / c.D) % c.H);
+  int p = int(i / (int64_t(c.D) * c.H));
+  int g = h / c.h_s, s = h % c.h_s;
+  int64_t row = (int64_t(g) * c.N + p) * c.h_s + s;
+  const float* w = c.gs + row * 3;
+  float v = w[0] * ld(static_cast<const T*>(c.o[0]) + row * c.D + e) +
+            w[1] * ld(static_cast<const T*>(c.o[1]) + row * c.D + e) +
+            w[2] * ld(static_cast<const T*>(c.o[2]) + row * c.D + e);
+  int dst = c.sorted_input ? p : c.perm[p];
+  st(static_cast<T*>(c.out) + (int64_t(dst) * c.H + h) * c.D + e, v);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Backward prologue: dgate_c = <dO, O_c> (caller order, dtype), D_c = omega_c * dgate_c (fp32).
+// ---------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_bwd_pre(Ctx c) {
+  int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // (g, p, s)
+  int64_t total = int64_t(c.N) * c.H;
+  if (row >= total) return;
+  const T* dos = static_cast<const T*>(c.dos);
+  float acc[3] = {0.f, 0.f, 0.f};
+  for (int e = 0; e < c.D; ++e) {
+    float d = ld(dos + row * c.D + e);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) acc[b] += d * ld(static_cast<const T*>(c.o[b]) + row * c.D + e);
+  }
+  const int s = int(row % c.h_s);
+  const int p = int((row / c.h_s) % c.N);
+  const int g = int(row / (int64_t(c.h_s) * c.N));
+  const int h = g * c.h_s + s;
+  const int dst = c.sorted_input ? p : c.perm[p];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    c.Dd[b][row] = c.gs[row * 3 + b] * acc[b];
+    st(static_cast<T*>(c.dgates) + (int64_t(dst) * c.H + h) * 3 + b, acc[b]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Inverse selection CSR: for every (selection block B, g), the ascending list of query blocks
+// whose top-k contains B (the KV-outer backward iterates it; sorted so sums are deterministic).
+// ---------------------------------------------------------------------------------------------
+__global__ void k_inv_count(Ctx c) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
+  if (i >= total) return;
+  int B = c.I[i];
+  int g = int((i / c.T) % c.h_kv);
+  if (B >= 0) atomicAdd(c.inv_cnt + int64_t(B) * c.h_kv + g, 1);
+}
+__global__ void k_inv_fill(Ctx c, int32_t* cursor) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
+  if (i >= total) return;
+  int B = c.I[i];
+  int g = int((i / c.T) % c.h_kv);
+  int Q = int(i / (int64_t(c.T) * c.h_kv));
+  if (B >= 0) {
+    int64_t key = int64_t(B) * c.h_kv + g;
+    int pos = atomicAdd(cursor + key, 1);
+    c.inv_list[c.inv_off[key] + pos] = Q;
+  }
+}
+__global__ void k_inv_sort(Ctx c) {
+  int64_t key = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (key >= int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv) return;
+  int a = c.inv_off[key], e = c.inv_off[key + 1];
+  int32_t* L = c.inv_list;
+  for (int i = a + 1; i < e; ++i) {
+    int v = L[i], j = i - 1;
+    while (j >= a && L[j] > v) { L[j + 1] = L[j]; --j; }
+    L[j + 1] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a9 (SIMT) dQ, Q-outer over the compression keys and the selected blocks (CTA per (Q, g)).
+// dS = P (dP - D_c), dP = omega_c <dO, v_j>, dq += scale * dS * k_j.
+// ---------------------------------------------------------------------------------------------
+template <class T, int D>
+__global__ void __launch_bounds__(kRows) k_dq(Ctx c) {
+  __shared__ float Kt[kKT * D];
+  __shared__ float Vt[kKT * D];
+  __shared__ int seg_s[65], seg_e[65];
+  __shared__ int nseg;
+  const int Q = c.q_order[blockIdx.x], g = blockIdx.y, tid = threadIdx.x;
+  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int b = c.q_batch[Q];
+  const int rows = (t1 - t0) * c.h_s;
+  if (tid == 0) {
+    seg_s[0] = c.bb[SSA_LEVEL_CMP][b];
+    seg_e[0] = c.bb[SSA_LEVEL_CMP][b + 1];
+    int n = 1;
+    for (int j = 0; j < c.T; ++j) {
+      int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+      if (B >= 0) { seg_s[n] = c.off[SSA_LEVEL_SLC][B]; seg_e[n] = c.off[SSA_LEVEL_SLC][B + 1]; ++n; }
+    }
+    nseg = n;
+  }
+  __syncthreads();
+  const T* qs = static_cast<const T*>(c.qs);
+  const T* dos = static_cast<const T*>(c.dos);
+  const int64_t row_base = (int64_t(g) * c.N + t0) * c.h_s;
+  const float l2s = c.scale * kLog2e;
+  for (int r0 = 0; r0 < rows; r0 += kRows) {
+    const int r = r0 + tid;
+    const bool valid = r < rows;
+    const int64_t row = row_base + (valid ? r : 0);
+    float q[D], dO[D], dq[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+      q[e] = ld(qs + row * D + e);
+      dO[e] = ld(dos + row * D + e);
+      dq[e] = 0.f;
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      const int br = sgi == 0 ? 0 : 1;
+      const T* kb = static_cast<const T*>(br == 0 ? c.kc : c.ks);
+      const T* vb = static_cast<const T*>(br == 0 ? c.vc : c.vs);
+      const int64_t kbase = int64_t(g) * (br == 0 ? c.n_blk[SSA_LEVEL_CMP] : c.N);
+      const float lse2 = c.lse[br][row] * kLog2e;
+      const float w = c.gs[row * 3 + br];
+      const float Dv = c.Dd[br][row];
+      for (int k0 = seg_s[sgi]; k0 < seg_e[sgi]; k0 += kKT) {
+        const int nt = min(kKT, seg_e[sgi] - k0);
+        __syncthreads();
+        for (int i = tid; i < nt * D; i += kRows) {
+          Kt[i] = ld(kb + (kbase + k0) * D + i);
+          Vt[i] = ld(vb + (kbase + k0) * D + i);
+        }
+        __syncthreads();
+        for (int j = 0; j < nt; ++j) {
+          float x = 0.f, dp = 0.f;
+#pragma unroll
+          for (int e = 0; e < D; ++e) {
+            x += q[e] * Kt[j * D + e];
+            dp += dO[e] * Vt[j * D + e];
+          }
+          const float p = exp2f(x * l2s - lse2);
+          const float ds = p * (w * dp - Dv) * c.scale;
+#pragma unroll
+          for (int e = 0; e < D; ++e) dq[e] += ds * Kt[j * D + e];
+        }
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < D; ++e) c.dq_acc[row * D + e] = dq[e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// KV-outer helper: a pair of threads owns one key (half the channels each). For every staged row:
+// s = scale <q_r, k_j>, p = exp(s - lse_r), dv_j += p w_r dO_r, dp = w_r <dO_r, v_j>,
+// ds = p (dp - D_r), dk_j += scale ds q_r.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+struct KvAcc {
+  float k[D / 2], v[D / 2], dk[D / 2], dv[D / 2];
+};
+
+template <class T, int D>
+__device__ __forceinline__ void kv_rows_tile(KvAcc<D>& a, bool kvalid, int half, const float* Qt, const float* Ot,
+                                             const float* st_lse2, const float* st_w, const float* st_D, int nr,
+                                             float scale) {
+  const float l2s = scale * kLog2e;
+  for (int rr = 0; rr < nr; ++rr) {
+    float x = 0.f, dp = 0.f;
+#pragma unroll
+    for (int e = 0; e < D / 2; ++e) {
+      x += Qt[rr * D + half * (D / 2) + e] * a.k[e];
+      dp += Ot[rr * D + half * (D / 2) + e] * a.v[e];
+    }
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    dp += __shfl_xor_sync(0xffffffffu, dp, 1);
+    if (!kvalid) continue;
+    const float p = exp2f(x * l2s - st_lse2[rr]);
+    const float w = st_w[rr];
+    const float ds = p * (w * dp - st_D[rr]) * scale;
+    const float pw = p * w;
+#pragma unroll
+    for (int e = 0; e < D / 2; ++e) {
+      a.dv[e] += pw * Ot[rr * D + half * (D / 2) + e];
+      a.dk[e] += ds * Qt[rr * D + half * (D / 2) + e];
+    }
+  }
+}
+
+template <class T, int D>
+__device__ __forceinline__ void stage_rows(const Ctx& c, int br, int64_t row0, int nr, float* Qt, float* Ot,
+                                           float* st_lse2, float* st_w, float* st_D) {
+  const T* qs = static_cast<const T*>(c.qs);
+  const T* dos = static_cast<const T*>(c.dos);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nr * D; i += blockDim.x) {
+    Qt[i] = ld(qs + row0 * D + i);
+    Ot[i] = ld(dos + row0 * D + i);
+  }
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    st_lse2[i] = c.lse[br][row0 + i] * kLog2e;
+    st_w[i] = c.gs[(row0 + i) * 3 + br];
+    st_D[i] = c.Dd[br][row0 + i];
+  }
+  __syncthreads();
+}
+
+constexpr int kRT = 32;  // rows per staged tile in KV-outer kernels
+
+// selection branch dK/dV: CTA per (selection block B, g); assigns dk_acc / dv_acc of B's tokens.
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_slc_dkdv(Ctx c) {
+  __shared__ float Qt[kRT * D], Ot[kRT * D], s_l[kRT], s_w[kRT], s_D[kRT];
+  const int B = blockIdx.x, g = blockIdx.y;
+  const int kk0 = c.off[SSA_LEVEL_SLC][B], kk1 = c.off[SSA_LEVEL_SLC][B + 1];
+  const int half = threadIdx.x & 1;
+  const int64_t key = int64_t(B) * c.h_kv + g;
+  const int la = c.inv_off[key], le = c.inv_off[key + 1];
+  const T* ks = static_cast<const T*>(c.ks);
+  const T* vs = static_cast<const T*>(c.vs);
+  for (int j0 = kk0; j0 < kk1; j0 += 64) {
+    const int j = j0 + (threadIdx.x >> 1);
+    const bool kvalid = j < kk1;
+    KvAcc<D> a;
+#pragma unroll
+    for (int e = 0; e < D / 2; ++e) {
+      int64_t idx = (int64_t(g) * c.N + (kvalid ? j : kk0)) * D + half * (D / 2) + e;
+      a.k[e] = ld(ks + idx);
+      a.v[e] = ld(vs + idx);
+      a.dk[e] = 0.f;
+      a.dv[e] = 0.f;
+    }
+    for (int li = la; li < le; ++li) {
+      const int Q = c.inv_list[li];
+      const int q0 = c.off[SSA_LEVEL_Q][Q], q1 = c.off[SSA_LEVEL_Q][Q + 1];
+      const int64_t rb = (int64_t(g) * c.N + q0) * c.h_s;
+      const int rows = (q1 - q0) * c.h_s;
+      for (int r0 = 0; r0 < rows; r0 += kRT) {
+        const int nr = min(kRT, rows - r0);
+        stage_rows<T, D>(c, 1, rb + r0, nr, Qt, Ot, s_l, s_w, s_D);
+        kv_rows_tile<T, D>(a, kvalid, half, Qt, Ot, s_l, s_w, s_D, nr, c.scale);
+      }
+    }
+    if (kvalid) {
+#pragma unroll
+      for (int e = 0; e < D / 2; ++e) {
+        int64_t idx = (int64_t(g) * c.N + j) * D + half * (D / 2) + e;
+        c.dk_acc[idx] = a.dk[e];
+        c.dv_acc[idx] = a.dv[e];
+      }
+    }
+  }
+}
+
+// window branch backward: CTA per (window W, g). dq_acc += (row-thread pass), dk/dv_acc += (key pass).
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_win_bwd(Ctx c) {
+  __shared__ float Qt[kRT * D], Ot[kRT * D], s_l[kRT], s_w[kRT], s_D[kRT];
+  const int W = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+  const int t0 = c.off[SSA_LEVEL_WIN][W], t1 = c.off[SSA_LEVEL_WIN][W + 1];
+  const int rows = (t1 - t0) * c.h_s;
+  const int64_t rb = (int64_t(g) * c.N + t0) * c.h_s;
+  const T* ks = static_cast<const T*>(c.ks);
+  const T* vs = static_cast<const T*>(c.vs);
+  const T* qs = static_cast<const T*>(c.qs);
+  const T* dos = static_cast<const T*>(c.dos);
+  const float l2s = c.scale * kLog2e;
+  // dq: thread = row, keys staged through Qt/Ot (reused as K/V tiles)
+  for (int r0 = 0; r0 < rows; r0 += 128) {
+    const int r = r0 + tid;
+    const bool valid = r < rows;
+    const int64_t row = rb + (valid ? r : 0);
+    float q[D], dO[D], dq[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+      q[e] = ld(qs + row * D + e);
+      dO[e] = ld(dos + row * D + e);
+      dq[e] = 0.f;
+    }
+    const float lse2 = c.lse[2][row] * kLog2e, w = c.gs[row * 3 + 2], Dv = c.Dd[2][row];
+    for (int k0 = t0; k0 < t1; k0 += kRT) {
+      const int nt = min(kRT, t1 - k0);
+      __syncthreads();
+      for (int i = tid; i < nt * D; i += 128) {
+        Qt[i] = ld(ks + (int64_t(g) * c.N + k0) * D + i);
+        Ot[i] = ld(vs + (int64_t(g) * c.N + k0) * D + i);
+      }
+      __syncthreads();
+      for (int j = 0; j < nt; ++j) {
+        float x = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < D; ++e) {
+          x += q[e] * Qt[j * D + e];
+          dp += dO[e] * Ot[j * D + e];
+        }
+        const float p = exp2f(x * l2s - lse2);
+        const float ds = p * (w * dp - Dv) * c.scale;
+#pragma unroll
+        for (int e = 0; e < D; ++e) dq[e] += ds * Qt[j * D + e];
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < D; ++e) c.dq_acc[row * D + e] += dq[e];
+    }
+  }
+  // dk/dv: key pairs
+  const int half = tid & 1;
+  for (int j0 = t0; j0 < t1; j0 += 64) {
+    const int j = j0 + (tid >> 1);
+    const bool kvalid = j < t1;
+    KvAcc<D> a;
+#pragma unroll
+    for (int e = 0; e < D / 2; ++e) {
+      int64_t idx = (int64_t(g) * c.N + (kvalid ? j : t0)) * D + half * (D / 2) + e;
+      a.k[e] = ld(ks + idx);
+      a.v[e] = ld(vs + idx);
+      a.dk[e] = 0.f;
+      a.dv[e] = 0.f;
+    }
+    for (int r0 = 0; r0 < rows; r0 += kRT) {
+      const int nr = min(kRT, rows - r0);
+      stage_rows<T, D>(c, 2, rb + r0, nr, Qt, Ot, s_l, s_w, s_D);
+      kv_rows_tile<T, D>(a, kvalid, half, Qt, Ot, s_l, s_w, s_D, nr, c.scale);
+    }
+    if (kvalid) {
+#pragma unroll
+      for (int e = 0; e < D / 2; ++e) {
+        int64_t idx = (int64_t(g) * c.N + j) * D + half * (D / 2) + e;
+        c.dk_acc[idx] += a.dk[e];
+        c.dv_acc[idx] += a.dv[e];
+      }
+    }
+  }
+}
+
+// compression branch dK^cmp/dV^cmp partials: grid (cmp tile, g, chunk). Tile = 64 compressed keys
+// of one batch item; chunk = a contiguous 1/n_chunk share of the batch item's rows.
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_cmp_dkdv(Ctx c) {
+  __shared__ float Qt[kRT * D], Ot[kRT * D], s_l[kRT], s_w[kRT], s_D[kRT];
+  const int tile = blockIdx.x, g = blockIdx.y, chunk = blockIdx.z;
+  const int b = c.cmp_tiles[2 * tile], j0 = c.cmp_tiles[2 * tile + 1];
+  const int c1 = c.bb[SSA_LEVEL_CMP][b + 1];
+  const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
+  const int half = threadIdx.x & 1;
+  const int j = j0 + (threadIdx.x >> 1);
+  const bool kvalid = j < c1;
+  const T* kc = static_cast<const T*>(c.kc);
+  const T* vc = static_cast<const T*>(c.vc);
+  KvAcc<D> a;
+#pragma unroll
+  for (int e = 0; e < D / 2; ++e) {
+    int64_t idx = (int64_t(g) * n_cmp + (kvalid ? j : j0)) * D + half * (D / 2) + e;
+    a.k[e] = ld(kc + idx);
+    a.v[e] = ld(vc + idx);
+    a.dk[e] = 0.f;
+    a.dv[e] = 0.f;
+  }
+  const int bt0 = c.batch_tokens[b], bt1 = c.batch_tokens[b + 1];
+  const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
+  const int64_t per = (rows + c.n_chunk - 1) / c.n_chunk;
+  const int64_t ra = min(rows, per * chunk), re = min(rows, per * (chunk + 1));
+  const int64_t rb = (int64_t(g) * c.N + bt0) * c.h_s;
+  for (int64_t r0 = ra; r0 < re; r0 += kRT) {
+    const int nr = int((re - r0) < kRT ? (re - r0) : kRT);
+    stage_rows<T, D>(c, 0, rb + r0, nr, Qt, Ot, s_l, s_w, s_D);
+    kv_rows_tile<T, D>(a, kvalid, half, Qt, Ot, s_l, s_w, s_D, nr, c.scale);
+  }
+  if (kvalid) {
+#pragma unroll
+    for (int e = 0; e < D / 2; ++e) {
+      int64_t idx = ((int64_t(chunk) * c.h_kv + g) * n_cmp + j) * D + half * (D / 2) + e;
+      c.dkc_part[idx] = a.dk[e];
+      c.dvc_part[idx] = a.dv[e];
+    }
+  }
+}
+
+__global__ void k_cmp_reduce(Ctx c) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t per = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * c.D;
+  if (i >= per) return;
+  float sk = 0.f, sv = 0.f;
+  for (int ch = 0; ch < c.n_chunk; ++ch) {
+    sk += c.dkc_part[ch * per + i];
+    sv += c.dvc_part[ch * per + i];
+  }
+  c.dkc[i] = sk;
+  c.dvc[i] = sv;
+}
+
+// epilogue: dq -> caller order; dk/dv = raw-token part + mean-pool backward of dk^cmp/dv^cmp
+template <class T>
+__global__ void k_bwd_final_q(Ctx c) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.H * c.D;
+  if (i >= total) return;
+  int e = int(i % c.D);
+  int h = int((i / c.D) % c.H);
+  int p = int(i / (int64_t(c.D) * c.H));
+  int g = h / c.h_s, s = h % c.h_s;
+  int dst = c.sorted_input ? p : c.perm[p];
+  st(static_cast<T*>(c.dq) + (int64_t(dst) * c.H + h) * c.D + e,
+     c.dq_acc[((int64_t(g) * c.N + p) * c.h_s + s) * c.D + e]);
+}
+template <class T>
+__global__ void k_bwd_final_kv(Ctx c) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t total = int64_t(c.N) * c.h_kv * c.D;
+  if (i >= total) return;
+  int e = int(i % c.D);
+  int g = int((i / c.D) % c.h_kv);
+  int p = int(i / (int64_t(c.D) * c.h_kv));
+  int j = c.tok_block[SSA_LEVEL_CMP][p];
+  float inv = 1.f / float(c.off[SSA_LEVEL_CMP][j + 1] - c.off[SSA_LEVEL_CMP][j]);
+  int64_t ki = (int64_t(g) * c.N + p) * c.D + e;
+  int64_t ci = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
+  int dst = c.sorted_input ? p : c.perm[p];
+  int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
+  st(static_cast<T*>(c.dk) + o, c.dk_acc[ki] + c.dkc[ci] * inv);
+  st(static_cast<T*>(c.dv) + o, c.dv_acc[ki] + c.dvc[ci] * inv);
+}
+
+template <class T, int D>
+ssa_status simt_fwd_t(const Ctx& c, cudaStream_t st, bool attention_only) {
+  const int nq = c.n_blk[SSA_LEVEL_Q];
+  if (!attention_only) {
+    size_t smem = (2 * kKT * D + kRows * (kKT + 1) + 4 * kKT + c.max_cmp_b + c.max_slc_b) * sizeof(float);
+    if (smem > 227 * 1024) { set_error("too many blocks per batch item for the SIMT kernel"); return SSA_ERR_UNSUPPORTED; }
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_cmp_fwd<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_cmp_fwd<T, D><<<dim3(nq, c.h_kv), kRows, smem, st>>>(c);
+    SSA_LAUNCH_CHECK("k_cmp_fwd");
+  }
+  k_attn_fwd<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c, 1);
+  SSA_LAUNCH_CHECK("k_attn_fwd(slc)");
+  k_attn_fwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), kRows, 0, st>>>(c, 2);
+  SSA_LAUNCH_CHECK("k_attn_fwd(win)");
+  return SSA_OK;
+}
+
+template <class T, int D>
+ssa_status simt_bwd_t(const Ctx& c, cudaStream_t st) {
+  const int nq = c.n_blk[SSA_LEVEL_Q];
+  k_dq<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_dq");
+  k_slc_dkdv<T, D><<<dim3(c.n_blk[SSA_LEVEL_SLC], c.h_kv), 128, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_slc_dkdv");
+  k_win_bwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), 128, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_win_bwd");
+  k_cmp_dkdv<T, D><<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), 128, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_cmp_dkdv");
+  int64_t per = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * c.D;
+  k_cmp_reduce<<<nblk(per, 256), 256, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_cmp_reduce");
+  return SSA_OK;
+}
+
+template <class T>
+ssa_status dispatch_d_fwd(const Ctx& c, cudaStream_t st, bool ao) {
+  switch (c.D) {
+    case 16: return simt_fwd_t<T, 16>(c, st, ao);
+    case 32: return simt_fwd_t<T, 32>(c, st, ao);
+    case 64: return simt_fwd_t<T, 64>(c, st, ao);
+  }
+  set_error("SIMT kernels support head dim 16, 32 or 64");
+  return SSA_ERR_UNSUPPORTED;
+}
+template <class T>
+ssa_status dispatch_d_bwd(const Ctx& c, cudaStream_t st) {
+  switch (c.D) {
+    case 16: return simt_bwd_t<T, 16>(c, st);
+    case 32: return simt_bwd_t<T, 32>(c, st);
+    case 64: return simt_bwd_t<T, 64>(c, st);
+  }
+  set_error("SIMT kernels support head dim 16, 32 or 64");
+  return SSA_ERR_UNSUPPORTED;
+}
+}  // namespace
+
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout) {
+  int64_t nr = int64_t(c.N) * c.H * c.D, nk = int64_t(c.N) * c.h_kv * c.D, ng = int64_t(c.N) * c.H * 3;
+  if (bf16) {
+    using T = __nv_bfloat16;
+    if (with_dout) {
+      k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.dout), static_cast<T*>(c.dos));
+      SSA_LAUNCH_CHECK("k_gather_rows(dout)");
+    }
+    k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
+    SSA_LAUNCH_CHECK("k_gather_rows");
+    k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
+                                                    static_cast<T*>(c.ks), static_cast<T*>(c.vs));
+    SSA_LAUNCH_CHECK("k_gather_keys");
+    k_gather_gates<T><<<nblk(ng, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+    SSA_LAUNCH_CHECK("k_gather_gates");
+  } else {
+    using T = float;
+    if (with_dout) {
+      k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.dout), static_cast<T*>(c.dos));
+      SSA_LAUNCH_CHECK("k_gather_rows(dout)");
+    }
+    k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
+    SSA_LAUNCH_CHECK("k_gather_rows");
+    k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
+                                                    static_cast<T*>(c.ks), static_cast<T*>(c.vs));
+    SSA_LAUNCH_CHECK("k_gather_keys");
+    k_gather_gates<T><<<nblk(ng, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+    SSA_LAUNCH_CHECK("k_gather_gates");
+  }
+  return SSA_OK;
+}
+
+ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st) {
+  dim3 grid(c.n_blk[SSA_LEVEL_CMP], c.h_kv);
+  if (bf16) k_pool<__nv_bfloat16><<<grid, c.D, 0, st>>>(c);
+  else k_pool<float><<<grid, c.D, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_pool");
+  return SSA_OK;
+}
+
+ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st) {
+  int64_t n = int64_t(c.N) * c.H * c.D;
+  if (bf16) k_combine<__nv_bfloat16><<<nblk(n, 256), 256, 0, st>>>(c);
+  else k_combine<float><<<nblk(n, 256), 256, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_combine");
+  return SSA_OK;
+}
+
+ssa_status simt_forward(const Ctx& c, bool bf16, cudaStream_t st, bool attention_only) {
+  return bf16 ? dispatch_d_fwd<__nv_bfloat16>(c, st, attention_only) : dispatch_d_fwd<float>(c, st, attention_only);
+}
+
+ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st) {
+  const int64_t nkeys = int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv;
+  const int64_t nI = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
+  SSA_CUDA_TRY(cudaMemsetAsync(c.inv_cnt, 0, nkeys * sizeof(int32_t), st));
+  k_inv_count<<<nblk(nI, 256), 256, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_inv_count");
+  ssa_status s = exclusive_scan(c.inv_cnt, c.inv_off, nkeys, c.inv_off + nkeys, scan_ws, st);
+  if (s != SSA_OK) return s;
+  SSA_CUDA_TRY(cudaMemsetAsync(c.inv_cnt, 0, nkeys * sizeof(int32_t), st));
+  k_inv_fill<<<nblk(nI, 256), 256, 0, st>>>(c, c.inv_cnt);
+  SSA_LAUNCH_CHECK("k_inv_fill");
+  k_inv_sort<<<nblk(nkeys, 128), 128, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_inv_sort");
+  return SSA_OK;
+}
+
+ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st) {
+  int64_t rows = int64_t(c.N) * c.H;
+  if (bf16) k_bwd_pre<__nv_bfloat16><<<nblk(rows, 256), 256, 0, st>>>(c);
+  else k_bwd_pre<float><<<nblk(rows, 256), 256, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_bwd_pre");
+  return SSA_OK;
+}
+
+ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st) {
+  int64_t nq = int64_t(c.N) * c.H * c.D, nk = int64_t(c.N) * c.h_kv * c.D;
+  if (bf16) {
+    k_bwd_final_q<__nv_bfloat16><<<nblk(nq, 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_bwd_final_q");
+    k_bwd_final_kv<__nv_bfloat16><<<nblk(nk, 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_bwd_final_kv");
+  } else {
+    k_bwd_final_q<float><<<nblk(nq, 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_bwd_final_q");
+    k_bwd_final_kv<float><<<nblk(nk, 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_bwd_final_kv");
+  }
+  return SSA_OK;
+}
+
+ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st) {
+  return bf16 ? dispatch_d_bwd<__nv_bfloat16>(c, st) : dispatch_d_bwd<float>(c, st);
+}
+
+}  // namespace ssa

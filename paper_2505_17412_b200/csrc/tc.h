@@ -1,0 +1,14 @@
+// tc.h — tcgen05/TMEM/TMA (sm_100a) kernels of the bf16, d = 64 hot path (tc_fwd.cu, tc_bwd.cu).
+#pragma once
+#include "internal.h"
+
+namespace ssa {
+bool tc_available();
+size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D);
+size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D);
+// forward after gather + pool: compression attention + scores + top-k, selection + window attention,
+// gated combine (writes c.out and the saved state).
+ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st);
+// backward after gather + prologue + inverse CSR: fills dq_acc, dk_acc, dv_acc, dkc, dvc.
+ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st);
+}  // namespace ssa

@@ -1,0 +1,362 @@
+"""Thin ctypes binding of libssa_b200.so (include/ssa.h). Argument marshalling only.
+
+Every step of SSA runs in the library's CUDA kernels; PyTorch supplies device memory (torch.empty on
+the tensors' device) and the current CUDA stream. There is NO CPU fallback: if the shared library is
+missing or a tensor is not on a CUDA device, these functions raise.
+
+Entry points (same names as the C ABI):
+    ssa_build_blocks(coords, grid, batch, m_cmp, m_slc, m_win, m_q)  -> Plan
+    ssa_forward(plan, cfg, q, k, v, gates)                          -> (out, Saved)
+    ssa_backward(plan, cfg, saved, q, k, v, gates, dout)            -> (dq, dk, dv, dgates)
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libssa_b200.so")
+
+SSA_F32, SSA_BF16 = 0, 1
+SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES = 1, 2, 4
+LEVEL_CMP, LEVEL_SLC, LEVEL_WIN, LEVEL_Q = 0, 1, 2, 3
+STATUS = ["SSA_OK", "SSA_ERR_ARG", "SSA_ERR_DUP_COORD", "SSA_ERR_COORD_RANGE", "SSA_ERR_HIERARCHY",
+          "SSA_ERR_BAD_STATE", "SSA_ERR_WORKSPACE", "SSA_ERR_UNSUPPORTED", "SSA_ERR_CUDA"]
+
+
+class SSAError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        self.code = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{where}: {self.code}: {detail}")
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("batch", ctypes.c_int32), ("grid", ctypes.c_int32 * 3),
+                ("m", ctypes.c_int32 * 4), ("n_blocks", ctypes.c_int32 * 4), ("max_fill", ctypes.c_int32 * 4),
+                ("max_blocks_per_batch", ctypes.c_int32 * 4), ("perm", ctypes.c_void_p),
+                ("inv_perm", ctypes.c_void_p), ("sorted_coords", ctypes.c_void_p),
+                ("offsets", ctypes.c_void_p * 4), ("block_coords", ctypes.c_void_p * 4),
+                ("batch_blocks", ctypes.c_void_p * 4), ("batch_tokens", ctypes.c_void_p),
+                ("cmp_to_slc", ctypes.c_void_p)]
+
+
+class AttnCfgC(ctypes.Structure):
+    _fields_ = [("h_q", ctypes.c_int32), ("h_kv", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p)]
+
+
+class SavedView(ctypes.Structure):
+    _fields_ = [("idx", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("o_branch", ctypes.c_void_p * 3),
+                ("lse_branch", ctypes.c_void_p * 3), ("k_cmp", ctypes.c_void_p), ("v_cmp", ctypes.c_void_p),
+                ("used_tcgen05", ctypes.c_int32)]
+
+
+_lib = None
+
+# symbol -> (restype, argtypes)
+_P = ctypes.c_void_p
+_SZ = ctypes.POINTER(ctypes.c_size_t)
+SIGNATURES = {
+    "ssa_build_blocks_size": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _SZ, _SZ]),
+    "ssa_build_blocks": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P,
+                                        ctypes.c_size_t, _P, ctypes.c_size_t, _P, ctypes.POINTER(_P)]),
+    "ssa_plan_destroy": (None, [_P]),
+    "ssa_get_plan_info": (ctypes.c_int, [_P, ctypes.POINTER(PlanInfo)]),
+    "ssa_forward_size": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _SZ, _SZ]),
+    "ssa_forward": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P,
+                                   ctypes.c_size_t, _P]),
+    "ssa_backward_size": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _SZ]),
+    "ssa_backward": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P, _P,
+                                    _P, _P, _P, ctypes.c_size_t, _P]),
+    "ssa_saved_state": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, ctypes.c_size_t,
+                                       ctypes.POINTER(SavedView)]),
+    "ssa_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+    "ssa_last_error": (ctypes.c_char_p, []),
+    "ssa_launch_count": (ctypes.c_int64, []),
+    "ssa_reset_launch_count": (None, []),
+    "ssa_build_info": (ctypes.c_char_p, []),
+}
+
+
+def lib():
+    """Load libssa_b200.so (raises if it has not been built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2505_17412_b200.build` "
+                              "(the SSA path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise SSAError(status, where, lib().ssa_last_error().decode())
+
+
+def _stream(device: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return SSA_F32
+    if dt == torch.bfloat16:
+        return SSA_BF16
+    raise ValueError(f"unsupported dtype {dt} (float32 or bfloat16)")
+
+
+class Plan:
+    """Owns the device plan buffer and the host handle of one block partition."""
+
+    def __init__(self, handle, plan_buf: torch.Tensor, coords: torch.Tensor):
+        self._handle = handle
+        self.buf = plan_buf
+        self.device = plan_buf.device
+        info = PlanInfo()
+        _check(lib().ssa_get_plan_info(handle, ctypes.byref(info)), "ssa_get_plan_info")
+        self.info = info
+        self.n = int(info.n)
+        self.batch = int(info.batch)
+        self.m = tuple(info.m)
+        self.n_blocks = tuple(info.n_blocks)
+        self.max_fill = tuple(info.max_fill)
+        self.max_blocks_per_batch = tuple(info.max_blocks_per_batch)
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def _i32(self, ptr: int, count: int) -> torch.Tensor:
+        """Copy `count` int32 from a device pointer inside the plan buffer (parity hooks)."""
+        base = self.buf.data_ptr()
+        off = (ptr - base) // 4
+        return self.buf.view(torch.int32)[off:off + count].clone()
+
+    def perm(self):
+        return self._i32(self.info.perm, self.n)
+
+    def offsets(self, level: int):
+        return self._i32(self.info.offsets[level], self.n_blocks[level] + 1)
+
+    def block_coords(self, level: int):
+        return self._i32(self.info.block_coords[level], 4 * self.n_blocks[level]).view(-1, 4)
+
+    def batch_blocks(self, level: int):
+        return self._i32(self.info.batch_blocks[level], self.batch + 1)
+
+    def cmp_to_slc(self):
+        return self._i32(self.info.cmp_to_slc, self.n_blocks[LEVEL_CMP])
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None and _lib is not None:
+            _lib.ssa_plan_destroy(self._handle)
+            self._handle = None
+
+
+def ssa_build_blocks(coords: torch.Tensor, grid, batch: int, m_cmp: int, m_slc: int, m_win: int,
+                     m_q: int) -> Plan:
+    """C: ssa_build_blocks. coords: CUDA int32 [N,4] (b,x,y,z)."""
+    L = lib()
+    if coords.dtype != torch.int32 or coords.dim() != 2 or coords.shape[1] != 4:
+        raise ValueError("coords must be int32 [N,4]")
+    cp = _dev(coords, "coords")
+    n = coords.shape[0]
+    g = (ctypes.c_int32 * 3)(*[int(x) for x in grid])
+    pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.ssa_build_blocks_size(n, batch, g, m_cmp, m_slc, m_win, m_q, ctypes.byref(pb), ctypes.byref(wb)),
+           "ssa_build_blocks_size")
+    plan_buf = torch.empty(pb.value, dtype=torch.uint8, device=coords.device)
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=coords.device)
+    h = ctypes.c_void_p()
+    _check(L.ssa_build_blocks(cp, n, batch, g, m_cmp, m_slc, m_win, m_q, ctypes.c_void_p(plan_buf.data_ptr()),
+                              pb.value, ctypes.c_void_p(ws.data_ptr()), wb.value, _stream(coords.device),
+                              ctypes.byref(h)), "ssa_build_blocks")
+    return Plan(h, plan_buf, coords)
+
+
+@dataclass
+class AttnCfg:
+    h_q: int
+    h_kv: int
+    d: int
+    top_k: int
+    dtype: torch.dtype = torch.bfloat16
+    scale: float = 0.0
+    flags: int = 0
+    pe_k: torch.Tensor | None = None
+    pe_v: torch.Tensor | None = None
+
+    def c(self) -> AttnCfgC:
+        return AttnCfgC(self.h_q, self.h_kv, self.d, self.top_k, float(self.scale), _dtype_code(self.dtype),
+                        int(self.flags), self.pe_k.data_ptr() if self.pe_k is not None else None,
+                        self.pe_v.data_ptr() if self.pe_v is not None else None)
+
+
+class Saved:
+    """Saved forward state (device buffer) + parity views into it."""
+
+    def __init__(self, plan: Plan, cfg: AttnCfg, buf: torch.Tensor):
+        self.plan, self.cfg, self.buf = plan, cfg, buf
+        v = SavedView()
+        cc = cfg.c()
+        _check(lib().ssa_saved_state(plan.handle, ctypes.byref(cc), ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                     ctypes.byref(v)), "ssa_saved_state")
+        self.view = v
+        self.used_tcgen05 = bool(v.used_tcgen05)
+
+    def _slice(self, ptr, count, dtype):
+        es = torch.tensor([], dtype=dtype).element_size()
+        off = ptr - self.buf.data_ptr()
+        assert off % es == 0
+        return self.buf[off:off + count * es].view(dtype)
+
+    def indices(self) -> torch.Tensor:
+        nq = self.plan.n_blocks[LEVEL_Q]
+        return self._slice(self.view.idx, nq * self.cfg.h_kv * self.cfg.top_k, torch.int32).view(
+            nq, self.cfg.h_kv, self.cfg.top_k)
+
+    def scores(self) -> torch.Tensor | None:
+        if not self.view.scores:
+            return None
+        nq = self.plan.n_blocks[LEVEL_Q]
+        ms = max(self.plan.max_blocks_per_batch[LEVEL_SLC], 1)
+        return self._slice(self.view.scores, nq * self.cfg.h_kv * ms, torch.float32).view(nq, self.cfg.h_kv, ms)
+
+    def branch(self, b: int):
+        """(o, lse) of branch b (0 cmp, 1 slc, 2 win), internal layout [h_kv][N][h_s][d], sorted order."""
+        n, hk, hs, d = self.plan.n, self.cfg.h_kv, self.cfg.h_q // self.cfg.h_kv, self.cfg.d
+        o = self._slice(self.view.o_branch[b], n * self.cfg.h_q * d, self.cfg.dtype).view(hk, n, hs, d)
+        lse = self._slice(self.view.lse_branch[b], n * self.cfg.h_q, torch.float32).view(hk, n, hs)
+        return o, lse
+
+    def k_cmp(self):
+        nc = self.plan.n_blocks[LEVEL_CMP]
+        return (self._slice(self.view.k_cmp, self.cfg.h_kv * nc * self.cfg.d, self.cfg.dtype).view(self.cfg.h_kv, nc, self.cfg.d),
+                self._slice(self.view.v_cmp, self.cfg.h_kv * nc * self.cfg.d, self.cfg.dtype).view(self.cfg.h_kv, nc, self.cfg.d))
+
+
+def _check_inputs(plan: Plan, cfg: AttnCfg, q, k, v, gates):
+    n = plan.n
+    if tuple(q.shape) != (n, cfg.h_q, cfg.d) or tuple(k.shape) != (n, cfg.h_kv, cfg.d) or \
+            tuple(v.shape) != (n, cfg.h_kv, cfg.d) or tuple(gates.shape) != (n, cfg.h_q, 3):
+        raise ValueError("shape mismatch: q [N,h_q,d], k/v [N,h_kv,d], gates [N,h_q,3]")
+    for t in (q, k, v, gates):
+        if t.dtype != cfg.dtype:
+            raise ValueError(f"tensor dtype {t.dtype} != cfg.dtype {cfg.dtype}")
+
+
+class Workspace:
+    """Reusable device scratch (grown on demand) so steady-state calls allocate nothing."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _ws(device, key):
+    return _default_ws.setdefault((str(device), key), Workspace())
+
+
+def ssa_forward(plan: Plan, cfg: AttnCfg, q, k, v, gates, out=None, saved: Saved | None = None,
+                ws: Workspace | None = None):
+    """C: ssa_forward. Returns (out [N,h_q,d], Saved)."""
+    L = lib()
+    _check_inputs(plan, cfg, q, k, v, gates)
+    cc = cfg.c()
+    wsb, svb = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.ssa_forward_size(plan.handle, ctypes.byref(cc), ctypes.byref(wsb), ctypes.byref(svb)), "ssa_forward_size")
+    dev = q.device
+    if out is None:
+        out = torch.empty_like(q)
+    if saved is None:
+        saved = Saved(plan, cfg, torch.empty(svb.value, dtype=torch.uint8, device=dev))
+    w = (ws or _ws(dev, "fwd")).get(wsb.value, dev)
+    _check(L.ssa_forward(plan.handle, ctypes.byref(cc), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                         _dev(gates, "gates"), _dev(out, "out"), ctypes.c_void_p(saved.buf.data_ptr()),
+                         saved.buf.numel(), ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_forward")
+    return out, saved
+
+
+def ssa_backward(plan: Plan, cfg: AttnCfg, saved: Saved, q, k, v, gates, dout, grads=None,
+                 ws: Workspace | None = None):
+    """C: ssa_backward. Returns (dq, dk, dv, dgates)."""
+    L = lib()
+    _check_inputs(plan, cfg, q, k, v, gates)
+    if tuple(dout.shape) != tuple(q.shape) or dout.dtype != cfg.dtype:
+        raise ValueError("dout must match q")
+    cc = cfg.c()
+    wsb = ctypes.c_size_t()
+    _check(L.ssa_backward_size(plan.handle, ctypes.byref(cc), ctypes.byref(wsb)), "ssa_backward_size")
+    dev = q.device
+    if grads is None:
+        grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(gates))
+    dq, dk, dv, dg = grads
+    w = (ws or _ws(dev, "bwd")).get(wsb.value, dev)
+    _check(L.ssa_backward(plan.handle, ctypes.byref(cc), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                          _dev(gates, "gates"), ctypes.c_void_p(saved.buf.data_ptr()), saved.buf.numel(),
+                          _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"), _dev(dg, "dgates"),
+                          ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_backward")
+    return dq, dk, dv, dg
+
+
+def launch_count() -> int:
+    return int(lib().ssa_launch_count())
+
+
+def reset_launch_count():
+    lib().ssa_reset_launch_count()
+
+
+def build_info() -> str:
+    return lib().ssa_build_info().decode()
+
+
+class SSAFunction(torch.autograd.Function):
+    """Autograd wrapper: out = SSA(q, k, v, gates) for a fixed plan (block structure) and cfg."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, gates, plan, cfg):
+        out, saved = ssa_forward(plan, cfg, q.contiguous(), k.contiguous(), v.contiguous(), gates.contiguous())
+        ctx.plan, ctx.cfg, ctx.saved = plan, cfg, saved
+        ctx.save_for_backward(q, k, v, gates)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        q, k, v, gates = ctx.saved_tensors
+        dq, dk, dv, dg = ssa_backward(ctx.plan, ctx.cfg, ctx.saved, q.contiguous(), k.contiguous(), v.contiguous(),
+                                      gates.contiguous(), dout.contiguous())
+        return dq, dk, dv, dg, None, None
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,152 @@
+"""GPU parity of the whole SSA path (forward a2-a8, backward a9) through the C ABI against the float64
+oracle, on the same seeded inputs (SURVEY §8c parity protocol):
+  * top-k isolated: oracle top-k on the GPU's fp32 scores == GPU indices, bit for bit;
+  * top-k end to end: GPU indices == oracle f64 top-k except rows inside the near-tie band;
+  * outputs / gradients: oracle run with the GPU's indices; max|x-ref|/rms(ref) <= 1e-4 (fp32) or
+    2e-2 (bf16 in, fp32 accumulate) — the north star's tolerances.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from gpu_util import rel_err, run_gpu, topk_end_to_end_check, topk_isolated_check
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+DELTA = {"f32": 1e-6, "bf16": 1e-4}
+
+
+def _oracle(inp, I, kw, backward=True, pe=None):
+    import oracle as O
+    N, H, d = inp.q.shape
+    f = O.ssa_forward(inp.coords, inp.grid, inp.batch, inp.q, inp.k, inp.v, inp.gates, I_override=I,
+                      pe_k=None if pe is None else pe[0], pe_v=None if pe is None else pe[1], **kw)
+    grads = O.ssa_backward(f, inp.q, inp.k, inp.v, inp.gates, inp.dout, h_kv=kw["h_kv"]) if backward else None
+    return f, grads
+
+
+def _check_all(inp, kw, flags=0, backward=True, pe=None, expect_tc=None):
+    import oracle as O
+    r = run_gpu(inp, flags=flags, backward=backward, pe=pe, **kw)
+    if expect_tc is not None:
+        assert r["saved"].used_tcgen05 == expect_tc
+    f_free, _ = _oracle(inp, None, kw, backward=False, pe=pe)
+    plan_o = f_free.plan
+    assert topk_isolated_check(plan_o, r["scores"], r["I"], kw["T"]) == 0
+    mism, amb = topk_end_to_end_check(plan_o, f_free.scores, r["I"], kw["T"], DELTA[inp.dtype])
+    assert mism == 0, (mism, amb)
+    f, grads = _oracle(inp, r["I"], kw, backward=backward, pe=pe)
+    tol = TOL[inp.dtype]
+    errs = {"out": rel_err(r["out"], f.out)}
+    for b, name in enumerate(("cmp", "slc", "win")):
+        from gpu_util import internal_to_orig
+        o, lse = r["saved"].branch(b)
+        errs["o_" + name] = rel_err(internal_to_orig(o, r["perm"]), f.o[name])
+        lg = internal_to_orig(lse, r["perm"])
+        errs["lse_" + name] = float(np.max(np.abs(lg - f.lse[name])))
+    if backward:
+        for name, g, ref in zip(("dq", "dk", "dv", "dgates"), (r["dq"], r["dk"], r["dv"], r["dgates"]), grads):
+            errs[name] = rel_err(g, ref)
+    bad = {k: v for k, v in errs.items() if v > tol}
+    assert not bad, (bad, errs)
+    return r, errs
+
+
+def test_c1_fp32_full():
+    """BASELINE config 1: 32^3 shell (4328 tokens), 1 head d=64, blocks 4^3, T=4, fp32 fwd+bwd."""
+    from ssa_workload import CONFIGS, config_coords, make_inputs
+    cfg = CONFIGS["C1"]
+    c, grid, batch = config_coords("C1")
+    inp = make_inputs(c, grid, batch, cfg["H"], cfg["h_kv"], cfg["d"], "f32", seed=cfg["seed"])
+    kw = dict(h_kv=1, T=4, m_cmp=4, m_slc=4, m_win=4, m_q=4)
+    _check_all(inp, kw)
+
+
+def test_c2_bf16_full():
+    """BASELINE config 2: 64^3 shell (24808 tokens), 16 heads (2 kv), d=64, bf16 fwd+bwd."""
+    from ssa_workload import CONFIGS, config_coords, make_inputs
+    cfg = CONFIGS["C2"]
+    c, grid, batch = config_coords("C2")
+    inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=cfg["seed"])
+    kw = dict(h_kv=2, T=8, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    _check_all(inp, kw)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("case", ["batch3_ragged", "mq1_pertoken", "win_lt_q", "T_exceeds", "d32_hs1"])
+def test_small_cases(dtype, case):
+    from conftest import random_coords
+    from ssa_workload import make_inputs
+    rng = np.random.Generator(np.random.PCG64(hash(case) % 1000))
+    H, h_kv, d = 8, 2, 64
+    kw = dict(h_kv=2, T=3, m_cmp=2, m_slc=4, m_win=4, m_q=4)
+    G, n, batch = 16, 500, 3
+    if case == "mq1_pertoken":
+        kw.update(m_q=1)
+    elif case == "win_lt_q":
+        kw.update(m_win=2, m_q=4)
+    elif case == "T_exceeds":
+        kw.update(T=64)
+        G, n = 8, 120
+    elif case == "d32_hs1":
+        H, h_kv, d = 2, 2, 32
+        kw.update(h_kv=2)
+    c = random_coords(rng, n, G, batch)
+    if case == "batch3_ragged":
+        c = c[rng.permutation(len(c))[: len(c) - 37]]             # ragged batch items, shuffled order
+    inp = make_inputs(c, (G, G, G), batch, H, h_kv, d, dtype, seed=7)
+    _check_all(inp, kw)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_single_token(dtype):
+    from ssa_workload import make_inputs
+    c = np.array([[0, 3, 4, 5]], dtype=np.int32)
+    inp = make_inputs(c, (8, 8, 8), 1, 4, 2, 64, dtype, seed=3)
+    kw = dict(h_kv=2, T=8, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    _check_all(inp, kw)
+
+
+def test_pe_tables():
+    from conftest import random_coords
+    from ssa_workload import make_inputs, round_to_bf16
+    rng = np.random.Generator(np.random.PCG64(9))
+    c = random_coords(rng, 400, 16, 1)
+    inp = make_inputs(c, (16, 16, 16), 1, 4, 2, 64, "f32", seed=1)
+    pe = (rng.standard_normal((64, 2, 64)).astype(np.float32), rng.standard_normal((64, 2, 64)).astype(np.float32))
+    _check_all(inp, dict(h_kv=2, T=3, m_cmp=4, m_slc=8, m_win=8, m_q=8), pe=pe)
+
+
+def test_planted_selection_bit_exact():
+    """Planted workload: the top-T gap is large, so GPU indices must equal the oracle's exactly."""
+    import oracle as O
+    from ssa_workload import config_coords, make_inputs, planted_inputs
+    c, grid, batch = config_coords("C1", shapes=[(32, 13.0, 2.0)])
+    inp = make_inputs(c, grid, batch, 8, 2, 64, "bf16", seed=4)
+    inp = planted_inputs(inp, m_q=8, m_slc=8, T=4, h_s=4)
+    kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    r = run_gpu(inp, backward=False, **kw)
+    f = O.ssa_forward(inp.coords, inp.grid, inp.batch, inp.q, inp.k, inp.v, inp.gates, **kw)
+    assert np.array_equal(r["I"], f.I)
+
+
+def test_gpu_sorted_input_flag():
+    """SSA_INPUT_SORTED: feeding block-sorted tensors gives the same (sorted) result."""
+    import torch
+    from conftest import random_coords
+    from gpu_util import to_dev
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import make_inputs
+    rng = np.random.Generator(np.random.PCG64(2))
+    c = random_coords(rng, 300, 16, 2)
+    inp = make_inputs(c, (16, 16, 16), 2, 4, 2, 64, "bf16", seed=2)
+    kw = dict(h_kv=2, T=3, m_cmp=2, m_slc=4, m_win=4, m_q=4)
+    r = run_gpu(inp, backward=False, **kw)
+    perm = r["perm"]
+    plan = r["plan"]
+    cfg = ssa.AttnCfg(h_q=4, h_kv=2, d=64, top_k=3, dtype=torch.bfloat16, flags=ssa.SSA_INPUT_SORTED)
+    q, k, v, g = (to_dev(x[perm], torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates))
+    out, _ = ssa.ssa_forward(plan, cfg, q, k, v, g)
+    assert np.array_equal(out.float().cpu().numpy(), r["out"][perm].astype(np.float32))
