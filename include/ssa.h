@@ -170,7 +170,7 @@ ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, c
  *   idx      int32 [n_blocks[Q], h_kv, top_k]  selected selection-block ids (global), -1 padded
  *   scores   fp32 [n_blocks[Q], h_kv, max_blocks_per_batch[SLC]] (NULL unless SSA_SAVE_SCORES);
  *            row (Q,g) holds the Eq. 8 score of the selection blocks of Q's batch item (local index)
- *   o_branch, lse_branch: branch outputs / fp32 LSEs, internal layout [h_kv][n][h_s][d] / [h_kv][n][h_s]
+ *   o_branch, lse_branch: fp32 branch outputs / LSEs, internal layout [h_kv][n][h_s][d] / [h_kv][n][h_s]
  *            in plan (sorted) order, branch 0=cmp 1=slc 2=win.
  * ----------------------------------------------------------------------------------------------*/
 typedef struct {
@@ -178,7 +178,7 @@ typedef struct {
   const float* scores;
   const void* o_branch[3];
   const float* lse_branch[3];
-  const void* k_cmp;   /* [h_kv][n_blocks[CMP]][d] dtype */
+  const void* k_cmp;   /* [h_kv][n_blocks[CMP]][d] fp32 */
   const void* v_cmp;
   int32_t used_tcgen05;  /* 1 if the forward ran the tcgen05 kernels */
 } ssa_saved_view;

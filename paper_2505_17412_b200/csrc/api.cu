@@ -58,9 +58,10 @@ bool use_tc(const Dims& d, const ssa_attn_cfg* cfg) {
 // saved state: kc, vc, o[3], lse[3], I, scores
 void carve_saved(Carve& c, const Dims& d, const ssa_attn_cfg* cfg, Ctx* x) {
   const int64_t rows = d.N * d.H;
-  x->kc = c.take<char>(size_t(d.h_kv) * d.n_cmp * d.D * d.esz);
-  x->vc = c.take<char>(size_t(d.h_kv) * d.n_cmp * d.D * d.esz);
-  for (int b = 0; b < 3; ++b) x->o[b] = c.take<char>(size_t(rows) * d.D * d.esz);
+  // pooled K/V and branch outputs are kept in fp32 (precision of the saved state)
+  x->kc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
+  x->vc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
+  for (int b = 0; b < 3; ++b) x->o[b] = c.take<float>(size_t(rows) * d.D);
   for (int b = 0; b < 3; ++b) x->lse[b] = c.take<float>(rows);
   x->I = c.take<int32_t>(size_t(d.n_q) * d.h_kv * d.T);
   x->scores = (cfg->flags & SSA_SAVE_SCORES) ? c.take<float>(size_t(d.n_q) * d.h_kv * std::max(d.max_slc_b, 1)) : nullptr;

@@ -98,8 +98,8 @@ __global__ void k_pool(Ctx c) {
   }
   const float inv = 1.f / float(t1 - t0);
   int64_t o = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
-  st(static_cast<T*>(c.kc) + o, sk * inv);
-  st(static_cast<T*>(c.vc) + o, sv * inv);
+  static_cast<float*>(c.kc)[o] = sk * inv;
+  static_cast<float*>(c.vc)[o] = sv * inv;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(kRows) k_cmp_fwd(Ctx c) {
   const int s0 = c.bb[SSA_LEVEL_SLC][b], s1 = c.bb[SSA_LEVEL_SLC][b + 1], ns = s1 - s0;
   const int rows = (t1 - t0) * c.h_s;
   const T* qs = static_cast<const T*>(c.qs);
-  const T* kc = static_cast<const T*>(c.kc);
-  const T* vc = static_cast<const T*>(c.vc);
+  const float* kc = static_cast<const float*>(c.kc);
+  const float* vc = static_cast<const float*>(c.vc);
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
   const float qscale = c.scale * kLog2e;
   for (int i = tid; i < nk; i += kRows) sc_cmp[i] = 0.f;
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(kRows) k_cmp_fwd(Ctx c) {
       if (tid < nt) sc_cmp[k0 + tid] += (red[tid] + red[kKT + tid]) + (red[2 * kKT + tid] + red[3 * kKT + tid]);
     }
     if (valid) {
-      T* oc = static_cast<T*>(c.o[0]);
+      float* oc = static_cast<float*>(c.o[0]);
 #pragma unroll
-      for (int e = 0; e < D; ++e) st(oc + (row_base + r) * D + e, o[e]);
+      for (int e = 0; e < D; ++e) oc[(row_base + r) * D + e] = o[e];
       c.lse[0][row_base + r] = lse2 * kLn2;
     }
   }
@@ -322,9 +322,9 @@ __global__ void __launch_bounds__(kRows) k_attn_fwd(Ctx c, int mode) {
     }
     if (valid) {
       const float inv = 1.f / l;
-      T* ob = static_cast<T*>(c.o[br]);
+      float* ob = static_cast<float*>(c.o[br]);
 #pragma unroll
-      for (int e = 0; e < D; ++e) st(ob + (row_base + r) * D + e, o[e] * inv);
+      for (int e = 0; e < D; ++e) ob[(row_base + r) * D + e] = o[e] * inv;
       c.lse[br][row_base + r] = (m + log2f(l)) * kLn2;
     }
   }
@@ -344,9 +344,9 @@ __global__ void k_combine(Ctx c) {
   int g = h / c.h_s, s = h % c.h_s;
   int64_t row = (int64_t(g) * c.N + p) * c.h_s + s;
   const float* w = c.gs + row * 3;
-  float v = w[0] * ld(static_cast<const T*>(c.o[0]) + row * c.D + e) +
-            w[1] * ld(static_cast<const T*>(c.o[1]) + row * c.D + e) +
-            w[2] * ld(static_cast<const T*>(c.o[2]) + row * c.D + e);
+  float v = w[0] * static_cast<const float*>(c.o[0])[row * c.D + e] +
+            w[1] * static_cast<const float*>(c.o[1])[row * c.D + e] +
+            w[2] * static_cast<const float*>(c.o[2])[row * c.D + e];
   int dst = c.sorted_input ? p : c.perm[p];
   st(static_cast<T*>(c.out) + (int64_t(dst) * c.H + h) * c.D + e, v);
 }
@@ -364,7 +364,7 @@ __global__ void k_bwd_pre(Ctx c) {
   for (int e = 0; e < c.D; ++e) {
     float d = ld(dos + row * c.D + e);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) acc[b] += d * ld(static_cast<const T*>(c.o[b]) + row * c.D + e);
+    for (int b = 0; b < 3; ++b) acc[b] += d * static_cast<const float*>(c.o[b])[row * c.D + e];
   }
   const int s = int(row % c.h_s);
   const int p = int((row / c.h_s) % c.N);
@@ -457,8 +457,10 @@ __global__ void __launch_bounds__(kRows) k_dq(Ctx c) {
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
       const int br = sgi == 0 ? 0 : 1;
-      const T* kb = static_cast<const T*>(br == 0 ? c.kc : c.ks);
-      const T* vb = static_cast<const T*>(br == 0 ? c.vc : c.vs);
+      const T* kb = static_cast<const T*>(c.ks);
+      const T* vb = static_cast<const T*>(c.vs);
+      const float* kcf = static_cast<const float*>(c.kc);
+      const float* vcf = static_cast<const float*>(c.vc);
       const int64_t kbase = int64_t(g) * (br == 0 ? c.n_blk[SSA_LEVEL_CMP] : c.N);
       const float lse2 = c.lse[br][row] * kLog2e;
       const float w = c.gs[row * 3 + br];
@@ -467,8 +469,8 @@ __global__ void __launch_bounds__(kRows) k_dq(Ctx c) {
         const int nt = min(kKT, seg_e[sgi] - k0);
         __syncthreads();
         for (int i = tid; i < nt * D; i += kRows) {
-          Kt[i] = ld(kb + (kbase + k0) * D + i);
-          Vt[i] = ld(vb + (kbase + k0) * D + i);
+          Kt[i] = br == 0 ? kcf[(kbase + k0) * D + i] : ld(kb + (kbase + k0) * D + i);
+          Vt[i] = br == 0 ? vcf[(kbase + k0) * D + i] : ld(vb + (kbase + k0) * D + i);
         }
         __syncthreads();
         for (int j = 0; j < nt; ++j) {
@@ -688,14 +690,14 @@ __global__ void __launch_bounds__(128) k_cmp_dkdv(Ctx c) {
   const int half = threadIdx.x & 1;
   const int j = j0 + (threadIdx.x >> 1);
   const bool kvalid = j < c1;
-  const T* kc = static_cast<const T*>(c.kc);
-  const T* vc = static_cast<const T*>(c.vc);
+  const float* kc = static_cast<const float*>(c.kc);
+  const float* vc = static_cast<const float*>(c.vc);
   KvAcc<D> a;
 #pragma unroll
   for (int e = 0; e < D / 2; ++e) {
     int64_t idx = (int64_t(g) * n_cmp + (kvalid ? j : j0)) * D + half * (D / 2) + e;
-    a.k[e] = ld(kc + idx);
-    a.v[e] = ld(vc + idx);
+    a.k[e] = kc[idx];
+    a.v[e] = vc[idx];
     a.dk[e] = 0.f;
     a.dv[e] = 0.f;
   }

@@ -247,14 +247,14 @@ class Saved:
     def branch(self, b: int):
         """(o, lse) of branch b (0 cmp, 1 slc, 2 win), internal layout [h_kv][N][h_s][d], sorted order."""
         n, hk, hs, d = self.plan.n, self.cfg.h_kv, self.cfg.h_q // self.cfg.h_kv, self.cfg.d
-        o = self._slice(self.view.o_branch[b], n * self.cfg.h_q * d, self.cfg.dtype).view(hk, n, hs, d)
+        o = self._slice(self.view.o_branch[b], n * self.cfg.h_q * d, torch.float32).view(hk, n, hs, d)
         lse = self._slice(self.view.lse_branch[b], n * self.cfg.h_q, torch.float32).view(hk, n, hs)
         return o, lse
 
     def k_cmp(self):
         nc = self.plan.n_blocks[LEVEL_CMP]
-        return (self._slice(self.view.k_cmp, self.cfg.h_kv * nc * self.cfg.d, self.cfg.dtype).view(self.cfg.h_kv, nc, self.cfg.d),
-                self._slice(self.view.v_cmp, self.cfg.h_kv * nc * self.cfg.d, self.cfg.dtype).view(self.cfg.h_kv, nc, self.cfg.d))
+        return (self._slice(self.view.k_cmp, self.cfg.h_kv * nc * self.cfg.d, torch.float32).view(self.cfg.h_kv, nc, self.cfg.d),
+                self._slice(self.view.v_cmp, self.cfg.h_kv * nc * self.cfg.d, torch.float32).view(self.cfg.h_kv, nc, self.cfg.d))
 
 
 def _check_inputs(plan: Plan, cfg: AttnCfg, q, k, v, gates):
