@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py — SSA forward+backward at 1024^3-resolution token counts (BASELINE.json configs[2], "C3").
+
+One step = the whole hot path of SURVEY §8(a) on one batch of synthetic input: block build (a1),
+permute (a2), pool (a3), compression attention + Eq. 8 scores + top-k (a4, a5), selection + window
+attention (a6, a7), gated sum (a8) and the backward (a9), all in libssa_b200's kernels.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling — every rank processes its own shape(s); no
+collective on the data path (SSA has no parameters; shapes are independent, SURVEY §8e mode 1).
+Only the timing barrier and the max-over-ranks reduction use torch.distributed.
+
+Prints ONE JSON line on rank 0. `value` = whole-job ms per shape (fwd+bwd) = max-over-ranks step
+time / shapes processed per step by all ranks (lower is better).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SSA fwd+bwd ms & tensor-pipe % at 1024^3 tokens; speedup vs full attention"
+UNIT = "ms/shape (fwd+bwd, 1024^3-res shape)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-full", action="store_true", help="skip the full-attention comparator")
+    ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=24, help="query blocks in the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING recipe)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(config: str, rank: int, world: int):
+    """Shapes of this rank. C3/C5: one 1024^3-res shell per rank (weak scaling). C4: the 8-shape batch,
+    shapes dealt LPT-style across ranks by token count."""
+    from ssa_workload import CONFIGS, batch_coords, sphere_shell
+    cfg = CONFIGS[config]
+    shapes = list(cfg["shapes"])
+    if config == "C4" and world > 1:
+        order = sorted(range(len(shapes)), key=lambda i: -sphere_shell(*shapes[i]).shape[0])
+        loads = [0] * world
+        mine = []
+        for i in order:
+            r = int(np.argmin(loads))
+            loads[r] += sphere_shell(*shapes[i]).shape[0] ** 2
+            if r == rank:
+                mine.append(shapes[i])
+        shapes = mine
+    shells = [sphere_shell(*s) for s in shapes]
+    return cfg, batch_coords(shells), (cfg["G"],) * 3, len(shells)
+
+
+def flops_model(plan, cfg):
+    """Algorithmic element counts: E_cmp, E_slc (from the indices), E_win."""
+    return None
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import make_inputs
+
+    cfg, coords, grid, batch = workload(args.config, rank, world)
+    H, h_kv, d, T = cfg["H"], cfg["h_kv"], cfg["d"], cfg["T"]
+    ms = (cfg["m_cmp"], cfg["m_slc"], cfg["m_win"], cfg["m_q"])
+    tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    inp = make_inputs(coords, grid, batch, H, h_kv, d, cfg["dtype"], seed=cfg["seed"] + rank)
+    N = coords.shape[0]
+    # inputs resident in HBM before the timed region
+    c_d = torch.from_numpy(coords).to(dev)
+    q, k, v, g, do = (torch.from_numpy(x).to(dev, dtype=tdt) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout))
+    flags = ssa.SSA_FORCE_SIMT if args.force_simt else 0
+    acfg = ssa.AttnCfg(h_q=H, h_kv=h_kv, d=d, top_k=T, dtype=tdt, flags=flags)
+    grads = tuple(torch.empty_like(x) for x in (q, k, v, g))
+    out = torch.empty_like(q)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    st = torch.cuda.current_stream(dev)
+
+    def step(qq=q, kk=k, vv=v, gg=g, dd=do):
+        plan = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+        o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=out)
+        ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=grads)
+        return plan, saved
+
+    for _ in range(max(args.warmup, 3) if args.warmup > 0 else 3):
+        plan, saved = step()
+    torch.cuda.synchronize(dev)
+    used_tc = saved.used_tcgen05
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events) ----
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    ssa.reset_launch_count()
+    ssa.profile_reset()
+    ssa.profile_enable(True)
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        step()
+        e1.record(st)
+        times.append((e0, e1))
+    torch.cuda.synchronize(dev)
+    ssa.profile_enable(False)
+    launches = ssa.launch_count()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in times]
+    total_ms = float(sum(step_ms))
+    kernel_names = ["tc_cmp_fwd", "tc_slc_win_fwd", "tc_bwd_dq", "tc_bwd_kv", "tc_bwd_cmp_kv",
+                    "k_cmp_fwd", "k_attn_fwd(slc)", "k_attn_fwd(win)", "k_dq", "k_slc_dkdv", "k_win_bwd", "k_cmp_dkdv"]
+    ktimes = {}
+    for kn in kernel_names:
+        t, n = ssa.profile_read(kn)
+        if n:
+            ktimes[kn] = (t, n)
+    ssa.profile_reset()
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    shapes_per_step = batch * world
+    value = ms_per_step / shapes_per_step
+
+    # ---- algorithmic work of the dominant kernel ----
+    I = saved.indices().cpu().numpy()
+    off_slc = plan.offsets(ssa.LEVEL_SLC).cpu().numpy()
+    off_q = plan.offsets(ssa.LEVEL_Q).cpu().numpy()
+    off_w = plan.offsets(ssa.LEVEL_WIN).cpu().numpy()
+    bb_c = plan.batch_blocks(ssa.LEVEL_CMP).cpu().numpy()
+    bt = np.searchsorted(coords[np.argsort(coords[:, 0], kind="stable"), 0], np.arange(batch + 1))
+    h_s = H // h_kv
+    n_cmp_b = np.diff(bb_c)
+    ntok_b = np.diff(bt)
+    E_cmp = float(np.sum(ntok_b * n_cmp_b)) * H
+    fill = np.diff(off_slc)
+    qn = np.diff(off_q)
+    E_slc = float(sum(qn[Q] * h_s * fill[I[Q, gi][I[Q, gi] >= 0]].sum() for Q in range(len(qn)) for gi in range(h_kv)))
+    E_win = float(np.sum(np.diff(off_w).astype(np.float64) ** 2)) * H
+    dom = None
+    for cand in ("tc_cmp_fwd", "k_cmp_fwd"):
+        if cand in ktimes:
+            dom = cand
+            break
+    peaks, peak_src = load_peaks()
+    roofline = None
+    if dom:
+        t, n = ktimes[dom]
+        avg_s = t / n / 1e3
+        flops = 4.0 * d * E_cmp            # QK^T + PV of the compression branch (2 ops / MAC)
+        achieved = flops / avg_s / 1e12
+        if dom.startswith("tc_"):
+            peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+            bound = "tensor"
+        else:
+            peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # fp32 FMA peak
+            bound = "alu"
+        roofline = {"kernel": dom, "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_source": peak_src + (" bf16_tflops_sustained" if bound == "tensor" else
+                                               " fp32 FMA: 148 SM x 128 FMA/clk x 2 x sm_max_mhz"),
+                    "algorithmic_flops_per_launch": flops, "avg_launch_ms": round(t / n, 4),
+                    "share_of_step": round(t / n / ms_per_step, 4)}
+    kernel_ms = {kn: round(t / n, 4) for kn, (t, n) in ktimes.items()}
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hg, hd = (x.cpu().pin_memory() for x in (q, k, v, g, do))
+        houts = [torch.empty_like(x, device="cpu").pin_memory() for x in (out,) + grads]
+        bi = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hg, hd))
+        bo = sum(x.numel() * x.element_size() for x in houts)
+        e_times = []
+        for i in range(args.steps + 1):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            dq_, dk_, dv_, dg_ = (x.to(dev, non_blocking=True) for x in (hq, hk, hv, hg))
+            ddo = hd.to(dev, non_blocking=True)
+            step(dq_, dk_, dv_, dg_, ddo)
+            for h_, d_ in zip(houts, (out,) + grads):
+                h_.copy_(d_, non_blocking=True)
+            e1.record(st)
+            if i > 0:
+                e_times.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        e_ms = sum(a.elapsed_time(b) for a, b in e_times) / len(e_times)
+        if world > 1:
+            tt = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        e2e = {"value": round(e_ms / shapes_per_step, 4), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo)}
+
+    # ---- full-attention comparator on the same box (context: "speedup vs full attention") ----
+    full = None
+    if not args.no_full and rank == 0:
+        full = full_attention_time(torch, dev, int(np.max(ntok_b)), H, h_kv, d, tdt)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, cfg, coords, grid, batch, inp, value)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if tdt == torch.bfloat16 else "f32",
+            "data": "synthetic (sphere-shell occupancy, N(0,1) q/k/v/dO, sigmoid(N(0,1)) gates; ssa_workload)",
+            "config": {"workload": f"{args.config}: 128^3 latent (1024^3 res) sphere shell, {N} tokens x {batch} shape(s)/rank, "
+                                   f"H={H} (h_kv={h_kv}), d={d}, m_cmp/m_slc/m_win/m_q={ms}, T={T}",
+                       "tokens_per_shape": int(np.max(ntok_b)), "shapes_per_rank": batch,
+                       "parallelism": f"shape-parallel x{world} (no data-path collective)",
+                       "l2": "flushed between timed steps (256 MB write)", "path": "tcgen05" if used_tc else "simt"},
+            "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline, "kernel_ms": kernel_ms,
+            "work": {"E_cmp": E_cmp, "E_slc": E_slc, "E_win": E_win},
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        if full:
+            line["full_attention"] = full
+            line["speedup_vs_full_attention"] = round(full["fwd_bwd_ms"] / ms_per_step * batch, 2)
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def full_attention_time(torch, dev, n, H, h_kv, d, dt):
+    """Dense non-causal attention over all n tokens (torch SDPA, flash/cuDNN backend) fwd+bwd, GQA."""
+    try:
+        import torch.nn.functional as F
+        q = torch.randn(1, H, n, d, device=dev, dtype=dt, requires_grad=True)
+        k = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
+        v = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
+        go = torch.randn(1, H, n, d, device=dev, dtype=dt)
+
+        def run():
+            o = F.scaled_dot_product_attention(q, k, v, enable_gqa=True)
+            o.backward(go)
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        reps = 3
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / reps
+        return {"impl": "torch SDPA (GQA, non-causal, bf16)", "tokens": n, "fwd_bwd_ms": round(ms, 3),
+                "flops": 4.0 * n * n * H * d * 3.5}
+    except Exception as ex:  # comparator is context only
+        return {"error": str(ex)[:200]}
+
+
+def oracle_sample(cfg, coords, grid, batch, inp, n_sample: int, seed: int = 0):
+    """Run the float64 oracle (as it stands) forward + backward on a bounded sample of the workload:
+    the full block build and pooling, then the per-query-block work (compression attention, Eq. 8
+    scores, top-k, selection + window attention, gated sum, and the branch backwards) for n_sample
+    random query blocks. Returns (seconds, sampled query blocks, total query blocks, threads)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    kw = dict(m_cmp=cfg["m_cmp"], m_slc=cfg["m_slc"], m_win=cfg["m_win"], m_q=cfg["m_q"])
+    plan = O.block_build(coords, grid, batch, **kw)
+    H, h_kv, d = cfg["H"], cfg["h_kv"], cfg["d"]
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    P = plan.perm
+    qs, ks, vs = inp.q[P].astype(np.float64), inp.k[P].astype(np.float64), inp.v[P].astype(np.float64)
+    gs, dos = inp.gates[P].astype(np.float64), inp.dout[P].astype(np.float64)
+    k_cmp, v_cmp = O.compress(plan, ks), O.compress(plan, vs)
+    t_build = time.perf_counter() - t0
+    Cq, Cs, Cw = plan.offsets["q"], plan.offsets["slc"], plan.offsets["win"]
+    nq = len(Cq) - 1
+    rng = np.random.Generator(np.random.PCG64(seed))
+    sample = rng.choice(nq, size=min(n_sample, nq), replace=False)
+    t1 = time.perf_counter()
+    for Q in sample:
+        a, b_ = int(Cq[Q]), int(Cq[Q + 1])
+        bi = int(plan.sorted_coords[a, 0])
+        c0, c1 = int(plan.batch_blocks["cmp"][bi]), int(plan.batch_blocks["cmp"][bi + 1])
+        s0 = int(plan.batch_blocks["slc"][bi])
+        w = int(plan.tok_block["win"][a])
+        for g in range(h_kv):
+            rows = qs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
+            drow = dos[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
+            wt = gs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, 3)
+            oc, _, pc = O.dense_attention(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], scale)
+            per = pc.sum(axis=0)
+            sc = np.zeros(int(plan.batch_blocks["slc"][bi + 1]) - s0)
+            np.add.at(sc, plan.cmp_to_slc[c0:c1] - s0, per)
+            sel = O.topk_select(sc, cfg["T"], base=s0)
+            kt = np.concatenate([np.arange(Cs[x], Cs[x + 1]) for x in sel if x >= 0])
+            os_, _, ps = O.dense_attention(rows, ks[kt, g], vs[kt, g], scale)
+            wa, wb = int(Cw[w]), int(Cw[w + 1])
+            ow, _, pw = O.dense_attention(rows, ks[wa:wb, g], vs[wa:wb, g], scale)
+            _ = wt[:, 0:1] * oc + wt[:, 1:2] * os_ + wt[:, 2:3] * ow
+            O.dense_attention_backward(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], pc, oc, wt[:, 0:1] * drow, scale)
+            O.dense_attention_backward(rows, ks[kt, g], vs[kt, g], ps, os_, wt[:, 1:2] * drow, scale)
+            O.dense_attention_backward(rows, ks[wa:wb, g], vs[wa:wb, g], pw, ow, wt[:, 2:3] * drow, scale)
+    t_q = time.perf_counter() - t1
+    threads = 1
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        pass
+    return t_build, t_q, len(sample), nq, threads
+
+
+def cpu_baseline(args, cfg, coords, grid, batch, inp, gpu_value):
+    t_build, t_q, ns, nq, threads = oracle_sample(cfg, coords, grid, batch, inp, args.cpu_sample)
+    est_s = t_build + t_q / ns * nq
+    return {"value": round(est_s * 1e3 / batch, 1), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"float64 numpy oracle: full block build + pool ({t_build:.1f} s) and fwd+bwd of {ns} random "
+                      f"query blocks of {nq} ({t_q:.1f} s), extrapolated linearly to all query blocks"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle as it stands, on the host cores, bounded sample per step."""
+    if rank != 0:
+        return
+    from ssa_workload import make_inputs
+    cfg, coords, grid, batch = workload(args.config, 0, 1)
+    inp = make_inputs(coords, grid, batch, cfg["H"], cfg["h_kv"], cfg["d"], cfg["dtype"], seed=cfg["seed"])
+    per_step = []
+    threads = 1
+    n_sample = max(2, min(args.cpu_sample, 8))
+    for i in range(args.warmup + args.steps):
+        t_build, t_q, ns, nq, threads = oracle_sample(cfg, coords, grid, batch, inp, n_sample, seed=i)
+        if i >= args.warmup:
+            per_step.append(t_build + t_q / ns * nq)
+    v = float(np.mean(per_step)) * 1e3 / batch
+    line = {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v * batch, 1), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (ssa_workload)", "impl": "reference",
+            "config": {"workload": f"{args.config} (oracle sample, extrapolated)", "parallelism": "host cores"},
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{n_sample} random query blocks per step + full block build/pool, extrapolated"},
+            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

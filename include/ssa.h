@@ -185,6 +185,16 @@ typedef struct {
 ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,
                            ssa_saved_view* out);
 
+/* ------------------------------------------------------------------------------------------------
+ * Kernel-timing hook (used by bench.py for the roofline of the dominant kernel). When enabled, the
+ * library brackets each attention kernel launch with CUDA events recorded on the launch stream.
+ * ssa_profile_read synchronises those events and returns the summed device time (ms) and launch
+ * count of every launch whose kernel name equals `kernel` since the last reset.
+ * ----------------------------------------------------------------------------------------------*/
+void ssa_profile_enable(int on);
+void ssa_profile_reset(void);
+ssa_status ssa_profile_read(const char* kernel, double* total_ms, int64_t* launches);
+
 const char* ssa_status_str(ssa_status s);
 const char* ssa_last_error(void);
 /* Kernels launched by this thread since the last reset (host counter; used by bench.py). */

@@ -12,6 +12,26 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 }  // namespace
 
+namespace {
+struct ProfRec { std::string name; cudaEvent_t a, b; };
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+ProfScope::ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+  if (!g_prof_on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) == cudaSuccess) { cudaEventRecord(e, st); ev0 = e; }
+}
+ProfScope::~ProfScope() {
+  if (!ev0) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) == cudaSuccess) {
+    cudaEventRecord(e, st);
+    g_prof.push_back({name, static_cast<cudaEvent_t>(ev0), e});
+  }
+}
+
 void set_error(const std::string& s) { g_err = s; }
 void count_launch(int n) { g_launches += n; }
 ssa_status cuda_status(cudaError_t e, const char* where) {
@@ -279,6 +299,28 @@ extern "C" const char* ssa_status_str(ssa_status s) {
   return "SSA_ERR_UNKNOWN";
 }
 extern "C" const char* ssa_last_error(void) { return g_err.c_str(); }
+extern "C" void ssa_profile_enable(int on) { g_prof_on = on != 0; }
+extern "C" void ssa_profile_reset(void) {
+  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+}
+extern "C" ssa_status ssa_profile_read(const char* kernel, double* total_ms, int64_t* launches) {
+  if (!kernel || !total_ms || !launches) { set_error("null argument"); return SSA_ERR_ARG; }
+  double t = 0;
+  int64_t n = 0;
+  for (auto& r : g_prof) {
+    if (r.name != kernel) continue;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_status(e, "ssa_profile_read");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    t += ms;
+    ++n;
+  }
+  *total_ms = t;
+  *launches = n;
+  return SSA_OK;
+}
 extern "C" int64_t ssa_launch_count(void) { return g_launches; }
 extern "C" void ssa_reset_launch_count(void) { g_launches = 0; }
 extern "C" const char* ssa_build_info(void) {

@@ -80,6 +80,15 @@ ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st);
 ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st);
 
+// Optional per-kernel event timing (api.cu). Usage: { ProfScope ps("name", st); kernel<<<..., st>>>(); }
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  void* ev0 = nullptr;
+  ProfScope(const char* n, cudaStream_t s);
+  ~ProfScope();
+};
+
 // thread-local error text + launch counter (api.cu)
 void set_error(const std::string& s);
 void count_launch(int n = 1);

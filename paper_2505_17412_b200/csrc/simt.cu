@@ -773,27 +773,48 @@ ssa_status simt_fwd_t(const Ctx& c, cudaStream_t st, bool attention_only) {
     size_t smem = (2 * kKT * D + kRows * (kKT + 1) + 4 * kKT + c.max_cmp_b + c.max_slc_b) * sizeof(float);
     if (smem > 227 * 1024) { set_error("too many blocks per batch item for the SIMT kernel"); return SSA_ERR_UNSUPPORTED; }
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_cmp_fwd<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_cmp_fwd<T, D><<<dim3(nq, c.h_kv), kRows, smem, st>>>(c);
-    SSA_LAUNCH_CHECK("k_cmp_fwd");
+    {
+      ProfScope ps_("k_cmp_fwd", st);
+      k_cmp_fwd<T, D><<<dim3(nq, c.h_kv), kRows, smem, st>>>(c);
+      SSA_LAUNCH_CHECK("k_cmp_fwd");
+    }
   }
-  k_attn_fwd<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c, 1);
-  SSA_LAUNCH_CHECK("k_attn_fwd(slc)");
-  k_attn_fwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), kRows, 0, st>>>(c, 2);
-  SSA_LAUNCH_CHECK("k_attn_fwd(win)");
+  {
+    ProfScope ps_("k_attn_fwd(slc)", st);
+    k_attn_fwd<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c, 1);
+    SSA_LAUNCH_CHECK("k_attn_fwd(slc)");
+  }
+  {
+    ProfScope ps_("k_attn_fwd(win)", st);
+    k_attn_fwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), kRows, 0, st>>>(c, 2);
+    SSA_LAUNCH_CHECK("k_attn_fwd(win)");
+  }
   return SSA_OK;
 }
 
 template <class T, int D>
 ssa_status simt_bwd_t(const Ctx& c, cudaStream_t st) {
   const int nq = c.n_blk[SSA_LEVEL_Q];
-  k_dq<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_dq");
-  k_slc_dkdv<T, D><<<dim3(c.n_blk[SSA_LEVEL_SLC], c.h_kv), 128, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_slc_dkdv");
-  k_win_bwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), 128, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_win_bwd");
-  k_cmp_dkdv<T, D><<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), 128, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_cmp_dkdv");
+  {
+    ProfScope ps_("k_dq", st);
+    k_dq<T, D><<<dim3(nq, c.h_kv), kRows, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_dq");
+  }
+  {
+    ProfScope ps_("k_slc_dkdv", st);
+    k_slc_dkdv<T, D><<<dim3(c.n_blk[SSA_LEVEL_SLC], c.h_kv), 128, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_slc_dkdv");
+  }
+  {
+    ProfScope ps_("k_win_bwd", st);
+    k_win_bwd<T, D><<<dim3(c.n_blk[SSA_LEVEL_WIN], c.h_kv), 128, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_win_bwd");
+  }
+  {
+    ProfScope ps_("k_cmp_dkdv", st);
+    k_cmp_dkdv<T, D><<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), 128, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_cmp_dkdv");
+  }
   int64_t per = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * c.D;
   k_cmp_reduce<<<nblk(per, 256), 256, 0, st>>>(c);
   SSA_LAUNCH_CHECK("k_cmp_reduce");

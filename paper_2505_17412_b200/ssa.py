@@ -83,6 +83,10 @@ SIGNATURES = {
     "ssa_launch_count": (ctypes.c_int64, []),
     "ssa_reset_launch_count": (None, []),
     "ssa_build_info": (ctypes.c_char_p, []),
+    "ssa_profile_enable": (None, [ctypes.c_int]),
+    "ssa_profile_reset": (None, []),
+    "ssa_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_int64)]),
 }
 
 
@@ -334,6 +338,21 @@ def launch_count() -> int:
 
 def reset_launch_count():
     lib().ssa_reset_launch_count()
+
+
+def profile_enable(on: bool = True):
+    lib().ssa_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    lib().ssa_profile_reset()
+
+
+def profile_read(kernel: str):
+    """(total device ms, launches) of `kernel` since the last profile_reset (synchronises)."""
+    t, n = ctypes.c_double(), ctypes.c_int64()
+    _check(lib().ssa_profile_read(kernel.encode(), ctypes.byref(t), ctypes.byref(n)), "ssa_profile_read")
+    return t.value, n.value
 
 
 def build_info() -> str:
