@@ -71,8 +71,15 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
   return SSA_OK;
 }
 
-bool use_tc(const Dims& d, const ssa_attn_cfg* cfg) {
-  return tc_available() && cfg->dtype == SSA_BF16 && d.D == 64 && !(cfg->flags & SSA_FORCE_SIMT);
+// The tcgen05 kernels assume bf16, d = 64 and that the window and the query block are the selection
+// block (m_win = m_q = m_slc, true for every tensor-core config C2-C5); anything else runs SIMT.
+bool use_tc(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
+  const int32_t* m = p->info.m;
+  return tc_available() && cfg->dtype == SSA_BF16 && d.D == 64 && !(cfg->flags & SSA_FORCE_SIMT) &&
+         m[SSA_LEVEL_WIN] == m[SSA_LEVEL_SLC] && m[SSA_LEVEL_Q] == m[SSA_LEVEL_SLC] && cfg->top_k <= 64;
+}
+bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
+  return tc_bwd_available() && use_tc(d, cfg, p);
 }
 
 // saved state: kc, vc, o[3], lse[3], I, scores
@@ -199,7 +206,7 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   const bool bf16 = cfg->dtype == SSA_BF16;
   if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
   if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
-  if (use_tc(d, cfg)) {
+  if (use_tc(d, cfg, p)) {
     if ((s = tc_forward(x, tc_ws, st)) != SSA_OK) return s;
   } else {
     if ((s = simt_forward(x, bf16, st, false)) != SSA_OK) return s;
@@ -256,7 +263,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;
   if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
   if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
-  if (use_tc(d, cfg)) {
+  if (use_tc_bwd(d, cfg, p)) {
     if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
   } else {
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
@@ -280,7 +287,7 @@ extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, co
   for (int b = 0; b < 3; ++b) { out->o_branch[b] = x.o[b]; out->lse_branch[b] = x.lse[b]; }
   out->k_cmp = x.kc;
   out->v_cmp = x.vc;
-  out->used_tcgen05 = use_tc(d, cfg) ? 1 : 0;
+  out->used_tcgen05 = use_tc(d, cfg, p) ? 1 : 0;
   return SSA_OK;
 }
 

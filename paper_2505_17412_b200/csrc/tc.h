@@ -4,6 +4,7 @@
 
 namespace ssa {
 bool tc_available();
+bool tc_bwd_available();
 size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D);
 size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D);
 // forward after gather + pool: compression attention + scores + top-k, selection + window attention,

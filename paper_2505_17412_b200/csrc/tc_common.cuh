@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -96,6 +97,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major,
          | (uint32_t(M >> 4) << 24);     // M
 }
 
+// instruction descriptor, kind::f16 with fp16 A/B and fp32 D (used for P.V: P <= 1 keeps 11 bits,
+// and bf16 values convert to fp16 exactly in the range the operands live in)
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) |
+         (uint32_t(M >> 4) << 24);
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -157,6 +165,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 // byte offset of 16-B chunk c (0..7) of 128-B line r
 __device__ __forceinline__ uint32_t sw128(uint32_t line, uint32_t chunk) {
   return line * 128u + ((chunk ^ (line & 7u)) << 4);
@@ -169,6 +181,7 @@ __device__ __forceinline__ uint32_t elect_lane0() { return (threadIdx.x & 31) ==
 
 }  // namespace tc
 
-// host: encode a 2D bf16 tensor map [rows][64] with 128-B swizzle and a box of (64, box_rows)
+// host: encode a 2D 16-bit (bf16 or fp16: TMA copies bytes, no conversion) tensor map [rows][64]
+// with 128-B swizzle and a box of (64, box_rows)
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows);
 }  // namespace ssa

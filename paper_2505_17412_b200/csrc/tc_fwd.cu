@@ -1,0 +1,687 @@
+// tc_fwd.cu — tcgen05/TMEM/TMA forward kernels of the bf16, d = 64 SSA path.
+//
+//  k_tc_prep      fp32 pooled K/V (Eq. 7) -> bf16 operand copies: K^cmp as a hi/lo bf16 pair (so the
+//                 compression scores that drive top-k keep ~16 mantissa bits), V^cmp in bf16.
+//  k_tc_cmp_fwd   compression attention + Eq. 8 block scores + top-k, CTA per (query block, kv group):
+//                 pass 1 S = Q K^T (rows on TMEM lanes) -> per-row LSE; pass 2 S^T = K Q^T (keys on TMEM
+//                 lanes) -> P^T = exp(S^T - LSE) so the Eq. 8 column sums are exact fp32 per-thread
+//                 sums, P^T goes to smem as the MN-major A operand of O += P V (accumulated in TMEM with
+//                 fixed normalisation). Scores stay in smem; top-k runs in the same CTA.
+//  k_tc_slcwin_fwd selection attention over the T selected blocks (Alg. 1 at query-block granularity)
+//                 and window attention with online softmax, then the gated sum of Eq. 6 and
+//                 the scatter to caller order. Key tiles are 128-token TMA boxes starting at each
+//                 block's offset C (variable fill handled by masking).
+//
+// Warp roles (192 threads): warps 0-3 softmax/epilogue (thread i <-> TMEM lane i), warp 4 TMA
+// producer, warp 5 MMA issuer (one elected lane) + TMEM owner.
+#include <cfloat>
+
+#include "internal.h"
+#include "tc.h"
+#include "tc_common.cuh"
+
+namespace ssa {
+namespace {
+using namespace tc;
+
+constexpr int kD = 64;
+constexpr int kTile = 128;
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kStages = 3;
+
+struct TcArgs {
+  Ctx c;
+  const __nv_bfloat16* kc_hi;   // [h_kv][n_cmp][64]
+  const __nv_bfloat16* kc_lo;
+  const __half* vc;
+};
+
+// K^cmp -> bf16 hi/lo pair, V^cmp -> fp16 (P.V runs in fp16), raw V -> fp16 copy (exact for bf16)
+__global__ void k_tc_prep(Ctx c, __nv_bfloat16* kc_hi, __nv_bfloat16* kc_lo, __half* vc16, __half* vs16) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
+  const int64_t nv = int64_t(c.h_kv) * c.N * kD;
+  if (i < n) {
+    const float k = static_cast<const float*>(c.kc)[i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(k);
+    kc_hi[i] = hi;
+    kc_lo[i] = __float2bfloat16_rn(k - __bfloat162float(hi));
+    vc16[i] = __float2half_rn(static_cast<const float*>(c.vc)[i]);
+  }
+  if (i < nv) vs16[i] = __float2half_rn(__bfloat162float(static_cast<const __nv_bfloat16*>(c.vs)[i]));
+}
+
+// simple (index, phase) ring cursor
+struct Ring {
+  int idx = 0;
+  uint32_t ph = 0;
+  int n;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++idx == n) { idx = 0; ph ^= 1u; }
+  }
+};
+
+// ================================================================================================
+// compression attention + scores + top-k
+// ================================================================================================
+struct CmpSmem {
+  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full, p_empty, o_full,
+      o_empty;
+  uint32_t tmem;
+  float lse[kTile];
+  float bv[4];
+  int bi[4];
+  int chosen[64];
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmKh,
+             __grid_constant__ const CUtensorMap tmKl, __grid_constant__ const CUtensorMap tmV) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                                  // 16 KB
+  uint8_t* sKV = sm + 16384;                         // kStages x {Khi, Klo, V} 48 KB
+  uint8_t* sP = sKV + kStages * 49152;               // 32 KB, P^T: 2 row blocks x [128 keys][128 B]
+  CmpSmem* S = reinterpret_cast<CmpSmem*>(sP + 32768);
+  float* sc_cmp = reinterpret_cast<float*>(S + 1);   // [max_cmp_b]
+  const Ctx& c = a.c;
+  float* sc_slc = sc_cmp + c.max_cmp_b;              // [max_slc_b]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int b = c.q_batch[Q];
+  const int c0 = c.bb[SSA_LEVEL_CMP][b], nk = c.bb[SSA_LEVEL_CMP][b + 1] - c0;
+  const int s0 = c.bb[SSA_LEVEL_SLC][b], ns = c.bb[SSA_LEVEL_SLC][b + 1] - s0;
+  const int rows = (t1 - t0) * c.h_s;
+  const int n_rt = (rows + kTile - 1) / kTile, n_kt = (nk + kTile - 1) / kTile;
+  const int qrow0 = (g * c.N + t0) * c.h_s;
+  const int krow0 = g * c.n_blk[SSA_LEVEL_CMP] + c0;
+
+  if (tid == 0) {
+    mbar_init(&S->q_full, 1);
+    mbar_init(&S->q_empty, 1);
+    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&S->s_full[i], 1); mbar_init(&S->s_empty[i], 128); }
+    mbar_init(&S->p_full, 128);
+    mbar_init(&S->p_empty, 1);
+    mbar_init(&S->o_full, 1);
+    mbar_init(&S->o_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmKh); tma_prefetch(&tmKl); tma_prefetch(&tmV); }
+  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  for (int i = tid; i < nk; i += kThreads) sc_cmp[i] = 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S->tmem;
+
+  if (warp == 4) {
+    // ---------------------------------------------------------------- TMA producer
+    Ring kv(kStages);
+    uint32_t qph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_empty, qph ^ 1u);
+      qph ^= 1u;
+      if (lane == 0) {
+        mbar_expect_tx(&S->q_full, 16384);
+        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * kTile);
+      }
+      for (int pass = 1; pass <= 2; ++pass) {
+        for (int kt = 0; kt < n_kt; ++kt) {
+          mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
+          if (lane == 0) {
+            uint8_t* st = sKV + kv.idx * 49152;
+            mbar_expect_tx(&S->kv_full[kv.idx], pass == 1 ? 32768u : 49152u);
+            tma_load_2d(st, &tmKh, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
+            tma_load_2d(st + 16384, &tmKl, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
+            if (pass == 2) tma_load_2d(st + 32768, &tmV, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
+          }
+          __syncwarp();
+          kv.next();
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idS = idesc_bf16(128, 128, false, false);
+    const uint32_t idO = idesc_f16(128, 64, true, true);
+    const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+    Ring kv(kStages), sb(2);
+    uint32_t qph = 0, pph = 0, oph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_full, qph);
+      qph ^= 1u;
+      tc_fence_after();
+      // pass 1: S = Q (Khi + Klo)^T
+      for (int kt = 0; kt < n_kt; ++kt) {
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
+        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(sKV + kv.idx * 49152);
+          const uint32_t d = tmem + sb.idx * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(st + k * 32, 0, 1024), idS, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(st + 16384 + k * 32, 0, 1024), idS, 1);
+          umma_commit(&S->s_full[sb.idx]);
+          umma_commit(&S->kv_empty[kv.idx]);
+        }
+        __syncwarp();
+        kv.next();
+        sb.next();
+      }
+      // pass 2: S^T = (Khi + Klo) Q^T, then O += P V (P^T in smem, MN-major A)
+      Ring kv_pv = kv;   // stage of the tile whose PV is pending
+      auto issue_st = [&](int kt_unused) {
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
+        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(sKV + kv.idx * 49152);
+          const uint32_t d = tmem + sb.idx * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(st + k * 32, 0, 1024), desc_sw128(aQ + k * 32, 0, 1024), idS, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(st + 16384 + k * 32, 0, 1024), desc_sw128(aQ + k * 32, 0, 1024), idS, 1);
+          umma_commit(&S->s_full[sb.idx]);
+        }
+        __syncwarp();
+        kv.next();
+        sb.next();
+        (void)kt_unused;
+      };
+      issue_st(0);
+      mbar_wait(&S->o_empty, oph ^ 1u);
+      oph ^= 1u;
+      for (int kt = 0; kt < n_kt; ++kt) {
+        if (kt + 1 < n_kt) issue_st(kt + 1);
+        mbar_wait(&S->p_full, pph);
+        pph ^= 1u;
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sv = smem_u32(sKV + kv_pv.idx * 49152 + 32768);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_bf16(tmem + 256, desc_sw128(aP + k * 2048, 16384, 1024), desc_sw128(sv + k * 2048, 0, 1024), idO,
+                      (kt > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->p_empty);
+          umma_commit(&S->kv_empty[kv_pv.idx]);
+        }
+        __syncwarp();
+        kv_pv.next();
+      }
+      if (lane == 0) {
+        umma_commit(&S->o_full);
+        umma_commit(&S->q_empty);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax / epilogue (128 threads)
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    const float cl2 = c.scale * kLog2e;
+    Ring sb(2);
+    uint32_t pph = 0, oph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      const int r = rt * kTile + tid;
+      const bool rvalid = r < rows;
+      // ---- pass 1: row LSE
+      float m = -1e30f, l = 0.f;
+      for (int kt = 0; kt < n_kt; ++kt) {
+        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        tc_fence_after();
+        const int nv = min(kTile, nk - kt * kTile);
+        for (int c0 = 0; c0 < kTile; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_base + sb.idx * 128 + c0, v);
+          tmem_wait_ld();
+          float mx = -1e30f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v[i] = (c0 + i < nv) ? v[i] * cl2 : -1e30f;
+            mx = fmaxf(mx, v[i]);
+          }
+          const float mn = fmaxf(m, mx);
+          float s = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s += exp2f(v[i] - mn);
+          l = l * exp2f(m - mn) + s;
+          m = mn;
+        }
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[sb.idx]);
+        sb.next();
+      }
+      const float lse2 = rvalid ? m + log2f(l) : INFINITY;
+      named_bar_sync(1, 128);          // previous row tile's pass 2 finished reading S->lse
+      S->lse[tid] = lse2;
+      if (rvalid) c.lse[0][qrow0 + r] = lse2 * kLn2;
+      named_bar_sync(1, 128);
+      // ---- pass 2: thread = key; P^T row -> smem; exact fp32 column sums
+      for (int kt = 0; kt < n_kt; ++kt) {
+        const bool kvalid = kt * kTile + tid < nk;
+        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        tc_fence_after();
+        uint32_t pk[64];
+        float colsum = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < kTile; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_base + sb.idx * 128 + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float p0 = kvalid ? exp2f(v[i] * cl2 - S->lse[c0 + i]) : 0.f;
+            float p1 = kvalid ? exp2f(v[i + 1] * cl2 - S->lse[c0 + i + 1]) : 0.f;
+            colsum += p0 + p1;
+            pk[(c0 + i) / 2] = pack_f16(p0, p1);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[sb.idx]);
+        sb.next();
+        mbar_wait(&S->p_empty, pph ^ 1u);
+        pph ^= 1u;
+        const uint32_t pbase = smem_u32(sP);
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {      // 16 chunks of 8 rows: row block ch/8, chunk ch%8
+          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+                       pk[4 * ch + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&S->p_full);
+        if (kvalid) sc_cmp[kt * kTile + tid] += colsum;
+      }
+      // ---- O (fixed normalisation, accumulated over all key tiles in TMEM)
+      mbar_wait(&S->o_full, oph);
+      oph ^= 1u;
+      tc_fence_after();
+      float* oc = static_cast<float*>(c.o[0]) + int64_t(qrow0 + r) * kD;
+#pragma unroll
+      for (int c0 = 0; c0 < kD; c0 += 32) {
+        float v[32];
+        tmem_ld32(lane_base + 256 + c0, v);
+        tmem_wait_ld();
+        if (rvalid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(oc + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&S->o_empty);
+    }
+    // ---- Eq. 8 selection-block scores and top-k (softmax warps only)
+    named_bar_sync(1, 128);
+    for (int B = tid; B < ns; B += 128) {
+      float s = 0.f;
+      for (int i = c.slc_cmp_begin[s0 + B]; i < c.slc_cmp_begin[s0 + B + 1]; ++i) s += sc_cmp[i - c0];
+      sc_slc[B] = s;
+      if (c.save_scores) c.scores[(int64_t(Q) * c.h_kv + g) * c.max_slc_b + B] = s;
+    }
+    named_bar_sync(1, 128);
+    const int Teff = min(c.T, ns);
+    for (int it = 0; it < Teff; ++it) {
+      float best = -2.f;
+      int bidx = 0x7fffffff;
+      for (int B = tid; B < ns; B += 128) {
+        const float v = sc_slc[B];
+        if (v > best) { best = v; bidx = B; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+      }
+      if (lane == 0) { S->bv[warp] = best; S->bi[warp] = bidx; }
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        float bb = S->bv[0];
+        int ii = S->bi[0];
+        for (int w = 1; w < 4; ++w)
+          if (S->bv[w] > bb || (S->bv[w] == bb && S->bi[w] < ii)) { bb = S->bv[w]; ii = S->bi[w]; }
+        S->chosen[it] = ii;
+        sc_slc[ii] = -1.f;
+      }
+      named_bar_sync(1, 128);
+    }
+    if (tid == 0) {
+      for (int i = 1; i < Teff; ++i) {
+        const int v = S->chosen[i];
+        int j = i - 1;
+        while (j >= 0 && S->chosen[j] > v) { S->chosen[j + 1] = S->chosen[j]; --j; }
+        S->chosen[j + 1] = v;
+      }
+    }
+    named_bar_sync(1, 128);
+    for (int j = tid; j < c.T; j += 128) c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + S->chosen[j] : -1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================================================
+// selection + window attention + gated sum
+// ================================================================================================
+constexpr int kMaxTiles = 4 * 64 + 8;
+struct SwSmem {
+  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_empty[2],
+      o_full[2], o_empty[2];
+  uint32_t tmem;
+  int n_tiles, n_slc_tiles;
+  int tile_row[kMaxTiles];
+  int tile_nv[kMaxTiles];
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmK,
+                __grid_constant__ const CUtensorMap tmV) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                          // 16 KB
+  uint8_t* sKV = sm + 16384;                 // kStages x {K, V} 32 KB
+  uint8_t* sP = sKV + kStages * 32768;       // 2 x 32 KB, P K-major: 2 key blocks x [128 rows][128 B]
+  SwSmem* S = reinterpret_cast<SwSmem*>(sP + 65536);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int rows = (t1 - t0) * c.h_s;
+  const int n_rt = (rows + kTile - 1) / kTile;
+  const int qrow0 = (g * c.N + t0) * c.h_s;
+  const int krow_g = g * c.N;
+
+  if (tid == 0) {
+    mbar_init(&S->q_full, 1);
+    mbar_init(&S->q_empty, 1);
+    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S->s_full[i], 1);
+      mbar_init(&S->s_empty[i], 128);
+      mbar_init(&S->p_full[i], 128);
+      mbar_init(&S->p_empty[i], 1);
+      mbar_init(&S->o_full[i], 1);
+      mbar_init(&S->o_empty[i], 128);
+    }
+    fence_barrier_init();
+    // key tile list: selected blocks (ascending), then the window (== the query block: m_win == m_q)
+    int n = 0;
+    for (int j = 0; j < c.T; ++j) {
+      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+      if (B < 0) continue;
+      const int a0 = c.off[SSA_LEVEL_SLC][B], a1 = c.off[SSA_LEVEL_SLC][B + 1];
+      for (int x = a0; x < a1 && n < kMaxTiles; x += kTile) { S->tile_row[n] = x; S->tile_nv[n] = min(kTile, a1 - x); ++n; }
+    }
+    S->n_slc_tiles = n;
+    for (int x = t0; x < t1 && n < kMaxTiles; x += kTile) { S->tile_row[n] = x; S->tile_nv[n] = min(kTile, t1 - x); ++n; }
+    S->n_tiles = n;
+  }
+  if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
+  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S->tmem;
+  const int n_tiles = S->n_tiles, n_slc_tiles = S->n_slc_tiles;
+
+  if (warp == 4) {
+    Ring kv(kStages);
+    uint32_t qph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_empty, qph ^ 1u);
+      qph ^= 1u;
+      if (lane == 0) {
+        mbar_expect_tx(&S->q_full, 16384);
+        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * kTile);
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
+        if (lane == 0) {
+          uint8_t* st = sKV + kv.idx * 32768;
+          mbar_expect_tx(&S->kv_full[kv.idx], 32768u);
+          tma_load_2d(st, &tmK, &S->kv_full[kv.idx], 0, krow_g + S->tile_row[j]);
+          tma_load_2d(st + 16384, &tmV, &S->kv_full[kv.idx], 0, krow_g + S->tile_row[j]);
+        }
+        __syncwarp();
+        kv.next();
+      }
+    }
+  } else if (warp == 5) {
+    const uint32_t idS = idesc_bf16(128, 128, false, false);
+    const uint32_t idO = idesc_f16(128, 64, false, true);
+    const uint32_t aQ = smem_u32(sQ);
+    Ring kv(kStages), sb(2), pb(2), ob(2);
+    uint32_t qph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_full, qph);
+      qph ^= 1u;
+      tc_fence_after();
+      Ring kv_pv = kv;
+      auto issue_s = [&]() {
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
+        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sk = smem_u32(sKV + kv.idx * 32768);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + sb.idx * 128, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS,
+                      k > 0);
+          umma_commit(&S->s_full[sb.idx]);
+        }
+        __syncwarp();
+        kv.next();
+        sb.next();
+      };
+      issue_s();
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s();
+        mbar_wait(&S->p_full[pb.idx], pb.ph);
+        mbar_wait(&S->o_empty[ob.idx], ob.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ap = smem_u32(sP + pb.idx * 32768);
+          const uint32_t sv = smem_u32(sKV + kv_pv.idx * 32768 + 16384);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_bf16(tmem + 256 + ob.idx * 64, desc_sw128(ap + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024),
+                      desc_sw128(sv + k * 2048, 0, 1024), idO, k > 0);
+          umma_commit(&S->o_full[ob.idx]);
+          umma_commit(&S->p_empty[pb.idx]);
+          umma_commit(&S->kv_empty[kv_pv.idx]);
+        }
+        __syncwarp();
+        kv_pv.next();
+        pb.next();
+        ob.next();
+      }
+      if (lane == 0) umma_commit(&S->q_empty);
+      __syncwarp();
+    }
+  } else {
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    const float cl2 = c.scale * kLog2e;
+    Ring sb(2), pb(2), ob(2);
+    for (int rt = 0; rt < n_rt; ++rt) {
+      const int r = rt * kTile + tid;
+      const bool rvalid = r < rows;
+      const int64_t row = qrow0 + (rvalid ? r : 0);
+      float o_acc[kD];
+      float lse_slc = 0.f;
+      float m = -1e30f, l = 0.f, m_acc = -1e30f, m_prev = -1e30f;
+#pragma unroll
+      for (int e = 0; e < kD; ++e) o_acc[e] = 0.f;
+      auto fold = [&](float m_tile) {   // add the pending O tile (relative to m_tile) into o_acc
+        mbar_wait(&S->o_full[ob.idx], ob.ph);
+        tc_fence_after();
+        const float a_old = exp2f(m_acc - m_tile);
+#pragma unroll
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_base + 256 + ob.idx * 64 + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o_acc[c0 + i] = o_acc[c0 + i] * a_old + v[i];
+        }
+        m_acc = m_tile;
+        tc_fence_before();
+        mbar_arrive(&S->o_empty[ob.idx]);
+        ob.next();
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j == n_slc_tiles && j > 0) {          // close the selection branch -> saved O_slc (fp32)
+          fold(m_prev);
+          const float inv = 1.f / l;
+          float* os = static_cast<float*>(c.o[1]) + row * kD;
+#pragma unroll
+          for (int e = 0; e < kD; e += 4) {
+            if (rvalid)
+              *reinterpret_cast<float4*>(os + e) =
+                  make_float4(o_acc[e] * inv, o_acc[e + 1] * inv, o_acc[e + 2] * inv, o_acc[e + 3] * inv);
+            o_acc[e] = o_acc[e + 1] = o_acc[e + 2] = o_acc[e + 3] = 0.f;
+          }
+          lse_slc = m + log2f(l);
+          m = -1e30f; l = 0.f; m_acc = -1e30f;
+        }
+        const bool first_of_branch = (j == 0 || j == n_slc_tiles);
+        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        tc_fence_after();
+        const int nv = S->tile_nv[j];
+        uint32_t pk[64];
+        float v[128];
+#pragma unroll
+        for (int c0 = 0; c0 < kTile; c0 += 32) tmem_ld32(lane_base + sb.idx * 128 + c0, v + c0);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[sb.idx]);
+        sb.next();
+        float mx = -1e30f;
+#pragma unroll
+        for (int i = 0; i < kTile; ++i) {
+          v[i] = i < nv ? v[i] * cl2 : -1e30f;
+          mx = fmaxf(mx, v[i]);
+        }
+        const float mn = fmaxf(m, mx);
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < kTile; i += 2) {
+          const float p0 = exp2f(v[i] - mn), p1 = exp2f(v[i + 1] - mn);
+          s += p0 + p1;
+          pk[i / 2] = pack_f16(p0, p1);
+        }
+        l = l * exp2f(m - mn) + s;
+        m = mn;
+        mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
+        const uint32_t pbase = smem_u32(sP + pb.idx * 32768);
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch)      // key chunk ch: key block ch/8, chunk ch%8 of line = row
+          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+                       pk[4 * ch + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(&S->p_full[pb.idx]);
+        pb.next();
+        if (!first_of_branch) fold(m_prev);   // previous tile's O (one-tile lag hides the PV latency)
+        m_prev = mn;
+      }
+      fold(m_prev);
+      const float inv = 1.f / l;
+      if (rvalid) {
+        // o_acc * inv is the window branch; the selection branch is in c.o[1] (written above)
+        float* ow = static_cast<float*>(c.o[2]) + row * kD;
+        const float* os = static_cast<const float*>(c.o[1]) + row * kD;
+        const float* ocm = static_cast<const float*>(c.o[0]) + row * kD;
+        c.lse[1][row] = lse_slc * kLn2;
+        c.lse[2][row] = (m + log2f(l)) * kLn2;
+        const float w0 = c.gs[row * 3], w1 = c.gs[row * 3 + 1], w2 = c.gs[row * 3 + 2];
+        const int t = t0 + r / c.h_s, hs = r % c.h_s;
+        const int dst = c.sorted_input ? t : c.perm[t];
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
+#pragma unroll
+        for (int e = 0; e < kD; e += 8) {
+          const float4 ca = *reinterpret_cast<const float4*>(ocm + e), cb = *reinterpret_cast<const float4*>(ocm + e + 4);
+          const float4 sa = *reinterpret_cast<const float4*>(os + e), sb4 = *reinterpret_cast<const float4*>(os + e + 4);
+          const float cm[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+          const float sl[8] = {sa.x, sa.y, sa.z, sa.w, sb4.x, sb4.y, sb4.z, sb4.w};
+          float wn[8];
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) wn[i] = o_acc[e + i] * inv;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2)
+            w[i / 2] = pack_bf16(w0 * cm[i] + w1 * sl[i] + w2 * wn[i], w0 * cm[i + 1] + w1 * sl[i + 1] + w2 * wn[i + 1]);
+          *reinterpret_cast<uint4*>(out + e) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<float4*>(ow + e) = make_float4(wn[0], wn[1], wn[2], wn[3]);
+          *reinterpret_cast<float4*>(ow + e + 4) = make_float4(wn[4], wn[5], wn[6], wn[7]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+bool tc_available() { return true; }
+
+size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
+  (void)H;
+  // bf16 hi/lo K^cmp + fp16 V^cmp (n_cmp <= N) + fp16 copy of V
+  return size_t(4) * size_t(h_kv) * size_t(N) * size_t(D) * 2 + 4 * 256;
+}
+
+bool tc_supported(const Ctx& c) {
+  return c.D == kD && c.m_cmp >= 1 && c.off[SSA_LEVEL_Q] && c.T <= 64;
+}
+
+ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
+  const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
+  Carve cw(ws, tc_fwd_ws_bytes(c.N, c.H, c.h_kv, c.D));
+  __nv_bfloat16* kc_hi = cw.take<__nv_bfloat16>(size_t(c.h_kv) * n_cmp * kD);
+  __nv_bfloat16* kc_lo = cw.take<__nv_bfloat16>(size_t(c.h_kv) * n_cmp * kD);
+  __half* vc = cw.take<__half>(size_t(c.h_kv) * n_cmp * kD);
+  __half* vs16 = cw.take<__half>(size_t(c.h_kv) * c.N * kD);
+  const int64_t n = int64_t(c.h_kv) * c.N * kD;   // >= h_kv * n_cmp * kD
+  k_tc_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16);
+  SSA_LAUNCH_CHECK("k_tc_prep");
+  CUtensorMap tmQ, tmKh, tmKl, tmVc, tmK, tmV;
+  const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
+  if (!make_tmap_bf16_2d(&tmQ, c.qs, qrows, kTile) || !make_tmap_bf16_2d(&tmKh, kc_hi, crows, kTile) ||
+      !make_tmap_bf16_2d(&tmKl, kc_lo, crows, kTile) || !make_tmap_bf16_2d(&tmVc, vc, crows, kTile) ||
+      !make_tmap_bf16_2d(&tmK, c.ks, krows, kTile) || !make_tmap_bf16_2d(&tmV, vs16, krows, kTile))
+    return SSA_ERR_CUDA;
+  TcArgs a{c, kc_hi, kc_lo, vc};
+  const int nq = c.n_blk[SSA_LEVEL_Q];
+  {
+    const size_t smem = 1024 + 16384 + kStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+                        (size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
+    if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ProfScope ps("tc_cmp_fwd", st);
+    k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
+    SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
+  }
+  {
+    const size_t smem = 1024 + 16384 + kStages * 32768 + 65536 + sizeof(SwSmem);
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ProfScope ps("tc_slc_win_fwd", st);
+    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kThreads, smem, st>>>(c, tmQ, tmK, tmV);
+    SSA_LAUNCH_CHECK("k_tc_slcwin_fwd");
+  }
+  return SSA_OK;
+}
+
+}  // namespace ssa

@@ -72,7 +72,17 @@ def test_c2_bf16_full():
     c, grid, batch = config_coords("C2")
     inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=cfg["seed"])
     kw = dict(h_kv=2, T=8, m_cmp=4, m_slc=8, m_win=8, m_q=8)
-    _check_all(inp, kw)
+    _check_all(inp, kw, expect_tc=True)
+
+
+def test_c2_bf16_full_simt():
+    """Same as test_c2_bf16_full on the SIMT kernels (SSA_FORCE_SIMT)."""
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import CONFIGS, config_coords, make_inputs
+    c, grid, batch = config_coords("C2")
+    inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=CONFIGS["C2"]["seed"])
+    kw = dict(h_kv=2, T=8, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    _check_all(inp, kw, flags=ssa.SSA_FORCE_SIMT, expect_tc=False)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
