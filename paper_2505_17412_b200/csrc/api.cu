@@ -76,7 +76,8 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
 bool use_tc(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   const int32_t* m = p->info.m;
   return tc_available() && cfg->dtype == SSA_BF16 && d.D == 64 && !(cfg->flags & SSA_FORCE_SIMT) &&
-         m[SSA_LEVEL_WIN] == m[SSA_LEVEL_SLC] && m[SSA_LEVEL_Q] == m[SSA_LEVEL_SLC] && cfg->top_k <= 64;
+         m[SSA_LEVEL_WIN] == m[SSA_LEVEL_SLC] && m[SSA_LEVEL_Q] == m[SSA_LEVEL_SLC] && cfg->top_k <= 64 &&
+         tc_plan_ok(p->info, cfg->top_k);
 }
 bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   return tc_bwd_available() && use_tc(d, cfg, p);
@@ -263,12 +264,14 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;
   if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
   if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
-  if (use_tc_bwd(d, cfg, p)) {
+  const bool tc = use_tc_bwd(d, cfg, p);
+  if (tc) {
     if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
+    if ((s = cmp_reduce(x, st)) != SSA_OK) return s;
   } else {
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
   }
-  return bwd_epilogue(x, bf16, st);
+  return bwd_epilogue(x, bf16, st, /*skip_q=*/tc);
 }
 
 extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,

@@ -362,11 +362,11 @@ extern "C" ssa_status ssa_build_blocks(const int32_t* coords, int64_t n, int32_t
     CTRY(cudaMemcpyAsync(p->q_order, order.data(), nq * 4, cudaMemcpyHostToDevice, st));
     CTRY(cudaStreamSynchronize(st));
   }
-  {  // 64-key compression tiles per batch item (KV-outer backward work list)
+  {  // 128-key compression tiles per batch item (KV-outer backward work list)
     std::vector<int32_t> tiles;
     const auto& bb = p->h_batch_blocks[SSA_LEVEL_CMP];
     for (int b = 0; b < batch; ++b)
-      for (int32_t j = bb[b]; j < bb[b + 1]; j += 64) { tiles.push_back(b); tiles.push_back(j); }
+      for (int32_t j = bb[b]; j < bb[b + 1]; j += 128) { tiles.push_back(b); tiles.push_back(j); }
     p->n_cmp_tiles = int32_t(tiles.size() / 2);
     if (!tiles.empty()) {
       CTRY(cudaMemcpyAsync(p->cmp_tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, st));

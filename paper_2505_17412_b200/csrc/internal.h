@@ -28,7 +28,7 @@ struct Plan {
   int32_t* slc_cmp_begin = nullptr;   // [n_slc+1] first compression block of each selection block
   int32_t* q_order = nullptr;         // [n_q] query blocks, largest first (LPT work order)
   int32_t* q_batch = nullptr;         // [n_q] batch item of each query block
-  int32_t* cmp_tiles = nullptr;       // [n_cmp_tiles][2] (batch item, first cmp block), 64-key tiles
+  int32_t* cmp_tiles = nullptr;       // [n_cmp_tiles][2] (batch item, first cmp block), 128-key tiles
   int32_t n_cmp_tiles = 0;
   std::vector<int32_t> h_batch_blocks[kLevels];
   std::vector<int32_t> h_batch_tokens;
@@ -78,7 +78,8 @@ ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st);
 ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st);
-ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st, bool skip_q);
+ssa_status cmp_reduce(const Ctx& c, cudaStream_t st);
 
 // Optional per-kernel event timing (api.cu). Usage: { ProfScope ps("name", st); kernel<<<..., st>>>(); }
 struct ProfScope {

@@ -678,45 +678,48 @@ __global__ void __launch_bounds__(128) k_win_bwd(Ctx c) {
   }
 }
 
-// compression branch dK^cmp/dV^cmp partials: grid (cmp tile, g, chunk). Tile = 64 compressed keys
-// of one batch item; chunk = a contiguous 1/n_chunk share of the batch item's rows.
+// compression branch dK^cmp/dV^cmp partials: grid (cmp tile, g, chunk). Tile = 128 compressed keys
+// of one batch item (processed as two 64-key halves); chunk = a contiguous 1/n_chunk share of the
+// batch item's rows.
 template <class T, int D>
 __global__ void __launch_bounds__(128) k_cmp_dkdv(Ctx c) {
   __shared__ float Qt[kRT * D], Ot[kRT * D], s_l[kRT], s_w[kRT], s_D[kRT];
   const int tile = blockIdx.x, g = blockIdx.y, chunk = blockIdx.z;
-  const int b = c.cmp_tiles[2 * tile], j0 = c.cmp_tiles[2 * tile + 1];
-  const int c1 = c.bb[SSA_LEVEL_CMP][b + 1];
+  const int b = c.cmp_tiles[2 * tile], jt = c.cmp_tiles[2 * tile + 1];
+  const int c1 = min(c.bb[SSA_LEVEL_CMP][b + 1], jt + 128);
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
   const int half = threadIdx.x & 1;
-  const int j = j0 + (threadIdx.x >> 1);
-  const bool kvalid = j < c1;
   const float* kc = static_cast<const float*>(c.kc);
   const float* vc = static_cast<const float*>(c.vc);
-  KvAcc<D> a;
-#pragma unroll
-  for (int e = 0; e < D / 2; ++e) {
-    int64_t idx = (int64_t(g) * n_cmp + (kvalid ? j : j0)) * D + half * (D / 2) + e;
-    a.k[e] = kc[idx];
-    a.v[e] = vc[idx];
-    a.dk[e] = 0.f;
-    a.dv[e] = 0.f;
-  }
   const int bt0 = c.batch_tokens[b], bt1 = c.batch_tokens[b + 1];
   const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
   const int64_t per = (rows + c.n_chunk - 1) / c.n_chunk;
   const int64_t ra = min(rows, per * chunk), re = min(rows, per * (chunk + 1));
   const int64_t rb = (int64_t(g) * c.N + bt0) * c.h_s;
-  for (int64_t r0 = ra; r0 < re; r0 += kRT) {
-    const int nr = int((re - r0) < kRT ? (re - r0) : kRT);
-    stage_rows<T, D>(c, 0, rb + r0, nr, Qt, Ot, s_l, s_w, s_D);
-    kv_rows_tile<T, D>(a, kvalid, half, Qt, Ot, s_l, s_w, s_D, nr, c.scale);
-  }
-  if (kvalid) {
+  for (int j0 = jt; j0 < c1; j0 += 64) {
+    const int j = j0 + (threadIdx.x >> 1);
+    const bool kvalid = j < c1;
+    KvAcc<D> a;
 #pragma unroll
     for (int e = 0; e < D / 2; ++e) {
-      int64_t idx = ((int64_t(chunk) * c.h_kv + g) * n_cmp + j) * D + half * (D / 2) + e;
-      c.dkc_part[idx] = a.dk[e];
-      c.dvc_part[idx] = a.dv[e];
+      int64_t idx = (int64_t(g) * n_cmp + (kvalid ? j : j0)) * D + half * (D / 2) + e;
+      a.k[e] = kc[idx];
+      a.v[e] = vc[idx];
+      a.dk[e] = 0.f;
+      a.dv[e] = 0.f;
+    }
+    for (int64_t r0 = ra; r0 < re; r0 += kRT) {
+      const int nr = int((re - r0) < kRT ? (re - r0) : kRT);
+      stage_rows<T, D>(c, 0, rb + r0, nr, Qt, Ot, s_l, s_w, s_D);
+      kv_rows_tile<T, D>(a, kvalid, half, Qt, Ot, s_l, s_w, s_D, nr, c.scale);
+    }
+    if (kvalid) {
+#pragma unroll
+      for (int e = 0; e < D / 2; ++e) {
+        int64_t idx = ((int64_t(chunk) * c.h_kv + g) * n_cmp + j) * D + half * (D / 2) + e;
+        c.dkc_part[idx] = a.dk[e];
+        c.dvc_part[idx] = a.dv[e];
+      }
     }
   }
 }
@@ -815,10 +818,7 @@ ssa_status simt_bwd_t(const Ctx& c, cudaStream_t st) {
     k_cmp_dkdv<T, D><<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), 128, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_cmp_dkdv");
   }
-  int64_t per = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * c.D;
-  k_cmp_reduce<<<nblk(per, 256), 256, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_cmp_reduce");
-  return SSA_OK;
+  return cmp_reduce(c, st);
 }
 
 template <class T>
@@ -919,16 +919,27 @@ ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st) {
   return SSA_OK;
 }
 
-ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st) {
+ssa_status cmp_reduce(const Ctx& c, cudaStream_t st) {
+  int64_t per = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * c.D;
+  k_cmp_reduce<<<nblk(per, 256), 256, 0, st>>>(c);
+  SSA_LAUNCH_CHECK("k_cmp_reduce");
+  return SSA_OK;
+}
+
+ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st, bool skip_q) {
   int64_t nq = int64_t(c.N) * c.H * c.D, nk = int64_t(c.N) * c.h_kv * c.D;
   if (bf16) {
-    k_bwd_final_q<__nv_bfloat16><<<nblk(nq, 256), 256, 0, st>>>(c);
-    SSA_LAUNCH_CHECK("k_bwd_final_q");
+    if (!skip_q) {
+      k_bwd_final_q<__nv_bfloat16><<<nblk(nq, 256), 256, 0, st>>>(c);
+      SSA_LAUNCH_CHECK("k_bwd_final_q");
+    }
     k_bwd_final_kv<__nv_bfloat16><<<nblk(nk, 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_bwd_final_kv");
   } else {
-    k_bwd_final_q<float><<<nblk(nq, 256), 256, 0, st>>>(c);
-    SSA_LAUNCH_CHECK("k_bwd_final_q");
+    if (!skip_q) {
+      k_bwd_final_q<float><<<nblk(nq, 256), 256, 0, st>>>(c);
+      SSA_LAUNCH_CHECK("k_bwd_final_q");
+    }
     k_bwd_final_kv<float><<<nblk(nk, 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_bwd_final_kv");
   }

@@ -1,8 +1,667 @@
-// tc_bwd.cu — tcgen05 backward kernels (bf16, d = 64). Until they land the backward runs the SIMT
-// kernels on the tcgen05 forward's saved state (same layout).
+// tc_bwd.cu — tcgen05/TMEM/TMA backward kernels of the bf16, d = 64 SSA path.
+// Probabilities are recomputed from the forward's saved LSEs (flash-style); the block structure and
+// the selected indices I are constants (hard routing, reading R15). With D_c = omega_c <dO, O_c>:
+//   dS = P (omega_c dP - D_c),  dP = dO V^T,  dq = scale dS K,  dk = scale dS^T q,  dv = (P omega_c)^T dO.
+//
+//  k_tc_dq    Q-outer: CTA per (query block, kv group); for every 128-row tile, S = Q K^T and dP = dO V^T
+//             over the compression keys, the selected blocks and the window (112-key tiles, S/dP double
+//             buffered in TMEM), dS -> smem, dQ += dS K accumulated in TMEM over all three branches,
+//             written once to the caller's dq (no atomics, deterministic).
+//  k_tc_dkdv  KV-outer: CTA per key tile; S^T = K Q^T and dP^T = V dO^T for 64-row tiles (keys on TMEM
+//             lanes), (P omega)^T and dS^T -> smem as K-major A operands, dV += (P omega)^T dO and
+//             dK += dS^T Q accumulated in TMEM. Raw keys (mode 1): the rows of every query block that
+//             selected the key's block (inverse CSR, ascending) + the window's own rows. Compressed keys
+//             (mode 0): a 1/n_chunk share of the batch item's rows -> per-chunk partials reduced in a
+//             fixed order (deterministic).
+#include <cfloat>
+
+#include "internal.h"
 #include "tc.h"
+#include "tc_common.cuh"
+
 namespace ssa {
-bool tc_bwd_available() { return false; }
-size_t tc_bwd_ws_bytes(int64_t, int, int, int) { return 0; }
-ssa_status tc_backward(const Ctx&, void*, cudaStream_t) { set_error("tcgen05 backward not built"); return SSA_ERR_UNSUPPORTED; }
+namespace {
+using namespace tc;
+
+constexpr int kD = 64;
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kStages = 3;
+
+struct Ring {
+  int idx = 0;
+  uint32_t ph = 0;
+  int n;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++idx == n) { idx = 0; ph ^= 1u; }
+  }
+};
+
+// fp16 operand copies for the backward MMAs. bf16 inputs convert exactly while |x| < 65504
+// (saturating beyond); dS and P*omega are then packed in fp16 (11-bit mantissa).
+__device__ __forceinline__ __half to_h(float x) {
+  __half h;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&h)) : "f"(x));
+  return h;
+}
+__global__ void k_tc_bwd_prep(Ctx c, __half* q16, __half* do16, __half* k16, __half* v16, __half* kc16, __half* vc16) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nr = int64_t(c.h_kv) * c.N * c.h_s * kD, nk = int64_t(c.h_kv) * c.N * kD;
+  const int64_t nc = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
+  if (i < nr) {
+    q16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.qs)[i]));
+    do16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.dos)[i]));
+  }
+  if (i < nk) {
+    k16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.ks)[i]));
+    v16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.vs)[i]));
+  }
+  if (i < nc) {
+    kc16[i] = to_h(static_cast<const float*>(c.kc)[i]);
+    vc16[i] = to_h(static_cast<const float*>(c.vc)[i]);
+  }
+}
+
+// ================================================================================================
+// dQ (Q-outer)
+// ================================================================================================
+constexpr int kKT = 112;                 // keys per tile: 2 x (S 112 + dP 112) + dQ 64 = 512 TMEM cols
+constexpr int kMaxKT = 64 + 4 * 64 * 2 + 16;
+struct DqSmem {
+  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], ds_full[2], ds_empty[2],
+      dq_full, dq_empty;
+  uint32_t tmem;
+  int n_tiles;
+  int tile_row[kMaxKT];                   // row in the key array of the tile's branch
+  int tile_nv[kMaxKT];
+  int8_t tile_br[kMaxKT];
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
+        __grid_constant__ const CUtensorMap tmKc, __grid_constant__ const CUtensorMap tmVc,
+        __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                       // 16 KB
+  uint8_t* sDO = sm + 16384;              // 16 KB
+  uint8_t* sKV = sm + 32768;              // kStages x {K 16 KB, V 16 KB}
+  uint8_t* sDS = sKV + kStages * 32768;   // 2 x 32 KB: dS K-major, 2 key blocks x [128 rows][128 B]
+  DqSmem* S = reinterpret_cast<DqSmem*>(sDS + 65536);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int rows = (t1 - t0) * c.h_s;
+  const int n_rt = (rows + 127) / 128;
+  const int qrow0 = (g * c.N + t0) * c.h_s;
+
+  if (tid == 0) {
+    mbar_init(&S->q_full, 1);
+    mbar_init(&S->q_empty, 1);
+    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S->s_full[i], 1);
+      mbar_init(&S->s_empty[i], 128);
+      mbar_init(&S->ds_full[i], 128);
+      mbar_init(&S->ds_empty[i], 1);
+    }
+    mbar_init(&S->dq_full, 1);
+    mbar_init(&S->dq_empty, 128);
+    fence_barrier_init();
+    int n = 0;
+    const int b = c.q_batch[Q];
+    const int c0 = c.bb[SSA_LEVEL_CMP][b], c1 = c.bb[SSA_LEVEL_CMP][b + 1];
+    const int ncmp = c.n_blk[SSA_LEVEL_CMP];
+    for (int x = c0; x < c1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * ncmp + x; S->tile_nv[n] = min(kKT, c1 - x); S->tile_br[n] = 0; ++n; }
+    for (int j = 0; j < c.T; ++j) {
+      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+      if (B < 0) continue;
+      const int a0 = c.off[SSA_LEVEL_SLC][B], a1 = c.off[SSA_LEVEL_SLC][B + 1];
+      for (int x = a0; x < a1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * c.N + x; S->tile_nv[n] = min(kKT, a1 - x); S->tile_br[n] = 1; ++n; }
+    }
+    for (int x = t0; x < t1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * c.N + x; S->tile_nv[n] = min(kKT, t1 - x); S->tile_br[n] = 2; ++n; }
+    S->n_tiles = n;
+  }
+  if (warp == 4 && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmKc); tma_prefetch(&tmVc); tma_prefetch(&tmK); tma_prefetch(&tmV);
+  }
+  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S->tmem;
+  const int n_tiles = S->n_tiles;
+
+  if (warp == 4) {
+    Ring kv(kStages);
+    uint32_t qph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_empty, qph ^ 1u);
+      qph ^= 1u;
+      if (lane == 0) {
+        mbar_expect_tx(&S->q_full, 32768);
+        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * 128);
+        tma_load_2d(sDO, &tmDO, &S->q_full, 0, qrow0 + rt * 128);
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
+        if (lane == 0) {
+          uint8_t* st = sKV + kv.idx * 32768;
+          const bool cmp = S->tile_br[j] == 0;
+          mbar_expect_tx(&S->kv_full[kv.idx], 2u * kKT * 128u);
+          tma_load_2d(st, cmp ? &tmKc : &tmK, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+          tma_load_2d(st + 16384, cmp ? &tmVc : &tmV, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+        }
+        __syncwarp();
+        kv.next();
+      }
+    }
+  } else if (warp == 5) {
+    const uint32_t idS = idesc_f16(128, kKT, false, false);    // S = Q K^T, dP = dO V^T
+    const uint32_t idQ = idesc_f16(128, 64, false, true);      // dQ += dS K (K as MN-major B)
+    const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO);
+    Ring kv(kStages), sb(2), db(2);
+    uint32_t qph = 0, dqph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      mbar_wait(&S->q_full, qph);
+      qph ^= 1u;
+      tc_fence_after();
+      Ring kv_q = kv;
+      auto issue_s = [&]() {
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
+        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sk = smem_u32(sKV + kv.idx * 32768);
+          const uint32_t d = tmem + sb.idx * 224;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d + kKT, desc_sw128(aDO + k * 32, 0, 1024), desc_sw128(sk + 16384 + k * 32, 0, 1024), idS, k > 0);
+          umma_commit(&S->s_full[sb.idx]);
+        }
+        __syncwarp();
+        kv.next();
+        sb.next();
+      };
+      issue_s();
+      mbar_wait(&S->dq_empty, dqph ^ 1u);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s();
+        mbar_wait(&S->ds_full[db.idx], db.ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ads = smem_u32(sDS + db.idx * 32768);
+          const uint32_t sk = smem_u32(sKV + kv_q.idx * 32768);
+#pragma unroll
+          for (int k = 0; k < kKT / 16; ++k)
+            umma_bf16(tmem + 448, desc_sw128(ads + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024),
+                      desc_sw128(sk + k * 2048, 0, 1024), idQ, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->ds_empty[db.idx]);
+          umma_commit(&S->kv_empty[kv_q.idx]);
+        }
+        __syncwarp();
+        kv_q.next();
+        db.next();
+      }
+      if (lane == 0) {
+        umma_commit(&S->dq_full);
+        umma_commit(&S->q_empty);
+      }
+      __syncwarp();
+      dqph ^= 1u;
+    }
+  } else {
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    const float cl2 = c.scale * kLog2e;
+    Ring sb(2), db(2);
+    uint32_t dqph = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      const int r = rt * 128 + tid;
+      const bool rvalid = r < rows;
+      const int64_t row = qrow0 + (rvalid ? r : 0);
+      float lse2[3], w[3], Dv[3];
+#pragma unroll
+      for (int br = 0; br < 3; ++br) {
+        lse2[br] = rvalid ? c.lse[br][row] * kLog2e : INFINITY;
+        w[br] = c.gs[row * 3 + br];
+        Dv[br] = c.Dd[br][row];
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const int br = S->tile_br[j], nv = S->tile_nv[j];
+        const float l2 = br == 0 ? lse2[0] : (br == 1 ? lse2[1] : lse2[2]);
+        const float wb = br == 0 ? w[0] : (br == 1 ? w[1] : w[2]);
+        const float Db = br == 0 ? Dv[0] : (br == 1 ? Dv[1] : Dv[2]);
+        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        tc_fence_after();
+        uint32_t pk[kKT / 2];
+#pragma unroll
+        for (int c0 = 0; c0 < kKT; c0 += 16) {
+          float s[16], dp[16];
+          tmem_ld16(lane_base + sb.idx * 224 + c0, s);
+          tmem_ld16(lane_base + sb.idx * 224 + kKT + c0, dp);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float p0 = (c0 + i < nv) ? exp2f(s[i] * cl2 - l2) : 0.f;
+            const float p1 = (c0 + i + 1 < nv) ? exp2f(s[i + 1] * cl2 - l2) : 0.f;
+            pk[(c0 + i) / 2] = pack_f16(p0 * (wb * dp[i] - Db), p1 * (wb * dp[i + 1] - Db));
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[sb.idx]);
+        sb.next();
+        mbar_wait(&S->ds_empty[db.idx], db.ph ^ 1u);
+        const uint32_t base = smem_u32(sDS + db.idx * 32768);
+#pragma unroll
+        for (int ch = 0; ch < kKT / 8; ++ch)
+          st_shared_v4(base + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+                       pk[4 * ch + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(&S->ds_full[db.idx]);
+        db.next();
+      }
+      mbar_wait(&S->dq_full, dqph);
+      dqph ^= 1u;
+      tc_fence_after();
+      float v[64];
+      tmem_ld32(lane_base + 448, v);
+      tmem_ld32(lane_base + 448 + 32, v + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&S->dq_empty);
+      if (rvalid) {
+        const int t = t0 + r / c.h_s, hs = r % c.h_s;
+        const int dst = c.sorted_input ? t : c.perm[t];
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
+#pragma unroll
+        for (int e = 0; e < kD; e += 8)
+          *reinterpret_cast<uint4*>(o + e) =
+              make_uint4(pack_bf16(v[e] * c.scale, v[e + 1] * c.scale), pack_bf16(v[e + 2] * c.scale, v[e + 3] * c.scale),
+                         pack_bf16(v[e + 4] * c.scale, v[e + 5] * c.scale), pack_bf16(v[e + 6] * c.scale, v[e + 7] * c.scale));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================================================
+// dK / dV (KV-outer)
+// ================================================================================================
+constexpr int kRT = 64;                  // rows per tile: 2 x (S^T 64 + dP^T 64) + dK 64 + dV 64 = 384
+struct KvSmem {
+  uint64_t k_full, k_empty, r_full[2], r_empty[2], s_full[2], s_empty[2], p_full[2], p_empty[2], acc_full, acc_empty;
+  uint32_t tmem;
+  float st_l2[2][kRT], st_w[2][kRT], st_D[2][kRT];
+};
+
+// Row-tile walker shared by the three roles: mode 0 = rows [ra, re) of the batch item (branch cmp);
+// mode 1 = rows of every query block in the inverse list (branch slc), then the window's rows (win).
+struct RowWalk {
+  int mode, g, li, le, t0w, t1w;
+  int64_t cur, end;     // current row range [cur, end)
+  int br;
+  const Ctx* c;
+  __device__ bool next_range() {
+    if (mode == 0) return false;
+    while (li < le) {
+      const int Qb = c->inv_list[li++];
+      const int q0 = c->off[SSA_LEVEL_Q][Qb], q1 = c->off[SSA_LEVEL_Q][Qb + 1];
+      cur = (int64_t(g) * c->N + q0) * c->h_s;
+      end = (int64_t(g) * c->N + q1) * c->h_s;
+      br = 1;
+      return true;
+    }
+    if (t0w >= 0) {
+      cur = (int64_t(g) * c->N + t0w) * c->h_s;
+      end = (int64_t(g) * c->N + t1w) * c->h_s;
+      br = 2;
+      t0w = -1;
+      return true;
+    }
+    return false;
+  }
+  // next 64-row tile: returns false when exhausted
+  __device__ bool next_tile(int64_t* r0, int* nr, int* b) {
+    while (cur >= end) {
+      if (!next_range()) return false;
+    }
+    *r0 = cur;
+    *nr = int((end - cur) < kRT ? (end - cur) : int64_t(kRT));
+    *b = br;
+    cur += kRT;
+    return true;
+  }
+};
+
+__device__ __forceinline__ RowWalk make_walk(const Ctx& c, int mode, int g, int key_block, int chunk, int b) {
+  RowWalk w;
+  w.c = &c;
+  w.mode = mode;
+  w.g = g;
+  if (mode == 0) {
+    const int bt0 = c.batch_tokens[b], bt1 = c.batch_tokens[b + 1];
+    const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
+    const int64_t per = ((rows + c.n_chunk - 1) / c.n_chunk + kRT - 1) / kRT * kRT;
+    const int64_t base = (int64_t(g) * c.N + bt0) * c.h_s;
+    w.cur = base + min(rows, per * chunk);
+    w.end = base + min(rows, per * (chunk + 1));
+    w.br = 0;
+    w.li = w.le = 0;
+    w.t0w = -1;
+  } else {
+    const int64_t key = int64_t(key_block) * c.h_kv + g;
+    w.li = c.inv_off[key];
+    w.le = c.inv_off[key + 1];
+    w.t0w = c.off[SSA_LEVEL_SLC][key_block];   // window == selection block (m_win == m_slc)
+    w.t1w = c.off[SSA_LEVEL_SLC][key_block + 1];
+    w.cur = w.end = 0;
+    w.br = 1;
+  }
+  return w;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
+          __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;                       // 16 KB
+  uint8_t* sV = sm + 16384;               // 16 KB
+  uint8_t* sR = sm + 32768;               // 2 stages x {Q 8 KB, dO 8 KB}
+  uint8_t* sP = sR + 32768;               // 2 x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
+  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 65536);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = blockIdx.y;
+  // key tiles of this CTA
+  int kbase, nkeys_total, b = 0, key_block = 0, chunk = 0;
+  int64_t krow_g;
+  if (mode == 0) {
+    b = c.cmp_tiles[2 * blockIdx.x];
+    kbase = c.cmp_tiles[2 * blockIdx.x + 1];
+    nkeys_total = min(128, c.bb[SSA_LEVEL_CMP][b + 1] - kbase);
+    chunk = blockIdx.z;
+    krow_g = int64_t(g) * c.n_blk[SSA_LEVEL_CMP];
+  } else {
+    key_block = blockIdx.x;
+    kbase = c.off[SSA_LEVEL_SLC][key_block];
+    nkeys_total = c.off[SSA_LEVEL_SLC][key_block + 1] - kbase;
+    krow_g = int64_t(g) * c.N;
+  }
+  const int n_kt = (nkeys_total + 127) / 128;
+
+  if (tid == 0) {
+    mbar_init(&S->k_full, 1);
+    mbar_init(&S->k_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S->r_full[i], 1);
+      mbar_init(&S->r_empty[i], 1);
+      mbar_init(&S->s_full[i], 1);
+      mbar_init(&S->s_empty[i], 128);
+      mbar_init(&S->p_full[i], 128);
+      mbar_init(&S->p_empty[i], 1);
+    }
+    mbar_init(&S->acc_full, 1);
+    mbar_init(&S->acc_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmK); tma_prefetch(&tmV); }
+  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S->tmem;
+
+  if (warp == 4) {
+    Ring rs(2);
+    uint32_t kph = 0;
+    for (int kt = 0; kt < n_kt; ++kt) {
+      mbar_wait(&S->k_empty, kph ^ 1u);
+      kph ^= 1u;
+      if (lane == 0) {
+        mbar_expect_tx(&S->k_full, 32768);
+        tma_load_2d(sK, &tmK, &S->k_full, 0, int(krow_g + kbase + kt * 128));
+        tma_load_2d(sV, &tmV, &S->k_full, 0, int(krow_g + kbase + kt * 128));
+      }
+      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
+      int64_t r0;
+      int nr, br;
+      while (wk.next_tile(&r0, &nr, &br)) {
+        mbar_wait(&S->r_empty[rs.idx], rs.ph ^ 1u);
+        if (lane == 0) {
+          uint8_t* st = sR + rs.idx * 16384;
+          mbar_expect_tx(&S->r_full[rs.idx], 16384);
+          tma_load_2d(st, &tmQ, &S->r_full[rs.idx], 0, int(r0));
+          tma_load_2d(st + 8192, &tmDO, &S->r_full[rs.idx], 0, int(r0));
+        }
+        __syncwarp();
+        rs.next();
+      }
+    }
+  } else if (warp == 5) {
+    const uint32_t idS = idesc_f16(128, kRT, false, false);    // S^T = K Q^T, dP^T = V dO^T
+    const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    Ring rs(2), sb(2), pb(2);
+    uint32_t kph = 0, aph = 0;
+    for (int kt = 0; kt < n_kt; ++kt) {
+      mbar_wait(&S->k_full, kph);
+      kph ^= 1u;
+      tc_fence_after();
+      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
+      int64_t r0;
+      int nr, br;
+      // count tiles first (the walker is cheap)
+      int n_tiles = 0;
+      {
+        RowWalk w2 = wk;
+        while (w2.next_tile(&r0, &nr, &br)) ++n_tiles;
+      }
+      Ring rs_a = rs;
+      auto issue_s = [&]() {
+        mbar_wait(&S->r_full[rs.idx], rs.ph);
+        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t aq = smem_u32(sR + rs.idx * 16384), ado = aq + 8192;
+          const uint32_t d = tmem + sb.idx * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, desc_sw128(aK + k * 32, 0, 1024), desc_sw128(aq + k * 32, 0, 1024), idS, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d + kRT, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
+          umma_commit(&S->s_full[sb.idx]);
+        }
+        __syncwarp();
+        rs.next();
+        sb.next();
+      };
+      if (n_tiles > 0) issue_s();
+      mbar_wait(&S->acc_empty, aph ^ 1u);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s();
+        mbar_wait(&S->p_full[pb.idx], pb.ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ap = smem_u32(sP + pb.idx * 32768), ads = ap + 16384;
+          const uint32_t aq = smem_u32(sR + rs_a.idx * 16384), ado = aq + 8192;
+#pragma unroll
+          for (int k = 0; k < kRT / 16; ++k)
+            umma_bf16(tmem + 448, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
+                      (j > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+          for (int k = 0; k < kRT / 16; ++k)
+            umma_bf16(tmem + 384, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
+                      (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->p_empty[pb.idx]);
+          umma_commit(&S->r_empty[rs_a.idx]);
+        }
+        __syncwarp();
+        rs_a.next();
+        pb.next();
+      }
+      if (lane == 0) {
+        umma_commit(&S->acc_full);
+        umma_commit(&S->k_empty);
+      }
+      __syncwarp();
+      aph ^= 1u;
+    }
+  } else {
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    const float cl2 = c.scale * kLog2e;
+    Ring sb(2), pb(2);
+    uint32_t aph = 0;
+    for (int kt = 0; kt < n_kt; ++kt) {
+      const int key = kt * 128 + tid;
+      const bool kvalid = key < nkeys_total;
+      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
+      int64_t r0;
+      int nr, br;
+      int n_tiles = 0;
+      while (wk.next_tile(&r0, &nr, &br)) {
+        // row stats of this tile (rows beyond nr or the chunk end get lse = +inf -> p = 0)
+        const int slot = n_tiles & 1;
+        if (tid < kRT) {
+          const bool ok = tid < nr;
+          const int64_t row = r0 + (ok ? tid : 0);
+          S->st_l2[slot][tid] = ok ? c.lse[br][row] * kLog2e : INFINITY;
+          S->st_w[slot][tid] = ok ? c.gs[row * 3 + br] : 0.f;
+          S->st_D[slot][tid] = ok ? c.Dd[br][row] : 0.f;
+        }
+        named_bar_sync(1, 128);
+        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        tc_fence_after();
+        uint32_t pw[kRT / 2], ds[kRT / 2];
+#pragma unroll
+        for (int c0 = 0; c0 < kRT; c0 += 16) {
+          float s[16], dp[16];
+          tmem_ld16(lane_base + sb.idx * 128 + c0, s);
+          tmem_ld16(lane_base + sb.idx * 128 + kRT + c0, dp);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float p0 = kvalid ? exp2f(s[i] * cl2 - S->st_l2[slot][c0 + i]) : 0.f;
+            const float p1 = kvalid ? exp2f(s[i + 1] * cl2 - S->st_l2[slot][c0 + i + 1]) : 0.f;
+            const float w0 = S->st_w[slot][c0 + i], w1 = S->st_w[slot][c0 + i + 1];
+            pw[(c0 + i) / 2] = pack_f16(p0 * w0, p1 * w1);
+            ds[(c0 + i) / 2] = pack_f16(p0 * (w0 * dp[i] - S->st_D[slot][c0 + i]),
+                                        p1 * (w1 * dp[i + 1] - S->st_D[slot][c0 + i + 1]));
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[sb.idx]);
+        sb.next();
+        mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
+        const uint32_t base = smem_u32(sP + pb.idx * 32768);
+#pragma unroll
+        for (int ch = 0; ch < kRT / 8; ++ch) {
+          st_shared_v4(base + sw128(tid, ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
+          st_shared_v4(base + 16384 + sw128(tid, ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2], ds[4 * ch + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&S->p_full[pb.idx]);
+        pb.next();
+        ++n_tiles;
+      }
+      // accumulators: dK at 384, dV at 448
+      mbar_wait(&S->acc_full, aph);
+      aph ^= 1u;
+      tc_fence_after();
+      float dk[64], dv[64];
+      tmem_ld32(lane_base + 384, dk);
+      tmem_ld32(lane_base + 384 + 32, dk + 32);
+      tmem_ld32(lane_base + 448, dv);
+      tmem_ld32(lane_base + 448 + 32, dv + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&S->acc_empty);
+      if (kvalid) {
+        float *ok, *ov;
+        if (mode == 0) {
+          const int64_t idx = ((int64_t(chunk) * c.h_kv + g) * c.n_blk[SSA_LEVEL_CMP] + kbase + key) * kD;
+          ok = c.dkc_part + idx;
+          ov = c.dvc_part + idx;
+        } else {
+          const int64_t idx = (int64_t(g) * c.N + kbase + key) * kD;
+          ok = c.dk_acc + idx;
+          ov = c.dv_acc + idx;
+        }
+        const bool none = n_tiles == 0;
+#pragma unroll
+        for (int e = 0; e < kD; e += 4) {
+          *reinterpret_cast<float4*>(ok + e) = none ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                    : make_float4(dk[e] * c.scale, dk[e + 1] * c.scale,
+                                                                  dk[e + 2] * c.scale, dk[e + 3] * c.scale);
+          *reinterpret_cast<float4*>(ov + e) = none ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                    : make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+bool tc_bwd_available() { return true; }
+
+size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
+  // fp16 copies: q, dO (rows), k, v (keys), K^cmp, V^cmp (n_cmp <= N)
+  return (size_t(2) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 6 * 256;
+}
+
+ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st) {
+  const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
+  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D));
+  const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
+  __half* q16 = cw.take<__half>(qrows * kD);
+  __half* do16 = cw.take<__half>(qrows * kD);
+  __half* k16 = cw.take<__half>(krows * kD);
+  __half* v16 = cw.take<__half>(krows * kD);
+  __half* kc = cw.take<__half>(crows * kD);
+  __half* vc = cw.take<__half>(crows * kD);
+  const int64_t n = int64_t(qrows) * kD;
+  k_tc_bwd_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, q16, do16, k16, v16, kc, vc);
+  SSA_LAUNCH_CHECK("k_tc_bwd_prep");
+  CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmK, tmV, tmKc128, tmVc128, tmK128, tmV128;
+  if (!make_tmap_bf16_2d(&tmQ, q16, qrows, 128) || !make_tmap_bf16_2d(&tmDO, do16, qrows, 128) ||
+      !make_tmap_bf16_2d(&tmQ64, q16, qrows, kRT) || !make_tmap_bf16_2d(&tmDO64, do16, qrows, kRT) ||
+      !make_tmap_bf16_2d(&tmKc, kc, crows, kKT) || !make_tmap_bf16_2d(&tmVc, vc, crows, kKT) ||
+      !make_tmap_bf16_2d(&tmK, k16, krows, kKT) || !make_tmap_bf16_2d(&tmV, v16, krows, kKT) ||
+      !make_tmap_bf16_2d(&tmKc128, kc, crows, 128) || !make_tmap_bf16_2d(&tmVc128, vc, crows, 128) ||
+      !make_tmap_bf16_2d(&tmK128, k16, krows, 128) || !make_tmap_bf16_2d(&tmV128, v16, krows, 128))
+    return SSA_ERR_CUDA;
+  {
+    const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(DqSmem);
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ProfScope ps("tc_bwd_dq", st);
+    k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
+    SSA_LAUNCH_CHECK("k_tc_dq");
+  }
+  const size_t smem = 1024 + 32768 + 32768 + 65536 + sizeof(KvSmem);
+  SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  {
+    ProfScope ps("tc_bwd_kv", st);
+    k_tc_dkdv<<<dim3(c.n_blk[SSA_LEVEL_SLC], c.h_kv, 1), kThreads, smem, st>>>(c, 1, tmQ64, tmDO64, tmK128, tmV128);
+    SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
+  }
+  {
+    ProfScope ps("tc_bwd_cmp_kv", st);
+    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kThreads, smem, st>>>(c, 0, tmQ64, tmDO64, tmKc128, tmVc128);
+    SSA_LAUNCH_CHECK("k_tc_dkdv(cmp)");
+  }
+  return SSA_OK;
+}
+
 }  // namespace ssa

@@ -643,8 +643,13 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
   return size_t(4) * size_t(h_kv) * size_t(N) * size_t(D) * 2 + 4 * 256;
 }
 
-bool tc_supported(const Ctx& c) {
-  return c.D == kD && c.m_cmp >= 1 && c.off[SSA_LEVEL_Q] && c.T <= 64;
+bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
+  const size_t smem = 1024 + 16384 + kStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+                      (size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
+  const int slc_tiles = (info.max_fill[SSA_LEVEL_SLC] + 111) / 112;
+  const int dq_tiles = (info.max_blocks_per_batch[SSA_LEVEL_CMP] + 111) / 112 + top_k * slc_tiles + slc_tiles;
+  return smem <= 232448 && dq_tiles <= 64 + 4 * 64 * 2 + 16 && top_k * ((info.max_fill[SSA_LEVEL_SLC] + 127) / 128) +
+         (info.max_fill[SSA_LEVEL_SLC] + 127) / 128 <= 4 * 64 + 8;
 }
 
 ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(128) k_umma_selftest(int mode, int N, int K, c
       uint32_t off = mb * (K * 128) + sw128(k, ch);
       *reinterpret_cast<uint4*>(sA + off) = v;
     }
-  } else if (mode == 2) {   // a = A [M=128][K]; K-major: K block kb (64 wide) at kb*16384, line = m
+  } else if (mode == 2 || mode == 3) {   // a = A [M=128][K]; K-major: K block kb (64 wide) at kb*16384, line = m
     for (int i = tid; i < 128 * (K / 8); i += 128) {
       int m = i / (K / 8), c = i % (K / 8), kb = c / 8, ch = c % 8;
       const uint4 v = *reinterpret_cast<const uint4*>(a + m * K + c * 8);
@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(128) k_umma_selftest(int mode, int N, int K, c
       for (int s = 0; s < K / 16; ++s)
         umma_bf16(tmem, desc_sw128(a0 + s * 2048, K * 128, 1024), desc_sw128(b0 + s * 2048, 0, 1024), id, s > 0);
     } else {
-      const uint32_t id = idesc_bf16(128, 64, false, true);
+      // mode 3: A and B fp16 (the P.V operand format)
+      const uint32_t id = mode == 3 ? idesc_f16(128, 64, false, true) : idesc_bf16(128, 64, false, true);
       for (int s = 0; s < K / 16; ++s)
         umma_bf16(tmem, desc_sw128(a0 + (s / 4) * 16384 + (s % 4) * 32, 0, 1024),
                   desc_sw128(b0 + s * 2048, 0, 1024), id, s > 0);

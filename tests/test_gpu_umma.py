@@ -50,3 +50,4 @@ def test_kmajor_a_mnmajor_b(k):
     d = _run(2, 64, k, a, b)
     ref = a.float() @ b.float()
     assert torch.allclose(d, ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
+
