@@ -227,7 +227,7 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   size_t scan = scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1);
-  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + 1024;
+  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]) + 1024;
   return SSA_OK;
 }
 
@@ -259,7 +259,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   void* scan_ws = cw.take<char>(scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1));
-  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
+  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
   const bool bf16 = cfg->dtype == SSA_BF16;
   if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;
   if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;

@@ -68,6 +68,9 @@ struct Ctx {
   int32_t *inv_off, *inv_list, *inv_cnt;   // inverse selection CSR over (slc block, g)
   int32_t *cmp_tiles;             // [n_cmp_tiles][2] (batch item, first cmp block) for the KV-outer cmp kernels
   int32_t n_cmp_tiles;
+  // tcgen05 raw-key KV-outer work items (tc_bwd.cu)
+  int32_t* kv_item_off;           // [n_slc * h_kv + 1] first work item of every (selection block, g)
+  float *kv_part_k, *kv_part_v;   // [items_bound][max_fill_slc][D] partials of items 1..
 };
 
 // SIMT kernels (simt.cu). Return SSA_OK or a launch error.

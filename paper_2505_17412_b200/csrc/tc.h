@@ -8,7 +8,7 @@ bool tc_bwd_available();
 // the plan's block statistics fit the tcgen05 kernels' shared-memory score arrays and tile lists
 bool tc_plan_ok(const ssa_plan_info& info, int top_k);
 size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D);
-size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D);
+size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc);
 // forward after gather + pool: compression attention + scores + top-k, selection + window attention,
 // gated combine (writes c.out and the saved state).
 ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st);

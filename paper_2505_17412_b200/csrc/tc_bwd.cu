@@ -247,8 +247,8 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const float p0 = (c0 + i < nv) ? exp2f(s[i] * cl2 - l2) : 0.f;
-            const float p1 = (c0 + i + 1 < nv) ? exp2f(s[i + 1] * cl2 - l2) : 0.f;
+            const float p0 = (c0 + i < nv) ? ex2(fmaf(s[i], cl2, -l2)) : 0.f;
+            const float p1 = (c0 + i + 1 < nv) ? ex2(fmaf(s[i + 1], cl2, -l2)) : 0.f;
             pk[(c0 + i) / 2] = pack_f16(p0 * (wb * dp[i] - Db), p1 * (wb * dp[i + 1] - Db));
           }
         }
@@ -295,39 +295,98 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
 // dK / dV (KV-outer)
 // ================================================================================================
 constexpr int kRT = 64;                  // rows per tile: 2 x (S^T 64 + dP^T 64) + dK 64 + dV 64 = 384
+constexpr int kRStages = 4;              // row-tile (Q, dO, stats) pipeline depth
+constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
 struct KvSmem {
-  uint64_t k_full, k_empty, r_full[2], r_empty[2], s_full[2], s_empty[2], p_full[2], p_empty[2], acc_full, acc_empty;
+  uint64_t k_full, k_empty, r_full[kRStages], r_empty[kRStages], s_full[2], s_empty[2], p_full[2], p_empty[2],
+      acc_full, acc_empty;
   uint32_t tmem;
-  float st_l2[2][kRT], st_w[2][kRT], st_D[2][kRT];
+  int item_ok;
+  alignas(16) float st_l2[kRStages][kRT];
+  alignas(16) float st_w[kRStages][kRT];
+  alignas(16) float st_D[kRStages][kRT];
 };
 
-// Row-tile walker shared by the three roles: mode 0 = rows [ra, re) of the batch item (branch cmp);
-// mode 1 = rows of every query block in the inverse list (branch slc), then the window's rows (win).
+// Work item -> (key block, g, query-block range, window?) and the row-tile walker shared by the roles.
+struct Item {
+  int mode, g, kblock, b, chunk, li, le, with_win, part_slot, first;
+  int64_t ra, re;       // mode 0 row range
+};
+
+__device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
+  it->mode = mode;
+  if (mode == 0) {
+    const int tile = blockIdx.x;
+    it->g = blockIdx.y;
+    it->b = c.cmp_tiles[2 * tile];
+    it->kblock = c.cmp_tiles[2 * tile + 1];
+    it->chunk = blockIdx.z;
+    const int bt0 = c.batch_tokens[it->b], bt1 = c.batch_tokens[it->b + 1];
+    const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
+    const int64_t per = ((rows + c.n_chunk - 1) / c.n_chunk + kRT - 1) / kRT * kRT;
+    const int64_t base = (int64_t(it->g) * c.N + bt0) * c.h_s;
+    it->ra = base + min(rows, per * it->chunk);
+    it->re = base + min(rows, per * (it->chunk + 1));
+    it->li = it->le = 0;
+    it->with_win = 0;
+    it->first = 1;
+    return true;
+  }
+  const int id = blockIdx.x;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  if (id >= c.kv_item_off[nkeys]) return false;
+  int lo = 0, hi = nkeys;                 // largest key with item_off[key] <= id
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (c.kv_item_off[mid] <= id) lo = mid; else hi = mid;
+  }
+  const int key = lo;
+  const int nch = c.kv_item_off[key + 1] - c.kv_item_off[key];
+  it->chunk = id - c.kv_item_off[key];
+  it->kblock = key / c.h_kv;
+  it->g = key % c.h_kv;
+  const int l0 = c.inv_off[key], l1 = c.inv_off[key + 1];
+  it->li = min(l1, l0 + it->chunk * kQBlocksPerItem);
+  it->le = min(l1, it->li + kQBlocksPerItem);
+  it->with_win = it->chunk == nch - 1;
+  it->first = it->chunk == 0;
+  it->part_slot = id;
+  it->ra = it->re = 0;
+  return true;
+}
+
 struct RowWalk {
-  int mode, g, li, le, t0w, t1w;
-  int64_t cur, end;     // current row range [cur, end)
+  Item it;
+  int li;
+  int64_t cur, end;
   int br;
+  int win_done;
   const Ctx* c;
+  __device__ void init(const Ctx& cc, const Item& i) {
+    c = &cc;
+    it = i;
+    li = i.li;
+    win_done = !i.with_win;
+    if (i.mode == 0) { cur = i.ra; end = i.re; br = 0; } else { cur = end = 0; br = 1; }
+  }
   __device__ bool next_range() {
-    if (mode == 0) return false;
-    while (li < le) {
+    if (it.mode == 0) return false;
+    if (li < it.le) {
       const int Qb = c->inv_list[li++];
-      const int q0 = c->off[SSA_LEVEL_Q][Qb], q1 = c->off[SSA_LEVEL_Q][Qb + 1];
-      cur = (int64_t(g) * c->N + q0) * c->h_s;
-      end = (int64_t(g) * c->N + q1) * c->h_s;
+      cur = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_Q][Qb]) * c->h_s;
+      end = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_Q][Qb + 1]) * c->h_s;
       br = 1;
       return true;
     }
-    if (t0w >= 0) {
-      cur = (int64_t(g) * c->N + t0w) * c->h_s;
-      end = (int64_t(g) * c->N + t1w) * c->h_s;
+    if (!win_done) {   // the window is the key block itself (m_win == m_slc)
+      win_done = 1;
+      cur = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_SLC][it.kblock]) * c->h_s;
+      end = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_SLC][it.kblock + 1]) * c->h_s;
       br = 2;
-      t0w = -1;
       return true;
     }
     return false;
   }
-  // next 64-row tile: returns false when exhausted
   __device__ bool next_tile(int64_t* r0, int* nr, int* b) {
     while (cur >= end) {
       if (!next_range()) return false;
@@ -340,33 +399,6 @@ struct RowWalk {
   }
 };
 
-__device__ __forceinline__ RowWalk make_walk(const Ctx& c, int mode, int g, int key_block, int chunk, int b) {
-  RowWalk w;
-  w.c = &c;
-  w.mode = mode;
-  w.g = g;
-  if (mode == 0) {
-    const int bt0 = c.batch_tokens[b], bt1 = c.batch_tokens[b + 1];
-    const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
-    const int64_t per = ((rows + c.n_chunk - 1) / c.n_chunk + kRT - 1) / kRT * kRT;
-    const int64_t base = (int64_t(g) * c.N + bt0) * c.h_s;
-    w.cur = base + min(rows, per * chunk);
-    w.end = base + min(rows, per * (chunk + 1));
-    w.br = 0;
-    w.li = w.le = 0;
-    w.t0w = -1;
-  } else {
-    const int64_t key = int64_t(key_block) * c.h_kv + g;
-    w.li = c.inv_off[key];
-    w.le = c.inv_off[key + 1];
-    w.t0w = c.off[SSA_LEVEL_SLC][key_block];   // window == selection block (m_win == m_slc)
-    w.t1w = c.off[SSA_LEVEL_SLC][key_block + 1];
-    w.cur = w.end = 0;
-    w.br = 1;
-  }
-  return w;
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
           __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
@@ -374,25 +406,24 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm;                       // 16 KB
   uint8_t* sV = sm + 16384;               // 16 KB
-  uint8_t* sR = sm + 32768;               // 2 stages x {Q 8 KB, dO 8 KB}
-  uint8_t* sP = sR + 32768;               // 2 x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
+  uint8_t* sR = sm + 32768;               // kRStages x {Q 8 KB, dO 8 KB}
+  uint8_t* sP = sR + kRStages * 16384;    // 2 x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
   KvSmem* S = reinterpret_cast<KvSmem*>(sP + 65536);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = blockIdx.y;
-  // key tiles of this CTA
-  int kbase, nkeys_total, b = 0, key_block = 0, chunk = 0;
+  Item it;
+  const bool ok = make_item(c, mode, &it);
+  if (!ok) return;                        // uniform for the whole CTA (grid is an upper bound)
+  const int g = it.g;
+  int kbase, nkeys_total;
   int64_t krow_g;
   if (mode == 0) {
-    b = c.cmp_tiles[2 * blockIdx.x];
-    kbase = c.cmp_tiles[2 * blockIdx.x + 1];
-    nkeys_total = min(128, c.bb[SSA_LEVEL_CMP][b + 1] - kbase);
-    chunk = blockIdx.z;
+    kbase = it.kblock;
+    nkeys_total = min(128, c.bb[SSA_LEVEL_CMP][it.b + 1] - kbase);
     krow_g = int64_t(g) * c.n_blk[SSA_LEVEL_CMP];
   } else {
-    key_block = blockIdx.x;
-    kbase = c.off[SSA_LEVEL_SLC][key_block];
-    nkeys_total = c.off[SSA_LEVEL_SLC][key_block + 1] - kbase;
+    kbase = c.off[SSA_LEVEL_SLC][it.kblock];
+    nkeys_total = c.off[SSA_LEVEL_SLC][it.kblock + 1] - kbase;
     krow_g = int64_t(g) * c.N;
   }
   const int n_kt = (nkeys_total + 127) / 128;
@@ -400,9 +431,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   if (tid == 0) {
     mbar_init(&S->k_full, 1);
     mbar_init(&S->k_empty, 1);
+    for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[i], 1); mbar_init(&S->r_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&S->r_full[i], 1);
-      mbar_init(&S->r_empty[i], 1);
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
       mbar_init(&S->p_full[i], 128);
@@ -420,7 +450,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   const uint32_t tmem = S->tmem;
 
   if (warp == 4) {
-    Ring rs(2);
+    // ------------------------------------------------ producer: K/V tile, then row tiles + row stats
+    Ring rs(kRStages);
     uint32_t kph = 0;
     for (int kt = 0; kt < n_kt; ++kt) {
       mbar_wait(&S->k_empty, kph ^ 1u);
@@ -430,11 +461,22 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         tma_load_2d(sK, &tmK, &S->k_full, 0, int(krow_g + kbase + kt * 128));
         tma_load_2d(sV, &tmV, &S->k_full, 0, int(krow_g + kbase + kt * 128));
       }
-      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
+      RowWalk wk;
+      wk.init(c, it);
       int64_t r0;
       int nr, br;
       while (wk.next_tile(&r0, &nr, &br)) {
         mbar_wait(&S->r_empty[rs.idx], rs.ph ^ 1u);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          const bool v = i < nr;
+          const int64_t row = r0 + (v ? i : 0);
+          S->st_l2[rs.idx][i] = v ? c.lse[br][row] * kLog2e : INFINITY;
+          S->st_w[rs.idx][i] = v ? c.gs[row * 3 + br] : 0.f;
+          S->st_D[rs.idx][i] = v ? c.Dd[br][row] : 0.f;
+        }
+        __syncwarp();
         if (lane == 0) {
           uint8_t* st = sR + rs.idx * 16384;
           mbar_expect_tx(&S->r_full[rs.idx], 16384);
@@ -446,24 +488,24 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       }
     }
   } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
     const uint32_t idS = idesc_f16(128, kRT, false, false);    // S^T = K Q^T, dP^T = V dO^T
     const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-    Ring rs(2), sb(2), pb(2);
+    Ring rs(kRStages), sb(2), pb(2);
     uint32_t kph = 0, aph = 0;
+    int n_tiles = 0;
+    {
+      RowWalk w2;
+      w2.init(c, it);
+      int64_t r0;
+      int nr, br;
+      while (w2.next_tile(&r0, &nr, &br)) ++n_tiles;
+    }
     for (int kt = 0; kt < n_kt; ++kt) {
       mbar_wait(&S->k_full, kph);
       kph ^= 1u;
       tc_fence_after();
-      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
-      int64_t r0;
-      int nr, br;
-      // count tiles first (the walker is cheap)
-      int n_tiles = 0;
-      {
-        RowWalk w2 = wk;
-        while (w2.next_tile(&r0, &nr, &br)) ++n_tiles;
-      }
       Ring rs_a = rs;
       auto issue_s = [&]() {
         mbar_wait(&S->r_full[rs.idx], rs.ph);
@@ -516,50 +558,54 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       aph ^= 1u;
     }
   } else {
+    // ------------------------------------------------ softmax: thread = key (TMEM lane)
     const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
     const float cl2 = c.scale * kLog2e;
-    Ring sb(2), pb(2);
+    Ring rs(kRStages), sb(2), pb(2);
     uint32_t aph = 0;
     for (int kt = 0; kt < n_kt; ++kt) {
       const int key = kt * 128 + tid;
       const bool kvalid = key < nkeys_total;
-      RowWalk wk = make_walk(c, mode, g, key_block, chunk, b);
+      RowWalk wk;
+      wk.init(c, it);
       int64_t r0;
       int nr, br;
       int n_tiles = 0;
       while (wk.next_tile(&r0, &nr, &br)) {
-        // row stats of this tile (rows beyond nr or the chunk end get lse = +inf -> p = 0)
-        const int slot = n_tiles & 1;
-        if (tid < kRT) {
-          const bool ok = tid < nr;
-          const int64_t row = r0 + (ok ? tid : 0);
-          S->st_l2[slot][tid] = ok ? c.lse[br][row] * kLog2e : INFINITY;
-          S->st_w[slot][tid] = ok ? c.gs[row * 3 + br] : 0.f;
-          S->st_D[slot][tid] = ok ? c.Dd[br][row] : 0.f;
-        }
-        named_bar_sync(1, 128);
+        mbar_wait(&S->r_full[rs.idx], rs.ph);      // row stats of this stage are visible
         mbar_wait(&S->s_full[sb.idx], sb.ph);
         tc_fence_after();
-        uint32_t pw[kRT / 2], ds[kRT / 2];
+        const float* L2 = S->st_l2[rs.idx];
+        const float* W = S->st_w[rs.idx];
+        const float* DD = S->st_D[rs.idx];
+        float s[kRT], dp[kRT];
 #pragma unroll
-        for (int c0 = 0; c0 < kRT; c0 += 16) {
-          float s[16], dp[16];
-          tmem_ld16(lane_base + sb.idx * 128 + c0, s);
-          tmem_ld16(lane_base + sb.idx * 128 + kRT + c0, dp);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const float p0 = kvalid ? exp2f(s[i] * cl2 - S->st_l2[slot][c0 + i]) : 0.f;
-            const float p1 = kvalid ? exp2f(s[i + 1] * cl2 - S->st_l2[slot][c0 + i + 1]) : 0.f;
-            const float w0 = S->st_w[slot][c0 + i], w1 = S->st_w[slot][c0 + i + 1];
-            pw[(c0 + i) / 2] = pack_f16(p0 * w0, p1 * w1);
-            ds[(c0 + i) / 2] = pack_f16(p0 * (w0 * dp[i] - S->st_D[slot][c0 + i]),
-                                        p1 * (w1 * dp[i + 1] - S->st_D[slot][c0 + i + 1]));
-          }
+        for (int c0 = 0; c0 < kRT; c0 += 32) {
+          tmem_ld32(lane_base + sb.idx * 128 + c0, s + c0);
+          tmem_ld32(lane_base + sb.idx * 128 + kRT + c0, dp + c0);
         }
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&S->s_empty[sb.idx]);
         sb.next();
+        uint32_t pw[kRT / 2], ds[kRT / 2];
+#pragma unroll
+        for (int i = 0; i < kRT; i += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(L2 + i);
+          const float4 w4 = *reinterpret_cast<const float4*>(W + i);
+          const float4 d4 = *reinterpret_cast<const float4*>(DD + i);
+          const float p0 = ex2(fmaf(s[i], cl2, -l4.x)), p1 = ex2(fmaf(s[i + 1], cl2, -l4.y));
+          const float p2 = ex2(fmaf(s[i + 2], cl2, -l4.z)), p3 = ex2(fmaf(s[i + 3], cl2, -l4.w));
+          pw[i / 2] = pack_f16(p0 * w4.x, p1 * w4.y);
+          pw[i / 2 + 1] = pack_f16(p2 * w4.z, p3 * w4.w);
+          ds[i / 2] = pack_f16(p0 * fmaf(w4.x, dp[i], -d4.x), p1 * fmaf(w4.y, dp[i + 1], -d4.y));
+          ds[i / 2 + 1] = pack_f16(p2 * fmaf(w4.z, dp[i + 2], -d4.z), p3 * fmaf(w4.w, dp[i + 3], -d4.w));
+        }
+        rs.next();
+        if (!kvalid) {
+#pragma unroll
+          for (int i = 0; i < kRT / 2; ++i) pw[i] = ds[i] = 0u;
+        }
         mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
         const uint32_t base = smem_u32(sP + pb.idx * 32768);
 #pragma unroll
@@ -587,13 +633,17 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       if (kvalid) {
         float *ok, *ov;
         if (mode == 0) {
-          const int64_t idx = ((int64_t(chunk) * c.h_kv + g) * c.n_blk[SSA_LEVEL_CMP] + kbase + key) * kD;
+          const int64_t idx = ((int64_t(it.chunk) * c.h_kv + g) * c.n_blk[SSA_LEVEL_CMP] + kbase + key) * kD;
           ok = c.dkc_part + idx;
           ov = c.dvc_part + idx;
-        } else {
+        } else if (it.first) {
           const int64_t idx = (int64_t(g) * c.N + kbase + key) * kD;
           ok = c.dk_acc + idx;
           ov = c.dv_acc + idx;
+        } else {
+          const int64_t idx = (int64_t(it.part_slot) * c.max_fill[SSA_LEVEL_SLC] + key) * kD;
+          ok = c.kv_part_k + idx;
+          ov = c.kv_part_v + idx;
         }
         const bool none = n_tiles == 0;
 #pragma unroll
@@ -612,18 +662,58 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   if (warp == 5) tmem_dealloc<512>(tmem);
 }
 
+// raw-key work items: ceil(len / kQBlocksPerItem) (at least 1, for the window) per (block, g)
+__global__ void k_kv_item_count(Ctx c, int32_t* cnt) {
+  const int key = blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= c.n_blk[SSA_LEVEL_SLC] * c.h_kv) return;
+  const int len = c.inv_off[key + 1] - c.inv_off[key];
+  cnt[key] = max(1, (len + kQBlocksPerItem - 1) / kQBlocksPerItem);
+}
+// fold the partials of items 1.. of every (block, g) into dk_acc / dv_acc, in item order
+__global__ void k_kv_reduce(Ctx c) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(c.N) * c.h_kv * kD) return;
+  const int e = int(i % kD);
+  const int g = int((i / kD) % c.h_kv);
+  const int p = int(i / (int64_t(kD) * c.h_kv));
+  const int B = c.tok_block[SSA_LEVEL_SLC][p];
+  const int key = B * c.h_kv + g;
+  const int i0 = c.kv_item_off[key], i1 = c.kv_item_off[key + 1];
+  if (i1 - i0 <= 1) return;
+  const int local = p - c.off[SSA_LEVEL_SLC][B];
+  float sk = 0.f, sv = 0.f;
+  for (int s = i0 + 1; s < i1; ++s) {
+    const int64_t idx = (int64_t(s) * c.max_fill[SSA_LEVEL_SLC] + local) * kD + e;
+    sk += c.kv_part_k[idx];
+    sv += c.kv_part_v[idx];
+  }
+  const int64_t o = (int64_t(g) * c.N + p) * kD + e;
+  c.dk_acc[o] += sk;
+  c.dv_acc[o] += sv;
+}
+
 }  // namespace
 
 bool tc_bwd_available() { return true; }
 
-size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
-  // fp16 copies: q, dO (rows), k, v (keys), K^cmp, V^cmp (n_cmp <= N)
-  return (size_t(2) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 6 * 256;
+static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T) {
+  return int64_t(n_slc) * h_kv + (int64_t(n_q) * h_kv * T + kQBlocksPerItem - 1) / kQBlocksPerItem + 1;
 }
 
-ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st) {
+size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc) {
+  // fp16 copies: q, dO (rows), k, v (keys), K^cmp, V^cmp (n_cmp <= N)
+  size_t b = (size_t(2) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 6 * 256;
+  const int64_t nkeys = int64_t(n_slc) * h_kv;
+  b += size_t(2 * nkeys + 2) * 4 + 512 + scan_ws_bytes(nkeys + 1);                  // item counts / offsets
+  b += size_t(2) * kv_items_bound(n_slc, n_q, h_kv, T) * max_fill_slc * D * 4 + 512;  // partials
+  return b;
+}
+
+ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
+  Ctx c = c_in;
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
-  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D));
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC];
+  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D, n_slc, c.n_blk[SSA_LEVEL_Q], c.T, c.max_fill[SSA_LEVEL_SLC]));
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
   __half* q16 = cw.take<__half>(qrows * kD);
   __half* do16 = cw.take<__half>(qrows * kD);
@@ -631,6 +721,13 @@ ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st) {
   __half* v16 = cw.take<__half>(krows * kD);
   __half* kc = cw.take<__half>(crows * kD);
   __half* vc = cw.take<__half>(crows * kD);
+  const int64_t nkeys = int64_t(n_slc) * c.h_kv;
+  int32_t* item_cnt = cw.take<int32_t>(nkeys + 1);
+  c.kv_item_off = cw.take<int32_t>(nkeys + 1);
+  void* scan_ws = cw.take<char>(scan_ws_bytes(nkeys + 1));
+  const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T);
+  c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
+  c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   const int64_t n = int64_t(qrows) * kD;
   k_tc_bwd_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, q16, do16, k16, v16, kc, vc);
   SSA_LAUNCH_CHECK("k_tc_bwd_prep");
@@ -649,12 +746,21 @@ ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st) {
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
-  const size_t smem = 1024 + 32768 + 32768 + 65536 + sizeof(KvSmem);
+  const size_t smem = 1024 + 32768 + kRStages * 16384 + 65536 + sizeof(KvSmem);
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
+    k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);
+    SSA_LAUNCH_CHECK("k_kv_item_count");
+    ssa_status s = exclusive_scan(item_cnt, c.kv_item_off, nkeys, c.kv_item_off + nkeys, scan_ws, st);
+    if (s != SSA_OK) return s;
     ProfScope ps("tc_bwd_kv", st);
-    k_tc_dkdv<<<dim3(c.n_blk[SSA_LEVEL_SLC], c.h_kv, 1), kThreads, smem, st>>>(c, 1, tmQ64, tmDO64, tmK128, tmV128);
+    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kThreads, smem, st>>>(c, 1, tmQ64, tmDO64, tmK128, tmV128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
+  }
+  {
+    const int64_t nk = int64_t(c.N) * c.h_kv * kD;
+    k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_kv_reduce");
   }
   {
     ProfScope ps("tc_bwd_cmp_kv", st);

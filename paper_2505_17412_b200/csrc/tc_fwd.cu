@@ -71,7 +71,7 @@ struct CmpSmem {
   uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full, p_empty, o_full,
       o_empty;
   uint32_t tmem;
-  float lse[kTile];
+  alignas(16) float lse[kTile];
   float bv[4];
   int bi[4];
   int chosen[64];
@@ -235,34 +235,35 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     for (int rt = 0; rt < n_rt; ++rt) {
       const int r = rt * kTile + tid;
       const bool rvalid = r < rows;
-      // ---- pass 1: row LSE
+      // ---- pass 1: row LSE (whole 128-key tile in registers, tree max/sum, one MUFU per element)
       float m = -1e30f, l = 0.f;
       for (int kt = 0; kt < n_kt; ++kt) {
         mbar_wait(&S->s_full[sb.idx], sb.ph);
         tc_fence_after();
         const int nv = min(kTile, nk - kt * kTile);
-        for (int c0 = 0; c0 < kTile; c0 += 32) {
-          float v[32];
-          tmem_ld32(lane_base + sb.idx * 128 + c0, v);
-          tmem_wait_ld();
-          float mx = -1e30f;
+        float v[kTile];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] = (c0 + i < nv) ? v[i] * cl2 : -1e30f;
-            mx = fmaxf(mx, v[i]);
-          }
-          const float mn = fmaxf(m, mx);
-          float s = 0.f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s += exp2f(v[i] - mn);
-          l = l * exp2f(m - mn) + s;
-          m = mn;
-        }
+        for (int c0 = 0; c0 < kTile; c0 += 32) tmem_ld32(lane_base + sb.idx * 128 + c0, v + c0);
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&S->s_empty[sb.idx]);
         sb.next();
+        if (nv < kTile) {
+#pragma unroll
+          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -1e30f;
+        }
+        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
+        const float mn = fmaxf(m, mx);
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < kTile; ++i) acc[i & 7] += ex2(fmaf(v[i], cl2, -mn));
+        const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        l = l * ex2(m - mn) + s;
+        m = mn;
       }
-      const float lse2 = rvalid ? m + log2f(l) : INFINITY;
+      const float lse2 = rvalid ? m + lg2(l) : INFINITY;
       named_bar_sync(1, 128);          // previous row tile's pass 2 finished reading S->lse
       S->lse[tid] = lse2;
       if (rvalid) c.lse[0][qrow0 + r] = lse2 * kLn2;
@@ -273,19 +274,27 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         mbar_wait(&S->s_full[sb.idx], sb.ph);
         tc_fence_after();
         uint32_t pk[64];
-        float colsum = 0.f;
+        float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c0 = 0; c0 < kTile; c0 += 32) {
           float v[32];
           tmem_ld32(lane_base + sb.idx * 128 + c0, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float p0 = kvalid ? exp2f(v[i] * cl2 - S->lse[c0 + i]) : 0.f;
-            float p1 = kvalid ? exp2f(v[i + 1] * cl2 - S->lse[c0 + i + 1]) : 0.f;
-            colsum += p0 + p1;
+          for (int i = 0; i < 32; i += 4) {
+            const float4 L = *reinterpret_cast<const float4*>(&S->lse[c0 + i]);
+            const float p0 = ex2(fmaf(v[i], cl2, -L.x)), p1 = ex2(fmaf(v[i + 1], cl2, -L.y));
+            const float p2 = ex2(fmaf(v[i + 2], cl2, -L.z)), p3 = ex2(fmaf(v[i + 3], cl2, -L.w));
+            cs[0] += p0; cs[1] += p1; cs[2] += p2; cs[3] += p3;
             pk[(c0 + i) / 2] = pack_f16(p0, p1);
+            pk[(c0 + i) / 2 + 1] = pack_f16(p2, p3);
           }
+        }
+        float colsum = (cs[0] + cs[1]) + (cs[2] + cs[3]);
+        if (!kvalid) {
+          colsum = 0.f;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) pk[i] = 0u;
         }
         tc_fence_before();
         mbar_arrive(&S->s_empty[sb.idx]);
@@ -526,7 +535,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       auto fold = [&](float m_tile) {   // add the pending O tile (relative to m_tile) into o_acc
         mbar_wait(&S->o_full[ob.idx], ob.ph);
         tc_fence_after();
-        const float a_old = exp2f(m_acc - m_tile);
+        const float a_old = ex2(m_acc - m_tile);
 #pragma unroll
         for (int c0 = 0; c0 < kD; c0 += 32) {
           float v[32];
@@ -552,7 +561,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
                   make_float4(o_acc[e] * inv, o_acc[e + 1] * inv, o_acc[e + 2] * inv, o_acc[e + 3] * inv);
             o_acc[e] = o_acc[e + 1] = o_acc[e + 2] = o_acc[e + 3] = 0.f;
           }
-          lse_slc = m + log2f(l);
+          lse_slc = m + lg2(l);
           m = -1e30f; l = 0.f; m_acc = -1e30f;
         }
         const bool first_of_branch = (j == 0 || j == n_slc_tiles);
@@ -567,21 +576,21 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         tc_fence_before();
         mbar_arrive(&S->s_empty[sb.idx]);
         sb.next();
-        float mx = -1e30f;
+        if (nv < kTile) {
 #pragma unroll
-        for (int i = 0; i < kTile; ++i) {
-          v[i] = i < nv ? v[i] * cl2 : -1e30f;
-          mx = fmaxf(mx, v[i]);
+          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -1e30f;
         }
+        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
         const float mn = fmaxf(m, mx);
-        float s = 0.f;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < kTile; i += 2) {
-          const float p0 = exp2f(v[i] - mn), p1 = exp2f(v[i + 1] - mn);
-          s += p0 + p1;
+          const float p0 = ex2(fmaf(v[i], cl2, -mn)), p1 = ex2(fmaf(v[i + 1], cl2, -mn));
+          acc[(i >> 1) & 3] += p0 + p1;
           pk[i / 2] = pack_f16(p0, p1);
         }
-        l = l * exp2f(m - mn) + s;
+        const float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        l = l * ex2(m - mn) + s;
         m = mn;
         mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
         const uint32_t pbase = smem_u32(sP + pb.idx * 32768);
@@ -603,7 +612,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         const float* os = static_cast<const float*>(c.o[1]) + row * kD;
         const float* ocm = static_cast<const float*>(c.o[0]) + row * kD;
         c.lse[1][row] = lse_slc * kLn2;
-        c.lse[2][row] = (m + log2f(l)) * kLn2;
+        c.lse[2][row] = (m + lg2(l)) * kLn2;
         const float w0 = c.gs[row * 3], w1 = c.gs[row * 3 + 1], w2 = c.gs[row * 3 + 2];
         const int t = t0 + r / c.h_s, hs = r % c.h_s;
         const int dst = c.sorted_input ? t : c.perm[t];
