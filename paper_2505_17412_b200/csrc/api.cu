@@ -226,7 +226,7 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   Carve cw(nullptr, 0);
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
-  size_t scan = scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1);
+  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q);
   *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]) + 1024;
   return SSA_OK;
 }
@@ -258,7 +258,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   Carve cw(ws, ws_bytes);
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
-  void* scan_ws = cw.take<char>(scan_ws_bytes(int64_t(d.n_slc) * d.h_kv + 1));
+  void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
   void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
   const bool bf16 = cfg->dtype == SSA_BF16;
   if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;

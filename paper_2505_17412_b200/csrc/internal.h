@@ -79,7 +79,8 @@ ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout);
 ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st);
-ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st);
+size_t inverse_csr_ws_bytes(int n_slc, int h_kv, int n_q);
+ssa_status build_inverse_csr(const Ctx& c, void* ws, cudaStream_t st);
 ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st, bool skip_q);
 ssa_status cmp_reduce(const Ctx& c, cudaStream_t st);

@@ -26,34 +26,35 @@ inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 // ---------------------------------------------------------------------------------------------
 // a2: gather caller tensors into the internal block-sorted layouts.
 // ---------------------------------------------------------------------------------------------
+// Both layouts keep the h_s heads of one (token, group) contiguous (h_s * D elements), so each thread
+// moves 16 B with coalesced reads and writes.
 template <class T>
 __global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ dst) {
-  // one thread per (p, h, element); src [N][H][D] caller order -> dst [h_kv][N][h_s][D]
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.N) * c.H * c.D;
-  if (i >= total) return;
-  int e = int(i % c.D);
-  int h = int((i / c.D) % c.H);
-  int p = int(i / (int64_t(c.D) * c.H));
-  int src_p = c.sorted_input ? p : c.perm[p];
-  int g = h / c.h_s, s = h % c.h_s;
-  dst[((int64_t(g) * c.N + p) * c.h_s + s) * c.D + e] = src[(int64_t(src_p) * c.H + h) * c.D + e];
+  const int per = c.h_s * c.D * int(sizeof(T)) / 16;     // 16-B chunks per (token, group)
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(c.N) * c.h_kv * per) return;
+  const int ch = int(i % per);
+  const int g = int((i / per) % c.h_kv);
+  const int p = int(i / (int64_t(per) * c.h_kv));
+  const int src_p = c.sorted_input ? p : c.perm[p];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t(g) * c.N + p) * c.h_s * c.D);
+  d4[ch] = s4[ch];
 }
 
 template <class T>
 __global__ void k_gather_keys(Ctx c, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ ks,
                               T* __restrict__ vs) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.N) * c.h_kv * c.D;
-  if (i >= total) return;
-  int e = int(i % c.D);
-  int g = int((i / c.D) % c.h_kv);
-  int p = int(i / (int64_t(c.D) * c.h_kv));
-  int src_p = c.sorted_input ? p : c.perm[p];
-  int64_t si = (int64_t(src_p) * c.h_kv + g) * c.D + e;
-  int64_t di = (int64_t(g) * c.N + p) * c.D + e;
-  ks[di] = k[si];
-  vs[di] = v[si];
+  const int per = c.D * int(sizeof(T)) / 16;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(c.N) * c.h_kv * per) return;
+  const int ch = int(i % per);
+  const int g = int((i / per) % c.h_kv);
+  const int p = int(i / (int64_t(per) * c.h_kv));
+  const int src_p = c.sorted_input ? p : c.perm[p];
+  const int64_t so = (int64_t(src_p) * c.h_kv + g) * c.D, dof = (int64_t(g) * c.N + p) * c.D;
+  reinterpret_cast<uint4*>(ks + dof)[ch] = reinterpret_cast<const uint4*>(k + so)[ch];
+  reinterpret_cast<uint4*>(vs + dof)[ch] = reinterpret_cast<const uint4*>(v + so)[ch];
 }
 
 template <class T>
@@ -356,16 +357,28 @@ __global__ void k_combine(Ctx c) {
 // ---------------------------------------------------------------------------------------------
 template <class T>
 __global__ void k_bwd_pre(Ctx c) {
-  int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // (g, p, s)
-  int64_t total = int64_t(c.N) * c.H;
-  if (row >= total) return;
-  const T* dos = static_cast<const T*>(c.dos);
+  // D/8 lanes per row (g, p, s), 8 elements each, reduced with shuffles
+  const int lpr = c.D / 8;
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = t / lpr;
+  const int sub = int(t % lpr);
+  const bool valid = row < int64_t(c.N) * c.H;
+  const int64_t rr = valid ? row : 0;
+  const T* dos = static_cast<const T*>(c.dos) + rr * c.D + sub * 8;
   float acc[3] = {0.f, 0.f, 0.f};
-  for (int e = 0; e < c.D; ++e) {
-    float d = ld(dos + row * c.D + e);
+  float d[8];
 #pragma unroll
-    for (int b = 0; b < 3; ++b) acc[b] += d * static_cast<const float*>(c.o[b])[row * c.D + e];
+  for (int e = 0; e < 8; ++e) d[e] = ld(dos + e);
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float4* o = reinterpret_cast<const float4*>(static_cast<const float*>(c.o[b]) + rr * c.D + sub * 8);
+    const float4 x = o[0], y = o[1];
+    acc[b] = d[0] * x.x + d[1] * x.y + d[2] * x.z + d[3] * x.w + d[4] * y.x + d[5] * y.y + d[6] * y.z + d[7] * y.w;
   }
+  for (int o = lpr / 2; o; o >>= 1)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+  if (!valid || sub != 0) return;
   const int s = int(row % c.h_s);
   const int p = int((row / c.h_s) % c.N);
   const int g = int(row / (int64_t(c.h_s) * c.N));
@@ -379,40 +392,52 @@ __global__ void k_bwd_pre(Ctx c) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Inverse selection CSR: for every (selection block B, g), the ascending list of query blocks
-// whose top-k contains B (the KV-outer backward iterates it; sorted so sums are deterministic).
+// Inverse selection CSR: for every (selection block B, g), the ascending list of query blocks whose
+// top-k contains B. Each (B, g, Q) is unique, so its dense index (B*h_kv + g)*n_q + Q marked in a
+// bitmap and ranked by popcount prefix sums IS its position in the (key, Q)-sorted list: a counting
+// sort with no comparisons and a deterministic result (same trick as the block build).
 // ---------------------------------------------------------------------------------------------
-__global__ void k_inv_count(Ctx c) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
-  if (i >= total) return;
-  int B = c.I[i];
-  int g = int((i / c.T) % c.h_kv);
-  if (B >= 0) atomicAdd(c.inv_cnt + int64_t(B) * c.h_kv + g, 1);
+__device__ __forceinline__ int32_t bit_rank(const uint32_t* bm, const int32_t* chunk_pre, int64_t bit) {
+  const int64_t w = bit >> 5, ch = bit >> 10;
+  int32_t r = chunk_pre[ch];
+  for (int64_t i = ch * 32; i < w; ++i) r += __popc(bm[i]);
+  return r + __popc(bm[w] & ((1u << (bit & 31)) - 1u));
 }
-__global__ void k_inv_fill(Ctx c, int32_t* cursor) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
-  if (i >= total) return;
-  int B = c.I[i];
-  int g = int((i / c.T) % c.h_kv);
-  int Q = int(i / (int64_t(c.T) * c.h_kv));
-  if (B >= 0) {
-    int64_t key = int64_t(B) * c.h_kv + g;
-    int pos = atomicAdd(cursor + key, 1);
-    c.inv_list[c.inv_off[key] + pos] = Q;
-  }
+__global__ void k_inv_mark(Ctx c, uint32_t* bm) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T) return;
+  const int B = c.I[i];
+  if (B < 0) return;
+  const int g = int((i / c.T) % c.h_kv);
+  const int Q = int(i / (int64_t(c.T) * c.h_kv));
+  const int64_t bit = (int64_t(B) * c.h_kv + g) * c.n_blk[SSA_LEVEL_Q] + Q;
+  atomicOr(bm + (bit >> 5), 1u << (bit & 31));
 }
-__global__ void k_inv_sort(Ctx c) {
-  int64_t key = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (key >= int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv) return;
-  int a = c.inv_off[key], e = c.inv_off[key + 1];
-  int32_t* L = c.inv_list;
-  for (int i = a + 1; i < e; ++i) {
-    int v = L[i], j = i - 1;
-    while (j >= a && L[j] > v) { L[j + 1] = L[j]; --j; }
-    L[j + 1] = v;
-  }
+__global__ void k_inv_chunk_popc(const uint32_t* __restrict__ bm, int64_t n_chunks, int32_t* __restrict__ cnt) {
+  const int64_t ch = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (ch >= n_chunks) return;
+  int v = __popc(bm[ch * 32 + (threadIdx.x & 31)]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) cnt[ch] = v;
+}
+__global__ void k_inv_place(Ctx c, const uint32_t* bm, const int32_t* chunk_pre) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T) return;
+  const int B = c.I[i];
+  if (B < 0) return;
+  const int g = int((i / c.T) % c.h_kv);
+  const int Q = int(i / (int64_t(c.T) * c.h_kv));
+  const int64_t bit = (int64_t(B) * c.h_kv + g) * c.n_blk[SSA_LEVEL_Q] + Q;
+  c.inv_list[bit_rank(bm, chunk_pre, bit)] = Q;
+}
+__global__ void k_inv_offsets(Ctx c, const uint32_t* bm, const int32_t* chunk_pre, int64_t total_bits) {
+  const int64_t key = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nkeys = int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv;
+  if (key > nkeys) return;
+  const int64_t bit = key * c.n_blk[SSA_LEVEL_Q];
+  c.inv_off[key] = bit < total_bits ? bit_rank(bm, chunk_pre, bit) : bit_rank(bm, chunk_pre, total_bits - 1) +
+                                                                       int((bm[(total_bits - 1) >> 5] >> ((total_bits - 1) & 31)) & 1u);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -844,7 +869,9 @@ ssa_status dispatch_d_bwd(const Ctx& c, cudaStream_t st) {
 }  // namespace
 
 ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout) {
-  int64_t nr = int64_t(c.N) * c.H * c.D, nk = int64_t(c.N) * c.h_kv * c.D, ng = int64_t(c.N) * c.H * 3;
+  const int esz = bf16 ? 2 : 4;
+  const int64_t nr = int64_t(c.N) * c.h_kv * (c.h_s * c.D * esz / 16), nk = int64_t(c.N) * c.h_kv * (c.D * esz / 16);
+  const int64_t ng = int64_t(c.N) * c.H * 3;
   if (bf16) {
     using T = __nv_bfloat16;
     if (with_dout) {
@@ -895,24 +922,38 @@ ssa_status simt_forward(const Ctx& c, bool bf16, cudaStream_t st, bool attention
   return bf16 ? dispatch_d_fwd<__nv_bfloat16>(c, st, attention_only) : dispatch_d_fwd<float>(c, st, attention_only);
 }
 
-ssa_status build_inverse_csr(const Ctx& c, void* scan_ws, cudaStream_t st) {
-  const int64_t nkeys = int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv;
+size_t inverse_csr_ws_bytes(int n_slc, int h_kv, int n_q) {
+  const int64_t bits = int64_t(n_slc) * h_kv * n_q + 1;
+  const int64_t n_chunks = (bits + 1023) / 1024;
+  return size_t(n_chunks) * 128 + size_t(n_chunks) * 8 + scan_ws_bytes(n_chunks) + 3 * 256;
+}
+
+ssa_status build_inverse_csr(const Ctx& c, void* ws, cudaStream_t st) {
+  const int64_t bits = int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv * c.n_blk[SSA_LEVEL_Q] + 1;
+  const int64_t n_chunks = (bits + 1023) / 1024;
   const int64_t nI = int64_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T;
-  SSA_CUDA_TRY(cudaMemsetAsync(c.inv_cnt, 0, nkeys * sizeof(int32_t), st));
-  k_inv_count<<<nblk(nI, 256), 256, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_inv_count");
-  ssa_status s = exclusive_scan(c.inv_cnt, c.inv_off, nkeys, c.inv_off + nkeys, scan_ws, st);
+  Carve cw(ws, inverse_csr_ws_bytes(c.n_blk[SSA_LEVEL_SLC], c.h_kv, c.n_blk[SSA_LEVEL_Q]));
+  uint32_t* bm = cw.take<uint32_t>(n_chunks * 32);
+  int32_t* cnt = cw.take<int32_t>(n_chunks);
+  int32_t* pre = cw.take<int32_t>(n_chunks);
+  void* scan_ws = cw.take<char>(scan_ws_bytes(n_chunks));
+  SSA_CUDA_TRY(cudaMemsetAsync(bm, 0, size_t(n_chunks) * 128, st));
+  k_inv_mark<<<nblk(nI, 256), 256, 0, st>>>(c, bm);
+  SSA_LAUNCH_CHECK("k_inv_mark");
+  k_inv_chunk_popc<<<nblk(n_chunks * 32, 256), 256, 0, st>>>(bm, n_chunks, cnt);
+  SSA_LAUNCH_CHECK("k_inv_chunk_popc");
+  ssa_status s = exclusive_scan(cnt, pre, n_chunks, nullptr, scan_ws, st);
   if (s != SSA_OK) return s;
-  SSA_CUDA_TRY(cudaMemsetAsync(c.inv_cnt, 0, nkeys * sizeof(int32_t), st));
-  k_inv_fill<<<nblk(nI, 256), 256, 0, st>>>(c, c.inv_cnt);
-  SSA_LAUNCH_CHECK("k_inv_fill");
-  k_inv_sort<<<nblk(nkeys, 128), 128, 0, st>>>(c);
-  SSA_LAUNCH_CHECK("k_inv_sort");
+  k_inv_place<<<nblk(nI, 256), 256, 0, st>>>(c, bm, pre);
+  SSA_LAUNCH_CHECK("k_inv_place");
+  const int64_t nkeys = int64_t(c.n_blk[SSA_LEVEL_SLC]) * c.h_kv;
+  k_inv_offsets<<<nblk(nkeys + 1, 256), 256, 0, st>>>(c, bm, pre, bits - 1);
+  SSA_LAUNCH_CHECK("k_inv_offsets");
   return SSA_OK;
 }
 
 ssa_status bwd_prologue(const Ctx& c, bool bf16, cudaStream_t st) {
-  int64_t rows = int64_t(c.N) * c.H;
+  int64_t rows = int64_t(c.N) * c.H * (c.D / 8);
   if (bf16) k_bwd_pre<__nv_bfloat16><<<nblk(rows, 256), 256, 0, st>>>(c);
   else k_bwd_pre<float><<<nblk(rows, 256), 256, 0, st>>>(c);
   SSA_LAUNCH_CHECK("k_bwd_pre");

@@ -431,7 +431,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   if (tid == 0) {
     mbar_init(&S->k_full, 1);
     mbar_init(&S->k_empty, 1);
-    for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[i], 1); mbar_init(&S->r_empty[i], 1); }
+    // r_full: 32 producer lanes' cp.async arrivals (row stats) + lane 0's expect_tx (Q/dO TMA)
+    for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[i], 33); mbar_init(&S->r_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
@@ -467,16 +468,18 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       int nr, br;
       while (wk.next_tile(&r0, &nr, &br)) {
         mbar_wait(&S->r_empty[rs.idx], rs.ph ^ 1u);
+        // row stats by cp.async (no register round trip; completion tracked by r_full)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = lane + 32 * h;
-          const bool v = i < nr;
-          const int64_t row = r0 + (v ? i : 0);
-          S->st_l2[rs.idx][i] = v ? c.lse[br][row] * kLog2e : INFINITY;
-          S->st_w[rs.idx][i] = v ? c.gs[row * 3 + br] : 0.f;
-          S->st_D[rs.idx][i] = v ? c.Dd[br][row] : 0.f;
+          if (i < nr) {
+            const int64_t row = r0 + i;
+            cp_async4(&S->st_l2[rs.idx][i], c.lse[br] + row);
+            cp_async4(&S->st_w[rs.idx][i], c.gs + row * 3 + br);
+            cp_async4(&S->st_D[rs.idx][i], c.Dd[br] + row);
+          }
         }
-        __syncwarp();
+        cp_async_mbar_arrive_noinc(&S->r_full[rs.idx]);
         if (lane == 0) {
           uint8_t* st = sR + rs.idx * 16384;
           mbar_expect_tx(&S->r_full[rs.idx], 16384);
@@ -591,11 +594,17 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         uint32_t pw[kRT / 2], ds[kRT / 2];
 #pragma unroll
         for (int i = 0; i < kRT; i += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(L2 + i);
+          const float4 l4 = *reinterpret_cast<const float4*>(L2 + i);   // natural-log LSE
           const float4 w4 = *reinterpret_cast<const float4*>(W + i);
           const float4 d4 = *reinterpret_cast<const float4*>(DD + i);
-          const float p0 = ex2(fmaf(s[i], cl2, -l4.x)), p1 = ex2(fmaf(s[i + 1], cl2, -l4.y));
-          const float p2 = ex2(fmaf(s[i + 2], cl2, -l4.z)), p3 = ex2(fmaf(s[i + 3], cl2, -l4.w));
+          float p0 = ex2(fmaf(s[i], cl2, -l4.x * kLog2e)), p1 = ex2(fmaf(s[i + 1], cl2, -l4.y * kLog2e));
+          float p2 = ex2(fmaf(s[i + 2], cl2, -l4.z * kLog2e)), p3 = ex2(fmaf(s[i + 3], cl2, -l4.w * kLog2e));
+          if (nr < kRT) {          // rows past the range: stats were not loaded
+            p0 = i < nr ? p0 : 0.f;
+            p1 = i + 1 < nr ? p1 : 0.f;
+            p2 = i + 2 < nr ? p2 : 0.f;
+            p3 = i + 3 < nr ? p3 : 0.f;
+          }
           pw[i / 2] = pack_f16(p0 * w4.x, p1 * w4.y);
           pw[i / 2 + 1] = pack_f16(p2 * w4.z, p3 * w4.w);
           ds[i / 2] = pack_f16(p0 * fmaf(w4.x, dp[i], -d4.x), p1 * fmaf(w4.y, dp[i + 1], -d4.y));
