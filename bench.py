@@ -123,15 +123,9 @@ def workload(config: str, rank: int, world: int):
     cfg = CONFIGS[config]
     shapes = list(cfg["shapes"])
     if config == "C4" and world > 1:
-        order = sorted(range(len(shapes)), key=lambda i: -sphere_shell(*shapes[i]).shape[0])
-        loads = [0] * world
-        mine = []
-        for i in order:
-            r = int(np.argmin(loads))
-            loads[r] += sphere_shell(*shapes[i]).shape[0] ** 2
-            if r == rank:
-                mine.append(shapes[i])
-        shapes = mine
+        from paper_2505_17412_b200.shard import rank_items
+        n_tok = [sphere_shell(*s).shape[0] for s in shapes]
+        shapes = [shapes[i] for i in rank_items(n_tok, rank, world)]
     shells = [sphere_shell(*s) for s in shapes]
     return cfg, batch_coords(shells), (cfg["G"],) * 3, len(shells)
 
@@ -213,10 +207,8 @@ def main():
         if n:
             ktimes[kn] = (t, n)
     ssa.profile_reset()
-    if world > 1:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    from paper_2505_17412_b200.shard import max_over_ranks
+    total_ms = max_over_ranks(total_ms, dev)
     ms_per_step = total_ms / args.steps
     shapes_per_step = batch * world
     value = ms_per_step / shapes_per_step
@@ -284,10 +276,7 @@ def main():
                 e_times.append((e0, e1))
         torch.cuda.synchronize(dev)
         e_ms = sum(a.elapsed_time(b) for a, b in e_times) / len(e_times)
-        if world > 1:
-            tt = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_ms = float(tt.item())
+        e_ms = max_over_ranks(e_ms, dev)
         e2e = {"value": round(e_ms / shapes_per_step, 4), "unit": UNIT, "h2d_bytes_per_step": int(bi),
                "d2h_bytes_per_step": int(bo)}
 
