@@ -246,8 +246,16 @@ def main():
         else:
             peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # fp32 FMA peak
             bound = "alu"
+        traffic = None
+        import glob
+        for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_*.json")))[-1:]:
+            tj = json.load(open(tf))
+            key = "k_" + dom if not dom.startswith("k_") else dom
+            for kname, val in tj.items():
+                if kname.endswith(key.replace("tc_cmp_fwd", "tc_cmp_fwd")):
+                    traffic = {"dram_bytes_per_launch": val, "source": os.path.relpath(tf, ROOT)}
         roofline = {"kernel": dom, "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1),
-                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                     "peak_source": peak_src + (" bf16_tflops_sustained" if bound == "tensor" else
                                                " fp32 FMA: 148 SM x 128 FMA/clk x 2 x sm_max_mhz"),
                     "algorithmic_flops_per_launch": flops, "avg_launch_ms": round(t / n, 4),
