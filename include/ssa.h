@@ -170,7 +170,7 @@ ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const void* q, c
  *   idx      int32 [n_blocks[Q], h_kv, top_k]  selected selection-block ids (global), -1 padded
  *   scores   fp32 [n_blocks[Q], h_kv, max_blocks_per_batch[SLC]] (NULL unless SSA_SAVE_SCORES);
  *            row (Q,g) holds the Eq. 8 score of the selection blocks of Q's batch item (local index)
- *   o_branch, lse_branch: fp32 branch outputs / LSEs, internal layout [h_kv][n][h_s][d] / [h_kv][n][h_s]
+ *   o_branch, lse_branch: fp32 branch outputs / log2-domain LSEs (log2 sum 2^(scale q.k log2 e)), layout [h_kv][n][h_s][d] / [h_kv][n][h_s]
  *            in plan (sorted) order, branch 0=cmp 1=slc 2=win.
  * ----------------------------------------------------------------------------------------------*/
 typedef struct {

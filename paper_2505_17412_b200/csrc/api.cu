@@ -86,7 +86,8 @@ bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
 // saved state: kc, vc, o[3], lse[3], I, scores
 void carve_saved(Carve& c, const Dims& d, const ssa_attn_cfg* cfg, Ctx* x) {
   const int64_t rows = d.N * d.H;
-  // pooled K/V and branch outputs are kept in fp32 (precision of the saved state)
+  // pooled K/V and branch outputs are kept in fp32 (precision of the saved state);
+  // LSEs are stored in the log2 domain (what the kernels consume)
   x->kc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
   x->vc = c.take<float>(size_t(d.h_kv) * d.n_cmp * d.D);
   for (int b = 0; b < 3; ++b) x->o[b] = c.take<float>(size_t(rows) * d.D);

@@ -56,7 +56,7 @@ struct Ctx {
   float* gs;                      // [h_kv][N][h_s][3]
   void *kc, *vc;                  // [h_kv][n_cmp][D]
   void* o[3];                     // branch outputs (rows layout, dtype)
-  float* lse[3];                  // [h_kv][N][h_s]
+  float* lse[3];                  // [h_kv][N][h_s], log2 domain: log2 sum_j 2^(scale log2e q.k_j)
   int32_t* I;                     // [n_q][h_kv][T]
   float* scores;                  // [n_q][h_kv][max_slc_b] or null
   // backward scratch

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kRows) k_cmp_fwd(Ctx c) {
       float* oc = static_cast<float*>(c.o[0]);
 #pragma unroll
       for (int e = 0; e < D; ++e) oc[(row_base + r) * D + e] = o[e];
-      c.lse[0][row_base + r] = lse2 * kLn2;
+      c.lse[0][row_base + r] = lse2;   // saved LSEs are log2-domain
     }
   }
   __syncthreads();
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kRows) k_attn_fwd(Ctx c, int mode) {
       float* ob = static_cast<float*>(c.o[br]);
 #pragma unroll
       for (int e = 0; e < D; ++e) ob[(row_base + r) * D + e] = o[e] * inv;
-      c.lse[br][row_base + r] = (m + log2f(l)) * kLn2;
+      c.lse[br][row_base + r] = m + log2f(l);
     }
   }
 }
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kRows) k_dq(Ctx c) {
       const float* kcf = static_cast<const float*>(c.kc);
       const float* vcf = static_cast<const float*>(c.vc);
       const int64_t kbase = int64_t(g) * (br == 0 ? c.n_blk[SSA_LEVEL_CMP] : c.N);
-      const float lse2 = c.lse[br][row] * kLog2e;
+      const float lse2 = c.lse[br][row];
       const float w = c.gs[row * 3 + br];
       const float Dv = c.Dd[br][row];
       for (int k0 = seg_s[sgi]; k0 < seg_e[sgi]; k0 += kKT) {
@@ -567,7 +567,7 @@ __device__ __forceinline__ void stage_rows(const Ctx& c, int br, int64_t row0, i
     Ot[i] = ld(dos + row0 * D + i);
   }
   for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-    st_lse2[i] = c.lse[br][row0 + i] * kLog2e;
+    st_lse2[i] = c.lse[br][row0 + i];
     st_w[i] = c.gs[(row0 + i) * 3 + br];
     st_D[i] = c.Dd[br][row0 + i];
   }
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(128) k_win_bwd(Ctx c) {
       dO[e] = ld(dos + row * D + e);
       dq[e] = 0.f;
     }
-    const float lse2 = c.lse[2][row] * kLog2e, w = c.gs[row * 3 + 2], Dv = c.Dd[2][row];
+    const float lse2 = c.lse[2][row], w = c.gs[row * 3 + 2], Dv = c.Dd[2][row];
     for (int k0 = t0; k0 < t1; k0 += kRT) {
       const int nt = min(kRT, t1 - k0);
       __syncthreads();

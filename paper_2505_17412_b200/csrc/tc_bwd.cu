@@ -227,7 +227,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       float lse2[3], w[3], Dv[3];
 #pragma unroll
       for (int br = 0; br < 3; ++br) {
-        lse2[br] = rvalid ? c.lse[br][row] * kLog2e : INFINITY;
+        lse2[br] = rvalid ? c.lse[br][row] : INFINITY;
         w[br] = c.gs[row * 3 + br];
         Dv[br] = c.Dd[br][row];
       }
@@ -294,14 +294,15 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
 // ================================================================================================
 // dK / dV (KV-outer)
 // ================================================================================================
-constexpr int kRT = 64;                  // rows per tile: 2 x (S^T 64 + dP^T 64) + dK 64 + dV 64 = 384
-constexpr int kRStages = 4;              // row-tile (Q, dO, stats) pipeline depth
+constexpr int kRT = 64;                  // rows per tile: S^T 64 + dP^T 64 + dK 64 + dV 64 = 256 TMEM cols
+constexpr int kRStages = 2;              // row-tile (Q, dO, stats) pipeline depth
 constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
+// Two CTAs per SM (256 TMEM columns and ~100 KB shared memory each): the second CTA's softmax warps
+// hide the first one's dependency and barrier latencies (one softmax warp per SMSP is not enough).
 struct KvSmem {
-  uint64_t k_full, k_empty, r_full[kRStages], r_empty[kRStages], s_full[2], s_empty[2], p_full[2], p_empty[2],
-      acc_full, acc_empty;
+  uint64_t k_full, k_empty, r_full[kRStages], r_empty[kRStages], s_full, s_empty, p_full, p_empty, acc_full,
+      acc_empty;
   uint32_t tmem;
-  int item_ok;
   alignas(16) float st_l2[kRStages][kRT];
   alignas(16) float st_w[kRStages][kRT];
   alignas(16) float st_D[kRStages][kRT];
@@ -399,7 +400,7 @@ struct RowWalk {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
           __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -407,8 +408,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   uint8_t* sK = sm;                       // 16 KB
   uint8_t* sV = sm + 16384;               // 16 KB
   uint8_t* sR = sm + 32768;               // kRStages x {Q 8 KB, dO 8 KB}
-  uint8_t* sP = sR + kRStages * 16384;    // 2 x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
-  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 65536);
+  uint8_t* sP = sR + kRStages * 16384;    // {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
+  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 32768);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Item it;
@@ -433,18 +434,16 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     mbar_init(&S->k_empty, 1);
     // r_full: 32 producer lanes' cp.async arrivals (row stats) + lane 0's expect_tx (Q/dO TMA)
     for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[i], 33); mbar_init(&S->r_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&S->s_full[i], 1);
-      mbar_init(&S->s_empty[i], 128);
-      mbar_init(&S->p_full[i], 128);
-      mbar_init(&S->p_empty[i], 1);
-    }
+    mbar_init(&S->s_full, 1);
+    mbar_init(&S->s_empty, 128);
+    mbar_init(&S->p_full, 128);
+    mbar_init(&S->p_empty, 1);
     mbar_init(&S->acc_full, 1);
     mbar_init(&S->acc_empty, 128);
     fence_barrier_init();
   }
   if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmK); tma_prefetch(&tmV); }
-  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  if (warp == 5) tmem_alloc<256>(&S->tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -495,7 +494,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     const uint32_t idS = idesc_f16(128, kRT, false, false);    // S^T = K Q^T, dP^T = V dO^T
     const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-    Ring rs(kRStages), sb(2), pb(2);
+    Ring rs(kRStages), sb(1), pb(1);
     uint32_t kph = 0, aph = 0;
     int n_tiles = 0;
     {
@@ -512,18 +511,17 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       Ring rs_a = rs;
       auto issue_s = [&]() {
         mbar_wait(&S->r_full[rs.idx], rs.ph);
-        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+        mbar_wait(&S->s_empty, sb.ph ^ 1u);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t aq = smem_u32(sR + rs.idx * 16384), ado = aq + 8192;
-          const uint32_t d = tmem + sb.idx * 128;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(aK + k * 32, 0, 1024), desc_sw128(aq + k * 32, 0, 1024), idS, k > 0);
+            umma_bf16(tmem, desc_sw128(aK + k * 32, 0, 1024), desc_sw128(aq + k * 32, 0, 1024), idS, k > 0);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(d + kRT, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
-          umma_commit(&S->s_full[sb.idx]);
+            umma_bf16(tmem + kRT, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
+          umma_commit(&S->s_full);
         }
         __syncwarp();
         rs.next();
@@ -532,21 +530,21 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       if (n_tiles > 0) issue_s();
       mbar_wait(&S->acc_empty, aph ^ 1u);
       for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s();
-        mbar_wait(&S->p_full[pb.idx], pb.ph);
+        if (j + 1 < n_tiles) issue_s();      // S^T of the next tile as soon as the softmax has read this one
+        mbar_wait(&S->p_full, pb.ph);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ap = smem_u32(sP + pb.idx * 32768), ads = ap + 16384;
+          const uint32_t ap = smem_u32(sP), ads = ap + 16384;
           const uint32_t aq = smem_u32(sR + rs_a.idx * 16384), ado = aq + 8192;
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_bf16(tmem + 448, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
+            umma_bf16(tmem + 192, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
                       (j > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_bf16(tmem + 384, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
+            umma_bf16(tmem + 128, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
                       (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&S->p_empty[pb.idx]);
+          umma_commit(&S->p_empty);
           umma_commit(&S->r_empty[rs_a.idx]);
         }
         __syncwarp();
@@ -564,7 +562,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     // ------------------------------------------------ softmax: thread = key (TMEM lane)
     const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
     const float cl2 = c.scale * kLog2e;
-    Ring rs(kRStages), sb(2), pb(2);
+    Ring rs(kRStages), sb(1), pb(1);
     uint32_t aph = 0;
     for (int kt = 0; kt < n_kt; ++kt) {
       const int key = kt * 128 + tid;
@@ -576,66 +574,71 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       int n_tiles = 0;
       while (wk.next_tile(&r0, &nr, &br)) {
         mbar_wait(&S->r_full[rs.idx], rs.ph);      // row stats of this stage are visible
-        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        mbar_wait(&S->s_full, sb.ph);
         tc_fence_after();
-        const float* L2 = S->st_l2[rs.idx];
-        const float* W = S->st_w[rs.idx];
-        const float* DD = S->st_D[rs.idx];
-        float s[kRT], dp[kRT];
+        const uint32_t sbase = smem_u32(&S->st_l2[rs.idx][0]);
+        const uint32_t wbase = smem_u32(&S->st_w[rs.idx][0]);
+        const uint32_t dbase = smem_u32(&S->st_D[rs.idx][0]);
+        const uint32_t pbase = smem_u32(sP);
 #pragma unroll
-        for (int c0 = 0; c0 < kRT; c0 += 32) {
-          tmem_ld32(lane_base + sb.idx * 128 + c0, s + c0);
-          tmem_ld32(lane_base + sb.idx * 128 + kRT + c0, dp + c0);
-        }
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&S->s_empty[sb.idx]);
-        sb.next();
-        uint32_t pw[kRT / 2], ds[kRT / 2];
-#pragma unroll
-        for (int i = 0; i < kRT; i += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(L2 + i);   // natural-log LSE
-          const float4 w4 = *reinterpret_cast<const float4*>(W + i);
-          const float4 d4 = *reinterpret_cast<const float4*>(DD + i);
-          float p0 = ex2(fmaf(s[i], cl2, -l4.x * kLog2e)), p1 = ex2(fmaf(s[i + 1], cl2, -l4.y * kLog2e));
-          float p2 = ex2(fmaf(s[i + 2], cl2, -l4.z * kLog2e)), p3 = ex2(fmaf(s[i + 3], cl2, -l4.w * kLog2e));
-          if (nr < kRT) {          // rows past the range: stats were not loaded
-            p0 = i < nr ? p0 : 0.f;
-            p1 = i + 1 < nr ? p1 : 0.f;
-            p2 = i + 2 < nr ? p2 : 0.f;
-            p3 = i + 3 < nr ? p3 : 0.f;
+        for (int half = 0; half < 2; ++half) {   // 32 rows at a time keeps the register file in budget
+          float s[32], dp[32];
+          tmem_ld32(lane_base + half * 32, s);
+          tmem_ld32(lane_base + kRT + half * 32, dp);
+          tmem_wait_ld();
+          if (half == 1) {
+            tc_fence_before();
+            mbar_arrive(&S->s_empty);            // S^T / dP^T fully read: the next tile's MMA may start
           }
-          pw[i / 2] = pack_f16(p0 * w4.x, p1 * w4.y);
-          pw[i / 2 + 1] = pack_f16(p2 * w4.z, p3 * w4.w);
-          ds[i / 2] = pack_f16(p0 * fmaf(w4.x, dp[i], -d4.x), p1 * fmaf(w4.y, dp[i + 1], -d4.y));
-          ds[i / 2 + 1] = pack_f16(p2 * fmaf(w4.z, dp[i + 2], -d4.z), p3 * fmaf(w4.w, dp[i + 3], -d4.w));
+          uint32_t pw[16], ds[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const int rr = half * 32 + i;
+            float4 l4, w4, d4;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w) : "r"(sbase + rr * 4));
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w4.x), "=f"(w4.y), "=f"(w4.z), "=f"(w4.w) : "r"(wbase + rr * 4));
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w) : "r"(dbase + rr * 4));
+            float p0 = ex2(fmaf(s[i], cl2, -l4.x)), p1 = ex2(fmaf(s[i + 1], cl2, -l4.y));
+            float p2 = ex2(fmaf(s[i + 2], cl2, -l4.z)), p3 = ex2(fmaf(s[i + 3], cl2, -l4.w));
+            if (nr < kRT) {          // rows past the range: stats were not loaded
+              p0 = rr < nr ? p0 : 0.f;
+              p1 = rr + 1 < nr ? p1 : 0.f;
+              p2 = rr + 2 < nr ? p2 : 0.f;
+              p3 = rr + 3 < nr ? p3 : 0.f;
+            }
+            pw[i / 2] = pack_f16(p0 * w4.x, p1 * w4.y);
+            pw[i / 2 + 1] = pack_f16(p2 * w4.z, p3 * w4.w);
+            ds[i / 2] = pack_f16(p0 * fmaf(w4.x, dp[i], -d4.x), p1 * fmaf(w4.y, dp[i + 1], -d4.y));
+            ds[i / 2 + 1] = pack_f16(p2 * fmaf(w4.z, dp[i + 2], -d4.z), p3 * fmaf(w4.w, dp[i + 3], -d4.w));
+          }
+          if (!kvalid) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pw[i] = ds[i] = 0u;
+          }
+          if (half == 0) mbar_wait(&S->p_empty, pb.ph ^ 1u);   // previous tile's dV/dK MMAs are done
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            st_shared_v4(pbase + sw128(tid, half * 4 + ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
+            st_shared_v4(pbase + 16384 + sw128(tid, half * 4 + ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2],
+                         ds[4 * ch + 3]);
+          }
         }
+        sb.next();
         rs.next();
-        if (!kvalid) {
-#pragma unroll
-          for (int i = 0; i < kRT / 2; ++i) pw[i] = ds[i] = 0u;
-        }
-        mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
-        const uint32_t base = smem_u32(sP + pb.idx * 32768);
-#pragma unroll
-        for (int ch = 0; ch < kRT / 8; ++ch) {
-          st_shared_v4(base + sw128(tid, ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
-          st_shared_v4(base + 16384 + sw128(tid, ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2], ds[4 * ch + 3]);
-        }
         fence_proxy_async_smem();
-        mbar_arrive(&S->p_full[pb.idx]);
+        mbar_arrive(&S->p_full);
         pb.next();
         ++n_tiles;
       }
-      // accumulators: dK at 384, dV at 448
+      // accumulators: dK at 128, dV at 192
       mbar_wait(&S->acc_full, aph);
       aph ^= 1u;
       tc_fence_after();
       float dk[64], dv[64];
-      tmem_ld32(lane_base + 384, dk);
-      tmem_ld32(lane_base + 384 + 32, dk + 32);
-      tmem_ld32(lane_base + 448, dv);
-      tmem_ld32(lane_base + 448 + 32, dv + 32);
+      tmem_ld32(lane_base + 128, dk);
+      tmem_ld32(lane_base + 128 + 32, dk + 32);
+      tmem_ld32(lane_base + 192, dv);
+      tmem_ld32(lane_base + 192 + 32, dv + 32);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&S->acc_empty);
@@ -668,7 +671,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 5) tmem_dealloc<256>(tmem);
 }
 
 // raw-key work items: ceil(len / kQBlocksPerItem) (at least 1, for the window) per (block, g)
@@ -755,7 +758,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
-  const size_t smem = 1024 + 32768 + kRStages * 16384 + 65536 + sizeof(KvSmem);
+  const size_t smem = 1024 + 32768 + kRStages * 16384 + 32768 + sizeof(KvSmem);
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
     k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);

@@ -266,7 +266,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       const float lse2 = rvalid ? m + lg2(l) : INFINITY;
       named_bar_sync(1, 128);          // previous row tile's pass 2 finished reading S->lse
       S->lse[tid] = lse2;
-      if (rvalid) c.lse[0][qrow0 + r] = lse2 * kLn2;
+      if (rvalid) c.lse[0][qrow0 + r] = lse2;   // saved LSEs are log2-domain
       named_bar_sync(1, 128);
       // ---- pass 2: thread = key; P^T row -> smem; exact fp32 column sums
       for (int kt = 0; kt < n_kt; ++kt) {
@@ -611,8 +611,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         float* ow = static_cast<float*>(c.o[2]) + row * kD;
         const float* os = static_cast<const float*>(c.o[1]) + row * kD;
         const float* ocm = static_cast<const float*>(c.o[0]) + row * kD;
-        c.lse[1][row] = lse_slc * kLn2;
-        c.lse[2][row] = (m + lg2(l)) * kLn2;
+        c.lse[1][row] = lse_slc;
+        c.lse[2][row] = m + lg2(l);
         const float w0 = c.gs[row * 3], w1 = c.gs[row * 3 + 1], w2 = c.gs[row * 3 + 2];
         const int t = t0 + r / c.h_s, hs = r % c.h_s;
         const int dst = c.sorted_input ? t : c.perm[t];

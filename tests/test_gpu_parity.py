@@ -45,7 +45,7 @@ def _check_all(inp, kw, flags=0, backward=True, pe=None, expect_tc=None):
         from gpu_util import internal_to_orig
         o, lse = r["saved"].branch(b)
         errs["o_" + name] = rel_err(internal_to_orig(o, r["perm"]), f.o[name], u)
-        lg = internal_to_orig(lse, r["perm"])
+        lg = internal_to_orig(lse, r["perm"]) * math.log(2.0)   # saved LSEs are log2-domain
         errs["lse_" + name] = float(np.max(np.abs(lg - f.lse[name]))) / 10.0   # LSE: absolute, vs tol*10
     if backward:
         for name, g, ref in zip(("dq", "dk", "dv", "dgates"), (r["dq"], r["dk"], r["dv"], r["dgates"]), grads):
