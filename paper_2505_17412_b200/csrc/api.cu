@@ -105,10 +105,12 @@ void carve_inputs(Carve& c, const Dims& d, Ctx* x, bool with_dout) {
   x->dos = with_dout ? c.take<char>(size_t(rows) * d.D * d.esz) : nullptr;
 }
 
+// Row chunks of the compressed-key KV-outer backward: ~16 waves of 296 CTAs (148 SMs x 2 CTAs), so
+// the last partial wave costs a few percent instead of up to a third (long CTAs, few waves).
 int pick_chunks(const Plan* p, int h_kv) {
   int tiles = std::max(1, p->n_cmp_tiles * h_kv);
-  int n = (4 * 148 + tiles - 1) / tiles;
-  return std::min(64, std::max(1, n));
+  int n = (16 * 296 + tiles - 1) / tiles;
+  return std::min(128, std::max(1, n));
 }
 
 void carve_bwd(Carve& c, const Dims& d, const Plan* p, Ctx* x) {

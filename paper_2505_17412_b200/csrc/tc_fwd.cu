@@ -65,30 +65,38 @@ struct Ring {
 };
 
 // ================================================================================================
-// compression attention + scores + top-k
+// compression attention + scores + top-k (two softmax warpgroups, FA4-style ping-pong)
 // ================================================================================================
+// 320 threads: warps 0-3 = softmax warpgroup 0, warps 4-7 = softmax warpgroup 1 (each owns one
+// 128-row tile of a row-tile pair and TMEM lanes 0-127 of its own S / O columns), warp 8 = TMA
+// producer, warp 9 = MMA issuer + TMEM owner (register budget 168/thread: softmax works on 64 columns
+// at a time). Both row tiles share every K/V tile load (half the L2
+// traffic of one tile per CTA) and one P^T buffer that the two warpgroups fill alternately.
+constexpr int kCmpThreads = 320;
+constexpr int kCmpStages = 2;
 struct CmpSmem {
-  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full, p_empty, o_full,
-      o_empty;
+  uint64_t q_full, q_empty, kv_full[kCmpStages], kv_empty[kCmpStages];
+  uint64_t s_full[2], s_empty[2], p_full[2], p_free[2], o_full[2], o_empty[2];
   uint32_t tmem;
-  alignas(16) float lse[kTile];
-  float bv[4];
-  int bi[4];
+  alignas(16) float lse[2][kTile];
+  float bv[8];
+  int bi[8];
   int chosen[64];
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kCmpThreads, 1)
 k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmKh,
              __grid_constant__ const CUtensorMap tmKl, __grid_constant__ const CUtensorMap tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                                  // 16 KB
-  uint8_t* sKV = sm + 16384;                         // kStages x {Khi, Klo, V} 48 KB
-  uint8_t* sP = sKV + kStages * 49152;               // 32 KB, P^T: 2 row blocks x [128 keys][128 B]
+  uint8_t* sQ = sm;                                  // 2 x 16 KB (row tiles a, b)
+  uint8_t* sKV = sm + 32768;                         // kCmpStages x {Khi, Klo, V} 48 KB
+  uint8_t* sP = sKV + kCmpStages * 49152;            // 32 KB, P^T: 2 row blocks x [128 keys][128 B]
   CmpSmem* S = reinterpret_cast<CmpSmem*>(sP + 32768);
-  float* sc_cmp = reinterpret_cast<float*>(S + 1);   // [max_cmp_b]
   const Ctx& c = a.c;
-  float* sc_slc = sc_cmp + c.max_cmp_b;              // [max_slc_b]
+  float* sc_cmp0 = reinterpret_cast<float*>(S + 1);  // [max_cmp_b] per warpgroup
+  float* sc_cmp1 = sc_cmp0 + c.max_cmp_b;
+  float* sc_slc = sc_cmp1 + c.max_cmp_b;             // [max_slc_b]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
@@ -98,38 +106,44 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   const int s0 = c.bb[SSA_LEVEL_SLC][b], ns = c.bb[SSA_LEVEL_SLC][b + 1] - s0;
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + kTile - 1) / kTile, n_kt = (nk + kTile - 1) / kTile;
+  const int n_pair = (n_rt + 1) / 2;
   const int qrow0 = (g * c.N + t0) * c.h_s;
   const int krow0 = g * c.n_blk[SSA_LEVEL_CMP] + c0;
 
   if (tid == 0) {
     mbar_init(&S->q_full, 1);
     mbar_init(&S->q_empty, 1);
-    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&S->s_full[i], 1); mbar_init(&S->s_empty[i], 128); }
-    mbar_init(&S->p_full, 128);
-    mbar_init(&S->p_empty, 1);
-    mbar_init(&S->o_full, 1);
-    mbar_init(&S->o_empty, 128);
+    for (int i = 0; i < kCmpStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S->s_full[i], 1);
+      mbar_init(&S->s_empty[i], 128);
+      mbar_init(&S->p_full[i], 128);
+      mbar_init(&S->p_free[i], 1);
+      mbar_init(&S->o_full[i], 1);
+      mbar_init(&S->o_empty[i], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmKh); tma_prefetch(&tmKl); tma_prefetch(&tmV); }
-  if (warp == 5) tmem_alloc<512>(&S->tmem);
-  for (int i = tid; i < nk; i += kThreads) sc_cmp[i] = 0.f;
+  if (warp == 8 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmKh); tma_prefetch(&tmKl); tma_prefetch(&tmV); }
+  if (warp == 9) tmem_alloc<512>(&S->tmem);
+  for (int i = tid; i < nk; i += kCmpThreads) { sc_cmp0[i] = 0.f; sc_cmp1[i] = 0.f; }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ---------------------------------------------------------------- TMA producer
-    Ring kv(kStages);
+    Ring kv(kCmpStages);
     uint32_t qph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool bval = 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_empty, qph ^ 1u);
       qph ^= 1u;
       if (lane == 0) {
-        mbar_expect_tx(&S->q_full, 16384);
-        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * kTile);
+        mbar_expect_tx(&S->q_full, bval ? 32768u : 16384u);
+        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + 2 * pr * kTile);
+        if (bval) tma_load_2d(sQ + 16384, &tmQ, &S->q_full, 0, qrow0 + (2 * pr + 1) * kTile);
       }
       for (int pass = 1; pass <= 2; ++pass) {
         for (int kt = 0; kt < n_kt; ++kt) {
@@ -146,204 +160,229 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idS = idesc_bf16(128, 128, false, false);
     const uint32_t idO = idesc_f16(128, 64, true, true);
-    const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-    Ring kv(kStages), sb(2);
-    uint32_t qph = 0, pph = 0, oph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    const uint32_t aP = smem_u32(sP);
+    Ring kv(kCmpStages), sb0(1), sb1(1);
+    uint32_t qph = 0, pph[2] = {0, 0}, oph[2] = {0, 0};
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool bval = 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_full, qph);
       qph ^= 1u;
       tc_fence_after();
-      // pass 1: S = Q (Khi + Klo)^T
-      for (int kt = 0; kt < n_kt; ++kt) {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
+      // S (pass 1) or S^T (pass 2) for warpgroup w from the current K stage
+      auto issue_s = [&](int w, uint32_t st, bool transposed) {
+        Ring& sb = w ? sb1 : sb0;
+        mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t st = smem_u32(sKV + kv.idx * 49152);
-          const uint32_t d = tmem + sb.idx * 128;
+          const uint32_t aq = smem_u32(sQ + w * 16384);
+          const uint32_t d = tmem + w * 128;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(st + k * 32, 0, 1024), idS, k > 0);
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t ak = st + h * 16384;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(st + 16384 + k * 32, 0, 1024), idS, 1);
-          umma_commit(&S->s_full[sb.idx]);
-          umma_commit(&S->kv_empty[kv.idx]);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t dq = desc_sw128(aq + k * 32, 0, 1024), dk = desc_sw128(ak + k * 32, 0, 1024);
+              umma_bf16(d, transposed ? dk : dq, transposed ? dq : dk, idS, (h | k) ? 1u : 0u);
+            }
+          }
+          umma_commit(&S->s_full[w]);
         }
         __syncwarp();
-        kv.next();
         sb.next();
-      }
-      // pass 2: S^T = (Khi + Klo) Q^T, then O += P V (P^T in smem, MN-major A)
-      Ring kv_pv = kv;   // stage of the tile whose PV is pending
-      auto issue_st = [&](int kt_unused) {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t st = smem_u32(sKV + kv.idx * 49152);
-          const uint32_t d = tmem + sb.idx * 128;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(st + k * 32, 0, 1024), desc_sw128(aQ + k * 32, 0, 1024), idS, k > 0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(st + 16384 + k * 32, 0, 1024), desc_sw128(aQ + k * 32, 0, 1024), idS, 1);
-          umma_commit(&S->s_full[sb.idx]);
-        }
-        __syncwarp();
-        kv.next();
-        sb.next();
-        (void)kt_unused;
       };
-      issue_st(0);
-      mbar_wait(&S->o_empty, oph ^ 1u);
-      oph ^= 1u;
+      // pass 1
       for (int kt = 0; kt < n_kt; ++kt) {
-        if (kt + 1 < n_kt) issue_st(kt + 1);
-        mbar_wait(&S->p_full, pph);
-        pph ^= 1u;
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sv = smem_u32(sKV + kv_pv.idx * 49152 + 32768);
+        const uint32_t st = smem_u32(sKV + kv.idx * 49152);
+        issue_s(0, st, false);
+        if (bval) issue_s(1, st, false);
+        if (lane == 0) umma_commit(&S->kv_empty[kv.idx]);
+        __syncwarp();
+        kv.next();
+      }
+      // pass 2
+      Ring kv_pv = kv;
+      auto issue_st = [&]() {
+        mbar_wait(&S->kv_full[kv.idx], kv.ph);
+        tc_fence_after();
+        const uint32_t st = smem_u32(sKV + kv.idx * 49152);
+        issue_s(0, st, true);
+        if (bval) issue_s(1, st, true);
+        kv.next();
+      };
+      issue_st();
+      for (int w = 0; w < 2; ++w) {
+        if (w == 1 && !bval) break;
+        mbar_wait(&S->o_empty[w], oph[w] ^ 1u);
+        oph[w] ^= 1u;
+      }
+      for (int kt = 0; kt < n_kt; ++kt) {
+        if (kt + 1 < n_kt) issue_st();
+        const uint32_t sv = smem_u32(sKV + kv_pv.idx * 49152 + 32768);
+        for (int w = 0; w < 2; ++w) {
+          if (w == 1 && !bval) break;
+          mbar_wait(&S->p_full[w], pph[w]);
+          pph[w] ^= 1u;
+          tc_fence_after();
+          if (lane == 0) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            umma_bf16(tmem + 256, desc_sw128(aP + k * 2048, 16384, 1024), desc_sw128(sv + k * 2048, 0, 1024), idO,
-                      (kt > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&S->p_empty);
-          umma_commit(&S->kv_empty[kv_pv.idx]);
+            for (int k = 0; k < 8; ++k)
+              umma_bf16(tmem + 256 + w * 64, desc_sw128(aP + k * 2048, 16384, 1024), desc_sw128(sv + k * 2048, 0, 1024),
+                        idO, (kt > 0 || k > 0) ? 1u : 0u);
+            // the shared P^T buffer passes to the other warpgroup (or back, when b is absent)
+            umma_commit(&S->p_free[(w == 0 && bval) ? 1 : 0]);
+          }
+          __syncwarp();
         }
+        if (lane == 0) umma_commit(&S->kv_empty[kv_pv.idx]);
         __syncwarp();
         kv_pv.next();
       }
       if (lane == 0) {
-        umma_commit(&S->o_full);
+        umma_commit(&S->o_full[0]);
+        if (bval) umma_commit(&S->o_full[1]);
         umma_commit(&S->q_empty);
       }
       __syncwarp();
     }
   } else {
-    // ---------------------------------------------------------------- softmax / epilogue (128 threads)
-    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    // ---------------------------------------------------------------- softmax warpgroup wg (128 threads)
+    const int wg = warp >> 2, t = tid & 127;
+    const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16) + wg * 128;
+    const uint32_t o_base = tmem + (uint32_t((warp & 3) * 32) << 16) + 256 + wg * 64;
     const float cl2 = c.scale * kLog2e;
-    Ring sb(2);
-    uint32_t pph = 0, oph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
-      const int r = rt * kTile + tid;
+    float* sc_cmp = wg ? sc_cmp1 : sc_cmp0;
+    float* lse_s = S->lse[wg];
+    Ring sb(1);
+    // warpgroup 0 writes the shared P^T first; warpgroup 1 waits for warpgroup 0's first P.V
+    uint32_t fph = wg ? 0u : 1u, oph = 0;
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const int rt = 2 * pr + wg;
+      if (rt >= n_rt) break;                          // only warpgroup 1 in the last, odd pair
+      const int r = rt * kTile + t;
       const bool rvalid = r < rows;
-      // ---- pass 1: row LSE (whole 128-key tile in registers, tree max/sum, one MUFU per element)
+      // ---- pass 1: row LSE
       float m = -1e30f, l = 0.f;
       for (int kt = 0; kt < n_kt; ++kt) {
-        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        mbar_wait(&S->s_full[wg], sb.ph);
         tc_fence_after();
         const int nv = min(kTile, nk - kt * kTile);
-        float v[kTile];
 #pragma unroll
-        for (int c0 = 0; c0 < kTile; c0 += 32) tmem_ld32(lane_base + sb.idx * 128 + c0, v + c0);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&S->s_empty[sb.idx]);
-        sb.next();
-        if (nv < kTile) {
+        for (int hh = 0; hh < 2; ++hh) {            // 64 columns at a time (register budget)
+          float v[64];
+          tmem_ld32(lane_base + hh * 64, v);
+          tmem_ld32(lane_base + hh * 64 + 32, v + 32);
+          tmem_wait_ld();
+          if (hh == 1) {
+            tc_fence_before();
+            mbar_arrive(&S->s_empty[wg]);
+          }
+          if (nv < kTile) {
 #pragma unroll
-          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -1e30f;
+            for (int i = 0; i < 64; ++i) v[i] = hh * 64 + i < nv ? v[i] : -1e30f;
+          }
+          const float mx = fmaxf(max32(v), max32(v + 32)) * cl2;
+          const float mn = fmaxf(m, mx);
+          float acc[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) acc[i & 7] += ex2(fmaf(v[i], cl2, -mn));
+          const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+          l = l * ex2(m - mn) + s;
+          m = mn;
         }
-        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
-        const float mn = fmaxf(m, mx);
-        float acc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-#pragma unroll
-        for (int i = 0; i < kTile; ++i) acc[i & 7] += ex2(fmaf(v[i], cl2, -mn));
-        const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        l = l * ex2(m - mn) + s;
-        m = mn;
+        sb.next();
       }
       const float lse2 = rvalid ? m + lg2(l) : INFINITY;
-      named_bar_sync(1, 128);          // previous row tile's pass 2 finished reading S->lse
-      S->lse[tid] = lse2;
+      named_bar_sync(1 + wg, 128);     // this warpgroup's previous pass 2 finished reading lse_s
+      lse_s[t] = lse2;
       if (rvalid) c.lse[0][qrow0 + r] = lse2;   // saved LSEs are log2-domain
-      named_bar_sync(1, 128);
-      // ---- pass 2: thread = key; P^T row -> smem; exact fp32 column sums
+      named_bar_sync(1 + wg, 128);
+      // ---- pass 2: thread = key; P^T row -> shared buffer; exact fp32 column sums
       for (int kt = 0; kt < n_kt; ++kt) {
-        const bool kvalid = kt * kTile + tid < nk;
-        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        const bool kvalid = kt * kTile + t < nk;
+        mbar_wait(&S->s_full[wg], sb.ph);
         tc_fence_after();
         uint32_t pk[64];
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c0 = 0; c0 < kTile; c0 += 32) {
+        for (int c00 = 0; c00 < kTile; c00 += 32) {
           float v[32];
-          tmem_ld32(lane_base + sb.idx * 128 + c0, v);
+          tmem_ld32(lane_base + c00, v);
           tmem_wait_ld();
+          if (c00 == kTile - 32) {
+            tc_fence_before();
+            mbar_arrive(&S->s_empty[wg]);
+          }
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 L = *reinterpret_cast<const float4*>(&S->lse[c0 + i]);
+            const float4 L = *reinterpret_cast<const float4*>(&lse_s[c00 + i]);
             const float p0 = ex2(fmaf(v[i], cl2, -L.x)), p1 = ex2(fmaf(v[i + 1], cl2, -L.y));
             const float p2 = ex2(fmaf(v[i + 2], cl2, -L.z)), p3 = ex2(fmaf(v[i + 3], cl2, -L.w));
             cs[0] += p0; cs[1] += p1; cs[2] += p2; cs[3] += p3;
-            pk[(c0 + i) / 2] = pack_f16(p0, p1);
-            pk[(c0 + i) / 2 + 1] = pack_f16(p2, p3);
+            pk[(c00 + i) / 2] = pack_f16(p0, p1);
+            pk[(c00 + i) / 2 + 1] = pack_f16(p2, p3);
           }
         }
+        sb.next();
         float colsum = (cs[0] + cs[1]) + (cs[2] + cs[3]);
         if (!kvalid) {
           colsum = 0.f;
 #pragma unroll
           for (int i = 0; i < 64; ++i) pk[i] = 0u;
         }
-        tc_fence_before();
-        mbar_arrive(&S->s_empty[sb.idx]);
-        sb.next();
-        mbar_wait(&S->p_empty, pph ^ 1u);
-        pph ^= 1u;
+        mbar_wait(&S->p_free[wg], fph);
+        fph ^= 1u;
         const uint32_t pbase = smem_u32(sP);
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {      // 16 chunks of 8 rows: row block ch/8, chunk ch%8
-          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+        for (int ch = 0; ch < 16; ++ch)      // 16 chunks of 8 rows: row block ch/8, chunk ch%8
+          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(t, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
                        pk[4 * ch + 3]);
-        }
         fence_proxy_async_smem();
-        mbar_arrive(&S->p_full);
-        if (kvalid) sc_cmp[kt * kTile + tid] += colsum;
+        mbar_arrive(&S->p_full[wg]);
+        if (kvalid) sc_cmp[kt * kTile + t] += colsum;
       }
+      // when b is absent in this pair, the MMA returned the buffer to warpgroup 0 (one extra phase)
       // ---- O (fixed normalisation, accumulated over all key tiles in TMEM)
-      mbar_wait(&S->o_full, oph);
+      mbar_wait(&S->o_full[wg], oph);
       oph ^= 1u;
       tc_fence_after();
       float* oc = static_cast<float*>(c.o[0]) + int64_t(qrow0 + r) * kD;
 #pragma unroll
-      for (int c0 = 0; c0 < kD; c0 += 32) {
+      for (int cc = 0; cc < kD; cc += 32) {
         float v[32];
-        tmem_ld32(lane_base + 256 + c0, v);
+        tmem_ld32(o_base + cc, v);
         tmem_wait_ld();
         if (rvalid) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(oc + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            *reinterpret_cast<float4*>(oc + cc + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         }
       }
       tc_fence_before();
-      mbar_arrive(&S->o_empty);
+      mbar_arrive(&S->o_empty[wg]);
     }
-    // ---- Eq. 8 selection-block scores and top-k (softmax warps only)
-    named_bar_sync(1, 128);
-    for (int B = tid; B < ns; B += 128) {
+    // ---- Eq. 8 selection-block scores and top-k (both softmax warpgroups, 256 threads)
+    named_bar_sync(3, 256);
+    for (int B = tid; B < ns; B += 256) {
       float s = 0.f;
-      for (int i = c.slc_cmp_begin[s0 + B]; i < c.slc_cmp_begin[s0 + B + 1]; ++i) s += sc_cmp[i - c0];
+      for (int i = c.slc_cmp_begin[s0 + B]; i < c.slc_cmp_begin[s0 + B + 1]; ++i)
+        s += sc_cmp0[i - c0] + sc_cmp1[i - c0];
       sc_slc[B] = s;
       if (c.save_scores) c.scores[(int64_t(Q) * c.h_kv + g) * c.max_slc_b + B] = s;
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(3, 256);
     const int Teff = min(c.T, ns);
     for (int it = 0; it < Teff; ++it) {
       float best = -2.f;
       int bidx = 0x7fffffff;
-      for (int B = tid; B < ns; B += 128) {
+      for (int B = tid; B < ns; B += 256) {
         const float v = sc_slc[B];
         if (v > best) { best = v; bidx = B; }
       }
@@ -354,16 +393,16 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
       }
       if (lane == 0) { S->bv[warp] = best; S->bi[warp] = bidx; }
-      named_bar_sync(1, 128);
+      named_bar_sync(3, 256);
       if (tid == 0) {
         float bb = S->bv[0];
         int ii = S->bi[0];
-        for (int w = 1; w < 4; ++w)
+        for (int w = 1; w < 8; ++w)
           if (S->bv[w] > bb || (S->bv[w] == bb && S->bi[w] < ii)) { bb = S->bv[w]; ii = S->bi[w]; }
         S->chosen[it] = ii;
         sc_slc[ii] = -1.f;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(3, 256);
     }
     if (tid == 0) {
       for (int i = 1; i < Teff; ++i) {
@@ -373,12 +412,12 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         S->chosen[j + 1] = v;
       }
     }
-    named_bar_sync(1, 128);
-    for (int j = tid; j < c.T; j += 128) c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + S->chosen[j] : -1;
+    named_bar_sync(3, 256);
+    for (int j = tid; j < c.T; j += 256) c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + S->chosen[j] : -1;
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 // ================================================================================================
@@ -653,8 +692,8 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
 }
 
 bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
-  const size_t smem = 1024 + 16384 + kStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
-                      (size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
+  const size_t smem = 1024 + 32768 + kCmpStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+                      (2 * size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
   const int slc_tiles = (info.max_fill[SSA_LEVEL_SLC] + 111) / 112;
   const int dq_tiles = (info.max_blocks_per_batch[SSA_LEVEL_CMP] + 111) / 112 + top_k * slc_tiles + slc_tiles;
   return smem <= 232448 && dq_tiles <= 64 + 4 * 64 * 2 + 16 && top_k * ((info.max_fill[SSA_LEVEL_SLC] + 127) / 128) +
@@ -680,12 +719,12 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
   TcArgs a{c, kc_hi, kc_lo, vc};
   const int nq = c.n_blk[SSA_LEVEL_Q];
   {
-    const size_t smem = 1024 + 16384 + kStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
-                        (size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
+    const size_t smem = 1024 + 32768 + kCmpStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+                        (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
     if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_cmp_fwd", st);
-    k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
+    k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
     SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
   }
   {
