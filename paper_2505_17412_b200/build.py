@@ -13,11 +13,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-LIB = os.path.join(HERE, "libssa_b200.so")
-OBJ = os.path.join(HERE, "_obj")
+LIB = os.environ.get("SSA_LIB_OUT", os.path.join(HERE, "libssa_b200.so"))
+OBJ = os.path.join(HERE, "_obj" + os.environ.get("SSA_OBJ_SUFFIX", ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", INCLUDE]
+FLAGS += [f for f in os.environ.get("SSA_EXTRA_NVCC_FLAGS", "").split() if f]   # e.g. -DSSA_TRACE (debug builds)
 
 
 def sources():

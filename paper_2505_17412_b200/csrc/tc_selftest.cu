@@ -81,14 +81,30 @@ __global__ void __launch_bounds__(128) k_umma_selftest(int mode, int N, int K, c
       *reinterpret_cast<uint4*>(sA + kb * 16384 + sw128(m, ch)) = v;
     }
   }
+  if (mode == 4 || mode == 5) {   // A [128][K] bf16 -> TMEM columns 128.., lane = row, two K per column
+    uint32_t w[32];
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      for (int i = 0; i < 16; ++i) {
+        const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(a + tid * K + 2 * (c0 + i));
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      tmem_st16(tmem + (uint32_t(warp * 32) << 16) + 128 + c0, w);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+  }
   fence_proxy_async_smem();
   __syncthreads();
+  tc_fence_after();
   if (tid == 0) {
     uint32_t bytes = 0;
     if (mode == 0) {
       tma_load_2d(sA, &tmA, &bar_ld, 0, 0);
       tma_load_2d(sB, &tmB, &bar_ld, 0, 0);
       bytes = 128 * 128 + N * 128;
+    } else if (mode == 5) {
+      tma_load_2d(sB, &tmB, &bar_ld, 0, 0);
+      bytes = N * 128;
     } else {
       tma_load_2d(sB, &tmB, &bar_ld, 0, 0);
       bytes = K * 128;
@@ -97,7 +113,15 @@ __global__ void __launch_bounds__(128) k_umma_selftest(int mode, int N, int K, c
     mbar_wait(&bar_ld, 0);
     tc_fence_after();
     const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-    if (mode == 0) {
+    if (mode == 4) {          // A in TMEM, B MN-major [K][64] (TMA)
+      const uint32_t id = idesc_bf16(128, 64, false, true);
+      for (int s = 0; s < K / 16; ++s)
+        umma_ts(tmem, tmem + 128 + s * 8, desc_sw128(b0 + s * 2048, 0, 1024), id, s > 0);
+    } else if (mode == 5) {   // A in TMEM (K = 64), B K-major [N][64] (TMA)
+      const uint32_t id = idesc_bf16(128, N, false, false);
+      for (int s = 0; s < 4; ++s)
+        umma_ts(tmem, tmem + 128 + s * 8, desc_sw128(b0 + s * 32, 0, 1024), id, s > 0);
+    } else if (mode == 0) {
       const uint32_t id = idesc_bf16(128, N, false, false);
       for (int s = 0; s < 4; ++s)
         umma_bf16(tmem, desc_sw128(a0 + s * 32, 0, 1024), desc_sw128(b0 + s * 32, 0, 1024), id, s > 0);
@@ -117,7 +141,7 @@ __global__ void __launch_bounds__(128) k_umma_selftest(int mode, int N, int K, c
   __syncwarp();
   mbar_wait(&bar_mma, 0);
   tc_fence_after();
-  const int ncol = mode == 0 ? N : 64;
+  const int ncol = (mode == 0 || mode == 5) ? N : 64;
   for (int c0 = 0; c0 < ncol; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
@@ -138,6 +162,8 @@ extern "C" ssa_status ssa_selftest_umma(int mode, int n, int k, const void* a, c
   CUtensorMap tmA{}, tmB{};
   if (mode == 0) {
     if (!make_tmap_bf16_2d(&tmA, a, 128, 128) || !make_tmap_bf16_2d(&tmB, b, n, n)) return SSA_ERR_CUDA;
+  } else if (mode == 5) {
+    if (!make_tmap_bf16_2d(&tmA, b, n, n) || !make_tmap_bf16_2d(&tmB, b, n, n)) return SSA_ERR_CUDA;
   } else {
     if (!make_tmap_bf16_2d(&tmA, b, k, k) || !make_tmap_bf16_2d(&tmB, b, k, k)) return SSA_ERR_CUDA;
   }

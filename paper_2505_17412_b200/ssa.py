@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssa_b200.so")
+LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa_b200.so"))   # SSA_LIB: debug builds only
 
 SSA_F32, SSA_BF16 = 0, 1
 SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES = 1, 2, 4

@@ -16,7 +16,7 @@ def _run(mode, n, k, a, b):
     f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                   ctypes.c_void_p]
     rows = 128
-    cols = n if mode == 0 else 64
+    cols = n if mode in (0, 5) else 64
     d = torch.zeros(rows, cols, dtype=torch.float32, device="cuda")
     st = f(mode, n, k, a.data_ptr(), b.data_ptr(), d.data_ptr(), torch.cuda.current_stream().cuda_stream)
     assert st == 0, L.ssa_last_error().decode()
@@ -51,3 +51,25 @@ def test_kmajor_a_mnmajor_b(k):
     ref = a.float() @ b.float()
     assert torch.allclose(d, ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
 
+
+
+@pytest.mark.parametrize("k", [64, 96, 128])
+def test_tmem_a_mnmajor_b(k):
+    """A operand in TMEM (threads write rows with tcgen05.st), B MN-major from TMA: (P w)^T dO shape."""
+    g = torch.Generator(device="cuda").manual_seed(40 + k)
+    a = torch.randn(128, k, device="cuda", generator=g).bfloat16()
+    b = torch.randn(k, 64, device="cuda", generator=g).bfloat16()
+    d = _run(4, 64, k, a, b)
+    ref = a.float() @ b.float()
+    assert torch.allclose(d, ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_tmem_a_kmajor_b(n):
+    """A operand in TMEM, B K-major [N][64] from TMA: S^T = K Q^T shape."""
+    g = torch.Generator(device="cuda").manual_seed(50 + n)
+    a = torch.randn(128, 64, device="cuda", generator=g).bfloat16()
+    b = torch.randn(n, 64, device="cuda", generator=g).bfloat16()
+    d = _run(5, n, 64, a, b)
+    ref = a.float() @ b.float().T
+    assert torch.allclose(d, ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
