@@ -165,8 +165,27 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     st = torch.cuda.current_stream(dev)
 
+    sharded = args.config == "C5"
+
     def step(qq=q, kk=k, vv=v, gg=g, dd=do):
         plan = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+        if sharded:
+            # one shape, query blocks sharded over the ranks (SURVEY §8e mode 2): K/V all-gather,
+            # dK/dV partial all-reduce; inputs in plan order, every rank builds the same plan
+            from paper_2505_17412_b200.shard import balanced_q_ranges, ssa_step_sharded
+            qo = plan.offsets(ssa.LEVEL_Q).cpu().numpy()
+            rngs = balanced_q_ranges(qo, world)
+            tok = [(int(qo[a]), int(qo[b])) for a, b in rngs]
+            p = plan.perm()
+            qs_, ks_, vs_, gs_, ds_ = (x[p] for x in (qq, kk, vv, gg, dd))
+            pad = max(b - a for a, b in tok)
+            a, b = tok[rank]
+            kl = torch.zeros((pad,) + tuple(ks_.shape[1:]), dtype=ks_.dtype, device=dev)
+            vl = torch.zeros_like(kl)
+            kl[:b - a] = ks_[a:b]
+            vl[:b - a] = vs_[a:b]
+            ssa_step_sharded(plan, acfg, qs_, kl, vl, gs_, ds_, tok, rank)
+            return plan, None
         o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=out)
         ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=grads)
         return plan, saved
@@ -174,6 +193,9 @@ def main():
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 3):
         plan, saved = step()
     torch.cuda.synchronize(dev)
+    if saved is None:     # sharded mode: run once unsharded for the work accounting below
+        saved = ssa.ssa_forward(plan, acfg, q, k, v, g, out=out)[1]
+        torch.cuda.synchronize(dev)
     used_tc = saved.used_tcgen05
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events) ----
@@ -210,7 +232,7 @@ def main():
     from paper_2505_17412_b200.shard import max_over_ranks
     total_ms = max_over_ranks(total_ms, dev)
     ms_per_step = total_ms / args.steps
-    shapes_per_step = batch * world
+    shapes_per_step = batch * (1 if sharded else world)
     value = ms_per_step / shapes_per_step
 
     # ---- algorithmic work of the dominant kernel ----
@@ -301,12 +323,14 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if tdt == torch.bfloat16 else "f32",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "bf16" if tdt == torch.bfloat16 else "f32",
             "data": "synthetic (sphere-shell occupancy, N(0,1) q/k/v/dO, sigmoid(N(0,1)) gates; ssa_workload)",
             "config": {"workload": f"{args.config}: 128^3 latent (1024^3 res) sphere shell, {N} tokens x {batch} shape(s)/rank, "
                                    f"H={H} (h_kv={h_kv}), d={d}, m_cmp/m_slc/m_win/m_q={ms}, T={T}",
                        "tokens_per_shape": int(np.max(ntok_b)), "shapes_per_rank": batch,
-                       "parallelism": f"shape-parallel x{world} (no data-path collective)",
+                       "parallelism": (f"query-block shards x{world} (NCCL K/V all-gather + dK/dV all-reduce)"
+                                       if sharded else f"shape-parallel x{world} (no data-path collective)"),
                        "l2": "flushed between timed steps (256 MB write)", "path": "tcgen05" if used_tc else "simt"},
             "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline, "kernel_ms": kernel_ms,
             "work": {"E_cmp": E_cmp, "E_slc": E_slc, "E_win": E_win},

@@ -121,11 +121,13 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *                  pooling (Eq. 7, reading R4); NULL = off. Not differentiated.
  *   flags        : SSA_INPUT_SORTED — tensors are already in plan order (no internal permute);
  *                  SSA_FORCE_SIMT   — use the SIMT kernels even where tcgen05 kernels exist;
- *                  SSA_SAVE_SCORES  — keep the fp32 selection scores in the saved state.
+ *                  SSA_SAVE_SCORES  — keep the fp32 selection scores in the saved state;
+ *                  SSA_KV_GRAD_FP32 — dk, dv buffers are fp32 (exact partial sums across shards).
  * ----------------------------------------------------------------------------------------------*/
 #define SSA_INPUT_SORTED 1u
 #define SSA_FORCE_SIMT 2u
 #define SSA_SAVE_SCORES 4u
+#define SSA_KV_GRAD_FP32 8u   /* dk / dv are written as fp32 (partials of a query-block shard)    */
 
 typedef struct {
   int32_t h_q, h_kv, d, top_k;
@@ -134,6 +136,13 @@ typedef struct {
   uint32_t flags;
   const void* pe_k;
   const void* pe_v;
+  /* Query-block sharding (SURVEY §8e mode 2): compute only the rows of the query blocks
+   * [q_begin, q_end) (plan order, SSA_LEVEL_Q; q_end <= 0 means all). Forward: only those rows of
+   * out / saved state are written. Backward: dq and dgates are written for those rows only; dk and
+   * dv receive the contributions of those rows to ALL keys (partials: the caller sums them across
+   * shards, e.g. with a reduce-scatter). k, v must be complete (e.g. all-gathered). A strict range
+   * requires m_win == m_q (a window is then exactly one query block). */
+  int32_t q_begin, q_end;
 } ssa_attn_cfg;
 
 /* ------------------------------------------------------------------------------------------------

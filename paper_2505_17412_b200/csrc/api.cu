@@ -56,6 +56,16 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
   if (cfg->top_k < 1 || cfg->top_k > 64) { set_error("top_k must be in [1, 64]"); return SSA_ERR_ARG; }
   if (cfg->dtype != SSA_F32 && cfg->dtype != SSA_BF16) { set_error("dtype must be SSA_F32 or SSA_BF16"); return SSA_ERR_ARG; }
   if (cfg->d != 16 && cfg->d != 32 && cfg->d != 64) { set_error("head dim must be 16, 32 or 64"); return SSA_ERR_UNSUPPORTED; }
+  if (cfg->q_end > 0) {
+    if (cfg->q_begin < 0 || cfg->q_begin > cfg->q_end || cfg->q_end > p->info.n_blocks[SSA_LEVEL_Q]) {
+      set_error("query-block range outside [0, n_blocks[Q]]");
+      return SSA_ERR_ARG;
+    }
+    if (p->info.m[SSA_LEVEL_WIN] != p->info.m[SSA_LEVEL_Q]) {
+      set_error("a query-block range requires m_win == m_q");
+      return SSA_ERR_UNSUPPORTED;
+    }
+  }
   d->N = p->info.n;
   d->H = cfg->h_q;
   d->h_kv = cfg->h_kv;
@@ -151,6 +161,7 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.D));
   x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
   x->save_scores = (cfg->flags & SSA_SAVE_SCORES) ? 1 : 0;
+  x->kv_grad_f32 = (cfg->flags & SSA_KV_GRAD_FP32) ? 1 : 0;
   x->perm = p->perm;
   x->inv_perm = p->inv_perm;
   x->sorted_coords = p->sorted_coords;
@@ -163,6 +174,11 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->n_cmp_tiles = p->n_cmp_tiles;
   x->pe_k = cfg->pe_k;
   x->pe_v = cfg->pe_v;
+  const int nq = p->info.n_blocks[SSA_LEVEL_Q];
+  x->q_begin = cfg->q_end > 0 ? std::max(0, cfg->q_begin) : 0;
+  x->q_end = cfg->q_end > 0 ? std::min(nq, cfg->q_end) : nq;
+  x->tok_begin = -1;   // resolved on device from the Q offsets (kernels read off[Q][q_begin / q_end])
+  x->tok_end = -1;
 }
 }  // namespace
 }  // namespace ssa

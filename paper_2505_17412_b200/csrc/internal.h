@@ -43,7 +43,10 @@ struct Ctx {
   int32_t max_fill[kLevels];
   float scale;                    // softmax scale (natural)
   int32_t sorted_input;
+  int32_t q_begin, q_end;         // owned query blocks [q_begin, q_end) (plan order)
+  int32_t tok_begin, tok_end;     // their token range
   int32_t save_scores;
+  int32_t kv_grad_f32;            // dk / dv written as fp32 (SSA_KV_GRAD_FP32)
   // plan (device)
   const int32_t *perm, *inv_perm, *sorted_coords;
   const int32_t *off[kLevels], *tok_block[kLevels], *bb[kLevels];

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kRows) k_cmp_fwd(Ctx c) {
   __shared__ int chosen[64];
 
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y, tid = threadIdx.x;
+  if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int b = c.q_batch[Q];
   const int c0 = c.bb[SSA_LEVEL_CMP][b], c1 = c.bb[SSA_LEVEL_CMP][b + 1], nk = c1 - c0;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kRows) k_attn_fwd(Ctx c, int mode) {
   int t0, t1;
   if (mode == 1) {
     const int Q = c.q_order[blockIdx.x];
+    if (Q < c.q_begin || Q >= c.q_end) return;
     t0 = c.off[SSA_LEVEL_Q][Q];
     t1 = c.off[SSA_LEVEL_Q][Q + 1];
     if (tid == 0) {
@@ -277,6 +279,7 @@ __global__ void __launch_bounds__(kRows) k_attn_fwd(Ctx c, int mode) {
     }
   } else {
     const int W = blockIdx.x;
+    if (c.q_end - c.q_begin < c.n_blk[SSA_LEVEL_Q] && (W < c.q_begin || W >= c.q_end)) return;  // m_win == m_q
     t0 = c.off[SSA_LEVEL_WIN][W];
     t1 = c.off[SSA_LEVEL_WIN][W + 1];
     if (tid == 0) { seg_s[0] = t0; seg_e[0] = t1; nseg = 1; }
@@ -343,6 +346,7 @@ __global__ void k_combine(Ctx c) {
   int h = int((i / c.D) % c.H);
   int p = int(i / (int64_t(c.D) * c.H));
   int g = h / c.h_s, s = h % c.h_s;
+  if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;
   int64_t row = (int64_t(g) * c.N + p) * c.h_s + s;
   const float* w = c.gs + row * 3;
   float v = w[0] * static_cast<const float*>(c.o[0])[row * c.D + e] +
@@ -381,6 +385,7 @@ __global__ void k_bwd_pre(Ctx c) {
   if (!valid || sub != 0) return;
   const int s = int(row % c.h_s);
   const int p = int((row / c.h_s) % c.N);
+  if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;
   const int g = int(row / (int64_t(c.h_s) * c.N));
   const int h = g * c.h_s + s;
   const int dst = c.sorted_input ? p : c.perm[p];
@@ -410,6 +415,7 @@ __global__ void k_inv_mark(Ctx c, uint32_t* bm) {
   if (B < 0) return;
   const int g = int((i / c.T) % c.h_kv);
   const int Q = int(i / (int64_t(c.T) * c.h_kv));
+  if (Q < c.q_begin || Q >= c.q_end) return;          // selections of rows this shard does not own
   const int64_t bit = (int64_t(B) * c.h_kv + g) * c.n_blk[SSA_LEVEL_Q] + Q;
   atomicOr(bm + (bit >> 5), 1u << (bit & 31));
 }
@@ -428,6 +434,7 @@ __global__ void k_inv_place(Ctx c, const uint32_t* bm, const int32_t* chunk_pre)
   if (B < 0) return;
   const int g = int((i / c.T) % c.h_kv);
   const int Q = int(i / (int64_t(c.T) * c.h_kv));
+  if (Q < c.q_begin || Q >= c.q_end) return;
   const int64_t bit = (int64_t(B) * c.h_kv + g) * c.n_blk[SSA_LEVEL_Q] + Q;
   c.inv_list[bit_rank(bm, chunk_pre, bit)] = Q;
 }
@@ -451,6 +458,7 @@ __global__ void __launch_bounds__(kRows) k_dq(Ctx c) {
   __shared__ int seg_s[65], seg_e[65];
   __shared__ int nseg;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y, tid = threadIdx.x;
+  if (Q < c.q_begin || Q >= c.q_end) return;
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int b = c.q_batch[Q];
   const int rows = (t1 - t0) * c.h_s;
@@ -626,6 +634,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_win_bwd(Ctx c) {
   __shared__ float Qt[kRT * D], Ot[kRT * D], s_l[kRT], s_w[kRT], s_D[kRT];
   const int W = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+  if (c.q_end - c.q_begin < c.n_blk[SSA_LEVEL_Q] && (W < c.q_begin || W >= c.q_end)) return;  // m_win == m_q
   const int t0 = c.off[SSA_LEVEL_WIN][W], t1 = c.off[SSA_LEVEL_WIN][W + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int64_t rb = (int64_t(g) * c.N + t0) * c.h_s;
@@ -716,7 +725,8 @@ __global__ void __launch_bounds__(128) k_cmp_dkdv(Ctx c) {
   const int half = threadIdx.x & 1;
   const float* kc = static_cast<const float*>(c.kc);
   const float* vc = static_cast<const float*>(c.vc);
-  const int bt0 = c.batch_tokens[b], bt1 = c.batch_tokens[b + 1];
+  const int bt0 = max(c.batch_tokens[b], c.off[SSA_LEVEL_Q][c.q_begin]);
+  const int bt1 = max(bt0, min(c.batch_tokens[b + 1], c.off[SSA_LEVEL_Q][c.q_end]));   // owned rows only
   const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
   const int64_t per = (rows + c.n_chunk - 1) / c.n_chunk;
   const int64_t ra = min(rows, per * chunk), re = min(rows, per * (chunk + 1));
@@ -772,6 +782,7 @@ __global__ void k_bwd_final_q(Ctx c) {
   int h = int((i / c.D) % c.H);
   int p = int(i / (int64_t(c.D) * c.H));
   int g = h / c.h_s, s = h % c.h_s;
+  if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;
   int dst = c.sorted_input ? p : c.perm[p];
   st(static_cast<T*>(c.dq) + (int64_t(dst) * c.H + h) * c.D + e,
      c.dq_acc[((int64_t(g) * c.N + p) * c.h_s + s) * c.D + e]);
@@ -790,8 +801,14 @@ __global__ void k_bwd_final_kv(Ctx c) {
   int64_t ci = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
   int dst = c.sorted_input ? p : c.perm[p];
   int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
-  st(static_cast<T*>(c.dk) + o, c.dk_acc[ki] + c.dkc[ci] * inv);
-  st(static_cast<T*>(c.dv) + o, c.dv_acc[ki] + c.dvc[ci] * inv);
+  const float gk = c.dk_acc[ki] + c.dkc[ci] * inv, gv = c.dv_acc[ki] + c.dvc[ci] * inv;
+  if (c.kv_grad_f32) {
+    static_cast<float*>(c.dk)[o] = gk;
+    static_cast<float*>(c.dv)[o] = gv;
+  } else {
+    st(static_cast<T*>(c.dk) + o, gk);
+    st(static_cast<T*>(c.dv) + o, gv);
+  }
 }
 
 template <class T, int D>

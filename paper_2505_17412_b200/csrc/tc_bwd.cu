@@ -101,6 +101,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + 127) / 128;
@@ -330,7 +331,8 @@ __device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
     it->b = c.cmp_tiles[2 * tile];
     it->kblock = c.cmp_tiles[2 * tile + 1];
     it->chunk = blockIdx.z;
-    const int bt0 = c.batch_tokens[it->b], bt1 = c.batch_tokens[it->b + 1];
+    const int bt0 = max(c.batch_tokens[it->b], c.off[SSA_LEVEL_Q][c.q_begin]);
+    const int bt1 = max(bt0, min(c.batch_tokens[it->b + 1], c.off[SSA_LEVEL_Q][c.q_end]));   // owned rows
     const int64_t rows = int64_t(bt1 - bt0) * c.h_s;
     const int64_t per = ((rows + c.n_chunk - 1) / c.n_chunk + kRT - 1) / kRT * kRT;
     const int64_t base = (int64_t(it->g) * c.N + bt0) * c.h_s;
@@ -357,7 +359,7 @@ __device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
   const int l0 = c.inv_off[key], l1 = c.inv_off[key + 1];
   it->li = min(l1, l0 + it->chunk * kQBlocksPerItem);
   it->le = min(l1, it->li + kQBlocksPerItem);
-  it->with_win = it->chunk == nch - 1;
+  it->with_win = it->chunk == nch - 1 && it->kblock >= c.q_begin && it->kblock < c.q_end;  // window = block
   it->first = it->chunk == 0;
   it->part_slot = id;
   it->ra = it->re = 0;

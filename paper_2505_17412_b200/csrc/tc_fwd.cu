@@ -100,6 +100,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int b = c.q_batch[Q];
   const int c0 = c.bb[SSA_LEVEL_CMP][b], nk = c.bb[SSA_LEVEL_CMP][b + 1] - c0;
@@ -445,6 +446,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
+  if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + kTile - 1) / kTile;

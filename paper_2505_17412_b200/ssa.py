@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa_b200.so"))   # SSA_LIB: debug builds only
 
 SSA_F32, SSA_BF16 = 0, 1
-SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES = 1, 2, 4
+SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32 = 1, 2, 4, 8
 LEVEL_CMP, LEVEL_SLC, LEVEL_WIN, LEVEL_Q = 0, 1, 2, 3
 STATUS = ["SSA_OK", "SSA_ERR_ARG", "SSA_ERR_DUP_COORD", "SSA_ERR_COORD_RANGE", "SSA_ERR_HIERARCHY",
           "SSA_ERR_BAD_STATE", "SSA_ERR_WORKSPACE", "SSA_ERR_UNSUPPORTED", "SSA_ERR_CUDA"]
@@ -48,7 +48,8 @@ class PlanInfo(ctypes.Structure):
 class AttnCfgC(ctypes.Structure):
     _fields_ = [("h_q", ctypes.c_int32), ("h_kv", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p),
+                ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32)]
 
 
 class SavedView(ctypes.Structure):
@@ -211,11 +212,13 @@ class AttnCfg:
     flags: int = 0
     pe_k: torch.Tensor | None = None
     pe_v: torch.Tensor | None = None
+    q_begin: int = 0            # query-block shard [q_begin, q_end) in plan order; q_end <= 0: all
+    q_end: int = 0
 
     def c(self) -> AttnCfgC:
         return AttnCfgC(self.h_q, self.h_kv, self.d, self.top_k, float(self.scale), _dtype_code(self.dtype),
                         int(self.flags), self.pe_k.data_ptr() if self.pe_k is not None else None,
-                        self.pe_v.data_ptr() if self.pe_v is not None else None)
+                        self.pe_v.data_ptr() if self.pe_v is not None else None, int(self.q_begin), int(self.q_end))
 
 
 class Saved:
@@ -322,7 +325,9 @@ def ssa_backward(plan: Plan, cfg: AttnCfg, saved: Saved, q, k, v, gates, dout, g
     _check(L.ssa_backward_size(plan.handle, ctypes.byref(cc), ctypes.byref(wsb)), "ssa_backward_size")
     dev = q.device
     if grads is None:
-        grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(gates))
+        kvd = torch.float32 if cfg.flags & SSA_KV_GRAD_FP32 else k.dtype
+        grads = (torch.empty_like(q), torch.empty_like(k, dtype=kvd), torch.empty_like(v, dtype=kvd),
+                 torch.empty_like(gates))
     dq, dk, dv, dg = grads
     w = (ws or _ws(dev, "bwd")).get(wsb.value, dev)
     _check(L.ssa_backward(plan.handle, ctypes.byref(cc), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),

@@ -56,3 +56,17 @@ def test_gloo_two_ranks():
     items = sorted(res[0][1] + res[1][1])
     assert items == [0, 1, 2, 3]
     assert res[0][1] == rank_items([100, 300, 200, 50], 0, 2)
+
+
+def test_balanced_q_ranges_cover():
+    from paper_2505_17412_b200.shard import balanced_q_ranges
+    import numpy as np
+    rng = np.random.Generator(np.random.PCG64(3))
+    sizes = rng.integers(1, 200, size=500)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    for world in (1, 2, 3, 8):
+        r = balanced_q_ranges(off, world)
+        assert r[0][0] == 0 and r[-1][1] == 500
+        assert all(a <= b for a, b in r) and all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+        loads = [off[b] - off[a] for a, b in r]
+        assert max(loads) <= off[-1] / world + sizes.max()
