@@ -31,6 +31,19 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kStages = 3;
 
+#ifdef SSA_TRACE
+// per-role shared-memory trace of one CTA (debug builds: -DSSA_TRACE); flushed at kernel end
+__device__ unsigned long long g_trace[3][128];
+__device__ int g_trace_cnt[3];
+#define TRACE_ON (blockIdx.x == 5 && blockIdx.y == 0 && (threadIdx.x & 31) == 0)
+#define TRACE_R(role, ev, j)                                                                              \
+  do {                                                                                                  \
+    if (TRACE_ON && tr_n < 128) S->trace[role][tr_n++] = (clock64() << 16) | (unsigned long long)(((ev) << 12) | ((j) & 0xfff)); \
+  } while (0)
+#else
+#define TRACE_R(role, ev, j) do { } while (0)
+#endif
+
 struct TcArgs {
   Ctx c;
   const __nv_bfloat16* kc_hi;   // [h_kv][n_cmp][64]
@@ -65,24 +78,40 @@ struct Ring {
 };
 
 // ================================================================================================
-// compression attention + scores + top-k (two softmax warpgroups, FA4-style ping-pong)
+// compression attention + scores + top-k (two softmax warpgroups)
 // ================================================================================================
-// 320 threads: warps 0-3 = softmax warpgroup 0, warps 4-7 = softmax warpgroup 1 (each owns one
-// 128-row tile of a row-tile pair and TMEM lanes 0-127 of its own S / O columns), warp 8 = TMA
-// producer, warp 9 = MMA issuer + TMEM owner (register budget 168/thread: softmax works on 64 columns
-// at a time). Both row tiles share every K/V tile load (half the L2
-// traffic of one tile per CTA) and one P^T buffer that the two warpgroups fill alternately.
-constexpr int kCmpThreads = 320;
+// 352 threads: warps 0-3 = softmax warpgroup 0, warps 4-7 = softmax warpgroup 1 (each owns one
+// 128-row tile of a row-tile pair; thread i <-> TMEM lane i of its own S / O / P columns), warp 8 =
+// TMA producer, warps 9 / 10 = MMA issuers of warpgroups 0 / 1 (warp 9 owns TMEM). Both row tiles
+// share every K/V tile load.
+//  pass 1 (rows on lanes): S = Q K^T -> online softmax with lazy rescaling (the reference max moves
+//         only when a row max exceeds it by kRescale, log2 units); P (fp16) is written to TMEM and
+//         O += P V runs with A from TMEM, so P never touches shared memory.
+//  pass 2 (keys on lanes): S^T = K Q^T -> p = exp2(S^T c - LSE) with the final row LSEs; each thread
+//         sums its key's column in fp32: the Eq. 8 column sums, exact per thread.
+// TMEM columns: S_0 S_1 [0, 256) | O_0 O_1 [256, 384) | P_0 P_1 [384, 512).
+constexpr int kCmpThreads = 352;
 constexpr int kCmpStages = 2;
+constexpr float kRescale = 8.f;
 struct CmpSmem {
-  uint64_t q_full, q_empty, kv_full[kCmpStages], kv_empty[kCmpStages];
+  uint64_t q_full, q_empty, k_full[kCmpStages], k_empty[kCmpStages], v_full[kCmpStages], v_empty[kCmpStages];
   uint64_t s_full[2], s_empty[2], p_full[2], p_free[2], o_full[2], o_empty[2];
   uint32_t tmem;
   alignas(16) float lse[2][kTile];
+#ifdef SSA_TRACE
+  unsigned long long trace[3][128];
+#endif
   float bv[8];
   int bi[8];
   int chosen[64];
 };
+
+__device__ __forceinline__ float4 ld_shared_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(smem_u32(p)));
+  return r;
+}
 
 __global__ void __launch_bounds__(kCmpThreads, 1)
 k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmKh,
@@ -90,11 +119,11 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;                                  // 2 x 16 KB (row tiles a, b)
-  uint8_t* sKV = sm + 32768;                         // kCmpStages x {Khi, Klo, V} 48 KB
-  uint8_t* sP = sKV + kCmpStages * 49152;            // 32 KB, P^T: 2 row blocks x [128 keys][128 B]
-  CmpSmem* S = reinterpret_cast<CmpSmem*>(sP + 32768);
+  uint8_t* sK = sm + 32768;                          // kCmpStages x {Khi, Klo} 32 KB
+  uint8_t* sV = sK + kCmpStages * 32768;             // kCmpStages x V 16 KB (pass 1 only)
+  CmpSmem* S = reinterpret_cast<CmpSmem*>(sV + kCmpStages * 16384);
   const Ctx& c = a.c;
-  float* sc_cmp0 = reinterpret_cast<float*>(S + 1);  // [max_cmp_b] per warpgroup
+  float* sc_cmp0 = reinterpret_cast<float*>(S + 1);  // [max_cmp_b] Eq. 8 column sums, per warpgroup
   float* sc_cmp1 = sc_cmp0 + c.max_cmp_b;
   float* sc_slc = sc_cmp1 + c.max_cmp_b;             // [max_slc_b]
 
@@ -113,8 +142,13 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 
   if (tid == 0) {
     mbar_init(&S->q_full, 1);
-    mbar_init(&S->q_empty, 1);
-    for (int i = 0; i < kCmpStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    mbar_init(&S->q_empty, 2);                       // one arrival per MMA issuer
+    for (int i = 0; i < kCmpStages; ++i) {
+      mbar_init(&S->k_full[i], 1);
+      mbar_init(&S->k_empty[i], 2);
+      mbar_init(&S->v_full[i], 1);
+      mbar_init(&S->v_empty[i], 2);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
@@ -132,10 +166,14 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem;
+#ifdef SSA_TRACE
+  int tr_n = 0;
+#endif
 
   if (warp == 8) {
     // ---------------------------------------------------------------- TMA producer
-    Ring kv(kCmpStages);
+    // K (hi, lo) every pass, V in pass 1 only; separate rings so K(kt+1) never waits behind V(kt)
+    Ring kr(kCmpStages), vr(kCmpStages);
     uint32_t qph = 0;
     for (int pr = 0; pr < n_pair; ++pr) {
       const bool bval = 2 * pr + 1 < n_rt;
@@ -148,174 +186,229 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       }
       for (int pass = 1; pass <= 2; ++pass) {
         for (int kt = 0; kt < n_kt; ++kt) {
-          mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
+          mbar_wait(&S->k_empty[kr.idx], kr.ph ^ 1u);
+          TRACE_R(0, pass, kt);
           if (lane == 0) {
-            uint8_t* st = sKV + kv.idx * 49152;
-            mbar_expect_tx(&S->kv_full[kv.idx], pass == 1 ? 32768u : 49152u);
-            tma_load_2d(st, &tmKh, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
-            tma_load_2d(st + 16384, &tmKl, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
-            if (pass == 2) tma_load_2d(st + 32768, &tmV, &S->kv_full[kv.idx], 0, krow0 + kt * kTile);
+            uint8_t* st = sK + kr.idx * 32768;
+            mbar_expect_tx(&S->k_full[kr.idx], 32768u);
+            tma_load_2d(st, &tmKh, &S->k_full[kr.idx], 0, krow0 + kt * kTile);
+            tma_load_2d(st + 16384, &tmKl, &S->k_full[kr.idx], 0, krow0 + kt * kTile);
           }
           __syncwarp();
-          kv.next();
+          kr.next();
+          if (pass == 1) {
+            mbar_wait(&S->v_empty[vr.idx], vr.ph ^ 1u);
+            if (lane == 0) {
+              mbar_expect_tx(&S->v_full[vr.idx], 16384u);
+              tma_load_2d(sV + vr.idx * 16384, &tmV, &S->v_full[vr.idx], 0, krow0 + kt * kTile);
+            }
+            __syncwarp();
+            vr.next();
+          }
         }
       }
     }
-  } else if (warp == 9) {
-    // ---------------------------------------------------------------- MMA issuer
+  } else if (warp >= 9) {
+    // ---------------------------------------------------------------- MMA issuers
+    // warp 9 issues for warpgroup 0, warp 10 for warpgroup 1 (tcgen05.mma issue is nearly synchronous
+    // with execution, so one issuer would make each warpgroup's S wait behind the other's P.V).
+    // Per warpgroup, in order: S(kt+1) as soon as S(kt) has been read, then P.V(kt).
+    const int w = warp - 9;
     const uint32_t idS = idesc_bf16(128, 128, false, false);
-    const uint32_t idO = idesc_f16(128, 64, true, true);
-    const uint32_t aP = smem_u32(sP);
-    Ring kv(kCmpStages), sb0(1), sb1(1);
-    uint32_t qph = 0, pph[2] = {0, 0}, oph[2] = {0, 0};
+    const uint32_t idO = idesc_f16(128, 64, false, true);   // P from TMEM, V MN-major
+    Ring kr(kCmpStages), vr(kCmpStages), sb(1);
+    uint32_t qph = 0, pph = 0, oph = 0;
+    auto mma_s = [&](int ki, bool transposed) {
+      const uint32_t aq = smem_u32(sQ + w * 16384), ak = smem_u32(sK + ki * 32768);
+      const uint32_t d = tmem + w * 128;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t dq = desc_sw128(aq + k * 32, 0, 1024), dk = desc_sw128(ak + h * 16384 + k * 32, 0, 1024);
+          umma_bf16(d, transposed ? dk : dq, transposed ? dq : dk, idS, (h | k) ? 1u : 0u);
+        }
+      umma_commit(&S->s_full[w]);
+    };
     for (int pr = 0; pr < n_pair; ++pr) {
-      const bool bval = 2 * pr + 1 < n_rt;
+      const bool mine = w == 0 || 2 * pr + 1 < n_rt;  // warpgroup 1 sits out the last, odd pair
       mbar_wait(&S->q_full, qph);
       qph ^= 1u;
       tc_fence_after();
-      // S (pass 1) or S^T (pass 2) for warpgroup w from the current K stage
-      auto issue_s = [&](int w, uint32_t st, bool transposed) {
-        Ring& sb = w ? sb1 : sb0;
-        mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t aq = smem_u32(sQ + w * 16384);
-          const uint32_t d = tmem + w * 128;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t ak = st + h * 16384;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t dq = desc_sw128(aq + k * 32, 0, 1024), dk = desc_sw128(ak + k * 32, 0, 1024);
-              umma_bf16(d, transposed ? dk : dq, transposed ? dq : dk, idS, (h | k) ? 1u : 0u);
+      if (lane == 0) {
+        if (!mine) {
+          // keep the shared K / V rings moving: release each stage after it has been filled
+          for (int pass = 1; pass <= 2; ++pass)
+            for (int kt = 0; kt < n_kt; ++kt) {
+              mbar_wait(&S->k_full[kr.idx], kr.ph);
+              mbar_arrive(&S->k_empty[kr.idx]);
+              kr.next();
+              if (pass == 1) {
+                mbar_wait(&S->v_full[vr.idx], vr.ph);
+                mbar_arrive(&S->v_empty[vr.idx]);
+                vr.next();
+              }
             }
-          }
-          umma_commit(&S->s_full[w]);
-        }
-        __syncwarp();
-        sb.next();
-      };
-      // pass 1
-      for (int kt = 0; kt < n_kt; ++kt) {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        tc_fence_after();
-        const uint32_t st = smem_u32(sKV + kv.idx * 49152);
-        issue_s(0, st, false);
-        if (bval) issue_s(1, st, false);
-        if (lane == 0) umma_commit(&S->kv_empty[kv.idx]);
-        __syncwarp();
-        kv.next();
-      }
-      // pass 2
-      Ring kv_pv = kv;
-      auto issue_st = [&]() {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        tc_fence_after();
-        const uint32_t st = smem_u32(sKV + kv.idx * 49152);
-        issue_s(0, st, true);
-        if (bval) issue_s(1, st, true);
-        kv.next();
-      };
-      issue_st();
-      for (int w = 0; w < 2; ++w) {
-        if (w == 1 && !bval) break;
-        mbar_wait(&S->o_empty[w], oph[w] ^ 1u);
-        oph[w] ^= 1u;
-      }
-      for (int kt = 0; kt < n_kt; ++kt) {
-        if (kt + 1 < n_kt) issue_st();
-        const uint32_t sv = smem_u32(sKV + kv_pv.idx * 49152 + 32768);
-        for (int w = 0; w < 2; ++w) {
-          if (w == 1 && !bval) break;
-          mbar_wait(&S->p_full[w], pph[w]);
-          pph[w] ^= 1u;
-          tc_fence_after();
-          if (lane == 0) {
+          mbar_arrive(&S->q_empty);
+        } else {
+          // pass 1: S(0); then per tile S(kt+1), P.V(kt)
+          auto issue_s_next = [&](bool transposed) {
+            mbar_wait(&S->k_full[kr.idx], kr.ph);
+            mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
+            tc_fence_after();
+            mma_s(kr.idx, transposed);
+            umma_commit(&S->k_empty[kr.idx]);
+            sb.next();
+            kr.next();
+          };
+          issue_s_next(false);
+          if (w == 0) TRACE_R(1, 3, 0);
+          mbar_wait(&S->o_empty[w], oph ^ 1u);
+          oph ^= 1u;
+          for (int kt = 0; kt < n_kt; ++kt) {
+            if (kt + 1 < n_kt) {
+              issue_s_next(false);
+              if (w == 0) TRACE_R(1, 3, kt + 1);
+            }
+            mbar_wait(&S->v_full[vr.idx], vr.ph);
+            mbar_wait(&S->p_full[w], pph);
+            pph ^= 1u;
+            tc_fence_after();
+            const uint32_t sv = smem_u32(sV + vr.idx * 16384);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              umma_bf16(tmem + 256 + w * 64, desc_sw128(aP + k * 2048, 16384, 1024), desc_sw128(sv + k * 2048, 0, 1024),
-                        idO, (kt > 0 || k > 0) ? 1u : 0u);
-            // the shared P^T buffer passes to the other warpgroup (or back, when b is absent)
-            umma_commit(&S->p_free[(w == 0 && bval) ? 1 : 0]);
+              umma_ts(tmem + 256 + w * 64, tmem + 384 + w * 64 + k * 8, desc_sw128(sv + k * 2048, 0, 1024), idO,
+                      (kt > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&S->p_free[w]);          // P_w may be rewritten, O_w is up to date
+            umma_commit(&S->v_empty[vr.idx]);
+            vr.next();
+            if (w == 0) TRACE_R(1, 5 + w, kt);
           }
-          __syncwarp();
+          umma_commit(&S->o_full[w]);
+          // pass 2: S^T per tile
+          for (int kt = 0; kt < n_kt; ++kt) {
+            issue_s_next(true);
+            if (w == 0) TRACE_R(1, 4, kt);
+          }
+          umma_commit(&S->q_empty);
         }
-        if (lane == 0) umma_commit(&S->kv_empty[kv_pv.idx]);
-        __syncwarp();
-        kv_pv.next();
       }
-      if (lane == 0) {
-        umma_commit(&S->o_full[0]);
-        if (bval) umma_commit(&S->o_full[1]);
-        umma_commit(&S->q_empty);
-      }
-      __syncwarp();
+      __syncwarp();   // lanes 1-31 only track q_full; the ring cursors live in lane 0
     }
   } else {
     // ---------------------------------------------------------------- softmax warpgroup wg (128 threads)
     const int wg = warp >> 2, t = tid & 127;
-    const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16) + wg * 128;
-    const uint32_t o_base = tmem + (uint32_t((warp & 3) * 32) << 16) + 256 + wg * 64;
+    const uint32_t lrow = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t s_base = tmem + lrow + wg * 128, o_base = tmem + lrow + 256 + wg * 64;
+    const uint32_t p_base = tmem + lrow + 384 + wg * 64;
     const float cl2 = c.scale * kLog2e;
     float* sc_cmp = wg ? sc_cmp1 : sc_cmp0;
     float* lse_s = S->lse[wg];
     Ring sb(1);
-    // warpgroup 0 writes the shared P^T first; warpgroup 1 waits for warpgroup 0's first P.V
-    uint32_t fph = wg ? 0u : 1u, oph = 0;
+    uint32_t fph = 1u, oph = 0;
     for (int pr = 0; pr < n_pair; ++pr) {
       const int rt = 2 * pr + wg;
-      if (rt >= n_rt) break;                          // only warpgroup 1 in the last, odd pair
+      if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
       const int r = rt * kTile + t;
       const bool rvalid = r < rows;
-      // ---- pass 1: row LSE
+      // ---- pass 1: online softmax, P -> TMEM, O += P V
       float m = -1e30f, l = 0.f;
       for (int kt = 0; kt < n_kt; ++kt) {
         mbar_wait(&S->s_full[wg], sb.ph);
+        if (warp == 0) TRACE_R(2, 7, kt);
         tc_fence_after();
         const int nv = min(kTile, nk - kt * kTile);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {            // 64 columns at a time (register budget)
-          float v[64];
-          tmem_ld32(lane_base + hh * 64, v);
-          tmem_ld32(lane_base + hh * 64 + 32, v + 32);
-          tmem_wait_ld();
-          if (hh == 1) {
-            tc_fence_before();
-            mbar_arrive(&S->s_empty[wg]);
-          }
-          if (nv < kTile) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = hh * 64 + i < nv ? v[i] : -1e30f;
-          }
-          const float mx = fmaxf(max32(v), max32(v + 32)) * cl2;
-          const float mn = fmaxf(m, mx);
-          float acc[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-#pragma unroll
-          for (int i = 0; i < 64; ++i) acc[i & 7] += ex2(fmaf(v[i], cl2, -mn));
-          const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-          l = l * ex2(m - mn) + s;
-          m = mn;
-        }
+        float v[128];
+        tmem_ld32(s_base, v);
+        tmem_ld32(s_base + 32, v + 32);
+        tmem_ld32(s_base + 64, v + 64);
+        tmem_ld32(s_base + 96, v + 96);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&S->s_empty[wg]);
         sb.next();
+        if (nv < kTile) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) v[i] = i < nv ? v[i] : -INFINITY;   // padded keys: p = 0
+        }
+        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
+        const bool bump = mx > m + kRescale;
+        const float m_new = bump ? mx : m;
+        const float alpha = ex2(m - m_new);           // 1 when the reference does not move
+        // P_w(kt-1) consumed and O_w up to date
+        mbar_wait(&S->p_free[wg], fph);
+        fph ^= 1u;
+        tc_fence_after();
+        if (warp == 0) TRACE_R(2, 9, kt);
+        l *= alpha;
+        m = m_new;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int cc = 0; cc < 128; cc += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(v[cc + i], cl2, -m)), p1 = ex2(fmaf(v[cc + i + 1], cl2, -m));
+            acc[(i >> 1) & 3] += p0 + p1;
+            pk[i >> 1] = pack_f16(p0, p1);
+          }
+          tmem_st16(p_base + cc / 2, pk);
+        }
+        l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        // the reference max moved: rescale O_w (P.V(kt-1) has completed: p_free)
+        if (kt > 0 && __any_sync(0xffffffffu, bump)) {
+#pragma unroll
+          for (int cc = 0; cc < kD; cc += 16) {
+            float o[16];
+            tmem_ld16(o_base + cc, o);
+            tmem_wait_ld();
+            uint32_t ou[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ou[i] = __float_as_uint(o[i] * alpha);
+            tmem_st16(o_base + cc, ou);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&S->p_full[wg]);
+        if (warp == 0) TRACE_R(2, 11, kt);
       }
-      const float lse2 = rvalid ? m + lg2(l) : INFINITY;
+      // ---- O = (sum_j p_j v_j) / l, LSE (log2 domain)
+      const float lse2 = rvalid ? m + lg2(l) : INFINITY;   // padded rows: p = 0 in pass 2
+      const float inv_l = 1.f / l;
+      mbar_wait(&S->o_full[wg], oph);
+      oph ^= 1u;
+      tc_fence_after();
+      float* oc = static_cast<float*>(c.o[0]) + int64_t(qrow0 + r) * kD;
+#pragma unroll
+      for (int cc = 0; cc < kD; cc += 32) {
+        float o[32];
+        tmem_ld32(o_base + cc, o);
+        tmem_wait_ld();
+        if (rvalid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(oc + cc + i) =
+                make_float4(o[i] * inv_l, o[i + 1] * inv_l, o[i + 2] * inv_l, o[i + 3] * inv_l);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&S->o_empty[wg]);
+      if (rvalid) c.lse[0][qrow0 + r] = lse2;   // saved LSEs are log2-domain
       named_bar_sync(1 + wg, 128);     // this warpgroup's previous pass 2 finished reading lse_s
       lse_s[t] = lse2;
-      if (rvalid) c.lse[0][qrow0 + r] = lse2;   // saved LSEs are log2-domain
       named_bar_sync(1 + wg, 128);
-      // ---- pass 2: thread = key; P^T row -> shared buffer; exact fp32 column sums
+      // ---- pass 2: thread = key; exact fp32 Eq. 8 column sums of exp2(S^T c - LSE)
       for (int kt = 0; kt < n_kt; ++kt) {
         const bool kvalid = kt * kTile + t < nk;
         mbar_wait(&S->s_full[wg], sb.ph);
+        if (warp == 0) TRACE_R(2, 8, kt);
         tc_fence_after();
-        uint32_t pk[64];
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c00 = 0; c00 < kTile; c00 += 32) {
           float v[32];
-          tmem_ld32(lane_base + c00, v);
+          tmem_ld32(s_base + c00, v);
           tmem_wait_ld();
           if (c00 == kTile - 32) {
             tc_fence_before();
@@ -323,51 +416,16 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           }
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 L = *reinterpret_cast<const float4*>(&lse_s[c00 + i]);
-            const float p0 = ex2(fmaf(v[i], cl2, -L.x)), p1 = ex2(fmaf(v[i + 1], cl2, -L.y));
-            const float p2 = ex2(fmaf(v[i + 2], cl2, -L.z)), p3 = ex2(fmaf(v[i + 3], cl2, -L.w));
-            cs[0] += p0; cs[1] += p1; cs[2] += p2; cs[3] += p3;
-            pk[(c00 + i) / 2] = pack_f16(p0, p1);
-            pk[(c00 + i) / 2 + 1] = pack_f16(p2, p3);
+            const float4 L = ld_shared_f4(&lse_s[c00 + i]);
+            cs[0] += ex2(fmaf(v[i], cl2, -L.x));
+            cs[1] += ex2(fmaf(v[i + 1], cl2, -L.y));
+            cs[2] += ex2(fmaf(v[i + 2], cl2, -L.z));
+            cs[3] += ex2(fmaf(v[i + 3], cl2, -L.w));
           }
         }
         sb.next();
-        float colsum = (cs[0] + cs[1]) + (cs[2] + cs[3]);
-        if (!kvalid) {
-          colsum = 0.f;
-#pragma unroll
-          for (int i = 0; i < 64; ++i) pk[i] = 0u;
-        }
-        mbar_wait(&S->p_free[wg], fph);
-        fph ^= 1u;
-        const uint32_t pbase = smem_u32(sP);
-#pragma unroll
-        for (int ch = 0; ch < 16; ++ch)      // 16 chunks of 8 rows: row block ch/8, chunk ch%8
-          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(t, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
-                       pk[4 * ch + 3]);
-        fence_proxy_async_smem();
-        mbar_arrive(&S->p_full[wg]);
-        if (kvalid) sc_cmp[kt * kTile + t] += colsum;
+        if (kvalid) sc_cmp[kt * kTile + t] += (cs[0] + cs[1]) + (cs[2] + cs[3]);
       }
-      // when b is absent in this pair, the MMA returned the buffer to warpgroup 0 (one extra phase)
-      // ---- O (fixed normalisation, accumulated over all key tiles in TMEM)
-      mbar_wait(&S->o_full[wg], oph);
-      oph ^= 1u;
-      tc_fence_after();
-      float* oc = static_cast<float*>(c.o[0]) + int64_t(qrow0 + r) * kD;
-#pragma unroll
-      for (int cc = 0; cc < kD; cc += 32) {
-        float v[32];
-        tmem_ld32(o_base + cc, v);
-        tmem_wait_ld();
-        if (rvalid) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(oc + cc + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&S->o_empty[wg]);
     }
     // ---- Eq. 8 selection-block scores and top-k (both softmax warpgroups, 256 threads)
     named_bar_sync(3, 256);
@@ -416,6 +474,13 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     named_bar_sync(3, 256);
     for (int j = tid; j < c.T; j += 256) c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + S->chosen[j] : -1;
   }
+#ifdef SSA_TRACE
+  if (TRACE_ON && (warp == 8 || warp == 9 || warp == 0)) {
+    const int role = warp == 8 ? 0 : (warp == 9 ? 1 : 2);
+    for (int i = 0; i < tr_n; ++i) g_trace[role][i] = S->trace[role][i];
+    g_trace_cnt[role] = tr_n;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tmem);
@@ -694,7 +759,7 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
 }
 
 bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
-  const size_t smem = 1024 + 32768 + kCmpStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+  const size_t smem = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16 +
                       (2 * size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
   const int slc_tiles = (info.max_fill[SSA_LEVEL_SLC] + 111) / 112;
   const int dq_tiles = (info.max_blocks_per_batch[SSA_LEVEL_CMP] + 111) / 112 + top_k * slc_tiles + slc_tiles;
@@ -721,7 +786,7 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
   TcArgs a{c, kc_hi, kc_lo, vc};
   const int nq = c.n_blk[SSA_LEVEL_Q];
   {
-    const size_t smem = 1024 + 32768 + kCmpStages * 49152 + 32768 + sizeof(CmpSmem) + 16 +
+    const size_t smem = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16 +
                         (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
     if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -740,3 +805,17 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
 }
 
 }  // namespace ssa
+
+#ifdef SSA_TRACE
+extern "C" int ssa_debug_trace(unsigned long long* host, int cap) {
+  int cnt[3];
+  unsigned long long buf[3][128];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(cnt, ssa::g_trace_cnt, sizeof(cnt));
+  cudaMemcpyFromSymbol(buf, ssa::g_trace, sizeof(buf));
+  int n = 0;
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < cnt[r] && n < cap; ++i) host[n++] = buf[r][i];
+  return n;
+}
+#endif
