@@ -306,11 +306,18 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     float* lse_s = S->lse[wg];
     Ring sb(1);
     uint32_t fph = 1u, oph = 0;
+    // MUFU ping-pong: the two warpgroups take turns in their exponential loops (named barriers 4 / 5),
+    // so each loop runs at the full MUFU rate while the other warpgroup loads S, waits or stores.
+    // Warpgroup 1 hands warpgroup 0 the first turn.
+    if (wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);
     for (int pr = 0; pr < n_pair; ++pr) {
       const int rt = 2 * pr + wg;
       if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
       const int r = rt * kTile + t;
       const bool rvalid = r < rows;
+      const bool duo = 2 * pr + 1 < n_rt;             // both warpgroups in this pair
+      auto turn_begin = [&]() { if (duo) named_bar_sync(4 + wg, 256); };
+      auto turn_end = [&]() { if (duo) named_bar_arrive(5 - wg, 256); };
       // ---- pass 1: online softmax, P -> TMEM, O += P V
       float m = -1e30f, l = 0.f;
       for (int kt = 0; kt < n_kt; ++kt) {
@@ -343,6 +350,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         l *= alpha;
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        turn_begin();
 #pragma unroll
         for (int cc = 0; cc < 128; cc += 32) {
           uint32_t pk[16];
@@ -354,6 +362,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           }
           tmem_st16(p_base + cc / 2, pk);
         }
+        turn_end();
         l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         // the reference max moved: rescale O_w (P.V(kt-1) has completed: p_free)
         if (kt > 0 && __any_sync(0xffffffffu, bump)) {
@@ -405,6 +414,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         if (warp == 0) TRACE_R(2, 8, kt);
         tc_fence_after();
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
+        turn_begin();
 #pragma unroll
         for (int c00 = 0; c00 < kTile; c00 += 32) {
           float v[32];
@@ -423,6 +433,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             cs[3] += ex2(fmaf(v[i + 3], cl2, -L.w));
           }
         }
+        turn_end();
         sb.next();
         if (kvalid) sc_cmp[kt * kTile + t] += (cs[0] + cs[1]) + (cs[2] + cs[3]);
       }
