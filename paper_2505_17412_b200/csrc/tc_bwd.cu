@@ -75,28 +75,53 @@ __global__ void k_tc_bwd_prep(Ctx c, __half* q16, __half* do16, __half* dow, __h
 // ================================================================================================
 // dQ (Q-outer)
 // ================================================================================================
-constexpr int kKT = 112;                 // keys per tile: 2 x (S 112 + dP 112) + dQ 64 = 512 TMEM cols
+// 352 threads: warps 0-3 / 4-7 = warpgroups 0 / 1, each owning one 128-row tile of a row-tile pair
+// (thread i <-> TMEM lane i), warp 8 = TMA producer, warps 9 / 10 = MMA issuers of warpgroups 0 / 1
+// (warp 9 owns TMEM). Both row tiles share every K/V tile load. TMEM per warpgroup w (256 columns
+// at w * 256): S [0, 96) | dP [96, 192) | dQ [192, 256). The warpgroups take turns in their
+// exponential loops (named barriers 4 / 5) so each runs at the full MUFU rate.
+constexpr int kKT = 96;                  // keys per tile
+constexpr int kDqThreads = 352;
 constexpr int kMaxKT = 64 + 4 * 64 * 2 + 16;
+constexpr int kKVBytes = kKT * 128;      // one K or V tile (bf16/fp16, 64 wide)
+#ifndef SSA_DQ_PINGPONG
+#define SSA_DQ_PINGPONG 1
+#endif
+constexpr bool kDqPingPong = SSA_DQ_PINGPONG;
+#ifdef SSA_TRACE
+__device__ unsigned long long g_trace_dq[3][128];
+__device__ int g_trace_dq_cnt[3];
+#define TRACE_ON (blockIdx.x == 5 && blockIdx.y == 0 && (threadIdx.x & 31) == 0)
+#define TRACE_R(role, ev, j)                                                                              \
+  do {                                                                                                  \
+    if (TRACE_ON && tr_n < 128) S->trace[role][tr_n++] = (clock64() << 16) | (unsigned long long)(((ev) << 12) | ((j) & 0xfff)); \
+  } while (0)
+#else
+#define TRACE_R(role, ev, j) do { } while (0)
+#endif
 struct DqSmem {
   uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], ds_full[2], ds_empty[2],
-      dq_full, dq_empty;
+      dq_full[2], dq_empty[2];
   uint32_t tmem;
   int n_tiles;
   int tile_row[kMaxKT];                   // row in the key array of the tile's branch
   int tile_nv[kMaxKT];
   int8_t tile_br[kMaxKT];
+#ifdef SSA_TRACE
+  unsigned long long trace[3][128];
+#endif
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDqThreads, 1)
 k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
         __grid_constant__ const CUtensorMap tmKc, __grid_constant__ const CUtensorMap tmVc,
         __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                       // 16 KB
-  uint8_t* sDO = sm + 16384;              // 16 KB
-  uint8_t* sKV = sm + 32768;              // kStages x {K 16 KB, V 16 KB}
-  uint8_t* sDS = sKV + kStages * 32768;   // 2 x 32 KB: dS K-major, 2 key blocks x [128 rows][128 B]
+  uint8_t* sQ = sm;                       // 2 x 16 KB (row tiles of the pair)
+  uint8_t* sDO = sm + 32768;              // 2 x 16 KB
+  uint8_t* sKV = sm + 65536;              // kStages x {K, V} (kKVBytes each)
+  uint8_t* sDS = sKV + kStages * 2 * kKVBytes;   // 2 x 32 KB: dS K-major, 2 key blocks x [128 rows][128 B]
   DqSmem* S = reinterpret_cast<DqSmem*>(sDS + 65536);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -105,20 +130,21 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + 127) / 128;
+  const int n_pair = (n_rt + 1) / 2;
   const int qrow0 = (g * c.N + t0) * c.h_s;
 
   if (tid == 0) {
     mbar_init(&S->q_full, 1);
-    mbar_init(&S->q_empty, 1);
-    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    mbar_init(&S->q_empty, 2);                        // one arrival per MMA issuer
+    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 2); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
       mbar_init(&S->ds_full[i], 128);
       mbar_init(&S->ds_empty[i], 1);
+      mbar_init(&S->dq_full[i], 1);
+      mbar_init(&S->dq_empty[i], 128);
     }
-    mbar_init(&S->dq_full, 1);
-    mbar_init(&S->dq_empty, 128);
     fence_barrier_init();
     int n = 0;
     const int b = c.q_batch[Q];
@@ -134,159 +160,195 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
     for (int x = t0; x < t1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * c.N + x; S->tile_nv[n] = min(kKT, t1 - x); S->tile_br[n] = 2; ++n; }
     S->n_tiles = n;
   }
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmKc); tma_prefetch(&tmVc); tma_prefetch(&tmK); tma_prefetch(&tmV);
   }
-  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem;
   const int n_tiles = S->n_tiles;
+#ifdef SSA_TRACE
+  int tr_n = 0;
+#endif
 
-  if (warp == 4) {
+  if (warp == 8) {
+    // ---------------------------------------------------------------- TMA producer
     Ring kv(kStages);
     uint32_t qph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool duo = 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_empty, qph ^ 1u);
       qph ^= 1u;
       if (lane == 0) {
-        mbar_expect_tx(&S->q_full, 32768);
-        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * 128);
-        tma_load_2d(sDO, &tmDO, &S->q_full, 0, qrow0 + rt * 128);
+        mbar_expect_tx(&S->q_full, duo ? 65536u : 32768u);
+        for (int w = 0; w < (duo ? 2 : 1); ++w) {
+          tma_load_2d(sQ + w * 16384, &tmQ, &S->q_full, 0, qrow0 + (2 * pr + w) * 128);
+          tma_load_2d(sDO + w * 16384, &tmDO, &S->q_full, 0, qrow0 + (2 * pr + w) * 128);
+        }
       }
       for (int j = 0; j < n_tiles; ++j) {
         mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
+        TRACE_R(0, 1, j);
         if (lane == 0) {
-          uint8_t* st = sKV + kv.idx * 32768;
+          uint8_t* st = sKV + kv.idx * 2 * kKVBytes;
           const bool cmp = S->tile_br[j] == 0;
-          mbar_expect_tx(&S->kv_full[kv.idx], 2u * kKT * 128u);
+          mbar_expect_tx(&S->kv_full[kv.idx], 2u * kKVBytes);
           tma_load_2d(st, cmp ? &tmKc : &tmK, &S->kv_full[kv.idx], 0, S->tile_row[j]);
-          tma_load_2d(st + 16384, cmp ? &tmVc : &tmV, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+          tma_load_2d(st + kKVBytes, cmp ? &tmVc : &tmV, &S->kv_full[kv.idx], 0, S->tile_row[j]);
         }
         __syncwarp();
         kv.next();
       }
     }
-  } else if (warp == 5) {
+  } else if (warp >= 9) {
+    // ---------------------------------------------------------------- MMA issuer of warpgroup w
+    const int w = warp - 9;
     const uint32_t idS = idesc_f16(128, kKT, false, false);    // S = Q K^T, dP = dO V^T
     const uint32_t idQ = idesc_f16(128, 64, false, true);      // dQ += dS K (K as MN-major B)
-    const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO);
-    Ring kv(kStages), sb(2), db(2);
+    const uint32_t aQ = smem_u32(sQ + w * 16384), aDO = smem_u32(sDO + w * 16384);
+    const uint32_t tS = tmem + w * 256, tQ = tS + 192;
+    Ring kv(kStages), sb(1), db(1);
     uint32_t qph = 0, dqph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool mine = w == 0 || 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_full, qph);
       qph ^= 1u;
       tc_fence_after();
-      Ring kv_q = kv;
-      auto issue_s = [&]() {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sk = smem_u32(sKV + kv.idx * 32768);
-          const uint32_t d = tmem + sb.idx * 224;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS, k > 0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(d + kKT, desc_sw128(aDO + k * 32, 0, 1024), desc_sw128(sk + 16384 + k * 32, 0, 1024), idS, k > 0);
-          umma_commit(&S->s_full[sb.idx]);
-        }
-        __syncwarp();
-        kv.next();
-        sb.next();
-      };
-      issue_s();
-      mbar_wait(&S->dq_empty, dqph ^ 1u);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s();
-        mbar_wait(&S->ds_full[db.idx], db.ph);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ads = smem_u32(sDS + db.idx * 32768);
-          const uint32_t sk = smem_u32(sKV + kv_q.idx * 32768);
-#pragma unroll
-          for (int k = 0; k < kKT / 16; ++k)
-            umma_bf16(tmem + 448, desc_sw128(ads + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024),
-                      desc_sw128(sk + k * 2048, 0, 1024), idQ, (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&S->ds_empty[db.idx]);
-          umma_commit(&S->kv_empty[kv_q.idx]);
-        }
-        __syncwarp();
-        kv_q.next();
-        db.next();
-      }
       if (lane == 0) {
-        umma_commit(&S->dq_full);
-        umma_commit(&S->q_empty);
+        if (!mine) {
+          for (int j = 0; j < n_tiles; ++j) {   // keep the shared K/V ring moving
+            mbar_wait(&S->kv_full[kv.idx], kv.ph);
+            mbar_arrive(&S->kv_empty[kv.idx]);
+            kv.next();
+          }
+          mbar_arrive(&S->q_empty);
+        } else {
+          Ring kv_q = kv;
+          auto issue_s = [&]() {
+            mbar_wait(&S->kv_full[kv.idx], kv.ph);
+            mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
+            tc_fence_after();
+            const uint32_t sk = smem_u32(sKV + kv.idx * 2 * kKVBytes);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tS, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS, k > 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tS + kKT, desc_sw128(aDO + k * 32, 0, 1024), desc_sw128(sk + kKVBytes + k * 32, 0, 1024), idS,
+                        k > 0);
+            umma_commit(&S->s_full[w]);
+            kv.next();
+            sb.next();
+          };
+          issue_s();
+          mbar_wait(&S->dq_empty[w], dqph ^ 1u);
+          dqph ^= 1u;
+          for (int j = 0; j < n_tiles; ++j) {
+            if (j + 1 < n_tiles) issue_s();
+            if (w == 0) TRACE_R(1, 3, j + 1);
+            mbar_wait(&S->ds_full[w], db.ph);
+            tc_fence_after();
+            const uint32_t ads = smem_u32(sDS + w * 32768);
+            const uint32_t sk = smem_u32(sKV + kv_q.idx * 2 * kKVBytes);
+#pragma unroll
+            for (int k = 0; k < kKT / 16; ++k)
+              umma_bf16(tQ, desc_sw128(ads + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024), desc_sw128(sk + k * 2048, 0, 1024),
+                        idQ, (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&S->ds_empty[w]);
+            umma_commit(&S->kv_empty[kv_q.idx]);
+            if (w == 0) TRACE_R(1, 5, j);
+            kv_q.next();
+            db.next();
+          }
+          umma_commit(&S->dq_full[w]);
+          umma_commit(&S->q_empty);
+        }
       }
-      __syncwarp();
-      dqph ^= 1u;
+      __syncwarp();   // lanes 1-31 only track q_full; the ring cursors live in lane 0
     }
   } else {
-    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    // ---------------------------------------------------------------- softmax / dS warpgroup wg
+    const int wg = warp >> 2, t = tid & 127;
+    const uint32_t lrow = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lrow + wg * 256, tQ = tS + 192;
     const float cl2 = c.scale * kLog2e;
-    Ring sb(2), db(2);
+    Ring sb(1), db(1);
     uint32_t dqph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
-      const int r = rt * 128 + tid;
+    if (kDqPingPong && wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);   // warpgroup 0 takes the first turn
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const int rt = 2 * pr + wg;
+      if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
+      const bool duo = 2 * pr + 1 < n_rt;
+      const int r = rt * 128 + t;
       const bool rvalid = r < rows;
       const int64_t row = qrow0 + (rvalid ? r : 0);
-      float lse2[3], w[3], Dv[3];
+      float lse2[3], wgt[3], Dv[3];
 #pragma unroll
       for (int br = 0; br < 3; ++br) {
         lse2[br] = rvalid ? c.lse[br][row] : INFINITY;
-        w[br] = c.gs[row * 3 + br];
+        wgt[br] = c.gs[row * 3 + br];
         Dv[br] = c.Dd[br][row];
       }
       for (int j = 0; j < n_tiles; ++j) {
         const int br = S->tile_br[j], nv = S->tile_nv[j];
         const float l2 = br == 0 ? lse2[0] : (br == 1 ? lse2[1] : lse2[2]);
-        const float wb = br == 0 ? w[0] : (br == 1 ? w[1] : w[2]);
+        const float wb = br == 0 ? wgt[0] : (br == 1 ? wgt[1] : wgt[2]);
         const float Db = br == 0 ? Dv[0] : (br == 1 ? Dv[1] : Dv[2]);
-        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        mbar_wait(&S->s_full[wg], sb.ph);
+        if (warp == 0) TRACE_R(2, 7, j);
         tc_fence_after();
         uint32_t pk[kKT / 2];
+        if (kDqPingPong && duo) named_bar_sync(4 + wg, 256);
+        if (warp == 0) TRACE_R(2, 8, j);
 #pragma unroll
-        for (int c0 = 0; c0 < kKT; c0 += 16) {
-          float s[16], dp[16];
-          tmem_ld16(lane_base + sb.idx * 224 + c0, s);
-          tmem_ld16(lane_base + sb.idx * 224 + kKT + c0, dp);
+        for (int c0 = 0; c0 < kKT; c0 += 32) {
+          float s[32], dp[32];
+          tmem_ld32(tS + c0, s);
+          tmem_ld32(tS + kKT + c0, dp);
           tmem_wait_ld();
+          if (c0 + 32 == kKT) {
+            tc_fence_before();
+            mbar_arrive(&S->s_empty[wg]);
+          }
+          if (nv < kKT) {                            // partial tile (uniform): padded keys get p = 0
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const float p0 = (c0 + i < nv) ? ex2(fmaf(s[i], cl2, -l2)) : 0.f;
-            const float p1 = (c0 + i + 1 < nv) ? ex2(fmaf(s[i + 1], cl2, -l2)) : 0.f;
-            pk[(c0 + i) / 2] = pack_f16(p0 * (wb * dp[i] - Db), p1 * (wb * dp[i + 1] - Db));
+            for (int i = 0; i < 32; ++i) s[i] = c0 + i < nv ? s[i] : -INFINITY;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(s[i], cl2, -l2)), p1 = ex2(fmaf(s[i + 1], cl2, -l2));
+            pk[(c0 + i) / 2] = pack_f16(p0 * fmaf(wb, dp[i], -Db), p1 * fmaf(wb, dp[i + 1], -Db));
           }
         }
-        tc_fence_before();
-        mbar_arrive(&S->s_empty[sb.idx]);
+        if (kDqPingPong && duo) named_bar_arrive(5 - wg, 256);
+        if (warp == 0) TRACE_R(2, 9, j);
         sb.next();
-        mbar_wait(&S->ds_empty[db.idx], db.ph ^ 1u);
-        const uint32_t base = smem_u32(sDS + db.idx * 32768);
+        mbar_wait(&S->ds_empty[wg], db.ph ^ 1u);
+        if (warp == 0) TRACE_R(2, 10, j);
+        const uint32_t base = smem_u32(sDS + wg * 32768);
 #pragma unroll
         for (int ch = 0; ch < kKT / 8; ++ch)
-          st_shared_v4(base + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+          st_shared_v4(base + (ch >> 3) * 16384 + sw128(t, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
                        pk[4 * ch + 3]);
         fence_proxy_async_smem();
-        mbar_arrive(&S->ds_full[db.idx]);
+        mbar_arrive(&S->ds_full[wg]);
+        if (warp == 0) TRACE_R(2, 11, j);
         db.next();
       }
-      mbar_wait(&S->dq_full, dqph);
+      mbar_wait(&S->dq_full[wg], dqph);
       dqph ^= 1u;
       tc_fence_after();
       float v[64];
-      tmem_ld32(lane_base + 448, v);
-      tmem_ld32(lane_base + 448 + 32, v + 32);
+      tmem_ld32(tQ, v);
+      tmem_ld32(tQ + 32, v + 32);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&S->dq_empty);
+      mbar_arrive(&S->dq_empty[wg]);
       if (rvalid) {
-        const int t = t0 + r / c.h_s, hs = r % c.h_s;
-        const int dst = c.sorted_input ? t : c.perm[t];
+        const int tok = t0 + r / c.h_s, hs = r % c.h_s;
+        const int dst = c.sorted_input ? tok : c.perm[tok];
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
 #pragma unroll
         for (int e = 0; e < kD; e += 8)
@@ -296,10 +358,19 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       }
     }
   }
+#ifdef SSA_TRACE
+  if (TRACE_ON && (warp == 8 || warp == 9 || warp == 0)) {
+    const int role = warp == 8 ? 0 : (warp == 9 ? 1 : 2);
+    for (int i = 0; i < tr_n; ++i) g_trace_dq[role][i] = S->trace[role][i];
+    g_trace_dq_cnt[role] = tr_n;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
+#undef TRACE_R
+#undef TRACE_ON
 
 // ================================================================================================
 // dK / dV (KV-outer)
@@ -758,10 +829,10 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
       !make_tmap_bf16_2d(&tmK128, k16, krows, 128) || !make_tmap_bf16_2d(&tmV128, v16, krows, 128))
     return SSA_ERR_CUDA;
   {
-    const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(DqSmem);
+    const size_t smem = 1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem);
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_bwd_dq", st);
-    k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
+    k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
   const size_t smem = 1024 + 32768 + kRStages * 16384 + 32768 + sizeof(KvSmem);
@@ -790,3 +861,17 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
 }
 
 }  // namespace ssa
+
+#ifdef SSA_TRACE
+extern "C" int ssa_debug_trace_dq(unsigned long long* host, int cap) {
+  int cnt[3];
+  unsigned long long buf[3][128];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(cnt, ssa::g_trace_dq_cnt, sizeof(cnt));
+  cudaMemcpyFromSymbol(buf, ssa::g_trace_dq, sizeof(buf));
+  int n = 0;
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < cnt[r] && n < cap; ++i) host[n++] = buf[r][i];
+  return n;
+}
+#endif

@@ -772,8 +772,8 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
 bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
   const size_t smem = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16 +
                       (2 * size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
-  const int slc_tiles = (info.max_fill[SSA_LEVEL_SLC] + 111) / 112;
-  const int dq_tiles = (info.max_blocks_per_batch[SSA_LEVEL_CMP] + 111) / 112 + top_k * slc_tiles + slc_tiles;
+  const int slc_tiles = (info.max_fill[SSA_LEVEL_SLC] + 95) / 96;      // dQ key tiles of 96 (tc_bwd.cu)
+  const int dq_tiles = (info.max_blocks_per_batch[SSA_LEVEL_CMP] + 95) / 96 + top_k * slc_tiles + slc_tiles;
   return smem <= 232448 && dq_tiles <= 64 + 4 * 64 * 2 + 16 && top_k * ((info.max_fill[SSA_LEVEL_SLC] + 127) / 128) +
          (info.max_fill[SSA_LEVEL_SLC] + 127) / 128 <= 4 * 64 + 8;
 }

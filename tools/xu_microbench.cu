@@ -7,6 +7,9 @@
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ unsigned pk(float a, float b) { __half2 h = __floats2half2_rn(a, b); return *(unsigned*)&h; }
 
+__device__ __forceinline__ unsigned ex2h2(unsigned x) { unsigned y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ unsigned ex2bf2(unsigned x) { unsigned y; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+
 template <int MODE>
 __global__ void k(float* out, int iters) {
   float a[8];
@@ -19,6 +22,8 @@ __global__ void k(float* out, int iters) {
       if (MODE == 0) a[i] = ex2(a[i]) - 1.0f;                  // ex2 only (+1 FADD)
       if (MODE == 1) { u ^= pk(a[i], a[(i + 1) & 7]); a[i] += 1e-7f; }   // pack only
       if (MODE == 2) { float e = ex2(a[i]) - 1.0f; u ^= pk(e, a[(i + 1) & 7]); a[i] = e; }  // ex2 + pack per element pair
+      if (MODE == 3) { unsigned h = ex2h2(__float_as_uint(a[i])); a[i] = __uint_as_float(h ^ 0x80008000u); }   // f16x2 ex2 (2 results)
+      if (MODE == 4) { unsigned h = ex2bf2(__float_as_uint(a[i])); a[i] = __uint_as_float(h ^ 0x80008000u); }  // bf16x2 ex2 (2 results)
     }
   }
   float s = 0;
@@ -55,5 +60,8 @@ int main() {
   run<2>("ex2+pack, full occ", 148 * 4, 512, 4000);
   run<2>("ex2+pack, 1 warp/SMSP", 148, 128, 4000);
   run<2>("ex2+pack, 2 warps/SMSP", 148, 256, 4000);
+  run<3>("ex2.f16x2 (x2 results)", 148 * 4, 512, 4000);
+  run<3>("ex2.f16x2 1 warp/SMSP", 148, 128, 4000);
+  run<4>("ex2.bf16x2 (x2 results)", 148 * 4, 512, 4000);
   return 0;
 }
