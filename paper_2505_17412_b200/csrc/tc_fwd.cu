@@ -26,9 +26,7 @@ using namespace tc;
 
 constexpr int kD = 64;
 constexpr int kTile = 128;
-constexpr int kThreads = 192;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kStages = 3;
 
 #ifdef SSA_TRACE
@@ -500,9 +498,16 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 // ================================================================================================
 // selection + window attention + gated sum
 // ================================================================================================
+// 352 threads, same roles as the compression kernel: warpgroups 0 / 1 own the two 128-row tiles of a
+// row-tile pair (thread i <-> TMEM lane i), warp 8 = TMA producer, warps 9 / 10 = MMA issuers.
+// Online softmax with lazy rescaling; P (fp16) goes to TMEM and O += P V runs with A from TMEM.
+// TMEM per warpgroup w (256 columns at w * 256): S [0, 128) | P [128, 192) | O [192, 256).
+// Key tiles: the T selected blocks (ascending), then the window (== the query block: m_win == m_q);
+// at the branch boundary the selection O is normalised and stored, and O restarts from zero.
 constexpr int kMaxTiles = 4 * 64 + 8;
+constexpr int kSwThreads = 352;
 struct SwSmem {
-  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_empty[2],
+  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_free[2],
       o_full[2], o_empty[2];
   uint32_t tmem;
   int n_tiles, n_slc_tiles;
@@ -510,15 +515,14 @@ struct SwSmem {
   int tile_nv[kMaxTiles];
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kSwThreads, 1)
 k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmK,
                 __grid_constant__ const CUtensorMap tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                          // 16 KB
-  uint8_t* sKV = sm + 16384;                 // kStages x {K, V} 32 KB
-  uint8_t* sP = sKV + kStages * 32768;       // 2 x 32 KB, P K-major: 2 key blocks x [128 rows][128 B]
-  SwSmem* S = reinterpret_cast<SwSmem*>(sP + 65536);
+  uint8_t* sQ = sm;                          // 2 x 16 KB (row tiles of the pair)
+  uint8_t* sKV = sm + 32768;                 // kStages x {K, V} 32 KB
+  SwSmem* S = reinterpret_cast<SwSmem*>(sKV + kStages * 32768);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
@@ -526,23 +530,23 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + kTile - 1) / kTile;
+  const int n_pair = (n_rt + 1) / 2;
   const int qrow0 = (g * c.N + t0) * c.h_s;
   const int krow_g = g * c.N;
 
   if (tid == 0) {
     mbar_init(&S->q_full, 1);
-    mbar_init(&S->q_empty, 1);
-    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 1); }
+    mbar_init(&S->q_empty, 2);                        // one arrival per MMA issuer
+    for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 2); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
       mbar_init(&S->p_full[i], 128);
-      mbar_init(&S->p_empty[i], 1);
+      mbar_init(&S->p_free[i], 1);
       mbar_init(&S->o_full[i], 1);
       mbar_init(&S->o_empty[i], 128);
     }
     fence_barrier_init();
-    // key tile list: selected blocks (ascending), then the window (== the query block: m_win == m_q)
     int n = 0;
     for (int j = 0; j < c.T; ++j) {
       const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
@@ -554,23 +558,26 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     for (int x = t0; x < t1 && n < kMaxTiles; x += kTile) { S->tile_row[n] = x; S->tile_nv[n] = min(kTile, t1 - x); ++n; }
     S->n_tiles = n;
   }
-  if (warp == 4 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
-  if (warp == 5) tmem_alloc<512>(&S->tmem);
+  if (warp == 8 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
+  if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem;
   const int n_tiles = S->n_tiles, n_slc_tiles = S->n_slc_tiles;
 
-  if (warp == 4) {
+  if (warp == 8) {
+    // ---------------------------------------------------------------- TMA producer
     Ring kv(kStages);
     uint32_t qph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool duo = 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_empty, qph ^ 1u);
       qph ^= 1u;
       if (lane == 0) {
-        mbar_expect_tx(&S->q_full, 16384);
-        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + rt * kTile);
+        mbar_expect_tx(&S->q_full, duo ? 32768u : 16384u);
+        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + 2 * pr * kTile);
+        if (duo) tma_load_2d(sQ + 16384, &tmQ, &S->q_full, 0, qrow0 + (2 * pr + 1) * kTile);
       }
       for (int j = 0; j < n_tiles; ++j) {
         mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
@@ -584,144 +591,175 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         kv.next();
       }
     }
-  } else if (warp == 5) {
+  } else if (warp >= 9) {
+    // ---------------------------------------------------------------- MMA issuer of warpgroup w
+    const int w = warp - 9;
     const uint32_t idS = idesc_bf16(128, 128, false, false);
-    const uint32_t idO = idesc_f16(128, 64, false, true);
-    const uint32_t aQ = smem_u32(sQ);
-    Ring kv(kStages), sb(2), pb(2), ob(2);
-    uint32_t qph = 0;
-    for (int rt = 0; rt < n_rt; ++rt) {
+    const uint32_t idO = idesc_f16(128, 64, false, true);    // P from TMEM, V MN-major
+    const uint32_t aQ = smem_u32(sQ + w * 16384);
+    const uint32_t tS = tmem + w * 256, tP = tS + 128, tO = tS + 192;
+    Ring kv(kStages), sb(1);
+    uint32_t qph = 0, pph = 0, oph = 0;
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const bool mine = w == 0 || 2 * pr + 1 < n_rt;
       mbar_wait(&S->q_full, qph);
       qph ^= 1u;
       tc_fence_after();
-      Ring kv_pv = kv;
-      auto issue_s = [&]() {
-        mbar_wait(&S->kv_full[kv.idx], kv.ph);
-        mbar_wait(&S->s_empty[sb.idx], sb.ph ^ 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sk = smem_u32(sKV + kv.idx * 32768);
+      if (lane == 0) {
+        if (!mine) {
+          for (int j = 0; j < n_tiles; ++j) {   // keep the shared K/V ring moving
+            mbar_wait(&S->kv_full[kv.idx], kv.ph);
+            mbar_arrive(&S->kv_empty[kv.idx]);
+            kv.next();
+          }
+          mbar_arrive(&S->q_empty);
+        } else {
+          Ring kv_pv = kv;
+          auto issue_s = [&]() {
+            mbar_wait(&S->kv_full[kv.idx], kv.ph);
+            mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
+            tc_fence_after();
+            const uint32_t sk = smem_u32(sKV + kv.idx * 32768);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + sb.idx * 128, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS,
-                      k > 0);
-          umma_commit(&S->s_full[sb.idx]);
-        }
-        __syncwarp();
-        kv.next();
-        sb.next();
-      };
-      issue_s();
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s();
-        mbar_wait(&S->p_full[pb.idx], pb.ph);
-        mbar_wait(&S->o_empty[ob.idx], ob.ph ^ 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ap = smem_u32(sP + pb.idx * 32768);
-          const uint32_t sv = smem_u32(sKV + kv_pv.idx * 32768 + 16384);
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tS, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS, k > 0);
+            umma_commit(&S->s_full[w]);
+            kv.next();
+            sb.next();
+          };
+          issue_s();
+          mbar_wait(&S->o_empty[w], oph ^ 1u);
+          oph ^= 1u;
+          for (int j = 0; j < n_tiles; ++j) {
+            if (j + 1 < n_tiles) issue_s();
+            mbar_wait(&S->p_full[w], pph);
+            pph ^= 1u;
+            tc_fence_after();
+            const uint32_t sv = smem_u32(sKV + kv_pv.idx * 32768 + 16384);
+            const bool fresh = j == 0 || j == n_slc_tiles;   // first tile of a branch: O restarts
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            umma_bf16(tmem + 256 + ob.idx * 64, desc_sw128(ap + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024),
-                      desc_sw128(sv + k * 2048, 0, 1024), idO, k > 0);
-          umma_commit(&S->o_full[ob.idx]);
-          umma_commit(&S->p_empty[pb.idx]);
-          umma_commit(&S->kv_empty[kv_pv.idx]);
+            for (int k = 0; k < 8; ++k)
+              umma_ts(tO, tP + k * 8, desc_sw128(sv + k * 2048, 0, 1024), idO, (!fresh || k > 0) ? 1u : 0u);
+            umma_commit(&S->p_free[w]);
+            umma_commit(&S->kv_empty[kv_pv.idx]);
+            kv_pv.next();
+          }
+          umma_commit(&S->o_full[w]);
+          umma_commit(&S->q_empty);
         }
-        __syncwarp();
-        kv_pv.next();
-        pb.next();
-        ob.next();
       }
-      if (lane == 0) umma_commit(&S->q_empty);
-      __syncwarp();
+      __syncwarp();   // lanes 1-31 only track q_full; the ring cursors live in lane 0
     }
   } else {
-    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    // ---------------------------------------------------------------- softmax warpgroup wg
+    const int wg = warp >> 2, t = tid & 127;
+    const uint32_t lrow = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lrow + wg * 256, tP = tS + 128, tO = tS + 192;
     const float cl2 = c.scale * kLog2e;
-    Ring sb(2), pb(2), ob(2);
-    for (int rt = 0; rt < n_rt; ++rt) {
-      const int r = rt * kTile + tid;
+    Ring sb(1);
+    uint32_t fph = 1u, oph = 0;
+    if (wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);   // warpgroup 0 takes the first turn
+    for (int pr = 0; pr < n_pair; ++pr) {
+      const int rt = 2 * pr + wg;
+      if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
+      const bool duo = 2 * pr + 1 < n_rt;
+      const int r = rt * kTile + t;
       const bool rvalid = r < rows;
       const int64_t row = qrow0 + (rvalid ? r : 0);
-      float o_acc[kD];
       float lse_slc = 0.f;
-      float m = -1e30f, l = 0.f, m_acc = -1e30f, m_prev = -1e30f;
-#pragma unroll
-      for (int e = 0; e < kD; ++e) o_acc[e] = 0.f;
-      auto fold = [&](float m_tile) {   // add the pending O tile (relative to m_tile) into o_acc
-        mbar_wait(&S->o_full[ob.idx], ob.ph);
-        tc_fence_after();
-        const float a_old = ex2(m_acc - m_tile);
-#pragma unroll
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          float v[32];
-          tmem_ld32(lane_base + 256 + ob.idx * 64 + c0, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o_acc[c0 + i] = o_acc[c0 + i] * a_old + v[i];
-        }
-        m_acc = m_tile;
-        tc_fence_before();
-        mbar_arrive(&S->o_empty[ob.idx]);
-        ob.next();
-      };
+      float m = -1e30f, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
-        if (j == n_slc_tiles && j > 0) {          // close the selection branch -> saved O_slc (fp32)
-          fold(m_prev);
+        const bool fresh = j == 0 || j == n_slc_tiles;
+        const bool closed = j == n_slc_tiles && j > 0;
+        if (closed) {             // close the selection branch -> saved O_slc (fp32), after P.V(j-1)
+          mbar_wait(&S->p_free[wg], fph);
+          fph ^= 1u;
+          tc_fence_after();
           const float inv = 1.f / l;
           float* os = static_cast<float*>(c.o[1]) + row * kD;
 #pragma unroll
-          for (int e = 0; e < kD; e += 4) {
-            if (rvalid)
-              *reinterpret_cast<float4*>(os + e) =
-                  make_float4(o_acc[e] * inv, o_acc[e + 1] * inv, o_acc[e + 2] * inv, o_acc[e + 3] * inv);
-            o_acc[e] = o_acc[e + 1] = o_acc[e + 2] = o_acc[e + 3] = 0.f;
+          for (int cc = 0; cc < kD; cc += 32) {
+            float o[32];
+            tmem_ld32(tO + cc, o);
+            tmem_wait_ld();
+            if (rvalid) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(os + cc + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
+            }
           }
           lse_slc = m + lg2(l);
-          m = -1e30f; l = 0.f; m_acc = -1e30f;
+          m = -1e30f;
+          l = 0.f;
         }
-        const bool first_of_branch = (j == 0 || j == n_slc_tiles);
-        mbar_wait(&S->s_full[sb.idx], sb.ph);
+        mbar_wait(&S->s_full[wg], sb.ph);
         tc_fence_after();
         const int nv = S->tile_nv[j];
-        uint32_t pk[64];
         float v[128];
-#pragma unroll
-        for (int c0 = 0; c0 < kTile; c0 += 32) tmem_ld32(lane_base + sb.idx * 128 + c0, v + c0);
+        tmem_ld32(tS, v);
+        tmem_ld32(tS + 32, v + 32);
+        tmem_ld32(tS + 64, v + 64);
+        tmem_ld32(tS + 96, v + 96);
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&S->s_empty[sb.idx]);
+        mbar_arrive(&S->s_empty[wg]);
         sb.next();
         if (nv < kTile) {
 #pragma unroll
-          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -1e30f;
+          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -INFINITY;   // padded keys: p = 0
+        }
+        if (!closed) {   // P.V(j-1) complete: O is up to date and P may be rewritten
+          mbar_wait(&S->p_free[wg], fph);
+          fph ^= 1u;
+          tc_fence_after();
         }
         const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
-        const float mn = fmaxf(m, mx);
+        const bool bump = fresh || mx > m + kRescale;
+        const float m_new = bump ? mx : m;
+        const float alpha = ex2(m - m_new);           // 1 when the reference does not move
+        l *= alpha;
+        m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (duo) named_bar_sync(4 + wg, 256);
 #pragma unroll
-        for (int i = 0; i < kTile; i += 2) {
-          const float p0 = ex2(fmaf(v[i], cl2, -mn)), p1 = ex2(fmaf(v[i + 1], cl2, -mn));
-          acc[(i >> 1) & 3] += p0 + p1;
-          pk[i / 2] = pack_f16(p0, p1);
+        for (int cc = 0; cc < kTile; cc += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(v[cc + i], cl2, -m)), p1 = ex2(fmaf(v[cc + i + 1], cl2, -m));
+            acc[(i >> 1) & 3] += p0 + p1;
+            pk[i >> 1] = pack_f16(p0, p1);
+          }
+          tmem_st16(tP + cc / 2, pk);
         }
-        const float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        l = l * ex2(m - mn) + s;
-        m = mn;
-        mbar_wait(&S->p_empty[pb.idx], pb.ph ^ 1u);
-        const uint32_t pbase = smem_u32(sP + pb.idx * 32768);
+        if (duo) named_bar_arrive(5 - wg, 256);
+        l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        // the reference max moved inside a branch: rescale O (P.V(j-1) has completed: p_free)
+        if (__any_sync(0xffffffffu, bump && !fresh)) {
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch)      // key chunk ch: key block ch/8, chunk ch%8 of line = row
-          st_shared_v4(pbase + (ch >> 3) * 16384 + sw128(tid, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
-                       pk[4 * ch + 3]);
-        fence_proxy_async_smem();
-        mbar_arrive(&S->p_full[pb.idx]);
-        pb.next();
-        if (!first_of_branch) fold(m_prev);   // previous tile's O (one-tile lag hides the PV latency)
-        m_prev = mn;
+          for (int cc = 0; cc < kD; cc += 16) {
+            float o[16];
+            tmem_ld16(tO + cc, o);
+            tmem_wait_ld();
+            uint32_t ou[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ou[i] = __float_as_uint(fresh ? o[i] : o[i] * alpha);
+            tmem_st16(tO + cc, ou);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&S->p_full[wg]);
       }
-      fold(m_prev);
+      mbar_wait(&S->o_full[wg], oph);
+      oph ^= 1u;
+      tc_fence_after();
+      float o_acc[kD];
+      tmem_ld32(tO, o_acc);
+      tmem_ld32(tO + 32, o_acc + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&S->o_empty[wg]);
       const float inv = 1.f / l;
       if (rvalid) {
         // o_acc * inv is the window branch; the selection branch is in c.o[1] (written above)
@@ -731,8 +769,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         c.lse[1][row] = lse_slc;
         c.lse[2][row] = m + lg2(l);
         const float w0 = c.gs[row * 3], w1 = c.gs[row * 3 + 1], w2 = c.gs[row * 3 + 2];
-        const int t = t0 + r / c.h_s, hs = r % c.h_s;
-        const int dst = c.sorted_input ? t : c.perm[t];
+        const int tok = t0 + r / c.h_s, hs = r % c.h_s;
+        const int dst = c.sorted_input ? tok : c.perm[tok];
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
 #pragma unroll
         for (int e = 0; e < kD; e += 8) {
@@ -741,13 +779,13 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           const float cm[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
           const float sl[8] = {sa.x, sa.y, sa.z, sa.w, sb4.x, sb4.y, sb4.z, sb4.w};
           float wn[8];
-          uint32_t w[4];
+          uint32_t wq[4];
 #pragma unroll
           for (int i = 0; i < 8; ++i) wn[i] = o_acc[e + i] * inv;
 #pragma unroll
           for (int i = 0; i < 8; i += 2)
-            w[i / 2] = pack_bf16(w0 * cm[i] + w1 * sl[i] + w2 * wn[i], w0 * cm[i + 1] + w1 * sl[i + 1] + w2 * wn[i + 1]);
-          *reinterpret_cast<uint4*>(out + e) = make_uint4(w[0], w[1], w[2], w[3]);
+            wq[i / 2] = pack_bf16(w0 * cm[i] + w1 * sl[i] + w2 * wn[i], w0 * cm[i + 1] + w1 * sl[i + 1] + w2 * wn[i + 1]);
+          *reinterpret_cast<uint4*>(out + e) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
           *reinterpret_cast<float4*>(ow + e) = make_float4(wn[0], wn[1], wn[2], wn[3]);
           *reinterpret_cast<float4*>(ow + e + 4) = make_float4(wn[4], wn[5], wn[6], wn[7]);
         }
@@ -756,7 +794,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 }  // namespace
@@ -806,10 +844,10 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
     SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
   }
   {
-    const size_t smem = 1024 + 16384 + kStages * 32768 + 65536 + sizeof(SwSmem);
+    const size_t smem = 1024 + 32768 + kStages * 32768 + sizeof(SwSmem);
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_slc_win_fwd", st);
-    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kThreads, smem, st>>>(c, tmQ, tmK, tmV);
+    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(c, tmQ, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_slcwin_fwd");
   }
   return SSA_OK;
