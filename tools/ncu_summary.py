@@ -54,7 +54,8 @@ def main(rep, launches, tag):
                      f"{g(r, 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active')[:5]} | {rd:.1f} | {wr:.1f} | "
                      f"{g(r, 'lts__throughput.avg.pct_of_peak_sustained_elapsed')[:5]} | {g(r, 'launch__registers_per_thread')} | "
                      + ", ".join(f"{n} {100*v/tot:.0f}%" for v, n in st[:4]) + " |")
-        traffic.setdefault(name, (rd + wr) * 1e6)   # bytes per launch
+        key = name if name not in traffic else f"{name}#{sum(1 for k in traffic if k.split('#')[0] == name)}"
+        traffic[key] = (rd + wr) * 1e6   # bytes per launch (repeated kernel names: #1, #2 ... in launch order)
     # launch list: device time share per kernel over the captured steps
     agg, cnt = defaultdict(float), defaultdict(int)
     text = open(launches).read().splitlines()
