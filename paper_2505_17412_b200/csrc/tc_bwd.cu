@@ -24,7 +24,6 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 64;
-constexpr int kThreads = 192;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kStages = 3;
 
@@ -378,15 +377,36 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
 constexpr int kRT = 64;                  // rows per tile: S^T 64 + dP^T 64 + dK 64 + dV 64 = 256 TMEM cols
 constexpr int kRStages = 2;              // row-tile (Q, dO, stats) pipeline depth
 constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
-// Two CTAs per SM (256 TMEM columns and ~100 KB shared memory each): the second CTA's softmax warps
-// hide the first one's dependency and barrier latencies (one softmax warp per SMSP is not enough).
+// One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
+// row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
+// dV 64), its own row-stage ring and its own MMA issuer (warps 9 / 10); warp 8 is the producer. The
+// warpgroups share the K/V tile and take turns in their exponential loops (named barriers 4 / 5).
+constexpr int kKvThreads = 352;
+#ifndef SSA_KV_PINGPONG
+#define SSA_KV_PINGPONG 1
+#endif
+constexpr bool kKvPingPong = SSA_KV_PINGPONG;
 struct KvSmem {
-  uint64_t k_full, k_empty, r_full[kRStages], r_empty[kRStages], s_full, s_empty, p_full, p_empty, acc_full,
-      acc_empty;
+  uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], p_full[2], acc_full[2],
+      acc_empty[2];
   uint32_t tmem;
-  alignas(16) float st_l2[kRStages][kRT];
-  alignas(16) float st_D[kRStages][kRT];
+  alignas(16) float st_l2[2][kRStages][kRT];
+  alignas(16) float st_D[2][kRStages][kRT];
+#ifdef SSA_TRACE
+  unsigned long long trace[3][128];
+#endif
 };
+#ifdef SSA_TRACE
+__device__ unsigned long long g_trace_kv[3][128];
+__device__ int g_trace_kv_cnt[3];
+#define TRACE_ON (blockIdx.x == 5 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0)
+#define TRACE_R(role, ev, j)                                                                              \
+  do {                                                                                                  \
+    if (TRACE_ON && tr_n < 128) S->trace[role][tr_n++] = (clock64() << 16) | (unsigned long long)(((ev) << 12) | ((j) & 0xfff)); \
+  } while (0)
+#else
+#define TRACE_R(role, ev, j) do { } while (0)
+#endif
 
 // Work item -> (key block, g, query-block range, window?) and the row-tile walker shared by the roles.
 struct Item {
@@ -481,7 +501,7 @@ struct RowWalk {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kKvThreads, 1)
 k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
           __grid_constant__ const CUtensorMap tmDO2, __grid_constant__ const CUtensorMap tmK,
           __grid_constant__ const CUtensorMap tmV) {
@@ -489,9 +509,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm;                       // 16 KB
   uint8_t* sV = sm + 16384;               // 16 KB
-  uint8_t* sR = sm + 32768;               // kRStages x {Q 8 KB, dO 8 KB}
-  uint8_t* sP = sR + kRStages * 16384;    // {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
-  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 32768);
+  uint8_t* sR = sm + 32768;               // [warpgroup][kRStages] x {Q 8 KB, (w) dO 8 KB}
+  KvSmem* S = reinterpret_cast<KvSmem*>(sR + 2 * kRStages * 16384);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Item it;
@@ -510,32 +529,44 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     krow_g = int64_t(g) * c.N;
   }
   const int n_kt = (nkeys_total + 127) / 128;
+  int n_tiles = 0;                        // row tiles of the item (the same for every key tile)
+  {
+    RowWalk w2;
+    w2.init(c, it);
+    int64_t r0;
+    int nr, br;
+    while (w2.next_tile(&r0, &nr, &br)) ++n_tiles;
+  }
+  const int n_own0 = (n_tiles + 1) / 2;   // warpgroup 0 takes row tiles 0, 2, 4 ..., warpgroup 1 1, 3, 5 ...
 
   if (tid == 0) {
     mbar_init(&S->k_full, 1);
-    mbar_init(&S->k_empty, 1);
-    // r_full: 32 producer lanes' cp.async arrivals (row stats) + lane 0's expect_tx (Q/dO TMA)
-    for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[i], 33); mbar_init(&S->r_empty[i], 1); }
-    mbar_init(&S->s_full, 1);
-    mbar_init(&S->s_empty, 128);
-    mbar_init(&S->p_full, 128);
-    mbar_init(&S->p_empty, 1);
-    mbar_init(&S->acc_full, 1);
-    mbar_init(&S->acc_empty, 128);
+    mbar_init(&S->k_empty, 2);            // one arrival per MMA issuer
+    for (int w = 0; w < 2; ++w) {
+      // r_full: 32 producer lanes' cp.async arrivals (row stats) + lane 0's expect_tx (Q/dO TMA)
+      for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[w][i], 33); mbar_init(&S->r_empty[w][i], 1); }
+      mbar_init(&S->s_full[w], 1);
+      mbar_init(&S->p_full[w], 128);
+      mbar_init(&S->acc_full[w], 1);
+      mbar_init(&S->acc_empty[w], 256);   // both warpgroups read both accumulator sets
+    }
     fence_barrier_init();
   }
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmDO2); tma_prefetch(&tmK); tma_prefetch(&tmV);
   }
-  if (warp == 5) tmem_alloc<256>(&S->tmem);
+  if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem;
+#ifdef SSA_TRACE
+  int tr_n = 0;
+#endif
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------ producer: K/V tile, then row tiles + row stats
-    Ring rs(kRStages);
+    Ring rs0(kRStages), rs1(kRStages);
     uint32_t kph = 0;
     for (int kt = 0; kt < n_kt; ++kt) {
       mbar_wait(&S->k_empty, kph ^ 1u);
@@ -549,128 +580,134 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       wk.init(c, it);
       int64_t r0;
       int nr, br;
+      int i = 0;
       while (wk.next_tile(&r0, &nr, &br)) {
-        mbar_wait(&S->r_empty[rs.idx], rs.ph ^ 1u);
-        // row stats by cp.async (no register round trip; completion tracked by r_full); rows past the
-        // range read lse = +inf, D = 0 -> p = 0 without per-element masking
+        const int w = i & 1;
+        Ring& rs = w ? rs1 : rs0;
+        mbar_wait(&S->r_empty[w][rs.idx], rs.ph ^ 1u);
+        TRACE_R(0, 1, i);
+        // row stats by cp.async (completion tracked by r_full); rows past the range read lse = +inf,
+        // D = 0 -> p = 0 without per-element masking
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int i = lane + 32 * h;
-          const int64_t row = r0 + i;
-          cp_async4(&S->st_l2[rs.idx][i], i < nr ? c.lse[br] + row : &g_pos_inf);
-          cp_async4(&S->st_D[rs.idx][i], i < nr ? c.Dd[br] + row : &g_zero);
+          const int e = lane + 32 * h;
+          const int64_t row = r0 + e;
+          cp_async4(&S->st_l2[w][rs.idx][e], e < nr ? c.lse[br] + row : &g_pos_inf);
+          cp_async4(&S->st_D[w][rs.idx][e], e < nr ? c.Dd[br] + row : &g_zero);
         }
-        cp_async_mbar_arrive_noinc(&S->r_full[rs.idx]);
+        cp_async_mbar_arrive_noinc(&S->r_full[w][rs.idx]);
         if (lane == 0) {
-          uint8_t* st = sR + rs.idx * 16384;
-          mbar_expect_tx(&S->r_full[rs.idx], 16384);
-          tma_load_2d(st, &tmQ, &S->r_full[rs.idx], 0, int(r0));
-          tma_load_2d(st + 8192, br == 2 ? &tmDO2 : &tmDO, &S->r_full[rs.idx], 0, int(r0));
+          uint8_t* st = sR + (w * kRStages + rs.idx) * 16384;
+          mbar_expect_tx(&S->r_full[w][rs.idx], 16384);
+          tma_load_2d(st, &tmQ, &S->r_full[w][rs.idx], 0, int(r0));
+          tma_load_2d(st + 8192, br == 2 ? &tmDO2 : &tmDO, &S->r_full[w][rs.idx], 0, int(r0));
         }
         __syncwarp();
         rs.next();
+        ++i;
       }
     }
-  } else if (warp == 5) {
-    // ------------------------------------------------ MMA issuer
+  } else if (warp >= 9) {
+    // ------------------------------------------------ MMA issuer of warpgroup w (lane 0)
+    // Per own row tile t: S^T(t), dP^T(t) -> the warpgroup writes (P w)^T and dS^T over them in TMEM ->
+    // dV += (P w)^T (w dO), dK += dS^T Q with A from TMEM, then S^T(t+1) (same thread: after dV/dK(t)
+    // in tensor-pipe order, so overwriting P / dS is safe).
+    const int w = warp - 9;
     const uint32_t idS = idesc_f16(128, kRT, false, false);    // S^T = K Q^T, dP^T = V dO^T
-    const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
+    const uint32_t idA = idesc_f16(128, 64, false, true);      // A from TMEM, B MN-major
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-    Ring rs(kRStages), sb(1), pb(1);
-    uint32_t kph = 0, aph = 0;
-    int n_tiles = 0;
-    {
-      RowWalk w2;
-      w2.init(c, it);
-      int64_t r0;
-      int nr, br;
-      while (w2.next_tile(&r0, &nr, &br)) ++n_tiles;
-    }
-    for (int kt = 0; kt < n_kt; ++kt) {
-      mbar_wait(&S->k_full, kph);
-      kph ^= 1u;
-      tc_fence_after();
-      Ring rs_a = rs;
-      auto issue_s = [&]() {
-        mbar_wait(&S->r_full[rs.idx], rs.ph);
-        mbar_wait(&S->s_empty, sb.ph ^ 1u);
+    const uint32_t tS = tmem + w * 256, tDP = tS + 64, tK = tS + 128, tV = tS + 192;
+    const int n_own = w == 0 ? n_own0 : n_tiles / 2;
+    Ring rs(kRStages);
+    uint32_t kph = 0, aph = 0, pph = 0;
+    if (lane == 0) {
+      for (int kt = 0; kt < n_kt; ++kt) {
+        mbar_wait(&S->k_full, kph);
+        kph ^= 1u;
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t aq = smem_u32(sR + rs.idx * 16384), ado = aq + 8192;
+        auto issue_s = [&]() {
+          mbar_wait(&S->r_full[w][rs.idx], rs.ph);
+          tc_fence_after();
+          const uint32_t aq = smem_u32(sR + (w * kRStages + rs.idx) * 16384), ado = aq + 8192;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem, desc_sw128(aK + k * 32, 0, 1024), desc_sw128(aq + k * 32, 0, 1024), idS, k > 0);
+            umma_bf16(tS, desc_sw128(aK + k * 32, 0, 1024), desc_sw128(aq + k * 32, 0, 1024), idS, k > 0);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + kRT, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
-          umma_commit(&S->s_full);
+            umma_bf16(tDP, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
+          umma_commit(&S->s_full[w]);
+          if (w == 0) TRACE_R(1, 3, 0);
+        };
+        Ring rs_a = rs;
+        if (n_own > 0) {
+          issue_s();
+          rs.next();
         }
-        __syncwarp();
-        rs.next();
-        sb.next();
-      };
-      if (n_tiles > 0) issue_s();
-      mbar_wait(&S->acc_empty, aph ^ 1u);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s();      // S^T of the next tile as soon as the softmax has read this one
-        mbar_wait(&S->p_full, pb.ph);
+        mbar_wait(&S->acc_empty[w], aph ^ 1u);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ap = smem_u32(sP), ads = ap + 16384;
-          const uint32_t aq = smem_u32(sR + rs_a.idx * 16384), ado = aq + 8192;
+        for (int q = 0; q < n_own; ++q) {
+          mbar_wait(&S->p_full[w], pph);
+          pph ^= 1u;
+          tc_fence_after();
+          const uint32_t aq = smem_u32(sR + (w * kRStages + rs_a.idx) * 16384), ado = aq + 8192;
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_bf16(tmem + 192, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
-                      (j > 0 || k > 0) ? 1u : 0u);
+            umma_ts(tV, tS + k * 8, desc_sw128(ado + k * 2048, 0, 1024), idA, (q > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_bf16(tmem + 128, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
-                      (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&S->p_empty);
-          umma_commit(&S->r_empty[rs_a.idx]);
+            umma_ts(tK, tDP + k * 8, desc_sw128(aq + k * 2048, 0, 1024), idA, (q > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->r_empty[w][rs_a.idx]);
+          if (w == 0) TRACE_R(1, 5, q);
+          rs_a.next();
+          if (q + 1 < n_own) {
+            issue_s();
+            rs.next();
+          }
         }
-        __syncwarp();
-        rs_a.next();
-        pb.next();
-      }
-      if (lane == 0) {
-        umma_commit(&S->acc_full);
+        umma_commit(&S->acc_full[w]);
         umma_commit(&S->k_empty);
+        aph ^= 1u;
       }
-      __syncwarp();
-      aph ^= 1u;
     }
+    __syncwarp();
   } else {
     // ------------------------------------------------ softmax: thread = key (TMEM lane)
-    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    const int wg = warp >> 2, t = tid & 127;
+    const uint32_t lrow = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lrow + wg * 256, tDP = tS + 64;
     const float cl2 = c.scale * kLog2e;
-    Ring rs(kRStages), sb(1), pb(1);
-    uint32_t aph = 0;
+    const int n_own = wg == 0 ? n_own0 : n_tiles / 2;
+    Ring rs(kRStages);
+    uint32_t sph = 0, aph = 0;
+    // MUFU ping-pong (named barriers 4 / 5); warpgroup 1 runs a turn for every warpgroup-0 tile (an
+    // empty one when it has no tile) so the turn counts always match
+    if (kKvPingPong && wg == 1 && n_own0 > 0) named_bar_arrive(4, 256);
     for (int kt = 0; kt < n_kt; ++kt) {
-      const int key = kt * 128 + tid;
+      const int key = kt * 128 + t;
       const bool kvalid = key < nkeys_total;
-      RowWalk wk;
-      wk.init(c, it);
-      int64_t r0;
-      int nr, br;
-      int n_tiles = 0;
-      while (wk.next_tile(&r0, &nr, &br)) {
-        mbar_wait(&S->r_full[rs.idx], rs.ph);      // row stats of this stage are visible
-        mbar_wait(&S->s_full, sb.ph);
+      for (int q = 0; q < n_own0; ++q) {
+        if (q >= n_own) {                        // warpgroup 1 without a tile: keep the turn order
+          if (kKvPingPong) {
+            named_bar_sync(5, 256);
+            named_bar_arrive(4, 256);
+          }
+          continue;
+        }
+        mbar_wait(&S->r_full[wg][rs.idx], rs.ph);      // row stats of this stage are visible
+        mbar_wait(&S->s_full[wg], sph);
+        sph ^= 1u;
+        if (warp == 0) TRACE_R(2, 7, q);
         tc_fence_after();
-        const uint32_t sbase = smem_u32(&S->st_l2[rs.idx][0]);
-        const uint32_t dbase = smem_u32(&S->st_D[rs.idx][0]);
-        const uint32_t pbase = smem_u32(sP);
+        const uint32_t sbase = smem_u32(&S->st_l2[wg][rs.idx][0]);
+        const uint32_t dbase = smem_u32(&S->st_D[wg][rs.idx][0]);
+        if (kKvPingPong) named_bar_sync(4 + wg, 256);
+        if (warp == 0) TRACE_R(2, 8, q);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {   // 32 rows at a time keeps the register file in budget
           float s[32], dp[32];
-          tmem_ld32(lane_base + half * 32, s);
-          tmem_ld32(lane_base + kRT + half * 32, dp);   // already (w dO) V^T
+          tmem_ld32(tS + half * 32, s);
+          tmem_ld32(tDP + half * 32, dp);        // already (w dO) V^T
           tmem_wait_ld();
-          if (half == 1) {
-            tc_fence_before();
-            mbar_arrive(&S->s_empty);            // S^T / dP^T fully read: the next tile's MMA may start
-          }
           uint32_t pw[16], ds[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -689,63 +726,74 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
 #pragma unroll
             for (int i = 0; i < 16; ++i) pw[i] = ds[i] = 0u;
           }
-          if (half == 0) mbar_wait(&S->p_empty, pb.ph ^ 1u);   // previous tile's dV/dK MMAs are done
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            st_shared_v4(pbase + sw128(tid, half * 4 + ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
-            st_shared_v4(pbase + 16384 + sw128(tid, half * 4 + ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2],
-                         ds[4 * ch + 3]);
-          }
+          // (P w)^T over S^T columns [0, 32), dS^T over dP^T columns [64, 96): two rows per column; the
+          // columns of the second half's rows (32-63) are not yet overwritten when half 1 loads them
+          tmem_st16(tS + half * 16, pw);
+          tmem_st16(tDP + half * 16, ds);
         }
-        sb.next();
+        if (kKvPingPong) named_bar_arrive(5 - wg, 256);
+        if (warp == 0) TRACE_R(2, 9, q);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&S->p_full[wg]);
+        if (warp == 0) TRACE_R(2, 11, q);
         rs.next();
-        fence_proxy_async_smem();
-        mbar_arrive(&S->p_full);
-        pb.next();
-        ++n_tiles;
       }
-      // accumulators: dK at 128, dV at 192
-      mbar_wait(&S->acc_full, aph);
+      // accumulators: dK at 128, dV at 192 of each warpgroup; warpgroup 0 writes dK = dK_0 + dK_1,
+      // warpgroup 1 writes dV = dV_0 + dV_1 (fixed order: deterministic)
+      const bool has1 = n_tiles > 1;
+      mbar_wait(&S->acc_full[0], aph);
+      if (has1) mbar_wait(&S->acc_full[1], aph);
       aph ^= 1u;
       tc_fence_after();
-      float dk[64], dv[64];
-      tmem_ld32(lane_base + 128, dk);
-      tmem_ld32(lane_base + 128 + 32, dk + 32);
-      tmem_ld32(lane_base + 192, dv);
-      tmem_ld32(lane_base + 192 + 32, dv + 32);
+      const uint32_t col = wg == 0 ? 128u : 192u;
+      float a0[64], a1[64];
+      tmem_ld32(tmem + lrow + col, a0);
+      tmem_ld32(tmem + lrow + col + 32, a0 + 32);
+      if (has1) {
+        tmem_ld32(tmem + lrow + 256 + col, a1);
+        tmem_ld32(tmem + lrow + 256 + col + 32, a1 + 32);
+      }
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&S->acc_empty);
+      mbar_arrive(&S->acc_empty[0]);
+      mbar_arrive(&S->acc_empty[1]);
       if (kvalid) {
-        float *ok, *ov;
+        float* o;
         if (mode == 0) {
           const int64_t idx = ((int64_t(it.chunk) * c.h_kv + g) * c.n_blk[SSA_LEVEL_CMP] + kbase + key) * kD;
-          ok = c.dkc_part + idx;
-          ov = c.dvc_part + idx;
+          o = (wg == 0 ? c.dkc_part : c.dvc_part) + idx;
         } else if (it.first) {
           const int64_t idx = (int64_t(g) * c.N + kbase + key) * kD;
-          ok = c.dk_acc + idx;
-          ov = c.dv_acc + idx;
+          o = (wg == 0 ? c.dk_acc : c.dv_acc) + idx;
         } else {
           const int64_t idx = (int64_t(it.part_slot) * c.max_fill[SSA_LEVEL_SLC] + key) * kD;
-          ok = c.kv_part_k + idx;
-          ov = c.kv_part_v + idx;
+          o = (wg == 0 ? c.kv_part_k : c.kv_part_v) + idx;
         }
         const bool none = n_tiles == 0;
+        const float sc = wg == 0 ? c.scale : 1.f;
 #pragma unroll
         for (int e = 0; e < kD; e += 4) {
-          *reinterpret_cast<float4*>(ok + e) = none ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                    : make_float4(dk[e] * c.scale, dk[e + 1] * c.scale,
-                                                                  dk[e + 2] * c.scale, dk[e + 3] * c.scale);
-          *reinterpret_cast<float4*>(ov + e) = none ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                    : make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
+          float4 v4;
+          v4.x = none ? 0.f : (a0[e] + (has1 ? a1[e] : 0.f)) * sc;
+          v4.y = none ? 0.f : (a0[e + 1] + (has1 ? a1[e + 1] : 0.f)) * sc;
+          v4.z = none ? 0.f : (a0[e + 2] + (has1 ? a1[e + 2] : 0.f)) * sc;
+          v4.w = none ? 0.f : (a0[e + 3] + (has1 ? a1[e + 3] : 0.f)) * sc;
+          *reinterpret_cast<float4*>(o + e) = v4;
         }
       }
     }
   }
+#ifdef SSA_TRACE
+  if (TRACE_ON && (warp == 8 || warp == 9 || warp == 0)) {
+    const int role = warp == 8 ? 0 : (warp == 9 ? 1 : 2);
+    for (int i = 0; i < tr_n; ++i) g_trace_kv[role][i] = S->trace[role][i];
+    g_trace_kv_cnt[role] = tr_n;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<256>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 // raw-key work items: ceil(len / kQBlocksPerItem) (at least 1, for the window) per (block, g)
@@ -835,7 +883,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
-  const size_t smem = 1024 + 32768 + kRStages * 16384 + 32768 + sizeof(KvSmem);
+  const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + sizeof(KvSmem);
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
     k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);
@@ -843,7 +891,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     ssa_status s = exclusive_scan(item_cnt, c.kv_item_off, nkeys, c.kv_item_off + nkeys, scan_ws, st);
     if (s != SSA_OK) return s;
     ProfScope ps("tc_bwd_kv", st);
-    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kThreads, smem, st>>>(c, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
+    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, st>>>(c, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
   }
   {
@@ -853,7 +901,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   }
   {
     ProfScope ps("tc_bwd_cmp_kv", st);
-    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kThreads, smem, st>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
+    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, st>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
                                                                               tmVc128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(cmp)");
   }
@@ -863,6 +911,17 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
 }  // namespace ssa
 
 #ifdef SSA_TRACE
+extern "C" int ssa_debug_trace_kv(unsigned long long* host, int cap) {
+  int cnt[3];
+  unsigned long long buf[3][128];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(cnt, ssa::g_trace_kv_cnt, sizeof(cnt));
+  cudaMemcpyFromSymbol(buf, ssa::g_trace_kv, sizeof(buf));
+  int n = 0;
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < cnt[r] && n < cap; ++i) host[n++] = buf[r][i];
+  return n;
+}
 extern "C" int ssa_debug_trace_dq(unsigned long long* host, int cap) {
   int cnt[3];
   unsigned long long buf[3][128];

@@ -8,7 +8,7 @@ from paper_2505_17412_b200 import ssa
 from ssa_workload import CONFIGS, config_coords, make_inputs
 L = ssa.lib()
 which = sys.argv[1] if len(sys.argv) > 1 else "cmp"
-f = L.ssa_debug_trace if which == "cmp" else L.ssa_debug_trace_dq
+f = {"cmp": L.ssa_debug_trace, "dq": L.ssa_debug_trace_dq, "kv": L.ssa_debug_trace_kv}[which]
 f.restype = ctypes.c_int
 f.argtypes = [ctypes.c_void_p, ctypes.c_int]
 cfg = CONFIGS["C3"]
@@ -18,7 +18,7 @@ t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v
 plan = ssa.ssa_build_blocks(torch.from_numpy(c).cuda(), grid, batch, 4, 8, 8, 8)
 acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16)
 out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
-if which == "dq":
+if which in ("dq", "kv"):
     ssa.ssa_backward(plan, acfg, saved, *t)
 buf = (ctypes.c_ulonglong * 1024)()
 n = f(buf, 768)
@@ -34,6 +34,9 @@ names = {1: "P load pass1", 2: "P load pass2", 3: "M issued S (p1)", 4: "M issue
 if which == "dq":
     names = {1: "P load", 3: "M issued S", 5: "M dQ issued", 7: "S S-ready", 8: "S turn-in", 9: "S turn-out",
              10: "S dS-free", 11: "S dS-written"}
+if which == "kv":
+    names = {1: "P row tile", 3: "M S^T issued", 5: "M dVdK issued", 7: "S S-ready", 8: "S turn-in", 9: "S turn-out",
+             11: "S P written"}
 print("events", n)
 for i in order[:400]:
     print(f"{clk[i]-t0:10d} {names.get(code[i], code[i]):14s} j={j[i]}")
