@@ -375,7 +375,10 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
 // dK / dV (KV-outer)
 // ================================================================================================
 constexpr int kRT = 64;                  // rows per tile: S^T 64 + dP^T 64 + dK 64 + dV 64 = 256 TMEM cols
-constexpr int kRStages = 2;              // row-tile (Q, dO, stats) pipeline depth
+#ifndef SSA_KV_RSTAGES
+#define SSA_KV_RSTAGES 3
+#endif
+constexpr int kRStages = SSA_KV_RSTAGES;   // row-tile (Q, dO, stats) pipeline depth per warpgroup
 constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
 // One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
 // row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
@@ -383,12 +386,12 @@ constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item
 // warpgroups share the K/V tile and take turns in their exponential loops (named barriers 4 / 5).
 constexpr int kKvThreads = 352;
 #ifndef SSA_KV_PINGPONG
-#define SSA_KV_PINGPONG 1
+#define SSA_KV_PINGPONG 0
 #endif
 constexpr bool kKvPingPong = SSA_KV_PINGPONG;
 struct KvSmem {
-  uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], p_full[2], acc_full[2],
-      acc_empty[2];
+  uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], s_empty[2], p_full[2],
+      p_empty[2], acc_full[2], acc_empty[2];
   uint32_t tmem;
   alignas(16) float st_l2[2][kRStages][kRT];
   alignas(16) float st_D[2][kRStages][kRT];
@@ -510,7 +513,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   uint8_t* sK = sm;                       // 16 KB
   uint8_t* sV = sm + 16384;               // 16 KB
   uint8_t* sR = sm + 32768;               // [warpgroup][kRStages] x {Q 8 KB, (w) dO 8 KB}
-  KvSmem* S = reinterpret_cast<KvSmem*>(sR + 2 * kRStages * 16384);
+  uint8_t* sP = sR + 2 * kRStages * 16384;  // [warpgroup] x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
+  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 2 * 32768);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Item it;
@@ -546,7 +550,9 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       // r_full: 32 producer lanes' cp.async arrivals (row stats) + lane 0's expect_tx (Q/dO TMA)
       for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[w][i], 33); mbar_init(&S->r_empty[w][i], 1); }
       mbar_init(&S->s_full[w], 1);
+      mbar_init(&S->s_empty[w], 128);
       mbar_init(&S->p_full[w], 128);
+      mbar_init(&S->p_empty[w], 1);
       mbar_init(&S->acc_full[w], 1);
       mbar_init(&S->acc_empty[w], 256);   // both warpgroups read both accumulator sets
     }
@@ -609,17 +615,17 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     }
   } else if (warp >= 9) {
     // ------------------------------------------------ MMA issuer of warpgroup w (lane 0)
-    // Per own row tile t: S^T(t), dP^T(t) -> the warpgroup writes (P w)^T and dS^T over them in TMEM ->
-    // dV += (P w)^T (w dO), dK += dS^T Q with A from TMEM, then S^T(t+1) (same thread: after dV/dK(t)
-    // in tensor-pipe order, so overwriting P / dS is safe).
+    // Per own row tile: S^T(t+1), dP^T(t+1) as soon as the warpgroup has read S^T(t), dP^T(t) (they
+    // overlap its softmax work), then dV += (P w)^T (w dO), dK += dS^T Q from the shared-memory P / dS.
     const int w = warp - 9;
     const uint32_t idS = idesc_f16(128, kRT, false, false);    // S^T = K Q^T, dP^T = V dO^T
-    const uint32_t idA = idesc_f16(128, 64, false, true);      // A from TMEM, B MN-major
+    const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     const uint32_t tS = tmem + w * 256, tDP = tS + 64, tK = tS + 128, tV = tS + 192;
+    const uint32_t ap = smem_u32(sP + w * 32768), ads = ap + 16384;
     const int n_own = w == 0 ? n_own0 : n_tiles / 2;
-    Ring rs(kRStages);
-    uint32_t kph = 0, aph = 0, pph = 0;
+    Ring rs(kRStages), sb(1), pb(1);
+    uint32_t kph = 0, aph = 0;
     if (lane == 0) {
       for (int kt = 0; kt < n_kt; ++kt) {
         mbar_wait(&S->k_full, kph);
@@ -627,6 +633,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         tc_fence_after();
         auto issue_s = [&]() {
           mbar_wait(&S->r_full[w][rs.idx], rs.ph);
+          mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
           tc_fence_after();
           const uint32_t aq = smem_u32(sR + (w * kRStages + rs.idx) * 16384), ado = aq + 8192;
 #pragma unroll
@@ -637,32 +644,31 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
             umma_bf16(tDP, desc_sw128(aV + k * 32, 0, 1024), desc_sw128(ado + k * 32, 0, 1024), idS, k > 0);
           umma_commit(&S->s_full[w]);
           if (w == 0) TRACE_R(1, 3, 0);
+          rs.next();
+          sb.next();
         };
         Ring rs_a = rs;
-        if (n_own > 0) {
-          issue_s();
-          rs.next();
-        }
+        if (n_own > 0) issue_s();
         mbar_wait(&S->acc_empty[w], aph ^ 1u);
         tc_fence_after();
         for (int q = 0; q < n_own; ++q) {
-          mbar_wait(&S->p_full[w], pph);
-          pph ^= 1u;
+          if (q + 1 < n_own) issue_s();
+          mbar_wait(&S->p_full[w], pb.ph);
           tc_fence_after();
           const uint32_t aq = smem_u32(sR + (w * kRStages + rs_a.idx) * 16384), ado = aq + 8192;
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_ts(tV, tS + k * 8, desc_sw128(ado + k * 2048, 0, 1024), idA, (q > 0 || k > 0) ? 1u : 0u);
+            umma_bf16(tV, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
+                      (q > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
-            umma_ts(tK, tDP + k * 8, desc_sw128(aq + k * 2048, 0, 1024), idA, (q > 0 || k > 0) ? 1u : 0u);
+            umma_bf16(tK, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
+                      (q > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->p_empty[w]);
           umma_commit(&S->r_empty[w][rs_a.idx]);
           if (w == 0) TRACE_R(1, 5, q);
           rs_a.next();
-          if (q + 1 < n_own) {
-            issue_s();
-            rs.next();
-          }
+          pb.next();
         }
         umma_commit(&S->acc_full[w]);
         umma_commit(&S->k_empty);
@@ -677,8 +683,9 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     const uint32_t tS = tmem + lrow + wg * 256, tDP = tS + 64;
     const float cl2 = c.scale * kLog2e;
     const int n_own = wg == 0 ? n_own0 : n_tiles / 2;
+    const uint32_t pbase = smem_u32(sP + wg * 32768);
     Ring rs(kRStages);
-    uint32_t sph = 0, aph = 0;
+    uint32_t sph = 0, aph = 0, pph = 0;
     // MUFU ping-pong (named barriers 4 / 5); warpgroup 1 runs a turn for every warpgroup-0 tile (an
     // empty one when it has no tile) so the turn counts always match
     if (kKvPingPong && wg == 1 && n_own0 > 0) named_bar_arrive(4, 256);
@@ -708,6 +715,10 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
           tmem_ld32(tS + half * 32, s);
           tmem_ld32(tDP + half * 32, dp);        // already (w dO) V^T
           tmem_wait_ld();
+          if (half == 1) {
+            tc_fence_before();
+            mbar_arrive(&S->s_empty[wg]);        // S^T / dP^T fully read: the next tile's MMA may start
+          }
           uint32_t pw[16], ds[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -726,15 +737,20 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
 #pragma unroll
             for (int i = 0; i < 16; ++i) pw[i] = ds[i] = 0u;
           }
-          // (P w)^T over S^T columns [0, 32), dS^T over dP^T columns [64, 96): two rows per column; the
-          // columns of the second half's rows (32-63) are not yet overwritten when half 1 loads them
-          tmem_st16(tS + half * 16, pw);
-          tmem_st16(tDP + half * 16, ds);
+          if (half == 0) {
+            mbar_wait(&S->p_empty[wg], pph ^ 1u);   // previous tile's dV/dK MMAs are done
+            pph ^= 1u;
+          }
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            st_shared_v4(pbase + sw128(t, half * 4 + ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
+            st_shared_v4(pbase + 16384 + sw128(t, half * 4 + ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2],
+                         ds[4 * ch + 3]);
+          }
         }
         if (kKvPingPong) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_R(2, 9, q);
-        tmem_wait_st();
-        tc_fence_before();
+        fence_proxy_async_smem();
         mbar_arrive(&S->p_full[wg]);
         if (warp == 0) TRACE_R(2, 11, q);
         rs.next();
@@ -883,7 +899,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
-  const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + sizeof(KvSmem);
+  const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + 2 * 32768 + sizeof(KvSmem);
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
     k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);
