@@ -39,35 +39,58 @@ struct Ring {
 
 // fp16 operand copies for the backward MMAs. bf16 inputs convert exactly while |x| < 65504
 // (saturating beyond); dS and P*omega are then packed in fp16 (11-bit mantissa).
-__device__ __forceinline__ __half to_h(float x) {
-  __half h;
-  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&h)) : "f"(x));
-  return h;
-}
 // (dO scaled by the row's gate of each branch feeds the KV-outer kernel: dV = P^T (w dO) and
 // dP = V (w dO)^T, which removes two multiplies per score element there.)
 __device__ float g_pos_inf = INFINITY;
 __device__ float g_zero = 0.f;
+// two floats -> f16x2 (saturating; element lo in the low half)
+__device__ __forceinline__ uint32_t h2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void bf16x8_to_f32(uint4 u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    f[2 * j] = __uint_as_float(w[j] << 16);
+    f[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ uint4 f32x8_to_h(const float* f, float s) {
+  return make_uint4(h2_sat(f[0] * s, f[1] * s), h2_sat(f[2] * s, f[3] * s), h2_sat(f[4] * s, f[5] * s),
+                    h2_sat(f[6] * s, f[7] * s));
+}
+// one thread per 8 consecutive elements (16-byte loads and stores; every count is a multiple of 64)
 __global__ void k_tc_bwd_prep(Ctx c, __half* q16, __half* do16, __half* dow, __half* k16, __half* v16, __half* kc16,
                               __half* vc16) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
   const int64_t nr = int64_t(c.h_kv) * c.N * c.h_s * kD, nk = int64_t(c.h_kv) * c.N * kD;
   const int64_t nc = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
+  float f[8];
   if (i < nr) {
-    q16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.qs)[i]));
-    const float d = __bfloat162float(static_cast<const __nv_bfloat16*>(c.dos)[i]);
-    do16[i] = to_h(d);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.qs) + i), f);
+    *reinterpret_cast<uint4*>(q16 + i) = f32x8_to_h(f, 1.f);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dos) + i), f);
+    *reinterpret_cast<uint4*>(do16 + i) = f32x8_to_h(f, 1.f);
     const float* w = c.gs + (i / kD) * 3;
 #pragma unroll
-    for (int br = 0; br < 3; ++br) dow[br * nr + i] = to_h(d * w[br]);
+    for (int br = 0; br < 3; ++br) *reinterpret_cast<uint4*>(dow + br * nr + i) = f32x8_to_h(f, w[br]);
   }
   if (i < nk) {
-    k16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.ks)[i]));
-    v16[i] = to_h(__bfloat162float(static_cast<const __nv_bfloat16*>(c.vs)[i]));
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.ks) + i), f);
+    *reinterpret_cast<uint4*>(k16 + i) = f32x8_to_h(f, 1.f);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.vs) + i), f);
+    *reinterpret_cast<uint4*>(v16 + i) = f32x8_to_h(f, 1.f);
   }
   if (i < nc) {
-    kc16[i] = to_h(static_cast<const float*>(c.kc)[i]);
-    vc16[i] = to_h(static_cast<const float*>(c.vc)[i]);
+    const float4* kc = reinterpret_cast<const float4*>(static_cast<const float*>(c.kc) + i);
+    const float4* vc = reinterpret_cast<const float4*>(static_cast<const float*>(c.vc) + i);
+    const float4 a0 = kc[0], a1 = kc[1], b0 = vc[0], b1 = vc[1];
+    const float fk[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float fv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    *reinterpret_cast<uint4*>(kc16 + i) = f32x8_to_h(fk, 1.f);
+    *reinterpret_cast<uint4*>(vc16 + i) = f32x8_to_h(fv, 1.f);
   }
 }
 
@@ -880,7 +903,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   const int64_t n = int64_t(qrows) * kD;
-  k_tc_bwd_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, q16, do16, dow, k16, v16, kc, vc);
+  k_tc_bwd_prep<<<unsigned((n / 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow, k16, v16, kc, vc);
   SSA_LAUNCH_CHECK("k_tc_bwd_prep");
   CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmK, tmV, tmKc128, tmVc128, tmK128, tmV128, tmDW[3];
   for (int br = 0; br < 3; ++br)
