@@ -354,7 +354,11 @@ def main():
         }
         if full:
             line["full_attention"] = full
-            line["speedup_vs_full_attention"] = round(full["fwd_bwd_ms"] / ms_per_step * batch, 2)
+            if "fwd_bwd_ms" in full:
+                line["speedup_vs_full_attention"] = round(full["fwd_bwd_ms"] / ms_per_step * batch, 2)
+            for key, val in full.get("others", {}).items():
+                if key.endswith("_ms"):
+                    line.setdefault("speedup_vs", {})[key[:-3]] = round(val / ms_per_step * batch, 2)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
@@ -362,32 +366,54 @@ def main():
 
 
 def full_attention_time(torch, dev, n, H, h_kv, d, dt):
-    """Dense non-causal attention over all n tokens (torch SDPA, flash/cuDNN backend) fwd+bwd, GQA."""
-    try:
-        import torch.nn.functional as F
-        q = torch.randn(1, H, n, d, device=dev, dtype=dt, requires_grad=True)
-        k = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
-        v = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
-        go = torch.randn(1, H, n, d, device=dev, dtype=dt)
+    """Dense non-causal attention over all n tokens, fwd+bwd, GQA (context only, SURVEY 8d comparators):
+    torch SDPA default dispatch, SDPA pinned to the cuDNN backend, and flash_attn (FA2) when it runs here."""
+    import torch.nn.functional as F
+    q = torch.randn(1, H, n, d, device=dev, dtype=dt, requires_grad=True)
+    k = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
+    v = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
+    go = torch.randn(1, H, n, d, device=dev, dtype=dt)
 
-        def run():
-            o = F.scaled_dot_product_attention(q, k, v, enable_gqa=True)
-            o.backward(go)
+    def timed(run, reps=3):
         for _ in range(2):
             run()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        reps = 3
         for _ in range(reps):
             run()
         e1.record()
         torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / reps
-        return {"impl": "torch SDPA (GQA, non-causal, bf16)", "tokens": n, "fwd_bwd_ms": round(ms, 3),
-                "flops": 4.0 * n * n * H * d * 3.5}
+        return round(e0.elapsed_time(e1) / reps, 3)
+
+    res = {"impl": "torch SDPA (GQA, non-causal, bf16)", "tokens": n, "flops": 4.0 * n * n * H * d * 3.5}
+    try:
+        res["fwd_bwd_ms"] = timed(lambda: F.scaled_dot_product_attention(q, k, v, enable_gqa=True).backward(go))
     except Exception as ex:  # comparator is context only
-        return {"error": str(ex)[:200]}
+        res["error"] = str(ex)[:200]
+    others = {}
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        def cudnn():
+            with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                kk = k.repeat_interleave(H // h_kv, dim=1)
+                vv = v.repeat_interleave(H // h_kv, dim=1)
+                F.scaled_dot_product_attention(q, kk, vv).backward(go)
+        others["cudnn_sdpa_ms"] = timed(cudnn)
+    except Exception as ex:
+        others["cudnn_sdpa_error"] = str(ex)[:160]
+    try:
+        from flash_attn import flash_attn_func
+        qf = q.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        kf = k.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        vf = v.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        gof = go.transpose(1, 2).contiguous()
+        others["flash_attn2_ms"] = timed(lambda: flash_attn_func(qf, kf, vf).backward(gof))
+    except Exception as ex:
+        others["flash_attn2_error"] = str(ex)[:160]
+    res["others"] = others
+    return res
 
 
 def oracle_sample(cfg, coords, grid, batch, inp, n_sample: int, seed: int = 0):
