@@ -167,8 +167,10 @@ def main():
 
     sharded = args.config == "C5"
 
-    def step(qq=q, kk=k, vv=v, gg=g, dd=do):
-        plan = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+    def step(qq=q, kk=k, vv=v, gg=g, dd=do, o_=out, gr_=grads, cc=c_d, after_build=None):
+        plan = ssa.ssa_build_blocks(cc, grid, batch, *ms)
+        if after_build is not None:
+            after_build()
         if sharded:
             # one shape, query blocks sharded over the ranks (SURVEY §8e mode 2): K/V all-gather,
             # dK/dV partial all-reduce; inputs in plan order, every rank builds the same plan
@@ -186,8 +188,8 @@ def main():
             vl[:b - a] = vs_[a:b]
             ssa_step_sharded(plan, acfg, qs_, kl, vl, gs_, ds_, tok, rank)
             return plan, None
-        o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=out)
-        ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=grads)
+        o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=o_)
+        ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=gr_)
         return plan, saved
 
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 3):
@@ -301,30 +303,58 @@ def main():
     kernel_ms = {kn: round(t / n, 4) for kn, (t, n) in ktimes.items()}
 
     # ---- e2e through the public API with host buffers ----
+    # Every step copies its inputs (coords, q, k, v, gates, dO) from pinned host memory and reads its
+    # results (out, dq, dk, dv, dgates) back to pinned host memory. Copies run on their own streams,
+    # double-buffered, so step i's compute overlaps step i+1's H2D and step i-1's D2H (PCIe is full
+    # duplex); the clock runs from the first H2D to the last D2H.
     e2e = None
     if not args.no_e2e:
-        hq, hk, hv, hg, hd = (x.cpu().pin_memory() for x in (q, k, v, g, do))
-        houts = [torch.empty_like(x, device="cpu").pin_memory() for x in (out,) + grads]
-        bi = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hg, hd))
-        bo = sum(x.numel() * x.element_size() for x in houts)
-        e_times = []
-        for i in range(args.steps + 1):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            dq_, dk_, dv_, dg_ = (x.to(dev, non_blocking=True) for x in (hq, hk, hv, hg))
-            ddo = hd.to(dev, non_blocking=True)
-            step(dq_, dk_, dv_, dg_, ddo)
-            for h_, d_ in zip(houts, (out,) + grads):
-                h_.copy_(d_, non_blocking=True)
-            e1.record(st)
-            if i > 0:
-                e_times.append((e0, e1))
+        hin = [x.cpu().pin_memory() for x in (c_d, q, k, v, g, do)]
+        bi = sum(x.numel() * x.element_size() for x in hin)
+        dev_in = [[torch.empty_like(x) for x in (c_d, q, k, v, g, do)] for _ in range(2)]
+        dev_out = [[torch.empty_like(out)] + [torch.empty_like(x) for x in grads] for _ in range(2)]
+        hout = [[torch.empty_like(x, device="cpu").pin_memory() for x in dev_out[0]] for _ in range(2)]
+        bo = sum(x.numel() * x.element_size() for x in hout[0])
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        n_e = args.steps + 2                      # the first two iterations are warm-up
+        ev = {key: [torch.cuda.Event() for _ in range(n_e)] for key in ("in", "done", "out")}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
-        e_ms = sum(a.elapsed_time(b) for a, b in e_times) / len(e_times)
+        def read_back(j):   # D2H of step j's results, on the D2H stream after step j is done
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev["done"][j])
+                for hx, dx in zip(hout[j % 2], dev_out[j % 2]):
+                    hx.copy_(dx, non_blocking=True)
+                ev["out"][j].record(s_out)
+
+        # The plan build reads a few counters back to the host (pageable, synchronous); it is issued
+        # before the previous step's large D2H so that small read never queues behind it.
+        for i in range(n_e):
+            slot = i % 2
+            if i == 2:
+                e0.record(s_in)
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev["done"][i - 2])            # the step that read this input slot is done
+                for hx, dx in zip(hin, dev_in[slot]):
+                    dx.copy_(hx, non_blocking=True)
+                ev["in"][i].record(s_in)
+            st.wait_event(ev["in"][i])
+            if i >= 2:
+                st.wait_event(ev["out"][i - 2])                   # this output slot has been read back
+            cc, qq, kk, vv, gg, dd = dev_in[slot]
+            step(qq, kk, vv, gg, dd, dev_out[slot][0], tuple(dev_out[slot][1:]), cc,
+                 after_build=(lambda j=i - 1: read_back(j)) if i >= 1 else None)
+            ev["done"][i].record(st)
+        read_back(n_e - 1)
+        e1.record(s_out)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1) / args.steps
         e_ms = max_over_ranks(e_ms, dev)
         e2e = {"value": round(e_ms / shapes_per_step, 4), "unit": UNIT, "h2d_bytes_per_step": int(bi),
-               "d2h_bytes_per_step": int(bo)}
+               "d2h_bytes_per_step": int(bo),
+               "method": "pinned host buffers; H2D / compute / D2H on three streams, double-buffered; "
+                         "timed from the first H2D to the last D2H over the K steps"}
 
     # ---- full-attention comparator on the same box (context: "speedup vs full attention") ----
     full = None

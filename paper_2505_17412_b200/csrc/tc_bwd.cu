@@ -110,6 +110,10 @@ constexpr int kKVBytes = kKT * 128;      // one K or V tile (bf16/fp16, 64 wide)
 #define SSA_DQ_PINGPONG 1
 #endif
 constexpr bool kDqPingPong = SSA_DQ_PINGPONG;
+#ifndef SSA_DQ_DS_TMEM
+#define SSA_DQ_DS_TMEM 0
+#endif
+constexpr bool kDqDsTmem = SSA_DQ_DS_TMEM;   // dS over S in TMEM (TS-form dQ): measured slower (7.7 vs 6.5 ms at C3), off
 #ifdef SSA_TRACE
 __device__ unsigned long long g_trace_dq[3][128];
 __device__ int g_trace_dq_cnt[3];
@@ -250,7 +254,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           Ring kv_q = kv;
           auto issue_s = [&]() {
             mbar_wait(&S->kv_full[kv.idx], kv.ph);
-            mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
+            if (!kDqDsTmem) mbar_wait(&S->s_empty[w], sb.ph ^ 1u);   // (TMEM dS: ordered after dQ instead)
             tc_fence_after();
             const uint32_t sk = smem_u32(sKV + kv.idx * 2 * kKVBytes);
 #pragma unroll
@@ -268,21 +272,30 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           mbar_wait(&S->dq_empty[w], dqph ^ 1u);
           dqph ^= 1u;
           for (int j = 0; j < n_tiles; ++j) {
-            if (j + 1 < n_tiles) issue_s();
+            if (!kDqDsTmem && j + 1 < n_tiles) issue_s();
             if (w == 0) TRACE_R(1, 3, j + 1);
             mbar_wait(&S->ds_full[w], db.ph);
             tc_fence_after();
-            const uint32_t ads = smem_u32(sDS + w * 32768);
             const uint32_t sk = smem_u32(sKV + kv_q.idx * 2 * kKVBytes);
+            if (kDqDsTmem) {
+              // dS (fp16, two keys per column) sits over S in TMEM: A from TMEM
 #pragma unroll
-            for (int k = 0; k < kKT / 16; ++k)
-              umma_bf16(tQ, desc_sw128(ads + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024), desc_sw128(sk + k * 2048, 0, 1024),
-                        idQ, (j > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < kKT / 16; ++k)
+                umma_ts(tQ, tS + k * 8, desc_sw128(sk + k * 2048, 0, 1024), idQ, (j > 0 || k > 0) ? 1u : 0u);
+            } else {
+              const uint32_t ads = smem_u32(sDS + w * 32768);
+#pragma unroll
+              for (int k = 0; k < kKT / 16; ++k)
+                umma_bf16(tQ, desc_sw128(ads + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024),
+                          desc_sw128(sk + k * 2048, 0, 1024), idQ, (j > 0 || k > 0) ? 1u : 0u);
+            }
             umma_commit(&S->ds_empty[w]);
             umma_commit(&S->kv_empty[kv_q.idx]);
             if (w == 0) TRACE_R(1, 5, j);
             kv_q.next();
             db.next();
+            // (TMEM dS) S(j+1) overwrites dS(j): issued after dQ(j) by the same thread, in pipe order
+            if (kDqDsTmem && j + 1 < n_tiles) issue_s();
           }
           umma_commit(&S->dq_full[w]);
           umma_commit(&S->q_empty);
@@ -330,7 +343,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           tmem_ld32(tS + c0, s);
           tmem_ld32(tS + kKT + c0, dp);
           tmem_wait_ld();
-          if (c0 + 32 == kKT) {
+          if (!kDqDsTmem && c0 + 32 == kKT) {
             tc_fence_before();
             mbar_arrive(&S->s_empty[wg]);
           }
@@ -343,18 +356,25 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
             const float p0 = ex2(fmaf(s[i], cl2, -l2)), p1 = ex2(fmaf(s[i + 1], cl2, -l2));
             pk[(c0 + i) / 2] = pack_f16(p0 * fmaf(wb, dp[i], -Db), p1 * fmaf(wb, dp[i + 1], -Db));
           }
+          // (TMEM dS) columns [c0/2, c0/2 + 16) hold keys c0..c0+31; S columns below c0 + 32 are read
+          if (kDqDsTmem) tmem_st16(tS + c0 / 2, pk + c0 / 2);
         }
         if (kDqPingPong && duo) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_R(2, 9, j);
         sb.next();
-        mbar_wait(&S->ds_empty[wg], db.ph ^ 1u);
-        if (warp == 0) TRACE_R(2, 10, j);
-        const uint32_t base = smem_u32(sDS + wg * 32768);
+        if (kDqDsTmem) {
+          tmem_wait_st();
+          tc_fence_before();
+        } else {
+          mbar_wait(&S->ds_empty[wg], db.ph ^ 1u);
+          if (warp == 0) TRACE_R(2, 10, j);
+          const uint32_t base = smem_u32(sDS + wg * 32768);
 #pragma unroll
-        for (int ch = 0; ch < kKT / 8; ++ch)
-          st_shared_v4(base + (ch >> 3) * 16384 + sw128(t, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
-                       pk[4 * ch + 3]);
-        fence_proxy_async_smem();
+          for (int ch = 0; ch < kKT / 8; ++ch)
+            st_shared_v4(base + (ch >> 3) * 16384 + sw128(t, ch & 7), pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2],
+                         pk[4 * ch + 3]);
+          fence_proxy_async_smem();
+        }
         mbar_arrive(&S->ds_full[wg]);
         if (warp == 0) TRACE_R(2, 11, j);
         db.next();
