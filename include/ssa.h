@@ -67,6 +67,8 @@ typedef struct ssa_plan_s* ssa_plan;
  * contiguous in that order; empty blocks are not materialised.
  *
  *   coords      device int32 [n,4] rows (b,x,y,z), 0 <= b < batch, 0 <= x < grid[0] ...
+ *   n           number of tokens, 1 <= n < 2^31 (an empty input, n = 0, is SSA_ERR_ARG: with no
+ *               token there is no block, no query and nothing to attend; callers skip the call)
  *   grid        HOST int32[3] grid extent per axis (latent resolution, e.g. 128 at 1024^3)
  *   m_*         block edge lengths; the distinct values must form a divisibility chain and
  *               m_cmp | m_slc (relaxed to >=, reading R2)

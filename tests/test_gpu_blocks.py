@@ -62,3 +62,17 @@ def test_error_codes():
     with pytest.raises(ssa.SSAError) as e:
         ssa.ssa_build_blocks(ok, (8, 8, 8), 1, 4, 6, 6, 6)
     assert e.value.code == "SSA_ERR_HIERARCHY"
+
+
+def test_empty_input():
+    """N = 0 is a documented argument error (include/ssa.h): raised cleanly, nothing launched."""
+    import torch
+    from paper_2505_17412_b200 import ssa
+    c = torch.zeros((0, 4), dtype=torch.int32).cuda()
+    with pytest.raises(ssa.SSAError) as e:
+        ssa.ssa_build_blocks(c, (8, 8, 8), 1, 4, 8, 8, 8)
+    assert e.value.code == "SSA_ERR_ARG"
+    torch.cuda.synchronize()
+    # the library stays usable afterwards
+    one = torch.tensor([[0, 1, 2, 3]], dtype=torch.int32).cuda()
+    assert ssa.ssa_build_blocks(one, (8, 8, 8), 1, 4, 8, 8, 8).n_blocks[0] == 1
