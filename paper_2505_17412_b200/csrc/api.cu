@@ -117,10 +117,25 @@ void carve_inputs(Carve& c, const Dims& d, Ctx* x, bool with_dout) {
 
 // Row chunks of the compressed-key KV-outer backward: ~16 waves of 296 CTAs (148 SMs x 2 CTAs), so
 // the last partial wave costs a few percent instead of up to a third (long CTAs, few waves).
+// Row chunks per compressed-key tile for the KV-outer compression backward (one CTA per SM): the
+// count in [8, 64] whose CTA total fills the last wave best (ties -> more chunks, better balance).
 int pick_chunks(const Plan* p, int h_kv) {
-  int tiles = std::max(1, p->n_cmp_tiles * h_kv);
-  int n = (16 * 296 + tiles - 1) / tiles;
-  return std::min(128, std::max(1, n));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  const int64_t tiles = std::max(1, p->n_cmp_tiles * h_kv);
+  int best = 1;
+  double best_eff = -1.0;
+  for (int n = 1; n <= 64; ++n) {
+    if (tiles * n < sms && n < 64) continue;               // at least one full wave when possible
+    const int64_t ctas = tiles * n, waves = (ctas + sms - 1) / sms;
+    const double eff = double(ctas) / double(waves * sms) - (n < 8 ? 0.05 : 0.0);
+    if (eff >= best_eff - 1e-9) { best_eff = eff; best = n; }
+  }
+  return best;
 }
 
 void carve_bwd(Carve& c, const Dims& d, const Plan* p, Ctx* x) {

@@ -27,7 +27,10 @@ using namespace tc;
 constexpr int kD = 64;
 constexpr int kTile = 128;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kStages = 3;
+#ifndef SSA_SW_STAGES
+#define SSA_SW_STAGES 3
+#endif
+constexpr int kStages = SSA_SW_STAGES;   // K/V stages of the selection+window kernel
 
 #ifdef SSA_TRACE
 // per-role shared-memory trace of one CTA (debug builds: -DSSA_TRACE); flushed at kernel end
