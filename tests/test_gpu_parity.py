@@ -161,3 +161,15 @@ def test_gpu_sorted_input_flag():
     q, k, v, g = (to_dev(x[perm], torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates))
     out, _ = ssa.ssa_forward(plan, cfg, q, k, v, g)
     assert np.array_equal(out.float().cpu().numpy(), r["out"][perm].astype(np.float32))
+
+
+@pytest.mark.parametrize("heads", [(8, 1), (32, 4), (4, 4), (16, 16)])
+def test_tc_head_layouts(heads):
+    """tcgen05 path with other GQA layouts (h_s = H / h_kv = 8, 8, 1, 1): the rows of a query block are
+    tokens x h_s, so 128-row tiles hold 16 or 128 tokens; parity and top-k as for C2."""
+    from ssa_workload import batch_coords, make_inputs, sphere_shell
+    H, h_kv = heads
+    c = batch_coords([sphere_shell(32, 13.0, 2.0)])
+    inp = make_inputs(c, (32, 32, 32), 1, H, h_kv, 64, "bf16", seed=5)
+    kw = dict(h_kv=h_kv, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    _check_all(inp, kw, expect_tc=True)
