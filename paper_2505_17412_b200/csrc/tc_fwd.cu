@@ -44,6 +44,29 @@ __device__ int g_trace_cnt[3];
 #else
 #define TRACE_R(role, ev, j) do { } while (0)
 #endif
+#ifdef SSA_TRACE
+// selection/window kernel event trace of CTA (5, 0), written straight to global memory (debug builds)
+__device__ unsigned long long g_trace_sw[3][512];
+__device__ int g_trace_sw_cnt[3];
+#define TRACE_SW(role, ev, j)                                                                             \
+  do {                                                                                                   \
+    if (blockIdx.x == 5 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && sw_n < 512) {                   \
+      g_trace_sw[role][sw_n++] = (clock64() << 16) | (unsigned long long)(((ev) << 12) | ((j) & 0xfff)); \
+      g_trace_sw_cnt[role] = sw_n;                                                                       \
+    }                                                                                                    \
+  } while (0)
+#else
+#define TRACE_SW(role, ev, j) do { } while (0)
+#endif
+#ifdef SSA_TRACE
+// per-CTA [start, end) globaltimer stamps + SM id of the selection/window kernel (debug builds)
+__device__ unsigned long long g_cta_stamp[2 * 4096][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 struct TcArgs {
   Ctx c;
@@ -510,13 +533,30 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 constexpr int kMaxTiles = 4 * 64 + 8;
 constexpr int kSwThreads = 352;
 struct SwSmem {
-  uint64_t q_full, q_empty, kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_free[2],
+  uint64_t q_full[2], q_empty[2], kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_free[2],
       o_full[2], o_empty[2];
   uint32_t tmem;
   int n_tiles, n_slc_tiles;
   int tile_row[kMaxTiles];
   int tile_nv[kMaxTiles];
 };
+
+// Per-warp staging of 32 rows x 64 fp32 (8 KB): the thread that owns a row (TMEM lane) writes it with
+// 16-byte chunks XOR-swizzled by the row, then the warp reads it back two rows per instruction (lanes
+// 0-15 row 2i, 16-31 row 2i+1) so every global access of the epilogue is a coalesced 512-byte row pair
+// instead of 32 rows touched by one instruction (measured: the per-row form cost ~10 us per row-tile
+// pair). Both directions are bank-conflict free.
+__device__ __forceinline__ void stage_row(float* wbuf, int lane, const float* v, float scale, int c0, int n) {
+#pragma unroll
+  for (int j = 0; j < n; j += 4) {
+    const int ch = (c0 + j) >> 2;
+    *reinterpret_cast<float4*>(wbuf + lane * 64 + 4 * (ch ^ (lane & 15))) =
+        make_float4(v[j] * scale, v[j + 1] * scale, v[j + 2] * scale, v[j + 3] * scale);
+  }
+}
+__device__ __forceinline__ float4 staged_chunk(const float* wbuf, int rl, int ch) {
+  return *reinterpret_cast<const float4*>(wbuf + rl * 64 + 4 * (ch ^ (rl & 15)));
+}
 
 __global__ void __launch_bounds__(kSwThreads, 1)
 k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmK,
@@ -525,11 +565,15 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;                          // 2 x 16 KB (row tiles of the pair)
   uint8_t* sKV = sm + 32768;                 // kStages x {K, V} 32 KB
-  SwSmem* S = reinterpret_cast<SwSmem*>(sKV + kStages * 32768);
+  uint8_t* sEpi = sKV + kStages * 32768;     // epilogue operands: 8 KB per softmax warp
+  SwSmem* S = reinterpret_cast<SwSmem*>(sEpi + 65536);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
   if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
+#ifdef SSA_TRACE
+  const unsigned long long stamp0 = gtimer();
+#endif
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + kTile - 1) / kTile;
@@ -538,8 +582,9 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   const int krow_g = g * c.N;
 
   if (tid == 0) {
-    mbar_init(&S->q_full, 1);
-    mbar_init(&S->q_empty, 2);                        // one arrival per MMA issuer
+    // per-warpgroup Q slots: slot w is released by its MMA issuer once the pair's last S MMA has read it,
+    // so the next pair's Q load overlaps the last tile's softmax, P.V and epilogue
+    for (int w = 0; w < 2; ++w) { mbar_init(&S->q_full[w], 1); mbar_init(&S->q_empty[w], 1); }
     for (int i = 0; i < kStages; ++i) { mbar_init(&S->kv_full[i], 1); mbar_init(&S->kv_empty[i], 2); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S->s_full[i], 1);
@@ -568,19 +613,25 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   tc_fence_after();
   const uint32_t tmem = S->tmem;
   const int n_tiles = S->n_tiles, n_slc_tiles = S->n_slc_tiles;
+#ifdef SSA_TRACE
+  int sw_n = 0;
+#endif
 
   if (warp == 8) {
     // ---------------------------------------------------------------- TMA producer
     Ring kv(kStages);
-    uint32_t qph = 0;
+    uint32_t qph[2] = {0u, 0u};
     for (int pr = 0; pr < n_pair; ++pr) {
       const bool duo = 2 * pr + 1 < n_rt;
-      mbar_wait(&S->q_empty, qph ^ 1u);
-      qph ^= 1u;
-      if (lane == 0) {
-        mbar_expect_tx(&S->q_full, duo ? 32768u : 16384u);
-        tma_load_2d(sQ, &tmQ, &S->q_full, 0, qrow0 + 2 * pr * kTile);
-        if (duo) tma_load_2d(sQ + 16384, &tmQ, &S->q_full, 0, qrow0 + (2 * pr + 1) * kTile);
+      for (int w = 0; w < (duo ? 2 : 1); ++w) {
+        mbar_wait(&S->q_empty[w], qph[w] ^ 1u);
+        qph[w] ^= 1u;
+        TRACE_SW(0, 1, pr * 2 + w);
+        if (lane == 0) {
+          mbar_expect_tx(&S->q_full[w], 16384u);
+          tma_load_2d(sQ + w * 16384, &tmQ, &S->q_full[w], 0, qrow0 + (2 * pr + w) * kTile);
+        }
+        __syncwarp();
       }
       for (int j = 0; j < n_tiles; ++j) {
         mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
@@ -605,9 +656,11 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     uint32_t qph = 0, pph = 0, oph = 0;
     for (int pr = 0; pr < n_pair; ++pr) {
       const bool mine = w == 0 || 2 * pr + 1 < n_rt;
-      mbar_wait(&S->q_full, qph);
-      qph ^= 1u;
-      tc_fence_after();
+      if (mine) {
+        mbar_wait(&S->q_full[w], qph);
+        qph ^= 1u;
+        tc_fence_after();
+      }
       if (lane == 0) {
         if (!mine) {
           for (int j = 0; j < n_tiles; ++j) {   // keep the shared K/V ring moving
@@ -615,9 +668,9 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             mbar_arrive(&S->kv_empty[kv.idx]);
             kv.next();
           }
-          mbar_arrive(&S->q_empty);
         } else {
           Ring kv_pv = kv;
+          int n_s = 0;
           auto issue_s = [&]() {
             mbar_wait(&S->kv_full[kv.idx], kv.ph);
             mbar_wait(&S->s_empty[w], sb.ph ^ 1u);
@@ -627,6 +680,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             for (int k = 0; k < 4; ++k)
               umma_bf16(tS, desc_sw128(aQ + k * 32, 0, 1024), desc_sw128(sk + k * 32, 0, 1024), idS, k > 0);
             umma_commit(&S->s_full[w]);
+            if (w == 0) TRACE_SW(1, 3, n_s);
+            if (++n_s == n_tiles) umma_commit(&S->q_empty[w]);   // last S of the pair: Q slot w is free
             kv.next();
             sb.next();
           };
@@ -644,14 +699,14 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             for (int k = 0; k < 8; ++k)
               umma_ts(tO, tP + k * 8, desc_sw128(sv + k * 2048, 0, 1024), idO, (!fresh || k > 0) ? 1u : 0u);
             umma_commit(&S->p_free[w]);
+            if (w == 0) TRACE_SW(1, 5, j);
             umma_commit(&S->kv_empty[kv_pv.idx]);
             kv_pv.next();
           }
           umma_commit(&S->o_full[w]);
-          umma_commit(&S->q_empty);
         }
       }
-      __syncwarp();   // lanes 1-31 only track q_full; the ring cursors live in lane 0
+      __syncwarp();   // the ring cursors live in lane 0
     }
   } else {
     // ---------------------------------------------------------------- softmax warpgroup wg
@@ -669,33 +724,47 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       const int r = rt * kTile + t;
       const bool rvalid = r < rows;
       const int64_t row = qrow0 + (rvalid ? r : 0);
+      const int wrow0 = rt * kTile + (warp & 3) * 32;   // first row of this warp
+      float* wbuf = reinterpret_cast<float*>(sEpi + wg * 32768 + (warp & 3) * 8192);
+      if (wrow0 + lane < rows) {
+        // pull this warp's O_cmp rows (HBM) and gates toward L2 now; the epilogue reads them a pair later
+        const char* pc = reinterpret_cast<const char*>(static_cast<const float*>(c.o[0]) + (qrow0 + wrow0 + lane) * int64_t(kD));
+        asm volatile("prefetch.global.L2 [%0];\n\tprefetch.global.L2 [%1];" :: "l"(pc), "l"(pc + 128));
+        if ((lane & 7) == 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(c.gs + (qrow0 + wrow0 + lane) * 3));
+      }
       float lse_slc = 0.f;
       float m = -1e30f, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
         const bool fresh = j == 0 || j == n_slc_tiles;
         const bool closed = j == n_slc_tiles && j > 0;
         if (closed) {             // close the selection branch -> saved O_slc (fp32), after P.V(j-1)
+          if (warp == 0) TRACE_SW(2, 12, j);
           mbar_wait(&S->p_free[wg], fph);
           fph ^= 1u;
           tc_fence_after();
           const float inv = 1.f / l;
-          float* os = static_cast<float*>(c.o[1]) + row * kD;
 #pragma unroll
           for (int cc = 0; cc < kD; cc += 32) {
             float o[32];
             tmem_ld32(tO + cc, o);
             tmem_wait_ld();
-            if (rvalid) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *reinterpret_cast<float4*>(os + cc + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
-            }
+            stage_row(wbuf, lane, o, inv, cc, 32);
           }
+          __syncwarp();
+          float* os = static_cast<float*>(c.o[1]);
+#pragma unroll 4
+          for (int i = 0; i < 16; ++i) {
+            const int rl = 2 * i + (lane >> 4), ch = lane & 15, rr = wrow0 + rl;
+            if (rr < rows) *reinterpret_cast<float4*>(os + (qrow0 + rr) * int64_t(kD) + 4 * ch) = staged_chunk(wbuf, rl, ch);
+          }
+          __syncwarp();
           lse_slc = m + lg2(l);
           m = -1e30f;
           l = 0.f;
         }
+        if (warp == 0) TRACE_SW(2, 6, j);
         mbar_wait(&S->s_full[wg], sb.ph);
+        if (warp == 0) TRACE_SW(2, 7, j);
         tc_fence_after();
         const int nv = S->tile_nv[j];
         float v[128];
@@ -723,7 +792,9 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         l *= alpha;
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (warp == 0) TRACE_SW(2, 8, j);
         if (duo) named_bar_sync(4 + wg, 256);
+        if (warp == 0) TRACE_SW(2, 9, j);
 #pragma unroll
         for (int cc = 0; cc < kTile; cc += 32) {
           uint32_t pk[16];
@@ -736,6 +807,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           tmem_st16(tP + cc / 2, pk);
         }
         if (duo) named_bar_arrive(5 - wg, 256);
+        if (warp == 0) TRACE_SW(2, 10, j);
         l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         // the reference max moved inside a branch: rescale O (P.V(j-1) has completed: p_free)
         if (__any_sync(0xffffffffu, bump && !fresh)) {
@@ -754,50 +826,87 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         tc_fence_before();
         mbar_arrive(&S->p_full[wg]);
       }
+      // Epilogue (gated sum, Eq. 6). The window output is staged through the warp's shared slot so every
+      // global access is a coalesced row pair (lanes 0-15 / 16-31 take rows 2i / 2i+1, four columns
+      // each); the gated sum's global operands (O_slc written at the branch close, O_cmp, gates,
+      // destination rows) come in two batches of 8 row pairs, the first issued before O is ready.
+      const int ch = lane & 15;
+      const float* os_g = static_cast<const float*>(c.o[1]);
+      const float* ocm_g = static_cast<const float*>(c.o[0]);
+      float4 e_sl[8], e_cm[8];
+      float e_w[8][3];
+      int e_dst[8];
+      auto epi_load = [&](int bt) {
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+          const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
+          const int64_t grow = qrow0 + rr;
+          e_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 4 * ch);
+          e_cm[ii] = *reinterpret_cast<const float4*>(ocm_g + grow * kD + 4 * ch);
+          e_w[ii][0] = c.gs[grow * 3];
+          e_w[ii][1] = c.gs[grow * 3 + 1];
+          e_w[ii][2] = c.gs[grow * 3 + 2];
+          const int tok = t0 + rr / c.h_s;
+          e_dst[ii] = c.sorted_input ? tok : c.perm[tok];
+        }
+      };
+      epi_load(0);
+      if (warp == 0) TRACE_SW(2, 13, pr);
       mbar_wait(&S->o_full[wg], oph);
       oph ^= 1u;
+      if (warp == 0) TRACE_SW(2, 14, pr);
       tc_fence_after();
-      float o_acc[kD];
-      tmem_ld32(tO, o_acc);
-      tmem_ld32(tO + 32, o_acc + 32);
-      tmem_wait_ld();
+      const float inv = 1.f / l;
+#pragma unroll
+      for (int cc = 0; cc < kD; cc += 32) {
+        float o[32];
+        tmem_ld32(tO + cc, o);
+        tmem_wait_ld();
+        stage_row(wbuf, lane, o, inv, cc, 32);
+      }
       tc_fence_before();
       mbar_arrive(&S->o_empty[wg]);
-      const float inv = 1.f / l;
       if (rvalid) {
-        // o_acc * inv is the window branch; the selection branch is in c.o[1] (written above)
-        float* ow = static_cast<float*>(c.o[2]) + row * kD;
-        const float* os = static_cast<const float*>(c.o[1]) + row * kD;
-        const float* ocm = static_cast<const float*>(c.o[0]) + row * kD;
         c.lse[1][row] = lse_slc;
         c.lse[2][row] = m + lg2(l);
-        const float w0 = c.gs[row * 3], w1 = c.gs[row * 3 + 1], w2 = c.gs[row * 3 + 2];
-        const int tok = t0 + r / c.h_s, hs = r % c.h_s;
-        const int dst = c.sorted_input ? tok : c.perm[tok];
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
+      }
+      __syncwarp();
+      if (warp == 0) TRACE_SW(2, 0, pr);
+      float* ow = static_cast<float*>(c.o[2]);
 #pragma unroll
-        for (int e = 0; e < kD; e += 8) {
-          const float4 ca = *reinterpret_cast<const float4*>(ocm + e), cb = *reinterpret_cast<const float4*>(ocm + e + 4);
-          const float4 sa = *reinterpret_cast<const float4*>(os + e), sb4 = *reinterpret_cast<const float4*>(os + e + 4);
-          const float cm[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-          const float sl[8] = {sa.x, sa.y, sa.z, sa.w, sb4.x, sb4.y, sb4.z, sb4.w};
-          float wn[8];
-          uint32_t wq[4];
+      for (int bt = 0; bt < 2; ++bt) {
+        if (bt == 1) epi_load(1);
+        if (warp == 0) TRACE_SW(2, 2 + 2 * bt, pr);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) wn[i] = o_acc[e + i] * inv;
-#pragma unroll
-          for (int i = 0; i < 8; i += 2)
-            wq[i / 2] = pack_bf16(w0 * cm[i] + w1 * sl[i] + w2 * wn[i], w0 * cm[i + 1] + w1 * sl[i + 1] + w2 * wn[i + 1]);
-          *reinterpret_cast<uint4*>(out + e) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
-          *reinterpret_cast<float4*>(ow + e) = make_float4(wn[0], wn[1], wn[2], wn[3]);
-          *reinterpret_cast<float4*>(ow + e + 4) = make_float4(wn[4], wn[5], wn[6], wn[7]);
+        for (int ii = 0; ii < 8; ++ii) {
+          const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = wrow0 + rl;
+          if (rr < rows) {
+            const int64_t grow = qrow0 + rr;
+            const float4 wn = staged_chunk(wbuf, rl, ch), sl = e_sl[ii], cm = e_cm[ii];
+            const float w0 = e_w[ii][0], w1 = e_w[ii][1], w2 = e_w[ii][2];
+            *reinterpret_cast<float4*>(ow + grow * kD + 4 * ch) = wn;
+            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) +
+                                 (int64_t(e_dst[ii]) * c.H + g * c.h_s + rr % c.h_s) * kD + 4 * ch;
+            *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y),
+                                                        pack_bf16(w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w));
+          }
         }
       }
+      __syncwarp();
+      if (warp == 0) TRACE_SW(2, 15, pr);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tmem);
+#ifdef SSA_TRACE
+  if (tid == 0 && blockIdx.x * gridDim.y + blockIdx.y < 2 * 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    auto* st = g_cta_stamp[blockIdx.y * gridDim.x + blockIdx.x];
+    st[0] = stamp0; st[1] = gtimer(); st[2] = smid;
+  }
+#endif
 }
 
 }  // namespace
@@ -847,7 +956,7 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
     SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
   }
   {
-    const size_t smem = 1024 + 32768 + kStages * 32768 + sizeof(SwSmem);
+    const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_slc_win_fwd", st);
     k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(c, tmQ, tmK, tmV);
@@ -859,6 +968,21 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
 }  // namespace ssa
 
 #ifdef SSA_TRACE
+extern "C" int ssa_debug_trace_sw(unsigned long long* host, int cap) {
+  int cnt[3];
+  unsigned long long buf[3][512];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(cnt, ssa::g_trace_sw_cnt, sizeof(cnt));
+  cudaMemcpyFromSymbol(buf, ssa::g_trace_sw, sizeof(buf));
+  int n = 0;
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < cnt[r] && n < cap; ++i) host[n++] = buf[r][i];
+  return n;
+}
+extern "C" int ssa_debug_cta_stamps(unsigned long long* host, int n) {   // [n][3] start, end, smid
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, ssa::g_cta_stamp, size_t(n) * 3 * 8) == cudaSuccess ? n : -1;
+}
 extern "C" int ssa_debug_trace(unsigned long long* host, int cap) {
   int cnt[3];
   unsigned long long buf[3][128];

@@ -8,7 +8,7 @@ from paper_2505_17412_b200 import ssa
 from ssa_workload import CONFIGS, config_coords, make_inputs
 L = ssa.lib()
 which = sys.argv[1] if len(sys.argv) > 1 else "cmp"
-f = {"cmp": L.ssa_debug_trace, "dq": L.ssa_debug_trace_dq, "kv": L.ssa_debug_trace_kv}[which]
+f = {"cmp": L.ssa_debug_trace, "dq": L.ssa_debug_trace_dq, "kv": L.ssa_debug_trace_kv, "sw": L.ssa_debug_trace_sw}[which]
 f.restype = ctypes.c_int
 f.argtypes = [ctypes.c_void_p, ctypes.c_int]
 cfg = CONFIGS["C3"]
@@ -20,8 +20,8 @@ acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16)
 out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
 if which in ("dq", "kv"):
     ssa.ssa_backward(plan, acfg, saved, *t)
-buf = (ctypes.c_ulonglong * 1024)()
-n = f(buf, 768)
+buf = (ctypes.c_ulonglong * 2048)()
+n = f(buf, 1536)
 ev = np.array(buf[:n], dtype=np.uint64)
 clk = (ev >> 16).astype(np.int64)
 code = ((ev >> 12) & 0xF).astype(int)
@@ -37,6 +37,9 @@ if which == "dq":
 if which == "kv":
     names = {1: "P row tile", 3: "M S^T issued", 5: "M dVdK issued", 7: "S S-ready", 8: "S turn-in", 9: "S turn-out",
              11: "S P written"}
+if which == "sw":
+    names = {0: "S epi staged", 2: "S epi batch0", 4: "S epi batch1", 1: "P Q load", 3: "M S issued", 5: "M PV issued", 6: "S wait S", 7: "S S-ready", 8: "S turn-wait",
+             9: "S turn-in", 10: "S turn-out", 12: "S close", 13: "S epi wait O", 14: "S epi O-ready", 15: "S epi done"}
 print("events", n)
-for i in order[:400]:
+for i in order[:1600]:
     print(f"{clk[i]-t0:10d} {names.get(code[i], code[i]):14s} j={j[i]}")
