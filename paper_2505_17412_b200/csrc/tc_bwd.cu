@@ -105,6 +105,8 @@ __global__ void k_tc_bwd_prep(Ctx c, __half* q16, __half* do16, __half* dow, __h
 constexpr int kKT = 96;                  // keys per tile
 constexpr int kDqThreads = 352;
 constexpr int kMaxKT = 64 + 4 * 64 * 2 + 16;
+constexpr int kMaxBlkDq = 4 * 64 + 8;    // >= top_k (tc_plan_ok)
+constexpr int kMaxSegDq = kMaxKT + kMaxBlkDq + 8;
 constexpr int kKVBytes = kKT * 128;      // one K or V tile (bf16/fp16, 64 wide)
 #ifndef SSA_DQ_PINGPONG
 #define SSA_DQ_PINGPONG 1
@@ -130,8 +132,12 @@ struct DqSmem {
       dq_full[2], dq_empty[2];
   uint32_t tmem;
   int n_tiles;
-  int tile_row[kMaxKT];                   // row in the key array of the tile's branch
-  int tile_nv[kMaxKT];
+  int tile_row[kMaxKT];                   // compressed-key tiles: first row (one 96-row box)
+  uint32_t tile_mask[kMaxKT][3];          // valid keys of the tile
+  int tile_seg[kMaxKT + 1];               // selection / window tiles: packed segments [tile_seg[j], tile_seg[j + 1])
+  int seg_row[kMaxSegDq];                 // first key row of an 8-row-aligned run of one block's keys
+  int seg_dst_len[kMaxSegDq];             // destination slot << 8 | rows
+  int blk_a0[kMaxBlkDq], blk_a1[kMaxBlkDq];   // key ranges of the selected blocks
   int8_t tile_br[kMaxKT];
 #ifdef SSA_TRACE
   unsigned long long trace[3][128];
@@ -141,7 +147,7 @@ struct DqSmem {
 __global__ void __launch_bounds__(kDqThreads, 1)
 k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
         __grid_constant__ const CUtensorMap tmKc, __grid_constant__ const CUtensorMap tmVc,
-        __grid_constant__ const CUtensorMap tmK, __grid_constant__ const CUtensorMap tmV) {
+        __grid_constant__ const TmapSet4 tmK, __grid_constant__ const TmapSet4 tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;                       // 2 x 16 KB (row tiles of the pair)
@@ -159,6 +165,14 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
   const int n_pair = (n_rt + 1) / 2;
   const int qrow0 = (g * c.N + t0) * c.h_s;
 
+  if (warp == 0) {   // the selected blocks' key ranges, fetched by all lanes at once
+    for (int j = lane; j < c.T; j += 32) {
+      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+      S->blk_a0[j] = B >= 0 ? c.off[SSA_LEVEL_SLC][B] : 0;
+      S->blk_a1[j] = B >= 0 ? c.off[SSA_LEVEL_SLC][B + 1] : 0;
+    }
+    __syncwarp();
+  }
   if (tid == 0) {
     mbar_init(&S->q_full, 1);
     mbar_init(&S->q_empty, 2);                        // one arrival per MMA issuer
@@ -172,22 +186,65 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       mbar_init(&S->dq_empty[i], 128);
     }
     fence_barrier_init();
-    int n = 0;
+    // compressed keys: contiguous 96-key tiles; selected blocks: keys packed back to back in 8-row
+    // granules (a 96-key tile mixes blocks); window: packed from a fresh tile (tiles never mix branches)
+    int n = 0, ns = 0, pos = kKT;
+    uint32_t mk[3] = {0u, 0u, 0u};
     const int b = c.q_batch[Q];
     const int c0 = c.bb[SSA_LEVEL_CMP][b], c1 = c.bb[SSA_LEVEL_CMP][b + 1];
     const int ncmp = c.n_blk[SSA_LEVEL_CMP];
-    for (int x = c0; x < c1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * ncmp + x; S->tile_nv[n] = min(kKT, c1 - x); S->tile_br[n] = 0; ++n; }
-    for (int j = 0; j < c.T; ++j) {
-      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
-      if (B < 0) continue;
-      const int a0 = c.off[SSA_LEVEL_SLC][B], a1 = c.off[SSA_LEVEL_SLC][B + 1];
-      for (int x = a0; x < a1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * c.N + x; S->tile_nv[n] = min(kKT, a1 - x); S->tile_br[n] = 1; ++n; }
+    auto set_bits = [&](int lo0, int hi0) {
+#pragma unroll
+      for (int w = 0; w < 3; ++w) {
+        const int lo = max(lo0, 32 * w), hi = min(hi0, 32 * w + 32);
+        if (hi > lo) mk[w] |= (hi - lo == 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << (lo - 32 * w);
+      }
+    };
+    for (int x = c0; x < c1 && n < kMaxKT; x += kKT) {
+      mk[0] = mk[1] = mk[2] = 0u;
+      set_bits(0, min(kKT, c1 - x));
+      S->tile_row[n] = g * ncmp + x;
+      S->tile_br[n] = 0;
+      S->tile_seg[n] = ns;
+      for (int w = 0; w < 3; ++w) S->tile_mask[n][w] = mk[w];
+      ++n;
     }
-    for (int x = t0; x < t1 && n < kMaxKT; x += kKT) { S->tile_row[n] = g * c.N + x; S->tile_nv[n] = min(kKT, t1 - x); S->tile_br[n] = 2; ++n; }
+    auto flush = [&]() { for (int w = 0; w < 3; ++w) S->tile_mask[n - 1][w] = mk[w]; };
+    auto add_block = [&](int a0, int a1, int br) {
+      const int len = a1 - a0, l8 = (len + 7) & ~7;
+      for (int x = 0; x < l8 && n <= kMaxKT;) {
+        if (pos == kKT) {
+          if (n > 0 && S->tile_br[n - 1] != 0) flush();
+          if (n == kMaxKT) { n = kMaxKT + 1; break; }
+          S->tile_seg[n] = ns;
+          S->tile_br[n] = int8_t(br);
+          mk[0] = mk[1] = mk[2] = 0u;
+          ++n;
+          pos = 0;
+        }
+        const int take = min(l8 - x, kKT - pos), valid = max(0, min(take, len - x));
+        if (ns < kMaxSegDq) { S->seg_row[ns] = g * c.N + a0 + x; S->seg_dst_len[ns] = (pos << 8) | take; ++ns; }
+        set_bits(pos, pos + valid);
+        pos += take;
+        x += take;
+      }
+    };
+    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], 1);   // (unselected: empty range)
+    if (n <= kMaxKT && n > 0 && S->tile_br[n - 1] != 0) flush();
+    pos = kKT;                                    // the window starts a fresh tile
+    add_block(t0, t1, 2);
+    if (n <= kMaxKT) flush();
+    n = min(n, kMaxKT);
+    S->tile_seg[n] = ns;
     S->n_tiles = n;
   }
+  // zero the K/V stages once: slots a packed tile leaves unfilled must hold finite values (dS = 0 there)
+  for (int i = tid; i < kStages * 2 * kKVBytes / 16; i += kDqThreads)
+    *reinterpret_cast<uint4*>(sKV + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
   if (warp == 8 && lane == 0) {
-    tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmKc); tma_prefetch(&tmVc); tma_prefetch(&tmK); tma_prefetch(&tmV);
+    tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmKc); tma_prefetch(&tmVc);
+    for (int bx = 0; bx < 4; ++bx) { tma_prefetch(&tmK.m[bx]); tma_prefetch(&tmV.m[bx]); }
   }
   if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
@@ -219,10 +276,25 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         TRACE_R(0, 1, j);
         if (lane == 0) {
           uint8_t* st = sKV + kv.idx * 2 * kKVBytes;
-          const bool cmp = S->tile_br[j] == 0;
-          mbar_expect_tx(&S->kv_full[kv.idx], 2u * kKVBytes);
-          tma_load_2d(st, cmp ? &tmKc : &tmK, &S->kv_full[kv.idx], 0, S->tile_row[j]);
-          tma_load_2d(st + kKVBytes, cmp ? &tmVc : &tmV, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+          if (S->tile_br[j] == 0) {
+            mbar_expect_tx(&S->kv_full[kv.idx], 2u * kKVBytes);
+            tma_load_2d(st, &tmKc, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+            tma_load_2d(st + kKVBytes, &tmVc, &S->kv_full[kv.idx], 0, S->tile_row[j]);
+          } else {
+            const int s0 = S->tile_seg[j], s1 = S->tile_seg[j + 1];
+            uint32_t rows_in = 0;
+            for (int q = s0; q < s1; ++q) rows_in += uint32_t(S->seg_dst_len[q] & 0xff);
+            mbar_expect_tx(&S->kv_full[kv.idx], rows_in * 256u);
+            for (int q = s0; q < s1; ++q) {
+              const int dst = S->seg_dst_len[q] >> 8, len = S->seg_dst_len[q] & 0xff, src = S->seg_row[q];
+              for (int off = 0; off < len;) {   // boxes of 64 / 32 / 16 / 8 rows
+                const int bx = len - off >= 64 ? 0 : (len - off >= 32 ? 1 : (len - off >= 16 ? 2 : 3));
+                tma_load_2d(st + (dst + off) * 128, &tmK.m[bx], &S->kv_full[kv.idx], 0, src + off);
+                tma_load_2d(st + kKVBytes + (dst + off) * 128, &tmV.m[bx], &S->kv_full[kv.idx], 0, src + off);
+                off += 64 >> bx;
+              }
+            }
+          }
         }
         __syncwarp();
         kv.next();
@@ -327,7 +399,9 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         Dv[br] = c.Dd[br][row];
       }
       for (int j = 0; j < n_tiles; ++j) {
-        const int br = S->tile_br[j], nv = S->tile_nv[j];
+        const int br = S->tile_br[j];
+        const uint32_t mk0 = S->tile_mask[j][0], mk1 = S->tile_mask[j][1], mk2 = S->tile_mask[j][2];
+        const bool full = (mk0 & mk1 & mk2) == 0xffffffffu;
         const float l2 = br == 0 ? lse2[0] : (br == 1 ? lse2[1] : lse2[2]);
         const float wb = br == 0 ? wgt[0] : (br == 1 ? wgt[1] : wgt[2]);
         const float Db = br == 0 ? Dv[0] : (br == 1 ? Dv[1] : Dv[2]);
@@ -347,9 +421,16 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
             tc_fence_before();
             mbar_arrive(&S->s_empty[wg]);
           }
-          if (nv < kKT) {                            // partial tile (uniform): padded keys get p = 0
+          if (!full) {                               // unfilled slots / granule padding: p = 0
+            const uint32_t mw = c0 == 0 ? mk0 : (c0 == 32 ? mk1 : mk2);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) s[i] = c0 + i < nv ? s[i] : -INFINITY;
+            for (int gr = 0; gr < 4; ++gr) {
+              const uint32_t bits = (mw >> (8 * gr)) & 0xffu;
+              if (bits != 0xffu) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s[8 * gr + i] = (bits >> i) & 1u ? s[8 * gr + i] : -INFINITY;
+              }
+            }
           }
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -925,18 +1006,20 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   const int64_t n = int64_t(qrows) * kD;
   k_tc_bwd_prep<<<unsigned((n / 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow, k16, v16, kc, vc);
   SSA_LAUNCH_CHECK("k_tc_bwd_prep");
-  CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmK, tmV, tmKc128, tmVc128, tmK128, tmV128, tmDW[3];
+  CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmKc128, tmVc128, tmK128, tmV128, tmDW[3];
+  TmapSet4 tmK, tmV;
   for (int br = 0; br < 3; ++br)
     if (!make_tmap_bf16_2d(&tmDW[br], dow + size_t(br) * qrows * kD, qrows, kRT)) return SSA_ERR_CUDA;
   if (!make_tmap_bf16_2d(&tmQ, q16, qrows, 128) || !make_tmap_bf16_2d(&tmDO, do16, qrows, 128) ||
       !make_tmap_bf16_2d(&tmQ64, q16, qrows, kRT) || !make_tmap_bf16_2d(&tmDO64, do16, qrows, kRT) ||
       !make_tmap_bf16_2d(&tmKc, kc, crows, kKT) || !make_tmap_bf16_2d(&tmVc, vc, crows, kKT) ||
-      !make_tmap_bf16_2d(&tmK, k16, krows, kKT) || !make_tmap_bf16_2d(&tmV, v16, krows, kKT) ||
+      !make_tmap_set4(&tmK, k16, krows) || !make_tmap_set4(&tmV, v16, krows) ||
       !make_tmap_bf16_2d(&tmKc128, kc, crows, 128) || !make_tmap_bf16_2d(&tmVc128, vc, crows, 128) ||
       !make_tmap_bf16_2d(&tmK128, k16, krows, 128) || !make_tmap_bf16_2d(&tmV128, v16, krows, 128))
     return SSA_ERR_CUDA;
   {
     const size_t smem = 1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem);
+    static_assert(1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem) <= 232448, "dQ shared memory");
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_bwd_dq", st);
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);

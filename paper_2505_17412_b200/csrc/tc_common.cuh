@@ -255,4 +255,12 @@ __device__ __forceinline__ uint32_t elect_lane0() { return (threadIdx.x & 31) ==
 // host: encode a 2D 16-bit (bf16 or fp16: TMA copies bytes, no conversion) tensor map [rows][64]
 // with 128-B swizzle and a box of (64, box_rows)
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows);
+// the same [rows][64] tensor with boxes of 64 / 32 / 16 / 8 rows: packed key tiles are assembled from
+// 8-row granules (any run of 8k rows = at most one box of each size)
+struct TmapSet4 { CUtensorMap m[4]; };
+inline bool make_tmap_set4(TmapSet4* t, const void* base, uint64_t rows) {
+  for (int b = 0; b < 4; ++b)
+    if (!make_tmap_bf16_2d(&t->m[b], base, rows, 64u >> b)) return false;
+  return true;
+}
 }  // namespace ssa

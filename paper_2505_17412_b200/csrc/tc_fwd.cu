@@ -9,8 +9,8 @@
 //                 fixed normalisation). Scores stay in smem; top-k runs in the same CTA.
 //  k_tc_slcwin_fwd selection attention over the T selected blocks (Alg. 1 at query-block granularity)
 //                 and window attention with online softmax, then the gated sum of Eq. 6 and
-//                 the scatter to caller order. Key tiles are 128-token TMA boxes starting at each
-//                 block's offset C (variable fill handled by masking).
+//                 the scatter to caller order. Key tiles pack the selected blocks' keys in 8-row
+//                 granules (TMA boxes of 64/32/16/8 rows); a per-tile bit mask drops granule padding.
 //
 // Warp roles (192 threads): warps 0-3 softmax/epilogue (thread i <-> TMEM lane i), warp 4 TMA
 // producer, warp 5 MMA issuer (one elected lane) + TMEM owner.
@@ -531,14 +531,20 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 // Key tiles: the T selected blocks (ascending), then the window (== the query block: m_win == m_q);
 // at the branch boundary the selection O is normalised and stored, and O restarts from zero.
 constexpr int kMaxTiles = 4 * 64 + 8;
+constexpr int kMaxSegs = 2 * kMaxTiles + 8;
 constexpr int kSwThreads = 352;
 struct SwSmem {
   uint64_t q_full[2], q_empty[2], kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_free[2],
       o_full[2], o_empty[2];
   uint32_t tmem;
   int n_tiles, n_slc_tiles;
-  int tile_row[kMaxTiles];
-  int tile_nv[kMaxTiles];
+  // packed key tiles: tile j = segments [tile_seg[j], tile_seg[j + 1]); segment = 8-row-aligned run of one
+  // block's keys (seg_row: first key row; seg_dst_len: destination slot << 8 | rows), tile_mask = valid keys
+  int tile_seg[kMaxTiles + 1];
+  uint32_t tile_mask[kMaxTiles][4];
+  int seg_row[kMaxSegs];
+  int seg_dst_len[kMaxSegs];
+  int blk_a0[kMaxTiles], blk_a1[kMaxTiles];   // key ranges of the selected blocks (T <= kMaxTiles)
 };
 
 // Per-warp staging of 32 rows x 64 fp32 (8 KB): the thread that owns a row (TMEM lane) writes it with
@@ -559,8 +565,8 @@ __device__ __forceinline__ float4 staged_chunk(const float* wbuf, int rl, int ch
 }
 
 __global__ void __launch_bounds__(kSwThreads, 1)
-k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmK,
-                __grid_constant__ const CUtensorMap tmV) {
+k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const TmapSet4 tmK,
+                __grid_constant__ const TmapSet4 tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;                          // 2 x 16 KB (row tiles of the pair)
@@ -581,6 +587,14 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   const int qrow0 = (g * c.N + t0) * c.h_s;
   const int krow_g = g * c.N;
 
+  if (warp == 0) {   // the selected blocks' key ranges, fetched by all lanes at once
+    for (int j = lane; j < c.T; j += 32) {
+      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
+      S->blk_a0[j] = B >= 0 ? c.off[SSA_LEVEL_SLC][B] : 0;
+      S->blk_a1[j] = B >= 0 ? c.off[SSA_LEVEL_SLC][B + 1] : 0;
+    }
+    __syncwarp();
+  }
   if (tid == 0) {
     // per-warpgroup Q slots: slot w is released by its MMA issuer once the pair's last S MMA has read it,
     // so the next pair's Q load overlaps the last tile's softmax, P.V and epilogue
@@ -595,18 +609,54 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       mbar_init(&S->o_empty[i], 128);
     }
     fence_barrier_init();
-    int n = 0;
-    for (int j = 0; j < c.T; ++j) {
-      const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + j];
-      if (B < 0) continue;
-      const int a0 = c.off[SSA_LEVEL_SLC][B], a1 = c.off[SSA_LEVEL_SLC][B + 1];
-      for (int x = a0; x < a1 && n < kMaxTiles; x += kTile) { S->tile_row[n] = x; S->tile_nv[n] = min(kTile, a1 - x); ++n; }
-    }
-    S->n_slc_tiles = n;
-    for (int x = t0; x < t1 && n < kMaxTiles; x += kTile) { S->tile_row[n] = x; S->tile_nv[n] = min(kTile, t1 - x); ++n; }
+    // Key tiles: the selected blocks' keys packed back to back in 8-row granules (a block of n keys takes
+    // ceil(n / 8) granules, so a 128-key tile mixes blocks instead of padding each block to 128), then
+    // the window (= the query block) from a fresh tile. Granules are TMA boxes of 8..64 rows at 1024-B
+    // aligned slots, so the 128-B swizzle pattern is the one a single 128-row box would produce.
+    int n = 0, ns = 0, pos = kTile;
+    uint32_t mk[4] = {0u, 0u, 0u, 0u};            // mask of the open tile, flushed when it closes
+    auto flush = [&]() {
+      if (n > 0) for (int w = 0; w < 4; ++w) S->tile_mask[n - 1][w] = mk[w];
+    };
+    auto add_block = [&](int a0, int a1) {
+      const int len = a1 - a0, l8 = (len + 7) & ~7;
+      for (int x = 0; x < l8 && n <= kMaxTiles;) {
+        if (pos == kTile) {
+          flush();
+          if (n == kMaxTiles) { n = kMaxTiles + 1; break; }
+          S->tile_seg[n] = ns;
+          mk[0] = mk[1] = mk[2] = mk[3] = 0u;
+          ++n;
+          pos = 0;
+        }
+        const int take = min(l8 - x, kTile - pos), valid = max(0, min(take, len - x));
+        if (ns < kMaxSegs) { S->seg_row[ns] = a0 + x; S->seg_dst_len[ns] = (pos << 8) | take; ++ns; }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {              // bits [pos, pos + valid) of the 128-bit mask
+          const int lo = max(pos, 32 * w), hi = min(pos + valid, 32 * w + 32);
+          if (hi > lo) mk[w] |= (hi - lo == 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << (lo - 32 * w);
+        }
+        pos += take;
+        x += take;
+      }
+    };
+    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j]);   // (unselected: empty range)
+    S->n_slc_tiles = min(n, kMaxTiles);
+    pos = kTile;                                  // the window starts a fresh tile
+    add_block(t0, t1);
+    if (n <= kMaxTiles) flush();
+    n = min(n, kMaxTiles);
+    S->tile_seg[n] = ns;
     S->n_tiles = n;
   }
-  if (warp == 8 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
+  // zero the K/V stages once: slots a packed tile leaves unfilled must hold finite values (P = 0 there)
+  for (int i = tid; i < kStages * 32768 / 16; i += kSwThreads)
+    *reinterpret_cast<uint4*>(sKV + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tmQ);
+    for (int b = 0; b < 4; ++b) { tma_prefetch(&tmK.m[b]); tma_prefetch(&tmV.m[b]); }
+  }
   if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
   __syncthreads();
@@ -637,9 +687,19 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         mbar_wait(&S->kv_empty[kv.idx], kv.ph ^ 1u);
         if (lane == 0) {
           uint8_t* st = sKV + kv.idx * 32768;
-          mbar_expect_tx(&S->kv_full[kv.idx], 32768u);
-          tma_load_2d(st, &tmK, &S->kv_full[kv.idx], 0, krow_g + S->tile_row[j]);
-          tma_load_2d(st + 16384, &tmV, &S->kv_full[kv.idx], 0, krow_g + S->tile_row[j]);
+          const int s0 = S->tile_seg[j], s1 = S->tile_seg[j + 1];
+          uint32_t rows_in = 0;
+          for (int q = s0; q < s1; ++q) rows_in += uint32_t(S->seg_dst_len[q] & 0xff);
+          mbar_expect_tx(&S->kv_full[kv.idx], rows_in * 256u);
+          for (int q = s0; q < s1; ++q) {
+            const int dst = S->seg_dst_len[q] >> 8, len = S->seg_dst_len[q] & 0xff, src = krow_g + S->seg_row[q];
+            for (int off = 0; off < len;) {   // boxes of 64 / 32 / 16 / 8 rows
+              const int b = len - off >= 64 ? 0 : (len - off >= 32 ? 1 : (len - off >= 16 ? 2 : 3));
+              tma_load_2d(st + (dst + off) * 128, &tmK.m[b], &S->kv_full[kv.idx], 0, src + off);
+              tma_load_2d(st + 16384 + (dst + off) * 128, &tmV.m[b], &S->kv_full[kv.idx], 0, src + off);
+              off += 64 >> b;
+            }
+          }
         }
         __syncwarp();
         kv.next();
@@ -766,7 +826,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         mbar_wait(&S->s_full[wg], sb.ph);
         if (warp == 0) TRACE_SW(2, 7, j);
         tc_fence_after();
-        const int nv = S->tile_nv[j];
+        const uint32_t mk0 = S->tile_mask[j][0], mk1 = S->tile_mask[j][1], mk2 = S->tile_mask[j][2], mk3 = S->tile_mask[j][3];
         float v[128];
         tmem_ld32(tS, v);
         tmem_ld32(tS + 32, v + 32);
@@ -776,9 +836,16 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         tc_fence_before();
         mbar_arrive(&S->s_empty[wg]);
         sb.next();
-        if (nv < kTile) {
+        if ((mk0 & mk1 & mk2 & mk3) != 0xffffffffu) {   // granule padding / unfilled slots: p = 0
+          const uint32_t mk[4] = {mk0, mk1, mk2, mk3};
 #pragma unroll
-          for (int i = 0; i < kTile; ++i) v[i] = i < nv ? v[i] : -INFINITY;   // padded keys: p = 0
+          for (int gr = 0; gr < kTile / 8; ++gr) {      // only granules with padding pay the selects
+            const uint32_t bits = (mk[gr >> 2] >> (8 * (gr & 3))) & 0xffu;
+            if (bits != 0xffu) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * gr + i] = (bits >> i) & 1u ? v[8 * gr + i] : -INFINITY;
+            }
+          }
         }
         if (!closed) {   // P.V(j-1) complete: O is up to date and P may be rewritten
           mbar_wait(&S->p_free[wg], fph);
@@ -938,11 +1005,10 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
   const int64_t n = int64_t(c.h_kv) * c.N * kD;   // >= h_kv * n_cmp * kD
   k_tc_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16);
   SSA_LAUNCH_CHECK("k_tc_prep");
-  CUtensorMap tmQ, tmKh, tmKl, tmVc, tmK, tmV;
+  CUtensorMap tmQ, tmKh, tmKl, tmVc;
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
   if (!make_tmap_bf16_2d(&tmQ, c.qs, qrows, kTile) || !make_tmap_bf16_2d(&tmKh, kc_hi, crows, kTile) ||
-      !make_tmap_bf16_2d(&tmKl, kc_lo, crows, kTile) || !make_tmap_bf16_2d(&tmVc, vc, crows, kTile) ||
-      !make_tmap_bf16_2d(&tmK, c.ks, krows, kTile) || !make_tmap_bf16_2d(&tmV, vs16, krows, kTile))
+      !make_tmap_bf16_2d(&tmKl, kc_lo, crows, kTile) || !make_tmap_bf16_2d(&tmVc, vc, crows, kTile))
     return SSA_ERR_CUDA;
   TcArgs a{c, kc_hi, kc_lo, vc};
   const int nq = c.n_blk[SSA_LEVEL_Q];
@@ -959,7 +1025,11 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
     const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_slc_win_fwd", st);
-    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(c, tmQ, tmK, tmV);
+    TmapSet4 tk, tv;
+    for (int b = 0; b < 4; ++b)
+      if (!make_tmap_bf16_2d(&tk.m[b], c.ks, krows, 64u >> b) || !make_tmap_bf16_2d(&tv.m[b], vs16, krows, 64u >> b))
+        return SSA_ERR_CUDA;
+    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(c, tmQ, tk, tv);
     SSA_LAUNCH_CHECK("k_tc_slcwin_fwd");
   }
   return SSA_OK;
