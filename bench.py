@@ -361,6 +361,25 @@ def main():
     if not args.no_full and rank == 0:
         full = full_attention_time(torch, dev, int(np.max(ntok_b)), H, h_kv, d, tdt)
 
+    # ---- context: sparse 3D window attention alone (SSA_WINDOW_ONLY; the SS-VAE layer) on the same tokens ----
+    win = None
+    if rank == 0 and used_tc and not sharded:
+        wcfg = ssa.AttnCfg(h_q=H, h_kv=h_kv, d=d, top_k=T, dtype=tdt, flags=ssa.SSA_WINDOW_ONLY)
+        plan_w = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+        wt = []
+        for i in range(8):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _, sv = ssa.ssa_forward(plan_w, wcfg, q, k, v, g, out=out)
+            ssa.ssa_backward(plan_w, wcfg, sv, q, k, v, g, do, grads=grads)
+            e1.record(st)
+            if i >= 3:
+                wt.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        win = {"impl": "SSA_WINDOW_ONLY (sparse 3D window attention alone, fwd+bwd, same tokens and windows)",
+               "fwd_bwd_ms": round(float(np.mean([a.elapsed_time(b) for a, b in wt])) / batch, 4)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, cfg, coords, grid, batch, inp, value)
@@ -382,6 +401,8 @@ def main():
             "work": {"E_cmp": E_cmp, "E_slc": E_slc, "E_win": E_win},
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if win:
+            line["window_attention"] = win
         if full:
             line["full_attention"] = full
             if "fwd_bwd_ms" in full:

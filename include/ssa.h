@@ -124,12 +124,20 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *   flags        : SSA_INPUT_SORTED — tensors are already in plan order (no internal permute);
  *                  SSA_FORCE_SIMT   — use the SIMT kernels even where tcgen05 kernels exist;
  *                  SSA_SAVE_SCORES  — keep the fp32 selection scores in the saved state;
- *                  SSA_KV_GRAD_FP32 — dk, dv buffers are fp32 (exact partial sums across shards).
+ *                  SSA_KV_GRAD_FP32 — dk, dv buffers are fp32 (exact partial sums across shards);
+ *                  SSA_WINDOW_ONLY  — only the sparse 3D window branch is computed: the
+ *                                     compression and selection branches are skipped (their saved
+ *                                     outputs are 0, indices -1), out = omega_win * O_win, and the
+ *                                     backward gives the window branch's gradients (dgates of the
+ *                                     skipped branches are 0). With gates (0, 0, 1) this is sparse 3D
+ *                                     window attention (the SS-VAE layer). tcgen05 path only
+ *                                     (bf16, d = 64, m_win == m_slc == m_q); SSA_ERR_UNSUPPORTED otherwise.
  * ----------------------------------------------------------------------------------------------*/
 #define SSA_INPUT_SORTED 1u
 #define SSA_FORCE_SIMT 2u
 #define SSA_SAVE_SCORES 4u
 #define SSA_KV_GRAD_FP32 8u   /* dk / dv are written as fp32 (partials of a query-block shard)    */
+#define SSA_WINDOW_ONLY 16u   /* window branch only (sparse 3D window attention)                   */
 
 typedef struct {
   int32_t h_q, h_kv, d, top_k;

@@ -175,6 +175,7 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
   x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.D));
   x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
+  x->win_only = (cfg->flags & SSA_WINDOW_ONLY) ? 1 : 0;
   x->save_scores = (cfg->flags & SSA_SAVE_SCORES) ? 1 : 0;
   x->kv_grad_f32 = (cfg->flags & SSA_KV_GRAD_FP32) ? 1 : 0;
   x->perm = p->perm;
@@ -241,6 +242,16 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   const bool bf16 = cfg->dtype == SSA_BF16;
   if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
   if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
+  if (x.win_only) {
+    if (!use_tc(d, cfg, p)) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path (bf16, d = 64, m_win == m_slc == m_q)"); return SSA_ERR_UNSUPPORTED; }
+    // skipped branches: O = 0, indices -1 (no selected blocks), LSE huge (p = exp2(s - LSE) = 0 anywhere)
+    const int64_t rows = int64_t(d.N) * d.H;
+    for (int b = 0; b < 2; ++b) {
+      SSA_CUDA_TRY(cudaMemsetAsync(x.o[b], 0, size_t(rows) * d.D * 4, st));
+      SSA_CUDA_TRY(cudaMemsetAsync(x.lse[b], 0x7f, size_t(rows) * 4, st));
+    }
+    SSA_CUDA_TRY(cudaMemsetAsync(x.I, 0xff, size_t(d.n_q) * d.h_kv * d.T * 4, st));
+  }
   if (use_tc(d, cfg, p)) {
     if ((s = tc_forward(x, tc_ws, st)) != SSA_OK) return s;
   } else {
@@ -299,9 +310,15 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
   if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
   const bool tc = use_tc_bwd(d, cfg, p);
+  if (x.win_only && !tc) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path"); return SSA_ERR_UNSUPPORTED; }
   if (tc) {
     if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
-    if ((s = cmp_reduce(x, st)) != SSA_OK) return s;
+    if (x.win_only) {   // no compressed-key gradients: the pool backward adds zeros
+      SSA_CUDA_TRY(cudaMemsetAsync(x.dkc, 0, size_t(d.h_kv) * d.n_cmp * d.D * 4, st));
+      SSA_CUDA_TRY(cudaMemsetAsync(x.dvc, 0, size_t(d.h_kv) * d.n_cmp * d.D * 4, st));
+    } else if ((s = cmp_reduce(x, st)) != SSA_OK) {
+      return s;
+    }
   } else {
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
   }

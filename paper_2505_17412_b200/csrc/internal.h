@@ -43,6 +43,7 @@ struct Ctx {
   int32_t max_fill[kLevels];
   float scale;                    // softmax scale (natural)
   int32_t sorted_input;
+  int32_t win_only;                   // SSA_WINDOW_ONLY: compression / selection branches skipped
   int32_t q_begin, q_end;         // owned query blocks [q_begin, q_end) (plan order)
   int32_t tok_begin, tok_end;     // their token range
   int32_t save_scores;

@@ -200,7 +200,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         if (hi > lo) mk[w] |= (hi - lo == 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << (lo - 32 * w);
       }
     };
-    for (int x = c0; x < c1 && n < kMaxKT; x += kKT) {
+    for (int x = c0; x < c1 && n < kMaxKT && !c.win_only; x += kKT) {   // (window-only: no compressed keys)
       mk[0] = mk[1] = mk[2] = 0u;
       set_bits(0, min(kKT, c1 - x));
       S->tile_row[n] = g * ncmp + x;
@@ -1041,7 +1041,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_kv_reduce");
   }
-  {
+  if (!c.win_only) {
     ProfScope ps("tc_bwd_cmp_kv", st);
     k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, st>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
                                                                               tmVc128);

@@ -1017,9 +1017,11 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
                         (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
     if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ProfScope ps("tc_cmp_fwd", st);
-    k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
-    SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
+    if (!c.win_only) {
+      ProfScope ps("tc_cmp_fwd", st);
+      k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
+      SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
+    }
   }
   {
     const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);

@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa_b200.so"))   # SSA_LIB: debug builds only
 
 SSA_F32, SSA_BF16 = 0, 1
-SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32 = 1, 2, 4, 8
+SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32, SSA_WINDOW_ONLY = 1, 2, 4, 8, 16
 LEVEL_CMP, LEVEL_SLC, LEVEL_WIN, LEVEL_Q = 0, 1, 2, 3
 STATUS = ["SSA_OK", "SSA_ERR_ARG", "SSA_ERR_DUP_COORD", "SSA_ERR_COORD_RANGE", "SSA_ERR_HIERARCHY",
           "SSA_ERR_BAD_STATE", "SSA_ERR_WORKSPACE", "SSA_ERR_UNSUPPORTED", "SSA_ERR_CUDA"]
@@ -335,6 +335,38 @@ def ssa_backward(plan: Plan, cfg: AttnCfg, saved: Saved, q, k, v, gates, dout, g
                           _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"), _dev(dg, "dgates"),
                           ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_backward")
     return dq, dk, dv, dg
+
+
+def window_attention(coords: torch.Tensor, grid, batch: int, m_win: int, q, k, v, *, h_kv: int, shift: int = 0,
+                     dtype: torch.dtype = torch.bfloat16, window_only: bool = True):
+    """Sparse 3D (shifted-)window attention, the SS-VAE's attention layer and SSA's window
+    branch on its own: every active token attends the active tokens of its own aligned
+    m_win^3 window; with shift = s the windows are those of coords + s (Swin-style shifted windows).
+
+    Composition over the C ABI only (no arithmetic here): the plan is built on the shifted coordinates
+    (grid + s) and ssa_forward runs with gates (0, 0, 1), which makes Eq. 6 return the window branch
+    exactly. window_only=True sets SSA_WINDOW_ONLY (the compression and selection branches are skipped
+    in the kernels); False runs the full SSA step with those gates (the reference composition).
+    Returns (out, ctx) with ctx = (plan, cfg, saved, gates) for window_attention_backward."""
+    if shift:
+        coords = coords.clone()
+        coords[:, 1:] += int(shift)
+        grid = tuple(int(g) + int(shift) for g in grid)
+    m_cmp = 4 if m_win % 4 == 0 else m_win
+    plan = ssa_build_blocks(coords, grid, batch, m_cmp, m_win, m_win, m_win)
+    cfg = AttnCfg(h_q=q.shape[1], h_kv=h_kv, d=q.shape[2], top_k=1, dtype=dtype,
+                  flags=SSA_WINDOW_ONLY if window_only else 0)
+    gates = torch.zeros(q.shape[0], q.shape[1], 3, dtype=q.dtype, device=q.device)
+    gates[..., 2] = 1
+    out, saved = ssa_forward(plan, cfg, q, k, v, gates)
+    return out, (plan, cfg, saved, gates)
+
+
+def window_attention_backward(ctx, q, k, v, dout):
+    """Gradients (dq, dk, dv) of window_attention (the gate gradients are dropped)."""
+    plan, cfg, saved, gates = ctx
+    dq, dk, dv, _ = ssa_backward(plan, cfg, saved, q, k, v, gates, dout)
+    return dq, dk, dv
 
 
 def launch_count() -> int:

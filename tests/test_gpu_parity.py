@@ -173,3 +173,20 @@ def test_tc_head_layouts(heads):
     inp = make_inputs(c, (32, 32, 32), 1, H, h_kv, 64, "bf16", seed=5)
     kw = dict(h_kv=h_kv, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
     _check_all(inp, kw, expect_tc=True)
+
+
+@pytest.mark.parametrize("T", [4, 32])
+def test_tc_dense_blocks(T):
+    """Solid ball (5 616 tokens): a full 8^3 selection block of 512 keys (4 tiles) among blocks of 47-416
+    keys, so packed key tiles hold segments of 64-row boxes that cross tile boundaries; T = 32 exceeds the
+    27 selection blocks (-1 padding) — tcgen05 path against the oracle."""
+    from ssa_workload import batch_coords, make_inputs
+    G, r = 24, 11.0
+    ax = np.arange(G)
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    ball = np.stack([X, Y, Z], -1)[(X - 11.5) ** 2 + (Y - 11.5) ** 2 + (Z - 11.5) ** 2 <= r * r].astype(np.int32)
+    c = batch_coords([ball])
+    inp = make_inputs(c, (G, G, G), 1, 8, 2, 64, "bf16", seed=13)
+    kw = dict(h_kv=2, T=T, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    r_, _ = _check_all(inp, kw, expect_tc=True)
+    assert (r_["I"] < 0).any() == (T > 27)

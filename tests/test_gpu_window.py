@@ -1,0 +1,94 @@
+"""Sparse 3D (shifted-)window attention (the SS-VAE's attention layer; SSA's window branch on
+its own) through ssa.window_attention, against an independent reference built from the pinned
+oracle dense attention (oracle.dense_attention / dense_attention_backward) applied window by window.
+Windows: floor((x + s) / m_win) per batch item, s = 0 (aligned) or m_win / 2 (shifted)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import rel_err, to_dev
+from paper_2505_17412_b200 import ssa
+from ssa_workload import batch_coords, make_inputs, sphere_shell
+
+pytestmark = pytest.mark.gpu
+
+
+def _reference(coords, q, k, v, dout, h_kv, m, shift):
+    N, H, d = q.shape
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    key = np.concatenate([coords[:, :1], (coords[:, 1:] + shift) // m], axis=1)
+    _, win = np.unique(key, axis=0, return_inverse=True)
+    out, dq, dk, dv = (np.zeros_like(x) for x in (q, q, k, v))
+    for w in np.unique(win):
+        t = np.nonzero(win.ravel() == w)[0]
+        for g in range(h_kv):
+            for s in range(h_s):
+                h = g * h_s + s
+                o, _, p = O.dense_attention(q[t, h], k[t, g], v[t, g], scale)
+                out[t, h] = o
+                gq, gk, gv = O.dense_attention_backward(q[t, h], k[t, g], v[t, g], p, o, dout[t, h], scale)
+                dq[t, h] += gq
+                dk[t, g] += gk
+                dv[t, g] += gv
+    return out, dq, dk, dv
+
+
+@pytest.mark.parametrize("window_only", [True, False])
+@pytest.mark.parametrize("shift", [0, 4])
+def test_window_attention(shift, window_only):
+    coords = batch_coords([sphere_shell(24, 9.0, 2.0), sphere_shell(24, 7.0, 2.0)])
+    grid = (24, 24, 24)
+    inp = make_inputs(coords, grid, 2, 8, 2, 64, "bf16", seed=11)
+    q, k, v, do = (to_dev(x, torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.dout))
+    out, ctx = ssa.window_attention(torch.from_numpy(coords).cuda(), grid, 2, 8, q, k, v, h_kv=2, shift=shift,
+                                    window_only=window_only)
+    assert ctx[2].used_tcgen05
+    dq, dk, dv = ssa.window_attention_backward(ctx, q, k, v, do)
+    torch.cuda.synchronize()
+    ref = _reference(coords, inp.q, inp.k, inp.v, inp.dout, 2, 8, shift)
+    u = 2.0 ** -8
+    errs = {n: rel_err(x.float().cpu().numpy().astype(np.float64), r, u)
+            for n, x, r in zip(("out", "dq", "dk", "dv"), (out, dq, dk, dv), ref)}
+    assert all(e <= 2e-2 for e in errs.values()), errs
+
+
+def test_window_covering_grid_is_full_attention():
+    """m_win >= grid: one window per batch item, i.e. full attention over the item."""
+    coords = batch_coords([sphere_shell(16, 6.0, 2.0)])
+    grid = (16, 16, 16)
+    inp = make_inputs(coords, grid, 1, 8, 2, 64, "bf16", seed=12)
+    q, k, v = (to_dev(x, torch.bfloat16) for x in (inp.q, inp.k, inp.v))
+    out, ctx = ssa.window_attention(torch.from_numpy(coords).cuda(), grid, 1, 16, q, k, v, h_kv=2)
+    torch.cuda.synchronize()
+    N, H, d = inp.q.shape
+    ref = np.zeros_like(inp.q)
+    for h in range(H):
+        ref[:, h] = O.dense_attention(inp.q[:, h], inp.k[:, h // 4], inp.v[:, h // 4], 1.0 / math.sqrt(d))[0]
+    assert rel_err(out.float().cpu().numpy().astype(np.float64), ref, 2.0 ** -8) <= 2e-2
+
+
+def test_window_only_skips_branches_and_matches_composition():
+    """SSA_WINDOW_ONLY launches neither the compression kernel nor the compressed-key backward, and gives
+    the same window-branch result as the full step with gates (0, 0, 1) (same kernels, same order)."""
+    coords = batch_coords([sphere_shell(32, 13.0, 2.0)])
+    grid = (32, 32, 32)
+    inp = make_inputs(coords, grid, 1, 16, 2, 64, "bf16", seed=14)
+    q, k, v, do = (to_dev(x, torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.dout))
+    c = torch.from_numpy(coords).cuda()
+    res = {}
+    for wo in (False, True):
+        ssa.profile_reset()
+        ssa.profile_enable(True)
+        out, ctx = ssa.window_attention(c, grid, 1, 8, q, k, v, h_kv=2, window_only=wo)
+        grads = ssa.window_attention_backward(ctx, q, k, v, do)
+        torch.cuda.synchronize()
+        ssa.profile_enable(False)
+        res[wo] = (out,) + tuple(grads), {n: ssa.profile_read(n)[1] for n in ("tc_cmp_fwd", "tc_bwd_cmp_kv")}
+    assert res[False][1] == {"tc_cmp_fwd": 1, "tc_bwd_cmp_kv": 1}
+    assert res[True][1] == {"tc_cmp_fwd": 0, "tc_bwd_cmp_kv": 0}
+    for a, b in zip(res[True][0], res[False][0]):
+        assert torch.equal(a, b) or rel_err(a.float().cpu().numpy(), b.float().cpu().numpy().astype(np.float64), 2.0 ** -8) <= 1e-3
