@@ -59,15 +59,17 @@ __global__ void k_gather_keys(Ctx c, const T* __restrict__ k, const T* __restric
 
 template <class T>
 __global__ void k_gather_gates(Ctx c, const T* __restrict__ gates, float* __restrict__ gs) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.N) * c.H * 3;
-  if (i >= total) return;
-  int br = int(i % 3);
-  int h = int((i / 3) % c.H);
-  int p = int(i / (3 * int64_t(c.H)));
-  int src_p = c.sorted_input ? p : c.perm[p];
-  int g = h / c.h_s, s = h % c.h_s;
-  gs[((int64_t(g) * c.N + p) * c.h_s + s) * 3 + br] = ld(gates + (int64_t(src_p) * c.H + h) * 3 + br);
+  // one thread per (token, head): its 3 gates; 32-bit index math (N * H < 2^31)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.N * c.H) return;
+  const int h = i % c.H, p = i / c.H;
+  const int src_p = c.sorted_input ? p : c.perm[p];
+  const int g = h / c.h_s, s = h % c.h_s;
+  const T* src = gates + (int64_t(src_p) * c.H + h) * 3;
+  float* dst = gs + ((int64_t(g) * c.N + p) * c.h_s + s) * 3;
+  dst[0] = ld(src);
+  dst[1] = ld(src + 1);
+  dst[2] = ld(src + 2);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -789,25 +791,32 @@ __global__ void k_bwd_final_q(Ctx c) {
 }
 template <class T>
 __global__ void k_bwd_final_kv(Ctx c) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t total = int64_t(c.N) * c.h_kv * c.D;
-  if (i >= total) return;
-  int e = int(i % c.D);
-  int g = int((i / c.D) % c.h_kv);
-  int p = int(i / (int64_t(c.D) * c.h_kv));
-  int j = c.tok_block[SSA_LEVEL_CMP][p];
-  float inv = 1.f / float(c.off[SSA_LEVEL_CMP][j + 1] - c.off[SSA_LEVEL_CMP][j]);
-  int64_t ki = (int64_t(g) * c.N + p) * c.D + e;
-  int64_t ci = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
-  int dst = c.sorted_input ? p : c.perm[p];
-  int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
-  const float gk = c.dk_acc[ki] + c.dkc[ci] * inv, gv = c.dv_acc[ki] + c.dvc[ci] * inv;
+  // 4 consecutive elements per thread (D is a multiple of 4), 32-bit index math
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int dq4 = c.D >> 2;
+  if (i >= c.N * c.h_kv * dq4) return;
+  const int e = (i % dq4) * 4;
+  const int g = (i / dq4) % c.h_kv;
+  const int p = i / (dq4 * c.h_kv);
+  const int j = c.tok_block[SSA_LEVEL_CMP][p];
+  const float inv = 1.f / float(c.off[SSA_LEVEL_CMP][j + 1] - c.off[SSA_LEVEL_CMP][j]);
+  const int64_t ki = (int64_t(g) * c.N + p) * c.D + e;
+  const int64_t ci = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
+  const int dst = c.sorted_input ? p : c.perm[p];
+  const int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
+  const float4 ak = *reinterpret_cast<const float4*>(c.dk_acc + ki), av = *reinterpret_cast<const float4*>(c.dv_acc + ki);
+  const float4 ck = *reinterpret_cast<const float4*>(c.dkc + ci), cv = *reinterpret_cast<const float4*>(c.dvc + ci);
+  const float gk[4] = {ak.x + ck.x * inv, ak.y + ck.y * inv, ak.z + ck.z * inv, ak.w + ck.w * inv};
+  const float gv[4] = {av.x + cv.x * inv, av.y + cv.y * inv, av.z + cv.z * inv, av.w + cv.w * inv};
   if (c.kv_grad_f32) {
-    static_cast<float*>(c.dk)[o] = gk;
-    static_cast<float*>(c.dv)[o] = gv;
+    *reinterpret_cast<float4*>(static_cast<float*>(c.dk) + o) = make_float4(gk[0], gk[1], gk[2], gk[3]);
+    *reinterpret_cast<float4*>(static_cast<float*>(c.dv) + o) = make_float4(gv[0], gv[1], gv[2], gv[3]);
   } else {
-    st(static_cast<T*>(c.dk) + o, gk);
-    st(static_cast<T*>(c.dv) + o, gv);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      st(static_cast<T*>(c.dk) + o + u, gk[u]);
+      st(static_cast<T*>(c.dv) + o + u, gv[u]);
+    }
   }
 }
 
@@ -900,7 +909,7 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
     k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
                                                     static_cast<T*>(c.ks), static_cast<T*>(c.vs));
     SSA_LAUNCH_CHECK("k_gather_keys");
-    k_gather_gates<T><<<nblk(ng, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+    k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
     SSA_LAUNCH_CHECK("k_gather_gates");
   } else {
     using T = float;
@@ -913,7 +922,7 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
     k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
                                                     static_cast<T*>(c.ks), static_cast<T*>(c.vs));
     SSA_LAUNCH_CHECK("k_gather_keys");
-    k_gather_gates<T><<<nblk(ng, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+    k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
     SSA_LAUNCH_CHECK("k_gather_gates");
   }
   return SSA_OK;
@@ -991,14 +1000,14 @@ ssa_status bwd_epilogue(const Ctx& c, bool bf16, cudaStream_t st, bool skip_q) {
       k_bwd_final_q<__nv_bfloat16><<<nblk(nq, 256), 256, 0, st>>>(c);
       SSA_LAUNCH_CHECK("k_bwd_final_q");
     }
-    k_bwd_final_kv<__nv_bfloat16><<<nblk(nk, 256), 256, 0, st>>>(c);
+    k_bwd_final_kv<__nv_bfloat16><<<nblk(nk / 4, 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_bwd_final_kv");
   } else {
     if (!skip_q) {
       k_bwd_final_q<float><<<nblk(nq, 256), 256, 0, st>>>(c);
       SSA_LAUNCH_CHECK("k_bwd_final_q");
     }
-    k_bwd_final_kv<float><<<nblk(nk, 256), 256, 0, st>>>(c);
+    k_bwd_final_kv<float><<<nblk(nk / 4, 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_bwd_final_kv");
   }
   return SSA_OK;

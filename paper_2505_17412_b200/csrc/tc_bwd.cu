@@ -945,25 +945,31 @@ __global__ void k_kv_item_count(Ctx c, int32_t* cnt) {
 }
 // fold the partials of items 1.. of every (block, g) into dk_acc / dv_acc, in item order
 __global__ void k_kv_reduce(Ctx c) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(c.N) * c.h_kv * kD) return;
-  const int e = int(i % kD);
-  const int g = int((i / kD) % c.h_kv);
-  const int p = int(i / (int64_t(kD) * c.h_kv));
+  // 4 consecutive elements per thread (float4), 32-bit index math
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.N * c.h_kv * (kD / 4)) return;
+  const int e = (i % (kD / 4)) * 4;
+  const int g = (i / (kD / 4)) % c.h_kv;
+  const int p = i / ((kD / 4) * c.h_kv);
   const int B = c.tok_block[SSA_LEVEL_SLC][p];
   const int key = B * c.h_kv + g;
   const int i0 = c.kv_item_off[key], i1 = c.kv_item_off[key + 1];
   if (i1 - i0 <= 1) return;
   const int local = p - c.off[SSA_LEVEL_SLC][B];
-  float sk = 0.f, sv = 0.f;
+  float4 sk = make_float4(0.f, 0.f, 0.f, 0.f), sv = sk;
+#pragma unroll 4
   for (int s = i0 + 1; s < i1; ++s) {
     const int64_t idx = (int64_t(s) * c.max_fill[SSA_LEVEL_SLC] + local) * kD + e;
-    sk += c.kv_part_k[idx];
-    sv += c.kv_part_v[idx];
+    const float4 a = *reinterpret_cast<const float4*>(c.kv_part_k + idx), b = *reinterpret_cast<const float4*>(c.kv_part_v + idx);
+    sk.x += a.x; sk.y += a.y; sk.z += a.z; sk.w += a.w;
+    sv.x += b.x; sv.y += b.y; sv.z += b.z; sv.w += b.w;
   }
   const int64_t o = (int64_t(g) * c.N + p) * kD + e;
-  c.dk_acc[o] += sk;
-  c.dv_acc[o] += sv;
+  float4* dk = reinterpret_cast<float4*>(c.dk_acc + o);
+  float4* dv = reinterpret_cast<float4*>(c.dv_acc + o);
+  const float4 k0 = *dk, v0 = *dv;
+  *dk = make_float4(k0.x + sk.x, k0.y + sk.y, k0.z + sk.z, k0.w + sk.w);
+  *dv = make_float4(v0.x + sv.x, v0.y + sv.y, v0.z + sv.z, v0.w + sv.w);
 }
 
 }  // namespace
@@ -1037,7 +1043,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
   }
   {
-    const int64_t nk = int64_t(c.N) * c.h_kv * kD;
+    const int64_t nk = int64_t(c.N) * c.h_kv * (kD / 4);
     k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, st>>>(c);
     SSA_LAUNCH_CHECK("k_kv_reduce");
   }
