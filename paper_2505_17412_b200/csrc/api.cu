@@ -306,10 +306,11 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
   void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
   const bool bf16 = cfg->dtype == SSA_BF16;
-  if ((s = gather_inputs(x, bf16, st, true)) != SSA_OK) return s;
-  if ((s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
-  if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
   const bool tc = use_tc_bwd(d, cfg, p);
+  // the tcgen05 backward gathers the q / dO rows and computes D_c, dgates in its own row prologue
+  if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc)) != SSA_OK) return s;
+  if (!tc && (s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
+  if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
   if (x.win_only && !tc) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path"); return SSA_ERR_UNSUPPORTED; }
   if (tc) {
     if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;

@@ -80,7 +80,8 @@ struct Ctx {
 // SIMT kernels (simt.cu). Return SSA_OK or a launch error.
 ssa_status simt_forward(const Ctx& c, bool bf16, cudaStream_t st, bool attention_only);
 ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
-ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout);
+// rows = false: only keys and gates are gathered (the tcgen05 backward reads q / dO rows itself)
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows = true);
 ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st);
 size_t inverse_csr_ws_bytes(int n_slc, int h_kv, int n_q);

@@ -31,11 +31,11 @@ inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 template <class T>
 __global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ dst) {
   const int per = c.h_s * c.D * int(sizeof(T)) / 16;     // 16-B chunks per (token, group)
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(c.N) * c.h_kv * per) return;
-  const int ch = int(i % per);
-  const int g = int((i / per) % c.h_kv);
-  const int p = int(i / (int64_t(per) * c.h_kv));
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // 32-bit index math: N * H * D * esz / 16 < 2^31
+  if (i >= c.N * c.h_kv * per) return;
+  const int ch = i % per;
+  const int g = (i / per) % c.h_kv;
+  const int p = i / (per * c.h_kv);
   const int src_p = c.sorted_input ? p : c.perm[p];
   const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
   uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t(g) * c.N + p) * c.h_s * c.D);
@@ -46,11 +46,11 @@ template <class T>
 __global__ void k_gather_keys(Ctx c, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ ks,
                               T* __restrict__ vs) {
   const int per = c.D * int(sizeof(T)) / 16;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(c.N) * c.h_kv * per) return;
-  const int ch = int(i % per);
-  const int g = int((i / per) % c.h_kv);
-  const int p = int(i / (int64_t(per) * c.h_kv));
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.N * c.h_kv * per) return;
+  const int ch = i % per;
+  const int g = (i / per) % c.h_kv;
+  const int p = i / (per * c.h_kv);
   const int src_p = c.sorted_input ? p : c.perm[p];
   const int64_t so = (int64_t(src_p) * c.h_kv + g) * c.D, dof = (int64_t(g) * c.N + p) * c.D;
   reinterpret_cast<uint4*>(ks + dof)[ch] = reinterpret_cast<const uint4*>(k + so)[ch];
@@ -894,18 +894,20 @@ ssa_status dispatch_d_bwd(const Ctx& c, cudaStream_t st) {
 }
 }  // namespace
 
-ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout) {
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows) {
   const int esz = bf16 ? 2 : 4;
   const int64_t nr = int64_t(c.N) * c.h_kv * (c.h_s * c.D * esz / 16), nk = int64_t(c.N) * c.h_kv * (c.D * esz / 16);
   const int64_t ng = int64_t(c.N) * c.H * 3;
   if (bf16) {
     using T = __nv_bfloat16;
-    if (with_dout) {
+    if (with_dout && rows) {
       k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.dout), static_cast<T*>(c.dos));
       SSA_LAUNCH_CHECK("k_gather_rows(dout)");
     }
-    k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
-    SSA_LAUNCH_CHECK("k_gather_rows");
+    if (rows) {
+      k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
+      SSA_LAUNCH_CHECK("k_gather_rows");
+    }
     k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
                                                     static_cast<T*>(c.ks), static_cast<T*>(c.vs));
     SSA_LAUNCH_CHECK("k_gather_keys");

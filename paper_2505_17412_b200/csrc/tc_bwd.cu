@@ -62,21 +62,57 @@ __device__ __forceinline__ uint4 f32x8_to_h(const float* f, float s) {
                     h2_sat(f[6] * s, f[7] * s));
 }
 // one thread per 8 consecutive elements (16-byte loads and stores; every count is a multiple of 64)
-__global__ void k_tc_bwd_prep(Ctx c, __half* q16, __half* do16, __half* dow, __half* k16, __half* v16, __half* kc16,
-                              __half* vc16) {
+// Row prologue of the backward, one pass over the query rows: 8 lanes per row (g, p, s) in plan order,
+// 8 elements each. Gathers q and dO straight from the caller's order (bf16), writes the fp16 MMA
+// operands q16, do16 and the gate-scaled dow[c] = omega_c dO, and reduces <dO, O_c> for the three
+// branches (shuffles over the 8 lanes): D_c = omega_c <dO, O_c> and dgates_c = <dO, O_c> (Eq. 6
+// backward). Replaces the separate row gathers, the SIMT prologue and the row part of the fp16 prep.
+__global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;     // 32-bit: N * H * 8 < 2^31
+  const int nrows = c.N * c.H;
+  const int row = t >> 3, sub = t & 7;
+  const bool valid = row < nrows;
+  const int rr = valid ? row : 0;
+  const int s = rr % c.h_s, p = (rr / c.h_s) % c.N, g = rr / (c.h_s * c.N);
+  const int h = g * c.h_s + s;
+  const int src_p = c.sorted_input ? p : c.perm[p];
+  const int64_t so = (int64_t(src_p) * c.H + h) * kD + sub * 8, io = int64_t(rr) * kD + sub * 8;
+  float fq[8], fd[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.q) + so), fq);
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dout) + so), fd);
+  const float* w = c.gs + int64_t(rr) * 3;
+  float acc[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float4* o = reinterpret_cast<const float4*>(static_cast<const float*>(c.o[b]) + io);
+    const float4 x = o[0], y = o[1];
+    acc[b] = fd[0] * x.x + fd[1] * x.y + fd[2] * x.z + fd[3] * x.w + fd[4] * y.x + fd[5] * y.y + fd[6] * y.z + fd[7] * y.w;
+  }
+  if (valid) {
+    *reinterpret_cast<uint4*>(q16 + io) = f32x8_to_h(fq, 1.f);
+    *reinterpret_cast<uint4*>(do16 + io) = f32x8_to_h(fd, 1.f);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) *reinterpret_cast<uint4*>(dow + int64_t(b) * nrows * kD + io) = f32x8_to_h(fd, w[b]);
+  }
+#pragma unroll
+  for (int o = 4; o; o >>= 1)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+  if (!valid || sub != 0) return;
+  if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;   // rows of other shards
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    c.Dd[b][rr] = w[b] * acc[b];
+    static_cast<__nv_bfloat16*>(c.dgates)[(int64_t(src_p) * c.H + h) * 3 + b] = __float2bfloat16_rn(acc[b]);
+  }
+}
+
+// fp16 copies of the keys (k, v in plan order) and of the pooled keys (fp32 -> fp16), 8 elements per thread
+__global__ void k_tc_bwd_prep(Ctx c, __half* k16, __half* v16, __half* kc16, __half* vc16) {
   const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
-  const int64_t nr = int64_t(c.h_kv) * c.N * c.h_s * kD, nk = int64_t(c.h_kv) * c.N * kD;
+  const int64_t nk = int64_t(c.h_kv) * c.N * kD;
   const int64_t nc = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
   float f[8];
-  if (i < nr) {
-    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.qs) + i), f);
-    *reinterpret_cast<uint4*>(q16 + i) = f32x8_to_h(f, 1.f);
-    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dos) + i), f);
-    *reinterpret_cast<uint4*>(do16 + i) = f32x8_to_h(f, 1.f);
-    const float* w = c.gs + (i / kD) * 3;
-#pragma unroll
-    for (int br = 0; br < 3; ++br) *reinterpret_cast<uint4*>(dow + br * nr + i) = f32x8_to_h(f, w[br]);
-  }
   if (i < nk) {
     bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.ks) + i), f);
     *reinterpret_cast<uint4*>(k16 + i) = f32x8_to_h(f, 1.f);
@@ -1009,8 +1045,10 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T);
   c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
-  const int64_t n = int64_t(qrows) * kD;
-  k_tc_bwd_prep<<<unsigned((n / 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow, k16, v16, kc, vc);
+  k_tc_bwd_rows<<<unsigned((int64_t(c.N) * c.H * 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow);
+  SSA_LAUNCH_CHECK("k_tc_bwd_rows");
+  const int64_t n = int64_t(krows) * kD;   // >= h_kv * n_cmp * kD
+  k_tc_bwd_prep<<<unsigned((n / 8 + 255) / 256), 256, 0, st>>>(c, k16, v16, kc, vc);
   SSA_LAUNCH_CHECK("k_tc_bwd_prep");
   CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmKc128, tmVc128, tmK128, tmV128, tmDW[3];
   TmapSet4 tmK, tmV;
