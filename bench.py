@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-full", action="store_true", help="skip the full-attention comparator")
+    ap.add_argument("--no-window", action="store_true", help="skip the window-only (SSA_WINDOW_ONLY) context timing")
     ap.add_argument("--force-simt", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=24, help="query blocks in the oracle sample")
     return ap.parse_args()
@@ -363,7 +364,7 @@ def main():
 
     # ---- context: sparse 3D window attention alone (SSA_WINDOW_ONLY; the SS-VAE layer) on the same tokens ----
     win = None
-    if rank == 0 and used_tc and not sharded:
+    if rank == 0 and used_tc and not sharded and not args.no_window:
         wcfg = ssa.AttnCfg(h_q=H, h_kv=h_kv, d=d, top_k=T, dtype=tdt, flags=ssa.SSA_WINDOW_ONLY)
         plan_w = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
         wt = []

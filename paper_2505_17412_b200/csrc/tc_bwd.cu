@@ -4,8 +4,8 @@
 //   dS = P (omega_c dP - D_c),  dP = dO V^T,  dq = scale dS K,  dk = scale dS^T q,  dv = (P omega_c)^T dO.
 //
 //  k_tc_dq    Q-outer: CTA per (query block, kv group); for every 128-row tile, S = Q K^T and dP = dO V^T
-//             over the compression keys, the selected blocks and the window (112-key tiles, S/dP double
-//             buffered in TMEM), dS -> smem, dQ += dS K accumulated in TMEM over all three branches,
+//             over the compression keys, the selected blocks and the window (96-key tiles; selected
+//             blocks packed in 8-row granules), dS -> smem, dQ += dS K accumulated in TMEM over all three branches,
 //             written once to the caller's dq (no atomics, deterministic).
 //  k_tc_dkdv  KV-outer: CTA per key tile; S^T = K Q^T and dP^T = V dO^T for 64-row tiles (keys on TMEM
 //             lanes), (P omega)^T and dS^T -> smem as K-major A operands, dV += (P omega)^T dO and

@@ -77,17 +77,32 @@ struct TcArgs {
 
 // K^cmp -> bf16 hi/lo pair, V^cmp -> fp16 (P.V runs in fp16), raw V -> fp16 copy (exact for bf16)
 __global__ void k_tc_prep(Ctx c, __nv_bfloat16* kc_hi, __nv_bfloat16* kc_lo, __half* vc16, __half* vs16) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // 4 elements per thread (every array is a multiple of 64 long and 256-B aligned)
+  const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   const int64_t n = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
   const int64_t nv = int64_t(c.h_kv) * c.N * kD;
   if (i < n) {
-    const float k = static_cast<const float*>(c.kc)[i];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(k);
-    kc_hi[i] = hi;
-    kc_lo[i] = __float2bfloat16_rn(k - __bfloat162float(hi));
-    vc16[i] = __float2half_rn(static_cast<const float*>(c.vc)[i]);
+    const float4 k = *reinterpret_cast<const float4*>(static_cast<const float*>(c.kc) + i);
+    const float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(c.vc) + i);
+    const float kk[4] = {k.x, k.y, k.z, k.w};
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      hi[u] = __float2bfloat16_rn(kk[u]);
+      lo[u] = __float2bfloat16_rn(kk[u] - __bfloat162float(hi[u]));
+    }
+    *reinterpret_cast<uint2*>(kc_hi + i) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(kc_lo + i) = *reinterpret_cast<const uint2*>(lo);
+    const __half2 v01 = __floats2half2_rn(v.x, v.y), v23 = __floats2half2_rn(v.z, v.w);
+    *reinterpret_cast<uint2*>(vc16 + i) = make_uint2(*reinterpret_cast<const uint32_t*>(&v01), *reinterpret_cast<const uint32_t*>(&v23));
   }
-  if (i < nv) vs16[i] = __float2half_rn(__bfloat162float(static_cast<const __nv_bfloat16*>(c.vs)[i]));
+  if (i < nv) {
+    const uint2 b = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(c.vs) + i);
+    const __nv_bfloat162 b01 = *reinterpret_cast<const __nv_bfloat162*>(&b.x), b23 = *reinterpret_cast<const __nv_bfloat162*>(&b.y);
+    const float2 f01 = __bfloat1622float2(b01), f23 = __bfloat1622float2(b23);
+    const __half2 h01 = __floats2half2_rn(f01.x, f01.y), h23 = __floats2half2_rn(f23.x, f23.y);
+    *reinterpret_cast<uint2*>(vs16 + i) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  }
 }
 
 // simple (index, phase) ring cursor
@@ -1003,7 +1018,7 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
   __half* vc = cw.take<__half>(size_t(c.h_kv) * n_cmp * kD);
   __half* vs16 = cw.take<__half>(size_t(c.h_kv) * c.N * kD);
   const int64_t n = int64_t(c.h_kv) * c.N * kD;   // >= h_kv * n_cmp * kD
-  k_tc_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16);
+  k_tc_prep<<<unsigned((n / 4 + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16);
   SSA_LAUNCH_CHECK("k_tc_prep");
   CUtensorMap tmQ, tmKh, tmKl, tmVc;
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
