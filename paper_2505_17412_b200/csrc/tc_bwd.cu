@@ -539,6 +539,13 @@ constexpr int kRT = 64;                  // rows per tile: S^T 64 + dP^T 64 + dK
 #define SSA_KV_RSTAGES 3
 #endif
 constexpr int kRStages = SSA_KV_RSTAGES;   // row-tile (Q, dO, stats) pipeline depth per warpgroup
+#ifndef SSA_KV_PBUF
+#define SSA_KV_PBUF 1
+#endif
+// (P w)^T / dS^T shared-memory buffers per warpgroup. Measured at C3: 2 buffers only fit
+// with 2 row stages, and 3 row stages / 1 buffer (3.18 + 6.29 ms) beat 2 / 2 (3.88 + 7.02) and 2 / 1
+// (4.15 + 7.62): the row-tile loads need the third stage more than the stores need a second buffer.
+constexpr int kPBuf = SSA_KV_PBUF;
 constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
 // One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
 // row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
@@ -550,8 +557,8 @@ constexpr int kKvThreads = 352;
 #endif
 constexpr bool kKvPingPong = SSA_KV_PINGPONG;
 struct KvSmem {
-  uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], s_empty[2], p_full[2],
-      p_empty[2], acc_full[2], acc_empty[2];
+  uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], s_empty[2], p_full[2][kPBuf],
+      p_empty[2][kPBuf], acc_full[2], acc_empty[2];
   uint32_t tmem;
   alignas(16) float st_l2[2][kRStages][kRT];
   alignas(16) float st_D[2][kRStages][kRT];
@@ -673,8 +680,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   uint8_t* sK = sm;                       // 16 KB
   uint8_t* sV = sm + 16384;               // 16 KB
   uint8_t* sR = sm + 32768;               // [warpgroup][kRStages] x {Q 8 KB, (w) dO 8 KB}
-  uint8_t* sP = sR + 2 * kRStages * 16384;  // [warpgroup] x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
-  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 2 * 32768);
+  uint8_t* sP = sR + 2 * kRStages * 16384;  // [warpgroup][kPBuf] x {(P w)^T 16 KB, dS^T 16 KB}, K-major [128 keys][64 rows]
+  KvSmem* S = reinterpret_cast<KvSmem*>(sP + 2 * kPBuf * 32768);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Item it;
@@ -711,8 +718,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[w][i], 33); mbar_init(&S->r_empty[w][i], 1); }
       mbar_init(&S->s_full[w], 1);
       mbar_init(&S->s_empty[w], 128);
-      mbar_init(&S->p_full[w], 128);
-      mbar_init(&S->p_empty[w], 1);
+      for (int b = 0; b < kPBuf; ++b) { mbar_init(&S->p_full[w][b], 128); mbar_init(&S->p_empty[w][b], 1); }
       mbar_init(&S->acc_full[w], 1);
       mbar_init(&S->acc_empty[w], 256);   // both warpgroups read both accumulator sets
     }
@@ -782,9 +788,9 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     const uint32_t idA = idesc_f16(128, 64, false, true);      // dV += (P w)^T dO, dK += dS^T Q
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     const uint32_t tS = tmem + w * 256, tDP = tS + 64, tK = tS + 128, tV = tS + 192;
-    const uint32_t ap = smem_u32(sP + w * 32768), ads = ap + 16384;
+    const uint32_t ap0 = smem_u32(sP + w * kPBuf * 32768);
     const int n_own = w == 0 ? n_own0 : n_tiles / 2;
-    Ring rs(kRStages), sb(1), pb(1);
+    Ring rs(kRStages), sb(1), pb(kPBuf);
     uint32_t kph = 0, aph = 0;
     if (lane == 0) {
       for (int kt = 0; kt < n_kt; ++kt) {
@@ -813,8 +819,9 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         tc_fence_after();
         for (int q = 0; q < n_own; ++q) {
           if (q + 1 < n_own) issue_s();
-          mbar_wait(&S->p_full[w], pb.ph);
+          mbar_wait(&S->p_full[w][pb.idx], pb.ph);
           tc_fence_after();
+          const uint32_t ap = ap0 + pb.idx * 32768, ads = ap + 16384;
           const uint32_t aq = smem_u32(sR + (w * kRStages + rs_a.idx) * 16384), ado = aq + 8192;
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
@@ -824,7 +831,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
           for (int k = 0; k < kRT / 16; ++k)
             umma_bf16(tK, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
                       (q > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&S->p_empty[w]);
+          umma_commit(&S->p_empty[w][pb.idx]);
           umma_commit(&S->r_empty[w][rs_a.idx]);
           if (w == 0) TRACE_R(1, 5, q);
           rs_a.next();
@@ -843,9 +850,9 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     const uint32_t tS = tmem + lrow + wg * 256, tDP = tS + 64;
     const float cl2 = c.scale * kLog2e;
     const int n_own = wg == 0 ? n_own0 : n_tiles / 2;
-    const uint32_t pbase = smem_u32(sP + wg * 32768);
-    Ring rs(kRStages);
-    uint32_t sph = 0, aph = 0, pph = 0;
+    const uint32_t pbase0 = smem_u32(sP + wg * kPBuf * 32768);
+    Ring rs(kRStages), pr(kPBuf);
+    uint32_t sph = 0, aph = 0;
     // MUFU ping-pong (named barriers 4 / 5); warpgroup 1 runs a turn for every warpgroup-0 tile (an
     // empty one when it has no tile) so the turn counts always match
     if (kKvPingPong && wg == 1 && n_own0 > 0) named_bar_arrive(4, 256);
@@ -897,10 +904,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
 #pragma unroll
             for (int i = 0; i < 16; ++i) pw[i] = ds[i] = 0u;
           }
-          if (half == 0) {
-            mbar_wait(&S->p_empty[wg], pph ^ 1u);   // previous tile's dV/dK MMAs are done
-            pph ^= 1u;
-          }
+          const uint32_t pbase = pbase0 + pr.idx * 32768;
+          if (half == 0) mbar_wait(&S->p_empty[wg][pr.idx], pr.ph ^ 1u);   // this buffer's dV/dK MMAs are done
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             st_shared_v4(pbase + sw128(t, half * 4 + ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
@@ -911,9 +916,10 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         if (kKvPingPong) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_R(2, 9, q);
         fence_proxy_async_smem();
-        mbar_arrive(&S->p_full[wg]);
+        mbar_arrive(&S->p_full[wg][pr.idx]);
         if (warp == 0) TRACE_R(2, 11, q);
         rs.next();
+        pr.next();
       }
       // accumulators: dK at 128, dV at 192 of each warpgroup; warpgroup 0 writes dK = dK_0 + dK_1,
       // warpgroup 1 writes dV = dV_0 + dV_1 (fixed order: deterministic)
@@ -1069,7 +1075,8 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
     k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
-  const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + 2 * 32768 + sizeof(KvSmem);
+  const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + 2 * kPBuf * 32768 + sizeof(KvSmem);
+  if (smem > 232448) { set_error("KV-outer shared memory exceeds 227 KB"); return SSA_ERR_UNSUPPORTED; }
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
     k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);
