@@ -1,0 +1,29 @@
+"""Per-token selection (m_q = 1, the paper's exact Alg. 1 granularity) runs on the SIMT kernels; time it
+at C2 next to the tensor-core query-block path (m_q = m_slc) for context."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2505_17412_b200 import ssa
+from ssa_workload import CONFIGS, config_coords, make_inputs
+
+cfg = CONFIGS["C2"]
+c, grid, batch = config_coords("C2")
+inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=1)
+t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
+cc = torch.from_numpy(c).cuda()
+for m_q in (8, 1):
+    plan = ssa.ssa_build_blocks(cc, grid, batch, 4, 8, 8, m_q)
+    acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16)
+    for i in range(4):
+        if i == 1:
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
+        ssa.ssa_backward(plan, acfg, saved, *t)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"C2 m_q={m_q}: {e0.elapsed_time(e1) / 3:.2f} ms fwd+bwd ({'tcgen05' if saved.used_tcgen05 else 'SIMT'})", flush=True)
