@@ -6,7 +6,10 @@ import torch
 from paper_2505_17412_b200 import ssa
 from ssa_workload import make_inputs, sphere_shell, batch_coords
 c = batch_coords([sphere_shell(24, 9.0, 2.0), sphere_shell(24, 6.0, 2.0)])
-for dt, flags in ((torch.bfloat16, 0), (torch.bfloat16, ssa.SSA_FORCE_SIMT), (torch.float32, 0)):
+CASES = ((torch.bfloat16, 0), (torch.bfloat16, ssa.SSA_WINDOW_ONLY), (torch.bfloat16, ssa.SSA_FORCE_SIMT),
+         (torch.float32, 0))
+only = [int(a) for a in sys.argv[1:]] or range(len(CASES))
+for dt, flags in (CASES[i] for i in only):
     inp = make_inputs(c, (24, 24, 24), 2, 8, 2, 64, "bf16" if dt == torch.bfloat16 else "f32", seed=3)
     plan = ssa.ssa_build_blocks(torch.from_numpy(c).cuda(), (24, 24, 24), 2, 4, 8, 8, 8)
     cfg = ssa.AttnCfg(h_q=8, h_kv=2, d=64, top_k=4, dtype=dt, flags=flags)
@@ -14,4 +17,5 @@ for dt, flags in ((torch.bfloat16, 0), (torch.bfloat16, ssa.SSA_FORCE_SIMT), (to
     out, saved = ssa.ssa_forward(plan, cfg, *t[:4])
     g = ssa.ssa_backward(plan, cfg, saved, *t)
     torch.cuda.synchronize()
-    print(dt, flags, "tc" if saved.used_tcgen05 else "simt", float(out.float().abs().sum()), float(g[0].float().abs().sum()))
+    print(dt, flags, "tc" if saved.used_tcgen05 else "simt", float(out.float().abs().sum()), float(g[0].float().abs().sum()),
+          flush=True)
