@@ -558,7 +558,7 @@ constexpr int kKvThreads = 352;
 constexpr bool kKvPingPong = SSA_KV_PINGPONG;
 struct KvSmem {
   uint64_t k_full, k_empty, r_full[2][kRStages], r_empty[2][kRStages], s_full[2], s_empty[2], p_full[2][kPBuf],
-      p_empty[2][kPBuf], acc_full[2], acc_empty[2];
+      p_empty[2][kPBuf], pv_empty[2][kPBuf], acc_full[2], acc_empty[2];
   uint32_t tmem;
   alignas(16) float st_l2[2][kRStages][kRT];
   alignas(16) float st_D[2][kRStages][kRT];
@@ -718,7 +718,11 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
       for (int i = 0; i < kRStages; ++i) { mbar_init(&S->r_full[w][i], 33); mbar_init(&S->r_empty[w][i], 1); }
       mbar_init(&S->s_full[w], 1);
       mbar_init(&S->s_empty[w], 128);
-      for (int b = 0; b < kPBuf; ++b) { mbar_init(&S->p_full[w][b], 128); mbar_init(&S->p_empty[w][b], 1); }
+      for (int b = 0; b < kPBuf; ++b) {
+        mbar_init(&S->p_full[w][b], 128);
+        mbar_init(&S->p_empty[w][b], 1);    // dK MMAs done: dS^T may be rewritten
+        mbar_init(&S->pv_empty[w][b], 1);   // dV MMAs done: (P w)^T may be rewritten
+      }
       mbar_init(&S->acc_full[w], 1);
       mbar_init(&S->acc_empty[w], 256);   // both warpgroups read both accumulator sets
     }
@@ -827,6 +831,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
           for (int k = 0; k < kRT / 16; ++k)
             umma_bf16(tV, desc_sw128(ap + k * 32, 0, 1024), desc_sw128(ado + k * 2048, 0, 1024), idA,
                       (q > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&S->pv_empty[w][pb.idx]);
 #pragma unroll
           for (int k = 0; k < kRT / 16; ++k)
             umma_bf16(tK, desc_sw128(ads + k * 32, 0, 1024), desc_sw128(aq + k * 2048, 0, 1024), idA,
@@ -905,13 +910,16 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
             for (int i = 0; i < 16; ++i) pw[i] = ds[i] = 0u;
           }
           const uint32_t pbase = pbase0 + pr.idx * 32768;
-          if (half == 0) mbar_wait(&S->p_empty[wg][pr.idx], pr.ph ^ 1u);   // this buffer's dV/dK MMAs are done
+          // (P w)^T may be rewritten once the previous tile's dV MMAs are done, dS^T once its dK MMAs are
+          if (half == 0) mbar_wait(&S->pv_empty[wg][pr.idx], pr.ph ^ 1u);
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
+          for (int ch = 0; ch < 4; ++ch)
             st_shared_v4(pbase + sw128(t, half * 4 + ch), pw[4 * ch], pw[4 * ch + 1], pw[4 * ch + 2], pw[4 * ch + 3]);
+          if (half == 0) mbar_wait(&S->p_empty[wg][pr.idx], pr.ph ^ 1u);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
             st_shared_v4(pbase + 16384 + sw128(t, half * 4 + ch), ds[4 * ch], ds[4 * ch + 1], ds[4 * ch + 2],
                          ds[4 * ch + 3]);
-          }
         }
         if (kKvPingPong) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_R(2, 9, q);
