@@ -302,6 +302,20 @@ def main():
                          "algorithmic_flops_per_launch": flops, "exp2_per_launch": exps,
                          "avg_launch_ms": round(t / n, 4), "share_of_step": round(t / n / ms_per_step, 4)})
     kernel_ms = {kn: round(t / n, 4) for kn, (t, n) in ktimes.items()}
+    # every tensor-core kernel against both of its units (same algorithmic work model as the roofline);
+    # "selected-block attention" (north star: >= 50% of dense bf16 peak) = tc_slc_win_fwd forward and
+    # tc_bwd_kv backward (selection + window keys)
+    kernel_roofline = {}
+    if cands:
+        mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        tc_peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+        xu_peak = 148 * 16 * mhz * 1e6 / 1e12
+        for kn in cands:
+            t, n = ktimes[kn]
+            avg_s = t / n / 1e3
+            flops, exps = models[kn]
+            kernel_roofline[kn] = {"tflops": round(flops / avg_s / 1e12, 1), "tensor_frac": round(flops / avg_s / 1e12 / tc_peak, 4),
+                                   "tex2_per_s": round(exps / avg_s / 1e12, 3), "mufu_frac": round(exps / avg_s / 1e12 / xu_peak, 4)}
 
     # ---- e2e through the public API with host buffers ----
     # Every step copies its inputs (coords, q, k, v, gates, dO) from pinned host memory and reads its
@@ -399,6 +413,7 @@ def main():
                                        if sharded else f"shape-parallel x{world} (no data-path collective)"),
                        "l2": "flushed between timed steps (256 MB write)", "path": "tcgen05" if used_tc else "simt"},
             "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline, "kernel_ms": kernel_ms,
+            "kernel_roofline": kernel_roofline,
             "work": {"E_cmp": E_cmp, "E_slc": E_slc, "E_win": E_win},
             "e2e": e2e, "cpu_baseline": cpu,
         }
