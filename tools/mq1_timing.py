@@ -27,3 +27,15 @@ for m_q in (8, 1):
     e1.record()
     torch.cuda.synchronize()
     print(f"C2 m_q={m_q}: {e0.elapsed_time(e1) / 3:.2f} ms fwd+bwd ({'tcgen05' if saved.used_tcgen05 else 'SIMT'})", flush=True)
+
+# per-kernel split of the per-token (SIMT) step
+ssa.profile_reset()
+ssa.profile_enable(True)
+out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
+ssa.ssa_backward(plan, acfg, saved, *t)
+torch.cuda.synchronize()
+ssa.profile_enable(False)
+for kn in ("k_cmp_fwd", "k_attn_fwd(slc)", "k_attn_fwd(win)", "k_dq", "k_slc_dkdv", "k_win_bwd", "k_cmp_dkdv"):
+    ms, n = ssa.profile_read(kn)
+    if n:
+        print(f"  {kn}: {ms:.2f} ms")
