@@ -31,6 +31,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define SSA_SW_STAGES 3
 #endif
 constexpr int kStages = SSA_SW_STAGES;   // K/V stages of the selection+window kernel
+#ifndef SSA_SW_PINGPONG
+#define SSA_SW_PINGPONG 1
+#endif
+constexpr bool kSwPingPong = SSA_SW_PINGPONG;   // MUFU turns alternate between the two softmax warpgroups
 
 #ifdef SSA_TRACE
 // per-role shared-memory trace of one CTA (debug builds: -DSSA_TRACE); flushed at kernel end
@@ -132,6 +136,10 @@ struct Ring {
 constexpr int kCmpThreads = 352;
 constexpr int kCmpStages = 2;
 constexpr float kRescale = 8.f;
+#ifndef SSA_CMP_P2_PINGPONG
+#define SSA_CMP_P2_PINGPONG 0   // 1: pass 2 (Eq. 8 column sums) also alternates MUFU turns (measured slower: 7.16 vs 6.96 ms)
+#endif
+constexpr bool kCmpP2PingPong = SSA_CMP_P2_PINGPONG;
 struct CmpSmem {
   uint64_t q_full, q_empty, k_full[kCmpStages], k_empty[kCmpStages], v_full[kCmpStages], v_empty[kCmpStages];
   uint64_t s_full[2], s_empty[2], p_full[2], p_free[2], o_full[2], o_empty[2];
@@ -453,7 +461,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         if (warp == 0) TRACE_R(2, 8, kt);
         tc_fence_after();
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
-        turn_begin();
+        if (kCmpP2PingPong) turn_begin();
 #pragma unroll
         for (int c00 = 0; c00 < kTile; c00 += 32) {
           float v[32];
@@ -472,7 +480,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             cs[3] += ex2(fmaf(v[i + 3], cl2, -L.w));
           }
         }
-        turn_end();
+        if (kCmpP2PingPong) turn_end();
         sb.next();
         if (kvalid) sc_cmp[kt * kTile + t] += (cs[0] + cs[1]) + (cs[2] + cs[3]);
       }
@@ -791,7 +799,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     const float cl2 = c.scale * kLog2e;
     Ring sb(1);
     uint32_t fph = 1u, oph = 0;
-    if (wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);   // warpgroup 0 takes the first turn
+    if (kSwPingPong && wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);   // warpgroup 0 takes the first turn
     for (int pr = 0; pr < n_pair; ++pr) {
       const int rt = 2 * pr + wg;
       if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
@@ -875,7 +883,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (warp == 0) TRACE_SW(2, 8, j);
-        if (duo) named_bar_sync(4 + wg, 256);
+        if (kSwPingPong && duo) named_bar_sync(4 + wg, 256);
         if (warp == 0) TRACE_SW(2, 9, j);
 #pragma unroll
         for (int cc = 0; cc < kTile; cc += 32) {
@@ -888,7 +896,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           }
           tmem_st16(tP + cc / 2, pk);
         }
-        if (duo) named_bar_arrive(5 - wg, 256);
+        if (kSwPingPong && duo) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_SW(2, 10, j);
         l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         // the reference max moved inside a branch: rescale O (P.V(j-1) has completed: p_free)
