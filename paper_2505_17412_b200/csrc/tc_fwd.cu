@@ -140,6 +140,10 @@ constexpr float kRescale = 8.f;
 #define SSA_CMP_P2_PINGPONG 0   // 1: pass 2 (Eq. 8 column sums) also alternates MUFU turns (measured slower: 7.16 vs 6.96 ms)
 #endif
 constexpr bool kCmpP2PingPong = SSA_CMP_P2_PINGPONG;
+#ifndef SSA_CMP_P1_PINGPONG
+#define SSA_CMP_P1_PINGPONG 1
+#endif
+constexpr bool kCmpP1PingPong = SSA_CMP_P1_PINGPONG;   // pass 1 (online softmax, P -> TMEM, P.V) alternates MUFU turns
 struct CmpSmem {
   uint64_t q_full, q_empty, k_full[kCmpStages], k_empty[kCmpStages], v_full[kCmpStages], v_empty[kCmpStages];
   uint64_t s_full[2], s_empty[2], p_full[2], p_free[2], o_full[2], o_empty[2];
@@ -356,7 +360,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     // MUFU ping-pong: the two warpgroups take turns in their exponential loops (named barriers 4 / 5),
     // so each loop runs at the full MUFU rate while the other warpgroup loads S, waits or stores.
     // Warpgroup 1 hands warpgroup 0 the first turn.
-    if (wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);
+    if (kCmpP1PingPong && wg == 1 && n_rt >= 2) named_bar_arrive(4, 256);
     for (int pr = 0; pr < n_pair; ++pr) {
       const int rt = 2 * pr + wg;
       if (rt >= n_rt) break;                          // warpgroup 1 sits out the last, odd pair
@@ -397,7 +401,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         l *= alpha;
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        turn_begin();
+        if (kCmpP1PingPong) turn_begin();
 #pragma unroll
         for (int cc = 0; cc < 128; cc += 32) {
           uint32_t pk[16];
@@ -409,7 +413,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           }
           tmem_st16(p_base + cc / 2, pk);
         }
-        turn_end();
+        if (kCmpP1PingPong) turn_end();
         l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         // the reference max moved: rescale O_w (P.V(kt-1) has completed: p_free)
         if (kt > 0 && __any_sync(0xffffffffu, bump)) {
