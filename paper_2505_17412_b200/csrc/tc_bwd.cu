@@ -546,7 +546,10 @@ constexpr int kRStages = SSA_KV_RSTAGES;   // row-tile (Q, dO, stats) pipeline d
 // with 2 row stages, and 3 row stages / 1 buffer (3.18 + 6.29 ms) beat 2 / 2 (3.88 + 7.02) and 2 / 1
 // (4.15 + 7.62): the row-tile loads need the third stage more than the stores need a second buffer.
 constexpr int kPBuf = SSA_KV_PBUF;
-constexpr int kQBlocksPerItem = 8;       // raw keys: query blocks per work item (splits popular blocks)
+#ifndef SSA_KV_QB_PER_ITEM
+#define SSA_KV_QB_PER_ITEM 8
+#endif
+constexpr int kQBlocksPerItem = SSA_KV_QB_PER_ITEM;       // raw keys: query blocks per work item (splits popular blocks)
 // One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
 // row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
 // dV 64), its own row-stage ring and its own MMA issuer (warps 9 / 10); warp 8 is the producer. The
