@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--no-full", action="store_true", help="skip the full-attention comparator")
     ap.add_argument("--no-window", action="store_true", help="skip the window-only (SSA_WINDOW_ONLY) context timing")
     ap.add_argument("--force-simt", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=24, help="query blocks in the oracle sample")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: validate the N>1 logic with several ranks on one GPU)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="query blocks in the oracle sample (0: 4 per core)")
+    ap.add_argument("--cpu-check-c2", type=int, default=1, help="also run the oracle on all of C2 (extrapolation check)")
     return ap.parse_args()
 
 
@@ -118,22 +121,70 @@ class ClockSampler:
 
 
 def workload(config: str, rank: int, world: int):
-    """Shapes of this rank. C3/C5: one 1024^3-res shell per rank (weak scaling). C4: the 8-shape batch,
-    shapes dealt LPT-style across ranks by token count."""
+    """Shapes of this rank. C3: one 1024^3-res shell per rank (weak scaling); C5: the same shell on every
+    rank, its query blocks sharded (strong scaling); C4: the whole 8-shape batch (N > 1: placed by
+    shard.hybrid_plan, see hybrid_step)."""
     from ssa_workload import CONFIGS, batch_coords, sphere_shell
     cfg = CONFIGS[config]
-    shapes = list(cfg["shapes"])
-    if config == "C4" and world > 1:
-        from paper_2505_17412_b200.shard import rank_items
-        n_tok = [sphere_shell(*s).shape[0] for s in shapes]
-        shapes = [shapes[i] for i in rank_items(n_tok, rank, world)]
-    shells = [sphere_shell(*s) for s in shapes]
+    shells = [sphere_shell(*s) for s in cfg["shapes"]]
     return cfg, batch_coords(shells), (cfg["G"],) * 3, len(shells)
 
 
-def flops_model(plan, cfg):
-    """Algorithmic element counts: E_cmp, E_slc (from the indices), E_win."""
-    return None
+def hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world):
+    """C4 on N > 1 ranks (SURVEY §8e hybrid): the batch's query blocks on one cost line cut into N equal
+    pieces (shard.hybrid_plan). Shapes a rank holds entirely run whole as one batch plan (mode 1, no
+    collective); shapes cut by a piece boundary run ssa_step_sharded over their sub-group (mode 2).
+    Every rank holds the batch's inputs (identical seeds per shape); a step includes every block build
+    and the gather of the rank's own rows. Returns step()."""
+    import numpy as np
+    from paper_2505_17412_b200.shard import hybrid_plan, ssa_step_sharded
+    from ssa_workload import batch_coords, make_inputs, sphere_shell
+    G = (cfg["G"],) * 3
+    ms = (cfg["m_cmp"], cfg["m_slc"], cfg["m_win"], cfg["m_q"])
+    tdt = acfg.dtype
+    shells = [sphere_shell(*sh) for sh in cfg["shapes"]]
+    coords = [batch_coords([sh]) for sh in shells]
+    tens = []
+    for s, c in enumerate(coords):
+        inp = make_inputs(c, G, 1, cfg["H"], cfg["h_kv"], cfg["d"], cfg["dtype"], seed=cfg["seed"] + s)
+        tens.append([torch.from_numpy(x).to(dev, dtype=tdt) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)])
+    cdev = [torch.from_numpy(c).to(dev) for c in coords]
+    qt = [np.diff(ssa.ssa_build_blocks(cd, G, 1, *ms).q_offsets_host()) for cd in cdev]
+    allp = hybrid_plan(qt, world)
+    groups, ranges = {}, {}
+    for s in range(len(shells)):                   # every rank creates every sub-group, in shape order
+        grp = next(g for items in allp for (ss, a, b, g) in items if ss == s)
+        if len(grp) > 1:
+            groups[s] = dist.new_group(list(grp))
+            ranges[s] = [next((a, b) for (ss, a, b, _) in allp[r] if ss == s) for r in grp]
+    mine = allp[rank]
+    whole = [s for (s, a, b, g) in mine if len(g) == 1]
+    split = [(s, g) for (s, a, b, g) in mine if len(g) > 1]
+    wb = None
+    if whole:
+        wc = batch_coords([shells[s] for s in whole])
+        wb = (torch.from_numpy(wc).to(dev), len(whole),
+              [torch.cat([tens[s][i] for s in whole]) for i in range(5)])
+    comm = torch.cuda.Stream(dev)
+    info = {"whole_shapes": whole, "split_shapes": [(s, list(g)) for s, g in split],
+            "plan": [[(s, a, b, len(g)) for (s, a, b, g) in items] for items in allp]}
+
+    def step():
+        if wb is not None:
+            cd, nb, (q, k, v, g, do) = wb
+            plan = ssa.ssa_build_blocks(cd, G, nb, *ms)
+            _, saved = ssa.ssa_forward(plan, acfg, q, k, v, g)
+            ssa.ssa_backward(plan, acfg, saved, q, k, v, g, do)
+        for s, grp in split:
+            plan = ssa.ssa_build_blocks(cdev[s], G, 1, *ms)
+            qo = plan.q_offsets_host()
+            a, b = ranges[s][grp.index(rank)]
+            rows = plan.perm()[int(qo[a]):int(qo[b])].long()
+            loc = [x[rows] for x in tens[s]]
+            ssa_step_sharded(plan, acfg, *loc, rank=grp.index(rank), world=len(grp), group=groups[s],
+                             comm_stream=comm, q_ranges=ranges[s])
+        return None, None
+    return step, info
 
 
 def main():
@@ -143,10 +194,14 @@ def main():
         return reference_arm(args, rank, world)
     import torch
     import torch.distributed as dist
+    local = local % max(1, torch.cuda.device_count())    # gloo validation runs: several ranks per GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     from paper_2505_17412_b200 import ssa
     from ssa_workload import make_inputs
 
@@ -167,27 +222,28 @@ def main():
     st = torch.cuda.current_stream(dev)
 
     sharded = args.config == "C5"
+    hybrid = args.config == "C4" and world > 1
+    hybrid_info = None
+    comm = torch.cuda.Stream(dev)
+    if hybrid:
+        hstep, hybrid_info = hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world)
 
     def step(qq=q, kk=k, vv=v, gg=g, dd=do, o_=out, gr_=grads, cc=c_d, after_build=None):
+        if hybrid:
+            return hstep()
         plan = ssa.ssa_build_blocks(cc, grid, batch, *ms)
         if after_build is not None:
             after_build()
         if sharded:
-            # one shape, query blocks sharded over the ranks (SURVEY §8e mode 2): K/V all-gather,
-            # dK/dV partial all-reduce; inputs in plan order, every rank builds the same plan
-            from paper_2505_17412_b200.shard import balanced_q_ranges, ssa_step_sharded
-            qo = plan.offsets(ssa.LEVEL_Q).cpu().numpy()
-            rngs = balanced_q_ranges(qo, world)
-            tok = [(int(qo[a]), int(qo[b])) for a, b in rngs]
-            p = plan.perm()
-            qs_, ks_, vs_, gs_, ds_ = (x[p] for x in (qq, kk, vv, gg, dd))
-            pad = max(b - a for a, b in tok)
+            # one shape, query blocks sharded over the ranks (SURVEY §8e mode 2): every rank builds the
+            # same plan and gathers its own rows (plan order); pooled-key all-reduce, K/V all-gather
+            # overlapped with the compression branch, dK/dV reduce-scatter (shard.ssa_step_sharded)
+            from paper_2505_17412_b200.shard import shard_ranges, ssa_step_sharded
+            _, tok = shard_ranges(plan, world)
             a, b = tok[rank]
-            kl = torch.zeros((pad,) + tuple(ks_.shape[1:]), dtype=ks_.dtype, device=dev)
-            vl = torch.zeros_like(kl)
-            kl[:b - a] = ks_[a:b]
-            vl[:b - a] = vs_[a:b]
-            ssa_step_sharded(plan, acfg, qs_, kl, vl, gs_, ds_, tok, rank)
+            rows = plan.perm()[a:b].long()
+            loc = [x[rows] for x in (qq, kk, vv, gg, dd)]
+            ssa_step_sharded(plan, acfg, *loc, rank=rank, world=world, comm_stream=comm)
             return plan, None
         o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=o_)
         ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=gr_)
@@ -196,7 +252,8 @@ def main():
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 3):
         plan, saved = step()
     torch.cuda.synchronize(dev)
-    if saved is None:     # sharded mode: run once unsharded for the work accounting below
+    if saved is None:     # sharded / hybrid: one unsharded forward of the batch for the work accounting below
+        plan = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
         saved = ssa.ssa_forward(plan, acfg, q, k, v, g, out=out)[1]
         torch.cuda.synchronize(dev)
     used_tc = saved.used_tcgen05
@@ -235,7 +292,7 @@ def main():
     from paper_2505_17412_b200.shard import max_over_ranks
     total_ms = max_over_ranks(total_ms, dev)
     ms_per_step = total_ms / args.steps
-    shapes_per_step = batch * (1 if sharded else world)
+    shapes_per_step = batch * (1 if (sharded or hybrid) else world)
     value = ms_per_step / shapes_per_step
 
     # ---- algorithmic work of the dominant kernel ----
@@ -253,17 +310,20 @@ def main():
     qn = np.diff(off_q)
     E_slc = float(sum(qn[Q] * h_s * fill[I[Q, gi][I[Q, gi] >= 0]].sum() for Q in range(len(qn)) for gi in range(h_kv)))
     E_win = float(np.sum(np.diff(off_w).astype(np.float64) ** 2)) * H
-    # Per-kernel ALGORITHMIC work: tensor flops (2 per MAC) and exponentials
-    # (one per score; the compression forward's second pass and bf16 hi/lo split are implementation
-    # overhead, not counted). The roofline reports the dominant kernel (largest share of the step)
-    # against the resource it uses most (tensor pipe or MUFU).
+    # Per-kernel ALGORITHMIC work, SURVEY §8(d) / DESIGN.md §5 (2 flops per MAC, E = score elements):
+    #   forward: 4d per element (QK^T, PV) + 2d for the a4 score pass (Eq. 8 needs S a second time
+    #            after the LSE is known), exponentials: 1 per element, 2 for a4 (LSE pass + Eq. 8 pass);
+    #   backward: 10d per element (FA convention: S, dP, dQ, dK, dV once). Our backward computes S and dP
+    #            in both the Q-outer (dQ) and the KV-outer (dK, dV) kernel, so the algorithmic 10d is
+    #            split 6d (S, dP, dQ) to tc_bwd_dq and 4d (dK, dV) to the KV-outer kernels; the 4d they
+    #            recompute is reported separately as "executed" work, not credited to the roofline.
     E_sw = E_slc + E_win
-    models = {
-        "tc_cmp_fwd": (2 * 2 * d * E_cmp, E_cmp),                            # QK^T, PV; one exp per score
-        "tc_slc_win_fwd": (2 * 2 * d * E_sw, E_sw),
-        "tc_bwd_dq": (3 * 2 * d * (E_cmp + E_sw), E_cmp + E_sw),             # S, dP, dQ
-        "tc_bwd_kv": (4 * 2 * d * E_sw, E_sw),                               # S^T, dP^T, dV, dK
-        "tc_bwd_cmp_kv": (4 * 2 * d * E_cmp, E_cmp),
+    models = {   # kernel: (algorithmic flops, algorithmic exps, executed flops)
+        "tc_cmp_fwd": (6 * d * E_cmp, 2 * E_cmp, 8 * d * E_cmp),      # executed: S twice in hi + lo (K^cmp split)
+        "tc_slc_win_fwd": (4 * d * E_sw, E_sw, 4 * d * E_sw),
+        "tc_bwd_dq": (6 * d * (E_cmp + E_sw), E_cmp + E_sw, 6 * d * (E_cmp + E_sw)),
+        "tc_bwd_kv": (4 * d * E_sw, 0.0, 8 * d * E_sw),
+        "tc_bwd_cmp_kv": (4 * d * E_cmp, 0.0, 8 * d * E_cmp),
     }
     peaks, peak_src = load_peaks()
     roofline = None
@@ -272,7 +332,7 @@ def main():
         dom = max(cands, key=lambda k: ktimes[k][0] / ktimes[k][1])
         t, n = ktimes[dom]
         avg_s = t / n / 1e3
-        flops, exps = models[dom]
+        flops, exps, _ = models[dom]
         mhz = float(peaks.get("sm_max_mhz", 1965.0))
         tc_peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))          # TFLOP/s (fp16 = bf16 rate)
         xu_peak = 148 * 16 * mhz * 1e6 / 1e12                                              # T ex2/s: 16 MUFU.EX2/clk/SM
@@ -289,8 +349,10 @@ def main():
         if xu_ach / xu_peak >= tc_ach / tc_peak:
             roofline = {"kernel": dom, "bound": "alu", "achieved": round(xu_ach, 4), "peak": round(xu_peak, 4),
                         "unit": "Tex2/s", "frac": round(xu_ach / xu_peak, 4),
-                        "peak_source": "MUFU.EX2 16/clk/SM (guide unit count; 15.8 measured, tools/xu_microbench.cu)"
-                                       " x 148 SMs x sm_max_mhz (" + peak_src + ")"}
+                        "peak_source": "MUFU.EX2 16/clk/SM (guide unit count) x 148 SMs x sm_max_mhz (" + peak_src + "); "
+                                       "measured on this B200: 15.8/clk/SM at full occupancy (tools/xu_microbench.cu, "
+                                       "DESIGN.md §5)",
+                        "frac_vs_measured_mufu": round(xu_ach / (xu_peak * 15.8 / 16), 4)}
         else:
             roofline = {"kernel": dom, "bound": "tensor", "achieved": round(tc_ach, 2), "peak": round(tc_peak, 1),
                         "unit": "TFLOP/s", "frac": round(tc_ach / tc_peak, 4),
@@ -301,6 +363,8 @@ def main():
                                        "frac": round(xu_ach / xu_peak, 4)},
                          "algorithmic_flops_per_launch": flops, "exp2_per_launch": exps,
                          "avg_launch_ms": round(t / n, 4), "share_of_step": round(t / n / ms_per_step, 4)})
+    if hybrid:      # a rank's kernels cover only its share of the batch: no per-kernel roofline at N > 1
+        roofline, cands = None, []
     kernel_ms = {kn: round(t / n, 4) for kn, (t, n) in ktimes.items()}
     # every tensor-core kernel against both of its units (same algorithmic work model as the roofline);
     # "selected-block attention" (north star: >= 50% of dense bf16 peak) = tc_slc_win_fwd forward and
@@ -313,9 +377,21 @@ def main():
         for kn in cands:
             t, n = ktimes[kn]
             avg_s = t / n / 1e3
-            flops, exps = models[kn]
+            flops, exps, xflops = models[kn]
             kernel_roofline[kn] = {"tflops": round(flops / avg_s / 1e12, 1), "tensor_frac": round(flops / avg_s / 1e12 / tc_peak, 4),
-                                   "tex2_per_s": round(exps / avg_s / 1e12, 3), "mufu_frac": round(exps / avg_s / 1e12 / xu_peak, 4)}
+                                   "tex2_per_s": round(exps / avg_s / 1e12, 3), "mufu_frac": round(exps / avg_s / 1e12 / xu_peak, 4),
+                                   "executed_tflops": round(xflops / avg_s / 1e12, 1)}
+        # step level: forward 4d ΣE + 2d E_cmp, backward 10d ΣE
+        fw = [kn for kn in ("tc_cmp_fwd", "tc_slc_win_fwd") if kn in ktimes]
+        bw = [kn for kn in ("tc_bwd_dq", "tc_bwd_kv", "tc_bwd_cmp_kv") if kn in ktimes]
+        if fw and bw:
+            t_f = sum(ktimes[kn][0] / ktimes[kn][1] for kn in fw) / 1e3
+            t_b = sum(ktimes[kn][0] / ktimes[kn][1] for kn in bw) / 1e3
+            E_all = E_cmp + E_sw
+            kernel_roofline["forward_kernels"] = {"tflops": round((4 * d * E_all + 2 * d * E_cmp) / t_f / 1e12, 1),
+                                                  "tensor_frac": round((4 * d * E_all + 2 * d * E_cmp) / t_f / 1e12 / tc_peak, 4)}
+            kernel_roofline["backward_kernels"] = {"tflops": round(10 * d * E_all / t_b / 1e12, 1),
+                                                   "tensor_frac": round(10 * d * E_all / t_b / 1e12 / tc_peak, 4)}
 
     # ---- e2e through the public API with host buffers ----
     # Every step copies its inputs (coords, q, k, v, gates, dO) from pinned host memory and reads its
@@ -323,7 +399,7 @@ def main():
     # double-buffered, so step i's compute overlaps step i+1's H2D and step i-1's D2H (PCIe is full
     # duplex); the clock runs from the first H2D to the last D2H.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not hybrid and not sharded:
         hin = [x.cpu().pin_memory() for x in (c_d, q, k, v, g, do)]
         bi = sum(x.numel() * x.element_size() for x in hin)
         dev_in = [[torch.empty_like(x) for x in (c_d, q, k, v, g, do)] for _ in range(2)]
@@ -374,7 +450,25 @@ def main():
     # ---- full-attention comparator on the same box (context: "speedup vs full attention") ----
     full = None
     if not args.no_full and rank == 0:
-        full = full_attention_time(torch, dev, int(np.max(ntok_b)), H, h_kv, d, tdt)
+        # every shape of the batch timed at its own token count (cost grows with n^2), summed
+        for n_b in sorted(set(int(x) for x in ntok_b)):
+            r_b = full_attention_time(torch, dev, n_b, H, h_kv, d, tdt)
+            mult = int(np.sum(ntok_b == n_b))
+            if full is None:
+                full = dict(r_b, tokens=[n_b] * mult, flops=r_b["flops"] * mult)
+                full["others"] = {kk: vv * mult if kk.endswith("_ms") else vv for kk, vv in r_b["others"].items()}
+                if "fwd_bwd_ms" in r_b:
+                    full["fwd_bwd_ms"] = r_b["fwd_bwd_ms"] * mult
+                continue
+            full["tokens"] += [n_b] * mult
+            full["flops"] += r_b["flops"] * mult
+            if "fwd_bwd_ms" in r_b and "fwd_bwd_ms" in full:
+                full["fwd_bwd_ms"] = round(full["fwd_bwd_ms"] + r_b["fwd_bwd_ms"] * mult, 3)
+            for kk, vv in r_b["others"].items():
+                if kk.endswith("_ms") and kk in full["others"]:
+                    full["others"][kk] = round(full["others"][kk] + vv * mult, 3)
+        if full is not None and batch > 1:
+            full["note"] = "each shape timed at its own token count; times summed over the batch"
 
     # ---- context: sparse 3D window attention alone (SSA_WINDOW_ONLY; the SS-VAE layer) on the same tokens ----
     win = None
@@ -403,14 +497,18 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
-            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "scaling": "strong" if (sharded or hybrid) else "weak", "vs_baseline": None,
             "dtype": "bf16" if tdt == torch.bfloat16 else "f32",
             "data": "synthetic (sphere-shell occupancy, N(0,1) q/k/v/dO, sigmoid(N(0,1)) gates; ssa_workload)",
             "config": {"workload": f"{args.config}: 128^3 latent (1024^3 res) sphere shell, {N} tokens x {batch} shape(s)/rank, "
                                    f"H={H} (h_kv={h_kv}), d={d}, m_cmp/m_slc/m_win/m_q={ms}, T={T}",
                        "tokens_per_shape": int(np.max(ntok_b)), "shapes_per_rank": batch,
-                       "parallelism": (f"query-block shards x{world} (NCCL K/V all-gather + dK/dV all-reduce)"
-                                       if sharded else f"shape-parallel x{world} (no data-path collective)"),
+                       "parallelism": (f"query-block shards x{world} ({args.backend}: pooled-key all-reduce, K/V "
+                                       "all-gather overlapped with the compression branch, dK/dV reduce-scatter)"
+                                       if sharded else
+                                       (f"hybrid x{world}: batch cost line cut into {world} pieces; whole shapes "
+                                        "per rank, cut shapes query-block sharded over sub-groups" if hybrid else
+                                        f"shape-parallel x{world} (no data-path collective)")),
                        "l2": "flushed between timed steps (256 MB write)", "path": "tcgen05" if used_tc else "simt"},
             "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline, "kernel_ms": kernel_ms,
             "kernel_roofline": kernel_roofline,
@@ -419,13 +517,15 @@ def main():
         }
         if win:
             line["window_attention"] = win
+        if hybrid_info:
+            line["config"]["hybrid_plan"] = hybrid_info["plan"]
         if full:
             line["full_attention"] = full
             if "fwd_bwd_ms" in full:
-                line["speedup_vs_full_attention"] = round(full["fwd_bwd_ms"] / ms_per_step * batch, 2)
+                line["speedup_vs_full_attention"] = round(full["fwd_bwd_ms"] / ms_per_step, 2)
             for key, val in full.get("others", {}).items():
                 if key.endswith("_ms"):
-                    line.setdefault("speedup_vs", {})[key[:-3]] = round(val / ms_per_step * batch, 2)
+                    line.setdefault("speedup_vs", {})[key[:-3]] = round(val / ms_per_step, 2)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
@@ -483,67 +583,108 @@ def full_attention_time(torch, dev, n, H, h_kv, d, dt):
     return res
 
 
+_OS = {}   # oracle state shared with forked sample workers (copy-on-write)
+
+
+def _oracle_one_q(Q):
+    """The oracle's per-query-block work, as oracle.ssa_forward / ssa_backward do it for one Q: compression
+    attention, Eq. 8 scores, top-k, selection + window attention, gated sum, and the three branch
+    backwards, for every kv group."""
+    import oracle as O
+    st = _OS
+    plan, cfg = st["plan"], st["cfg"]
+    qs, ks, vs, gs, dos, k_cmp, v_cmp = (st[x] for x in ("qs", "ks", "vs", "gs", "dos", "k_cmp", "v_cmp"))
+    H, h_kv, d = cfg["H"], cfg["h_kv"], cfg["d"]
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    Cq, Cs, Cw = plan.offsets["q"], plan.offsets["slc"], plan.offsets["win"]
+    a, b_ = int(Cq[Q]), int(Cq[Q + 1])
+    bi = int(plan.sorted_coords[a, 0])
+    c0, c1 = int(plan.batch_blocks["cmp"][bi]), int(plan.batch_blocks["cmp"][bi + 1])
+    s0 = int(plan.batch_blocks["slc"][bi])
+    w = int(plan.tok_block["win"][a])
+    for g in range(h_kv):
+        rows = qs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
+        drow = dos[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
+        wt = gs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, 3)
+        oc, _, pc = O.dense_attention(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], scale)
+        per = pc.sum(axis=0)
+        sc = np.zeros(int(plan.batch_blocks["slc"][bi + 1]) - s0)
+        np.add.at(sc, plan.cmp_to_slc[c0:c1] - s0, per)
+        sel = O.topk_select(sc, cfg["T"], base=s0)
+        kt = np.concatenate([np.arange(Cs[x], Cs[x + 1]) for x in sel if x >= 0])
+        os_, _, ps = O.dense_attention(rows, ks[kt, g], vs[kt, g], scale)
+        wa, wb = int(Cw[w]), int(Cw[w + 1])
+        ow, _, pw = O.dense_attention(rows, ks[wa:wb, g], vs[wa:wb, g], scale)
+        _ = wt[:, 0:1] * oc + wt[:, 1:2] * os_ + wt[:, 2:3] * ow
+        O.dense_attention_backward(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], pc, oc, wt[:, 0:1] * drow, scale)
+        O.dense_attention_backward(rows, ks[kt, g], vs[kt, g], ps, os_, wt[:, 1:2] * drow, scale)
+        O.dense_attention_backward(rows, ks[wa:wb, g], vs[wa:wb, g], pw, ow, wt[:, 2:3] * drow, scale)
+
+
+def _oracle_worker(Qs):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):           # one worker process per core, BLAS single-threaded (BASELINE.md §3)
+        t = time.perf_counter()
+        for Q in Qs:
+            _oracle_one_q(int(Q))
+        return time.perf_counter() - t
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
 def oracle_sample(cfg, coords, grid, batch, inp, n_sample: int, seed: int = 0):
-    """Run the float64 oracle (as it stands) forward + backward on a bounded sample of the workload:
-    the full block build and pooling, then the per-query-block work (compression attention, Eq. 8
-    scores, top-k, selection + window attention, gated sum, and the branch backwards) for n_sample
-    random query blocks. Returns (seconds, sampled query blocks, total query blocks, threads)."""
+    """Time the float64 oracle (as it stands) on a bounded sample of the workload, one worker process per
+    host core: the full block build and pooling (sequential, once), then the per-query-
+    block work for n_sample random query blocks dealt evenly to the workers. Returns (build s, parallel
+    wall s of the sample, sampled blocks, total blocks, workers); the step estimate is
+    build + wall * total / sampled."""
+    import multiprocessing as mp
     import oracle as O
     t0 = time.perf_counter()
     kw = dict(m_cmp=cfg["m_cmp"], m_slc=cfg["m_slc"], m_win=cfg["m_win"], m_q=cfg["m_q"])
     plan = O.block_build(coords, grid, batch, **kw)
-    H, h_kv, d = cfg["H"], cfg["h_kv"], cfg["d"]
-    h_s = H // h_kv
-    scale = 1.0 / math.sqrt(d)
     P = plan.perm
     qs, ks, vs = inp.q[P].astype(np.float64), inp.k[P].astype(np.float64), inp.v[P].astype(np.float64)
     gs, dos = inp.gates[P].astype(np.float64), inp.dout[P].astype(np.float64)
     k_cmp, v_cmp = O.compress(plan, ks), O.compress(plan, vs)
     t_build = time.perf_counter() - t0
-    Cq, Cs, Cw = plan.offsets["q"], plan.offsets["slc"], plan.offsets["win"]
-    nq = len(Cq) - 1
+    _OS.update(plan=plan, cfg=cfg, qs=qs, ks=ks, vs=vs, gs=gs, dos=dos, k_cmp=k_cmp, v_cmp=v_cmp)
+    nq = plan.n_blocks("q")
     rng = np.random.Generator(np.random.PCG64(seed))
     sample = rng.choice(nq, size=min(n_sample, nq), replace=False)
+    workers = max(1, min(host_cores(), len(sample)))
+    parts = [x for x in np.array_split(sample, workers) if len(x)]
     t1 = time.perf_counter()
-    for Q in sample:
-        a, b_ = int(Cq[Q]), int(Cq[Q + 1])
-        bi = int(plan.sorted_coords[a, 0])
-        c0, c1 = int(plan.batch_blocks["cmp"][bi]), int(plan.batch_blocks["cmp"][bi + 1])
-        s0 = int(plan.batch_blocks["slc"][bi])
-        w = int(plan.tok_block["win"][a])
-        for g in range(h_kv):
-            rows = qs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
-            drow = dos[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, d)
-            wt = gs[a:b_, g * h_s:(g + 1) * h_s].reshape(-1, 3)
-            oc, _, pc = O.dense_attention(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], scale)
-            per = pc.sum(axis=0)
-            sc = np.zeros(int(plan.batch_blocks["slc"][bi + 1]) - s0)
-            np.add.at(sc, plan.cmp_to_slc[c0:c1] - s0, per)
-            sel = O.topk_select(sc, cfg["T"], base=s0)
-            kt = np.concatenate([np.arange(Cs[x], Cs[x + 1]) for x in sel if x >= 0])
-            os_, _, ps = O.dense_attention(rows, ks[kt, g], vs[kt, g], scale)
-            wa, wb = int(Cw[w]), int(Cw[w + 1])
-            ow, _, pw = O.dense_attention(rows, ks[wa:wb, g], vs[wa:wb, g], scale)
-            _ = wt[:, 0:1] * oc + wt[:, 1:2] * os_ + wt[:, 2:3] * ow
-            O.dense_attention_backward(rows, k_cmp[c0:c1, g], v_cmp[c0:c1, g], pc, oc, wt[:, 0:1] * drow, scale)
-            O.dense_attention_backward(rows, ks[kt, g], vs[kt, g], ps, os_, wt[:, 1:2] * drow, scale)
-            O.dense_attention_backward(rows, ks[wa:wb, g], vs[wa:wb, g], pw, ow, wt[:, 2:3] * drow, scale)
+    with mp.get_context("fork").Pool(len(parts)) as pool:
+        pool.map(_oracle_worker, parts)
     t_q = time.perf_counter() - t1
-    threads = 1
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        pass
-    return t_build, t_q, len(sample), nq, threads
+    _OS.clear()
+    return t_build, t_q, len(sample), nq, workers
 
 
 def cpu_baseline(args, cfg, coords, grid, batch, inp, gpu_value):
-    t_build, t_q, ns, nq, threads = oracle_sample(cfg, coords, grid, batch, inp, args.cpu_sample)
-    est_s = t_build + t_q / ns * nq
-    return {"value": round(est_s * 1e3 / batch, 1), "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"float64 numpy oracle: full block build + pool ({t_build:.1f} s) and fwd+bwd of {ns} random "
-                      f"query blocks of {nq} ({t_q:.1f} s), extrapolated linearly to all query blocks"}
+    n_sample = args.cpu_sample or 4 * host_cores()
+    t_build, t_q, ns, nq, workers = oracle_sample(cfg, coords, grid, batch, inp, n_sample)
+    est_s = t_build + t_q * nq / ns
+    res = {"value": round(est_s * 1e3 / batch, 1), "unit": UNIT, "cores": workers, "kind": "oracle",
+           "sample": f"float64 numpy oracle, {workers} worker processes (one per host core, BLAS 1 thread each): full "
+                     f"block build + pool ({t_build:.1f} s) and fwd+bwd of {ns} random query blocks of {nq} "
+                     f"({t_q:.1f} s wall), extrapolated to all query blocks"}
+    if args.cpu_check_c2 and args.config != "C2":
+        # the extrapolation, checked where the oracle finishes: C2 sampled the same way vs every query block
+        from ssa_workload import CONFIGS, config_coords, make_inputs
+        c2 = CONFIGS["C2"]
+        cc, gg, bb = config_coords("C2")
+        inp2 = make_inputs(cc, gg, bb, c2["H"], c2["h_kv"], c2["d"], c2["dtype"], seed=c2["seed"])
+        tb, tq, ns2, nq2, w2 = oracle_sample(c2, cc, gg, bb, inp2, n_sample)
+        tb_f, tq_f, _, nq_f, _ = oracle_sample(c2, cc, gg, bb, inp2, 10 ** 9)     # every query block
+        res["c2_check"] = {"sampled_estimate_s": round(tb + tq * nq2 / ns2, 2), "all_blocks_s": round(tb_f + tq_f, 2),
+                           "note": f"C2 (24 808 tokens): the same {w2}-process oracle on {ns2} sampled query blocks "
+                                   f"(extrapolated) vs on all {nq_f} query blocks (no extrapolation)"}
+    return res
 
 
 def reference_arm(args, rank, world):
@@ -554,19 +695,20 @@ def reference_arm(args, rank, world):
     cfg, coords, grid, batch = workload(args.config, 0, 1)
     inp = make_inputs(coords, grid, batch, cfg["H"], cfg["h_kv"], cfg["d"], cfg["dtype"], seed=cfg["seed"])
     per_step = []
-    threads = 1
-    n_sample = max(2, min(args.cpu_sample, 8))
+    workers = 1
+    n_sample = args.cpu_sample or 2 * host_cores()
     for i in range(args.warmup + args.steps):
-        t_build, t_q, ns, nq, threads = oracle_sample(cfg, coords, grid, batch, inp, n_sample, seed=i)
+        t_build, t_q, ns, nq, workers = oracle_sample(cfg, coords, grid, batch, inp, n_sample, seed=i)
         if i >= args.warmup:
-            per_step.append(t_build + t_q / ns * nq)
+            per_step.append(t_build + t_q * nq / ns)
     v = float(np.mean(per_step)) * 1e3 / batch
     line = {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(v * batch, 1), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (ssa_workload)", "impl": "reference",
-            "config": {"workload": f"{args.config} (oracle sample, extrapolated)", "parallelism": "host cores"},
-            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": f"{n_sample} random query blocks per step + full block build/pool, extrapolated"},
+            "config": {"workload": f"{args.config} (oracle sample, extrapolated)", "parallelism": f"{workers} host processes"},
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": workers, "kind": "oracle",
+                             "sample": f"per step: full block build/pool + {n_sample} random query blocks on {workers} "
+                                       "worker processes (one per core), extrapolated to all query blocks"},
             "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 

@@ -117,8 +117,11 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *   h_q, h_kv, d : heads (h_q multiple of h_kv), head dim. top_k : T, the number of selected
  *   blocks (clamped per batch item to N_slc(b), padded slots hold -1, reading R9).
  *   scale        : softmax scale; <= 0 means 1/sqrt(d) (Eq. 5).
- *   dtype        : SSA_F32 (SIMT fp32 kernels) or SSA_BF16 (tcgen05 tensor-core kernels when
- *                  d == 64 and SSA_FORCE_SIMT is not set; SIMT otherwise).
+ *   dtype        : SSA_F32 (SIMT fp32 kernels, the fp32 mode) or SSA_BF16 (tcgen05 tensor-core
+ *                  kernels: d == 64, m_win == m_slc == m_q, block counts within the kernels' on-chip
+ *                  limits). A bf16 request outside those returns SSA_ERR_UNSUPPORTED (reason in
+ *                  ssa_last_error) unless SSA_FORCE_SIMT opts into the SIMT kernels — there is no
+ *                  silent fallback. Every check happens before any work is enqueued.
  *   pe_k, pe_v   : optional device [m_cmp^3, h_kv, d] (dtype) intra-block PE tables added before
  *                  pooling (Eq. 7, reading R4); NULL = off. Not differentiated.
  *   flags        : SSA_INPUT_SORTED — tensors are already in plan order (no internal permute);
@@ -127,7 +130,8 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *                  SSA_KV_GRAD_FP32 — dk, dv buffers are fp32 (exact partial sums across shards);
  *                  SSA_WINDOW_ONLY  — only the sparse 3D window branch is computed: the
  *                                     compression and selection branches are skipped (their saved
- *                                     outputs are 0, indices -1), out = omega_win * O_win, and the
+ *                                     outputs are 0, their LSEs the 0x7f7f7f7f sentinel, indices -1),
+ *                                     out = omega_win * O_win, and the
  *                                     backward gives the window branch's gradients (dgates of the
  *                                     skipped branches are 0). With gates (0, 0, 1) this is sparse 3D
  *                                     window attention (the SS-VAE layer). tcgen05 path only
@@ -138,6 +142,7 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
 #define SSA_SAVE_SCORES 4u
 #define SSA_KV_GRAD_FP32 8u   /* dk / dv are written as fp32 (partials of a query-block shard)    */
 #define SSA_WINDOW_ONLY 16u   /* window branch only (sparse 3D window attention)                   */
+#define SSA_LOCAL_ROWS 32u    /* q / gates / dout / out / dq / dgates hold only the owned rows       */
 
 typedef struct {
   int32_t h_q, h_kv, d, top_k;
@@ -153,7 +158,33 @@ typedef struct {
    * shards, e.g. with a reduce-scatter). k, v must be complete (e.g. all-gathered). A strict range
    * requires m_win == m_q (a window is then exactly one query block). */
   int32_t q_begin, q_end;
+  /* Query-block sharding, continued (SURVEY §8e mode 2, one shape over several GPUs):
+   *   SSA_LOCAL_ROWS (needs SSA_INPUT_SORTED and a range): the row tensors q, gates, dout, out, dq,
+   *     dgates hold ONLY the owned rows, i.e. plan-order tokens [C_q[q_begin], C_q[q_end]) — the rows a
+   *     rank keeps; k, v stay complete. No kernel touches a row outside that range.
+   *   kc_in, vc_in: optional device fp32 [h_kv][n_cmp][d] pooled keys / values (Eq. 7) supplied by
+   *     the caller (e.g. every rank's ssa_pool output summed across ranks); the forward then does not
+   *     pool and needs the raw k, v only for the selection and window branches.
+   *   kv_event: optional cudaEvent_t. When set, the forward enqueues cudaStreamWaitEvent(stream,
+   *     kv_event) right before its first read of the raw k, v — after the compression attention when
+   *     kc_in / vc_in are given — so a K/V all-gather recorded on another stream overlaps the
+   *     compression branch (a4/a5). NULL: k, v are ready when the call is made. */
+  const void* kc_in;
+  const void* vc_in;
+  void* kv_event;
 } ssa_attn_cfg;
+
+/* ------------------------------------------------------------------------------------------------
+ * ssa_pool — the compression pool alone (Eq. 7; delta = masked mean, reading R4, plus the
+ * optional intra-block PE of cfg): kc[g][j][:] = mean over the tokens of compression block j of
+ * k[t][g][:] (+ pe_k), likewise vc, fp32 [h_kv][n_cmp][d] (device, caller-owned). For sharded use
+ * (SSA_LOCAL_ROWS + a query-block range) k, v hold the owned rows only and only the compression blocks
+ * inside the owned rows are pooled; every other block of kc / vc is written as 0, so a SUM over ranks
+ * (all-reduce) assembles the complete pooled keys. Needs SSA_INPUT_SORTED. No workspace.
+ * Errors: SSA_ERR_ARG, SSA_ERR_BAD_STATE, SSA_ERR_CUDA.
+ * ----------------------------------------------------------------------------------------------*/
+ssa_status ssa_pool(ssa_plan plan, const ssa_attn_cfg* cfg, const void* k, const void* v, void* kc, void* vc,
+                    void* stream);
 
 /* ------------------------------------------------------------------------------------------------
  * ssa_forward — one SSA forward (Eq. 6): pool (Eq. 7) -> compression attention + Eq. 8 block

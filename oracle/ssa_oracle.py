@@ -459,3 +459,284 @@ def ssa_backward(fwd: ForwardResult, q, k, v, gates, dout, *, h_kv, scale=None):
         dv[Cc[j]:Cc[j + 1]] += dv_cmp[j] / n
     inv = plan.inv_perm
     return dq[inv], dk[inv], dv[inv], dgates[inv]
+
+
+# --------------------------------------------------------------------------------------------------
+# Per-block gradients for full-size parity (BASELINE configs C3 / C4, where the whole oracle backward
+# takes minutes): the same arithmetic as ssa_backward, restricted to the keys of a few blocks. Tested
+# equal to ssa_backward on small cases (tests/test_oracle_backward.py), so they inherit its pins
+# (central finite differences, closed forms).
+# --------------------------------------------------------------------------------------------------
+def compression_kv_grad(plan: BlockPlan, q_sorted, k_cmp, v_cmp, gates_sorted, dout_sorted, h_kv: int,
+                        scale: float, b: int, cols, chunk: int = 2048, workers: int = 1):
+    """dK^cmp, dV^cmp [len(cols), h_kv, d] of the compression branch (Eq. 6 term 1 backward, R15) for the
+    compression blocks `cols` (global ids, all in batch item b): the sum over EVERY row (t, h) of item b.
+    Rows are processed in chunks of `chunk` (each chunk is dense_attention over all compression keys of
+    the item, then dense_attention_backward restricted to the requested key columns — D = <dO_c, O>
+    uses the full row); chunk results are summed in chunk order. `workers` > 1 evaluates chunks on a
+    thread pool (numpy releases the GIL); the summation order is unchanged."""
+    cols = np.asarray(cols, np.int64)
+    N, H, d = q_sorted.shape
+    h_s = H // h_kv
+    t0, t1 = int(plan.batch_tokens[b]), int(plan.batch_tokens[b + 1])
+    c0, c1 = int(plan.batch_blocks["cmp"][b]), int(plan.batch_blocks["cmp"][b + 1])
+    assert ((cols >= c0) & (cols < c1)).all(), "cols must lie in batch item b"
+    loc = cols - c0
+    dk = np.zeros((len(cols), h_kv, v_cmp.shape[2]))
+    dv = np.zeros((len(cols), h_kv, v_cmp.shape[2]))
+    for g in range(h_kv):
+        R = _rows(q_sorted, t0, t1, g, h_s)
+        DO = _rows(np.asarray(gates_sorted, np.float64)[..., 0:1] * np.asarray(dout_sorted, np.float64),
+                   t0, t1, g, h_s)
+        Kb = np.asarray(k_cmp[c0:c1, g], np.float64)
+        Vb = np.asarray(v_cmp[c0:c1, g], np.float64)
+
+        def one(r0):
+            r1 = min(r0 + chunk, R.shape[0])
+            o, _, p = dense_attention(R[r0:r1], Kb, Vb, scale)
+            _, dkc, dvc = dense_attention_backward(R[r0:r1], Kb[loc], Vb[loc], p[:, loc], o, DO[r0:r1], scale)
+            return dkc, dvc
+
+        starts = list(range(0, R.shape[0], chunk))
+        if workers > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(workers) as ex:
+                parts = list(ex.map(one, starts))
+        else:
+            parts = [one(r0) for r0 in starts]
+        for dkc, dvc in parts:
+            dk[:, g] += dkc
+            dv[:, g] += dvc
+    return dk, dv
+
+
+def raw_kv_grad_block(plan: BlockPlan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv: int,
+                      scale: float, B: int, g: int):
+    """dk, dv [n_B, d] of the raw tokens of selection block B for kv group g from the selection branch
+    (every (Q, g) with B in I[Q, g], attention over all of Q's selected tokens, Alg. 1 / O6) and the
+    window branch (every window holding a token of B, O7) — everything but the compression pool share."""
+    N, H, d = q_sorted.shape
+    h_s = H // h_kv
+    C = plan.offsets["slc"]
+    b0, b1 = int(C[B]), int(C[B + 1])
+    gs = np.asarray(gates_sorted, np.float64)
+    dos = np.asarray(dout_sorted, np.float64)
+    dk = np.zeros((b1 - b0, d))
+    dv = np.zeros((b1 - b0, v_sorted.shape[2]))
+    Cq = plan.offsets["q"]
+    for Q in range(len(Cq) - 1):
+        if B not in set(int(x) for x in I[Q, g]):
+            continue
+        t0, t1 = int(Cq[Q]), int(Cq[Q + 1])
+        kt = _selected_tokens(plan, I, Q, g)
+        rows = _rows(q_sorted, t0, t1, g, h_s)
+        dor = _rows(gs[..., 1:2] * dos, t0, t1, g, h_s)
+        o, _, p = dense_attention(rows, k_sorted[kt, g], v_sorted[kt, g], scale)
+        m = (kt >= b0) & (kt < b1)
+        _, dkr, dvr = dense_attention_backward(rows, k_sorted[kt[m], g], v_sorted[kt[m], g], p[:, m], o, dor, scale)
+        dk[kt[m] - b0] += dkr
+        dv[kt[m] - b0] += dvr
+    Cw = plan.offsets["win"]
+    for w in sorted(set(int(x) for x in plan.tok_block["win"][b0:b1])):
+        t0, t1 = int(Cw[w]), int(Cw[w + 1])
+        kt = np.arange(t0, t1)
+        rows = _rows(q_sorted, t0, t1, g, h_s)
+        dor = _rows(gs[..., 2:3] * dos, t0, t1, g, h_s)
+        o, _, p = dense_attention(rows, k_sorted[kt, g], v_sorted[kt, g], scale)
+        m = (kt >= b0) & (kt < b1)
+        _, dkr, dvr = dense_attention_backward(rows, k_sorted[kt[m], g], v_sorted[kt[m], g], p[:, m], o, dor, scale)
+        dk[kt[m] - b0] += dkr
+        dv[kt[m] - b0] += dvr
+    return dk, dv
+
+
+def block_kv_grad(plan: BlockPlan, q_sorted, k_sorted, v_sorted, k_cmp, v_cmp, gates_sorted, dout_sorted, I,
+                  h_kv: int, scale: float, blocks, workers: int = 1) -> dict:
+    """{B: (dk, dv) [n_B, h_kv, d]}: total gradients of the tokens of each selection block B (sorted
+    order) = raw-key part (raw_kv_grad_block) + the mean-pool share dk^cmp_c / n_c of every compression
+    block c inside B (Eq. 7 backward with delta = mean, R4). One compression_kv_grad pass per batch item
+    covers all requested blocks of that item."""
+    C = plan.offsets["slc"]
+    Cc = plan.offsets["cmp"]
+    d = q_sorted.shape[2]
+    by_item = {}
+    for B in blocks:
+        by_item.setdefault(int(plan.sorted_coords[int(C[B]), 0]), []).append(int(B))
+    out = {}
+    for bi, Bs in by_item.items():
+        cols = sorted(set(int(x) for B in Bs for x in plan.tok_block["cmp"][int(C[B]):int(C[B + 1])]))
+        dkc, dvc = compression_kv_grad(plan, q_sorted, k_cmp, v_cmp, gates_sorted, dout_sorted, h_kv, scale, bi,
+                                       np.array(cols, np.int64), workers=workers)
+        col_of = {c: i for i, c in enumerate(cols)}
+        for B in Bs:
+            b0, b1 = int(C[B]), int(C[B + 1])
+            dk = np.zeros((b1 - b0, h_kv, d))
+            dv = np.zeros((b1 - b0, h_kv, v_sorted.shape[2]))
+            for g in range(h_kv):
+                rk, rv = raw_kv_grad_block(plan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv,
+                                           scale, B, g)
+                dk[:, g] += rk
+                dv[:, g] += rv
+            for c in sorted(set(int(x) for x in plan.tok_block["cmp"][b0:b1])):
+                a, e = int(Cc[c]), int(Cc[c + 1])
+                dk[a - b0:e - b0] += dkc[col_of[c]] / (e - a)
+                dv[a - b0:e - b0] += dvc[col_of[c]] / (e - a)
+            out[B] = (dk, dv)
+    return out
+
+
+# --------------------------------------------------------------------------------------------------
+# §8f row 2 — learned compression delta and the gate projection.
+# Eq. 7 (P:157-162): k^cmp = delta(k + PE(k)), delta = "sparse 3D convolution followed by sparse 3D mean
+# pooling" that "compress[es] the entire block". READING R17: the convolution has kernel = stride =
+# m_cmp (one output per m_cmp^3 block, one weight matrix per intra-block offset, grouped per kv head),
+# evaluated over the ACTIVE tokens only (sparse), and the sparse mean pooling divides by the number of
+# active tokens:  k^cmp_B = (1/n_B) sum_{j in B} W[loc(j), g] (k_j + PE[loc(j), g]) + b[g].
+# W[loc, g] is a d_out x d_in matrix applied as W @ x. W[loc] = I, b = 0 is the plain mean pool (R4).
+# Eq. 6 gates (P:153): omega_t = sigmoid(x_t W_g + b_g) — "a linear layer followed by a sigmoid
+# activation to the input features" x_t [C]; READING R18: one gate per (head, branch), W_g [C, 3 h_q]
+# with column h*3 + c for head h, branch c (cmp, slc, win).
+# --------------------------------------------------------------------------------------------------
+def compress_learned(plan: BlockPlan, x_sorted, W, b=None, pe=None):
+    """x_sorted [N, h_kv, d] -> [N_cmp, h_kv, d_out] (READING R17). W [m^3, h_kv, d_out, d], b [h_kv, d_out]."""
+    x = np.asarray(x_sorted, np.float64)
+    m = plan.sizes["cmp"]
+    loc = local_index(plan.sorted_coords, m)
+    if pe is not None:
+        x = x + np.asarray(pe, np.float64)[loc]
+    W = np.asarray(W, np.float64)
+    C = plan.offsets["cmp"]
+    out = np.zeros((len(C) - 1, x.shape[1], W.shape[2]))
+    for j in range(len(C) - 1):
+        for t in range(int(C[j]), int(C[j + 1])):
+            for g in range(x.shape[1]):
+                out[j, g] += W[loc[t], g] @ x[t, g]
+        out[j] /= C[j + 1] - C[j]
+    if b is not None:
+        out += np.asarray(b, np.float64)[None]
+    return out
+
+
+def compress_learned_backward(plan: BlockPlan, x_sorted, W, dout_cmp, pe=None):
+    """Gradients of compress_learned w.r.t. x (sorted order), W and b for the upstream dout_cmp
+    [N_cmp, h_kv, d_out] (PE is a constant input)."""
+    x = np.asarray(x_sorted, np.float64)
+    m = plan.sizes["cmp"]
+    loc = local_index(plan.sorted_coords, m)
+    if pe is not None:
+        x = x + np.asarray(pe, np.float64)[loc]
+    W = np.asarray(W, np.float64)
+    dy = np.asarray(dout_cmp, np.float64)
+    C = plan.offsets["cmp"]
+    dx = np.zeros_like(x)
+    dW = np.zeros_like(W)
+    for j in range(len(C) - 1):
+        n = C[j + 1] - C[j]
+        for t in range(int(C[j]), int(C[j + 1])):
+            for g in range(x.shape[1]):
+                dx[t, g] = W[loc[t], g].T @ dy[j, g] / n
+                dW[loc[t], g] += np.outer(dy[j, g], x[t, g]) / n
+    db = dy.sum(axis=0)
+    return dx, dW, db
+
+
+def gate_projection(x, Wg, bg, h_q: int):
+    """omega = sigmoid(x Wg + bg) -> [N, h_q, 3] (READING R18)."""
+    z = np.asarray(x, np.float64) @ np.asarray(Wg, np.float64) + np.asarray(bg, np.float64)
+    return (1.0 / (1.0 + np.exp(-z))).reshape(len(z), h_q, 3)
+
+
+def gate_projection_backward(x, Wg, bg, dgates):
+    """(dx, dWg, dbg) of gate_projection for the upstream dgates [N, h_q, 3]."""
+    x = np.asarray(x, np.float64)
+    s = 1.0 / (1.0 + np.exp(-(x @ np.asarray(Wg, np.float64) + np.asarray(bg, np.float64))))
+    dz = np.asarray(dgates, np.float64).reshape(len(x), -1) * s * (1.0 - s)
+    return dz @ np.asarray(Wg, np.float64).T, x.T @ dz, dz.sum(axis=0)
+
+
+def ssa_forward_learned(coords, grid, batch, q, k, v, x, *, conv_k, conv_v, gate, h_kv, T, m_cmp, m_slc, m_win,
+                        m_q, pe_k=None, pe_v=None, I_override=None):
+    """SSA with the learned delta (compress_learned with conv_k = (W_k, b_k), conv_v = (W_v, b_v)) and
+    gates from the projection gate = (W_g, b_g) of the input features x [N, C] (original order).
+    Returns (ForwardResult, gates [N, H, 3])."""
+    q = np.asarray(q, np.float64)
+    N, H, d = q.shape
+    scale = 1.0 / math.sqrt(d)
+    plan = block_build(coords, grid, batch, m_cmp, m_slc, m_win, m_q)
+    gates = gate_projection(x, gate[0], gate[1], H)
+    P = plan.perm
+    qs, ks, vs, gs = q[P], np.asarray(k, np.float64)[P], np.asarray(v, np.float64)[P], gates[P]
+    k_cmp = compress_learned(plan, ks, conv_k[0], conv_k[1], pe_k)
+    v_cmp = compress_learned(plan, vs, conv_v[0], conv_v[1], pe_v)
+    o_c, l_c, probs = compression_attention(plan, qs, k_cmp, v_cmp, h_kv, scale)
+    scores = block_scores(plan, probs, h_kv)
+    I = topk_all(plan, scores, h_kv, T) if I_override is None else np.asarray(I_override, np.int64)
+    o_s, l_s = selection_attention(plan, qs, ks, vs, I, h_kv, scale)
+    o_w, l_w = window_attention(plan, qs, ks, vs, h_kv, scale)
+    out = gate_combine(o_c, o_s, o_w, gs)
+    inv = plan.inv_perm
+    f = ForwardResult(out=out[inv], o=dict(cmp=o_c[inv], slc=o_s[inv], win=o_w[inv]),
+                      lse=dict(cmp=l_c[inv], slc=l_s[inv], win=l_w[inv]), I=I, scores=scores,
+                      k_cmp=k_cmp, v_cmp=v_cmp, plan=plan)
+    return f, gates
+
+
+def ssa_backward_learned(fwd: ForwardResult, q, k, v, x, gates, dout, *, conv_k, conv_v, gate, h_kv,
+                         pe_k=None, pe_v=None):
+    """Gradients of ssa_forward_learned: (dq, dk, dv, dx, dW_k, db_k, dW_v, db_v, dW_g, db_g), original
+    order. Same chain as ssa_backward with the learned delta in place of the mean pool and the gate
+    projection after the gates."""
+    plan = fwd.plan
+    q = np.asarray(q, np.float64)
+    N, H, d = q.shape
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    P = plan.perm
+    qs = q[P]
+    ks = np.asarray(k, np.float64)[P]
+    vs = np.asarray(v, np.float64)[P]
+    gs = np.asarray(gates, np.float64)[P]
+    dos = np.asarray(dout, np.float64)[P]
+    o = {c: fwd.o[c][P] for c in fwd.o}
+    dgates = np.stack([(dos * o[c]).sum(axis=2) for c in ("cmp", "slc", "win")], axis=2)
+    dq = np.zeros_like(qs)
+    dk = np.zeros_like(ks)
+    dv = np.zeros_like(vs)
+    dk_cmp = np.zeros_like(fwd.k_cmp)
+    dv_cmp = np.zeros_like(fwd.v_cmp)
+    Cq, Cw = plan.offsets["q"], plan.offsets["win"]
+    do_c = {c: gs[..., i:i + 1] * dos for i, c in enumerate(("cmp", "slc", "win"))}
+
+    def run(t0, t1, g, kmat, vmat, branch):
+        qr = _rows(qs, t0, t1, g, h_s)
+        dor = _rows(do_c[branch], t0, t1, g, h_s)
+        oo, _, pp = dense_attention(qr, kmat, vmat, scale)
+        dqr, dkr, dvr = dense_attention_backward(qr, kmat, vmat, pp, oo, dor, scale)
+        dq[t0:t1, g * h_s:(g + 1) * h_s] += dqr.reshape(t1 - t0, h_s, d)
+        return dkr, dvr
+
+    for Q in range(len(Cq) - 1):
+        t0, t1 = int(Cq[Q]), int(Cq[Q + 1])
+        b = int(plan.sorted_coords[t0, 0])
+        c0, c1 = int(plan.batch_blocks["cmp"][b]), int(plan.batch_blocks["cmp"][b + 1])
+        for g in range(h_kv):
+            dkr, dvr = run(t0, t1, g, fwd.k_cmp[c0:c1, g], fwd.v_cmp[c0:c1, g], "cmp")
+            dk_cmp[c0:c1, g] += dkr
+            dv_cmp[c0:c1, g] += dvr
+            kt = _selected_tokens(plan, fwd.I, Q, g)
+            dkr, dvr = run(t0, t1, g, ks[kt, g], vs[kt, g], "slc")
+            np.add.at(dk[:, g], kt, dkr)
+            np.add.at(dv[:, g], kt, dvr)
+    for w in range(len(Cw) - 1):
+        t0, t1 = int(Cw[w]), int(Cw[w + 1])
+        for g in range(h_kv):
+            dkr, dvr = run(t0, t1, g, ks[t0:t1, g], vs[t0:t1, g], "win")
+            dk[t0:t1, g] += dkr
+            dv[t0:t1, g] += dvr
+    dxk, dWk, dbk = compress_learned_backward(plan, ks, conv_k[0], dk_cmp, pe_k)
+    dxv, dWv, dbv = compress_learned_backward(plan, vs, conv_v[0], dv_cmp, pe_v)
+    dk += dxk
+    dv += dxv
+    inv = plan.inv_perm
+    dx, dWg, dbg = gate_projection_backward(x, gate[0], gate[1], dgates[inv])
+    return dq[inv], dk[inv], dv[inv], dx, dWk, dbk, dWv, dbv, dWg, dbg

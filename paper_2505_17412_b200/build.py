@@ -23,8 +23,9 @@ FLAGS += [f for f in os.environ.get("SSA_EXTRA_NVCC_FLAGS", "").split() if f]   
 
 def sources():
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    if os.path.exists(os.path.join(CSRC, "tc_fwd.cu")):
-        srcs = [s for s in srcs if not s.endswith("tc_stub.cu")]
+    for need in ("tc_fwd.cu", "tc_bwd.cu"):      # the tcgen05 kernels are the product path: no stub build
+        if not os.path.exists(os.path.join(CSRC, need)):
+            raise RuntimeError(f"missing {need}")
     return srcs
 
 

@@ -2,6 +2,7 @@
 // forward / backward orchestration. Every step of the path runs in this library's kernels.
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "internal.h"
 #include "tc.h"
@@ -66,6 +67,11 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
       return SSA_ERR_UNSUPPORTED;
     }
   }
+  if ((cfg->flags & SSA_LOCAL_ROWS) && (!(cfg->flags & SSA_INPUT_SORTED) || cfg->q_end <= 0)) {
+    set_error("SSA_LOCAL_ROWS needs SSA_INPUT_SORTED and a query-block range");
+    return SSA_ERR_ARG;
+  }
+  if ((cfg->kc_in == nullptr) != (cfg->vc_in == nullptr)) { set_error("kc_in and vc_in go together"); return SSA_ERR_ARG; }
   d->N = p->info.n;
   d->H = cfg->h_q;
   d->h_kv = cfg->h_kv;
@@ -91,6 +97,31 @@ bool use_tc(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
 }
 bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   return tc_bwd_available() && use_tc(d, cfg, p);
+}
+// Why a bf16 request cannot take the tcgen05 path (nullptr if it can).
+const char* tc_reason(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
+  const int32_t* m = p->info.m;
+  if (!tc_available()) return "library built without the tcgen05 kernels";
+  if (d.D != 64) return "head dim != 64";
+  if (m[SSA_LEVEL_WIN] != m[SSA_LEVEL_SLC] || m[SSA_LEVEL_Q] != m[SSA_LEVEL_SLC]) return "m_win or m_q != m_slc";
+  if (!tc_plan_ok(p->info, cfg->top_k)) return "a batch item's block counts exceed the kernels' on-chip limits";
+  return nullptr;
+}
+// Path selection, before any work is enqueued: fp32 runs the SIMT kernels (the fp32 mode); bf16 runs
+// the tcgen05 kernels, and a bf16 request they cannot take is an error unless the caller opts into the
+// (100-500x slower) SIMT kernels with SSA_FORCE_SIMT — no silent fallback.
+ssa_status choose_path(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p, bool* tc) {
+  *tc = use_tc(d, cfg, p);
+  if (cfg->flags & SSA_WINDOW_ONLY) {
+    if (!*tc) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path (bf16, d = 64, m_win == m_slc == m_q)"); return SSA_ERR_UNSUPPORTED; }
+    return SSA_OK;
+  }
+  if (cfg->dtype == SSA_BF16 && !*tc && !(cfg->flags & SSA_FORCE_SIMT)) {
+    set_error(std::string("bf16 request outside the tcgen05 kernels (") + tc_reason(d, cfg, p) +
+              "); set SSA_FORCE_SIMT to run the SIMT kernels");
+    return SSA_ERR_UNSUPPORTED;
+  }
+  return SSA_OK;
 }
 
 // saved state: kc, vc, o[3], lse[3], I, scores
@@ -195,6 +226,18 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->q_end = cfg->q_end > 0 ? std::min(nq, cfg->q_end) : nq;
   x->tok_begin = -1;   // resolved on device from the Q offsets (kernels read off[Q][q_begin / q_end])
   x->tok_end = -1;
+  const bool ranged = cfg->q_end > 0 && p->h_q_offsets.size() == size_t(nq) + 1;
+  x->row_lo = ranged ? p->h_q_offsets[x->q_begin] : 0;
+  x->row_hi = ranged ? p->h_q_offsets[x->q_end] : int32_t(d.N);
+  x->row_base = (cfg->flags & SSA_LOCAL_ROWS) ? x->row_lo : 0;
+}
+
+// SSA_LOCAL_ROWS: the caller's row tensors start at row row_base; kernels index rows by their plan
+// position p (p in [row_lo, row_hi) only), so the base pointers are moved back by row_base rows.
+template <class P>
+P rows_at(P ptr, const Ctx& x, int64_t elems_per_row, size_t esz) {
+  using B = typename std::conditional<std::is_const<typename std::remove_pointer<P>::type>::value, const char*, char*>::type;
+  return ptr ? reinterpret_cast<P>(reinterpret_cast<B>(ptr) - x.row_base * elems_per_row * int64_t(esz)) : ptr;
 }
 }  // namespace
 }  // namespace ssa
@@ -230,20 +273,37 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   if (s != SSA_OK) return s;
   if (ws_bytes < need_ws || saved_bytes < need_saved) { set_error("ws/saved buffer too small"); return SSA_ERR_WORKSPACE; }
   if (d.max_slc_b > 0 && p->info.max_blocks_per_batch[SSA_LEVEL_SLC] < 1) { set_error("empty plan"); return SSA_ERR_BAD_STATE; }
+  bool tc = false;
+  if ((s = choose_path(d, cfg, p, &tc)) != SSA_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Ctx x{};
   fill_common(&x, p, d, cfg);
-  x.q = q; x.k = k; x.v = v; x.gates = gates; x.out = out;
+  x.q = rows_at(q, x, int64_t(d.H) * d.D, d.esz);
+  x.gates = rows_at(gates, x, int64_t(d.H) * 3, d.esz);
+  x.out = rows_at(out, x, int64_t(d.H) * d.D, d.esz);
+  x.k = k; x.v = v;
   Carve cs(saved, saved_bytes);
   carve_saved(cs, d, cfg, &x);
   Carve cw(ws, ws_bytes);
   carve_inputs(cw, d, &x, false);
   void* tc_ws = cw.take<char>(tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
   const bool bf16 = cfg->dtype == SSA_BF16;
-  if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
-  if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
+  // caller-supplied pooled keys (mode 2): no pooling; raw k / v are first read by the selection /
+  // window branch, after cfg.kv_event (tcgen05 path) — the compression branch overlaps the K/V exchange
+  const bool ext_kc = cfg->kc_in != nullptr;
+  cudaEvent_t kv_ev = static_cast<cudaEvent_t>(cfg->kv_event);
+  const size_t kc_bytes = size_t(d.h_kv) * d.n_cmp * d.D * 4;
+  if (ext_kc) {
+    SSA_CUDA_TRY(cudaMemcpyAsync(x.kc, cfg->kc_in, kc_bytes, cudaMemcpyDeviceToDevice, st));
+    SSA_CUDA_TRY(cudaMemcpyAsync(x.vc, cfg->vc_in, kc_bytes, cudaMemcpyDeviceToDevice, st));
+    if (!tc && kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
+    if ((s = gather_inputs(x, bf16, st, false, true, /*keys=*/!tc)) != SSA_OK) return s;
+  } else {
+    if (kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
+    if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
+    if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
+  }
   if (x.win_only) {
-    if (!use_tc(d, cfg, p)) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path (bf16, d = 64, m_win == m_slc == m_q)"); return SSA_ERR_UNSUPPORTED; }
     // skipped branches: O = 0, indices -1 (no selected blocks), LSE huge (p = exp2(s - LSE) = 0 anywhere)
     const int64_t rows = int64_t(d.N) * d.H;
     for (int b = 0; b < 2; ++b) {
@@ -252,8 +312,8 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
     }
     SSA_CUDA_TRY(cudaMemsetAsync(x.I, 0xff, size_t(d.n_q) * d.h_kv * d.T * 4, st));
   }
-  if (use_tc(d, cfg, p)) {
-    if ((s = tc_forward(x, tc_ws, st)) != SSA_OK) return s;
+  if (tc) {
+    if ((s = tc_forward(x, tc_ws, st, ext_kc ? kv_ev : nullptr, ext_kc)) != SSA_OK) return s;
   } else {
     if ((s = simt_forward(x, bf16, st, false)) != SSA_OK) return s;
     if ((s = combine_forward(x, bf16, st)) != SSA_OK) return s;
@@ -293,11 +353,17 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   if ((s = ssa_forward_size(plan, cfg, &need_ws_f, &need_saved)) != SSA_OK) return s;
   if (saved_bytes < need_saved) { set_error("saved buffer smaller than this cfg's saved state"); return SSA_ERR_BAD_STATE; }
   if (ws_bytes < need_ws) { set_error("ws buffer too small"); return SSA_ERR_WORKSPACE; }
+  bool tc_path = false;
+  if ((s = choose_path(d, cfg, p, &tc_path)) != SSA_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Ctx x{};
   fill_common(&x, p, d, cfg);
-  x.q = q; x.k = k; x.v = v; x.gates = gates; x.dout = dout;
-  x.dq = dq; x.dk = dk; x.dv = dv; x.dgates = dgates;
+  x.q = rows_at(q, x, int64_t(d.H) * d.D, d.esz);
+  x.gates = rows_at(gates, x, int64_t(d.H) * 3, d.esz);
+  x.dout = rows_at(dout, x, int64_t(d.H) * d.D, d.esz);
+  x.dq = rows_at(dq, x, int64_t(d.H) * d.D, d.esz);
+  x.dgates = rows_at(dgates, x, int64_t(d.H) * 3, d.esz);
+  x.k = k; x.v = v; x.dk = dk; x.dv = dv;
   Carve cs(const_cast<void*>(saved), saved_bytes);
   carve_saved(cs, d, cfg, &x);
   Carve cw(ws, ws_bytes);
@@ -311,7 +377,6 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc)) != SSA_OK) return s;
   if (!tc && (s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
   if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
-  if (x.win_only && !tc) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path"); return SSA_ERR_UNSUPPORTED; }
   if (tc) {
     if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
     if (x.win_only) {   // no compressed-key gradients: the pool backward adds zeros
@@ -324,6 +389,20 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
   }
   return bwd_epilogue(x, bf16, st, /*skip_q=*/tc);
+}
+
+extern "C" ssa_status ssa_pool(ssa_plan plan, const ssa_attn_cfg* cfg, const void* k, const void* v, void* kc, void* vc,
+                               void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  Dims d;
+  ssa_status s = check_cfg(p, cfg, &d);
+  if (s != SSA_OK) return s;
+  if (!k || !v || !kc || !vc) { set_error("null tensor pointer"); return SSA_ERR_ARG; }
+  if (!(cfg->flags & SSA_INPUT_SORTED)) { set_error("ssa_pool needs SSA_INPUT_SORTED (plan-order k, v)"); return SSA_ERR_ARG; }
+  Ctx x{};
+  fill_common(&x, p, d, cfg);
+  return pool_rows(x, cfg->dtype == SSA_BF16, k, v, static_cast<float*>(kc), static_cast<float*>(vc),
+                   static_cast<cudaStream_t>(stream));
 }
 
 extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,

@@ -356,6 +356,7 @@ extern "C" ssa_status ssa_build_blocks(const int32_t* coords, int64_t n, int32_t
     std::vector<int32_t> off(nq + 1), order(nq);
     CTRY(cudaMemcpyAsync(off.data(), p->offsets[SSA_LEVEL_Q], (nq + 1) * 4, cudaMemcpyDeviceToHost, st));
     CTRY(cudaStreamSynchronize(st));
+    p->h_q_offsets = off;
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(),
                      [&](int32_t a, int32_t b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });

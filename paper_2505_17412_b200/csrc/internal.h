@@ -32,6 +32,7 @@ struct Plan {
   int32_t n_cmp_tiles = 0;
   std::vector<int32_t> h_batch_blocks[kLevels];
   std::vector<int32_t> h_batch_tokens;
+  std::vector<int32_t> h_q_offsets;   // [n_q+1] token offsets of the query blocks (host copy)
 };
 
 // Everything a forward/backward kernel needs, by value (kernel parameter space).
@@ -46,6 +47,9 @@ struct Ctx {
   int32_t win_only;                   // SSA_WINDOW_ONLY: compression / selection branches skipped
   int32_t q_begin, q_end;         // owned query blocks [q_begin, q_end) (plan order)
   int32_t tok_begin, tok_end;     // their token range
+  int32_t row_lo, row_hi;         // rows (plan order) whose caller row tensors may be touched: the owned
+                                  // range with a query-block range, [0, N) otherwise
+  int64_t row_base;               // SSA_LOCAL_ROWS: first row held by the caller's row tensors (else 0)
   int32_t save_scores;
   int32_t kv_grad_f32;            // dk / dv written as fp32 (SSA_KV_GRAD_FP32)
   // plan (device)
@@ -69,6 +73,7 @@ struct Ctx {
   float *dkc, *dvc;               // fp32 [h_kv][n_cmp][D]
   float *dkc_part, *dvc_part;     // fp32 [n_chunk][h_kv][n_cmp][D]
   int32_t n_chunk;
+  const uint32_t* do_amax;        // tcgen05 backward: max |dO| (float bits) -> power-of-two operand scale
   int32_t *inv_off, *inv_list, *inv_cnt;   // inverse selection CSR over (slc block, g)
   int32_t *cmp_tiles;             // [n_cmp_tiles][2] (batch item, first cmp block) for the KV-outer cmp kernels
   int32_t n_cmp_tiles;
@@ -81,7 +86,10 @@ struct Ctx {
 ssa_status simt_forward(const Ctx& c, bool bf16, cudaStream_t st, bool attention_only);
 ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
 // rows = false: only keys and gates are gathered (the tcgen05 backward reads q / dO rows itself)
-ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows = true);
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows = true, bool keys = true,
+                         bool gates = true);
+// ssa_pool's kernel: pooled keys of the owned compression blocks from caller-layout (sorted) k, v
+ssa_status pool_rows(const Ctx& c, bool bf16, const void* k, const void* v, float* kc, float* vc, cudaStream_t st);
 ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status combine_forward(const Ctx& c, bool bf16, cudaStream_t st);
 size_t inverse_csr_ws_bytes(int n_slc, int h_kv, int n_q);

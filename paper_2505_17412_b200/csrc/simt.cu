@@ -36,6 +36,7 @@ __global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ 
   const int ch = i % per;
   const int g = (i / per) % c.h_kv;
   const int p = i / (per * c.h_kv);
+  if (p < c.row_lo || p >= c.row_hi) return;             // rows of other shards are never read
   const int src_p = c.sorted_input ? p : c.perm[p];
   const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
   uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t(g) * c.N + p) * c.h_s * c.D);
@@ -63,6 +64,7 @@ __global__ void k_gather_gates(Ctx c, const T* __restrict__ gates, float* __rest
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.N * c.H) return;
   const int h = i % c.H, p = i / c.H;
+  if (p < c.row_lo || p >= c.row_hi) return;             // rows of other shards are never read
   const int src_p = c.sorted_input ? p : c.perm[p];
   const int g = h / c.h_s, s = h % c.h_s;
   const T* src = gates + (int64_t(src_p) * c.H + h) * 3;
@@ -894,7 +896,7 @@ ssa_status dispatch_d_bwd(const Ctx& c, cudaStream_t st) {
 }
 }  // namespace
 
-ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows) {
+ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows, bool keys, bool gates) {
   const int esz = bf16 ? 2 : 4;
   const int64_t nr = int64_t(c.N) * c.h_kv * (c.h_s * c.D * esz / 16), nk = int64_t(c.N) * c.h_kv * (c.D * esz / 16);
   const int64_t ng = int64_t(c.N) * c.H * 3;
@@ -908,11 +910,15 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
       k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
       SSA_LAUNCH_CHECK("k_gather_rows");
     }
-    k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
-                                                    static_cast<T*>(c.ks), static_cast<T*>(c.vs));
-    SSA_LAUNCH_CHECK("k_gather_keys");
-    k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
-    SSA_LAUNCH_CHECK("k_gather_gates");
+    if (keys) {
+      k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
+                                                      static_cast<T*>(c.ks), static_cast<T*>(c.vs));
+      SSA_LAUNCH_CHECK("k_gather_keys");
+    }
+    if (gates) {
+      k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+      SSA_LAUNCH_CHECK("k_gather_gates");
+    }
   } else {
     using T = float;
     if (with_dout) {
@@ -921,12 +927,65 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
     }
     k_gather_rows<T><<<nblk(nr, 256), 256, 0, st>>>(c, static_cast<const T*>(c.q), static_cast<T*>(c.qs));
     SSA_LAUNCH_CHECK("k_gather_rows");
-    k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
-                                                    static_cast<T*>(c.ks), static_cast<T*>(c.vs));
-    SSA_LAUNCH_CHECK("k_gather_keys");
-    k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
-    SSA_LAUNCH_CHECK("k_gather_gates");
+    if (keys) {
+      k_gather_keys<T><<<nblk(nk, 256), 256, 0, st>>>(c, static_cast<const T*>(c.k), static_cast<const T*>(c.v),
+                                                      static_cast<T*>(c.ks), static_cast<T*>(c.vs));
+      SSA_LAUNCH_CHECK("k_gather_keys");
+    }
+    if (gates) {
+      k_gather_gates<T><<<nblk(ng / 3, 256), 256, 0, st>>>(c, static_cast<const T*>(c.gates), c.gs);
+      SSA_LAUNCH_CHECK("k_gather_gates");
+    }
   }
+  return SSA_OK;
+}
+
+// ssa_pool (sharded mode 2): Eq. 7 (delta = mean, reading R4, optional PE) straight from the caller's
+// plan-order k, v, for the compression blocks inside the owned rows [row_lo, row_hi); every other
+// block is written as 0 so that a sum over ranks assembles the complete pooled keys. k, v point at
+// row row_lo (SSA_LOCAL_ROWS) or row 0. grid (n_cmp, h_kv), block D threads.
+template <class T>
+__global__ void k_pool_rows(Ctx c, const T* __restrict__ k, const T* __restrict__ v, int64_t row_base,
+                            float* __restrict__ kc, float* __restrict__ vc) {
+  const int j = blockIdx.x, g = blockIdx.y, e = threadIdx.x;
+  const int t0 = c.off[SSA_LEVEL_CMP][j], t1 = c.off[SSA_LEVEL_CMP][j + 1];
+  const int64_t o = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
+  if (t0 < c.row_lo || t1 > c.row_hi) {           // not owned (compression blocks nest in query blocks)
+    kc[o] = 0.f;
+    vc[o] = 0.f;
+    return;
+  }
+  const T* pek = static_cast<const T*>(c.pe_k);
+  const T* pev = static_cast<const T*>(c.pe_v);
+  const int m = c.m_cmp;
+  float sk = 0.f, sv = 0.f;
+  for (int p = t0; p < t1; ++p) {
+    const int64_t idx = ((int64_t(p) - row_base) * c.h_kv + g) * c.D + e;
+    float kk = ld(k + idx), vv = ld(v + idx);
+    if (pek || pev) {
+      const int4 cc = reinterpret_cast<const int4*>(c.sorted_coords)[p];
+      const int loc = ((cc.y % m) * m + (cc.z % m)) * m + (cc.w % m);
+      const int64_t pi = (int64_t(loc) * c.h_kv + g) * c.D + e;
+      if (pek) kk += ld(pek + pi);
+      if (pev) vv += ld(pev + pi);
+    }
+    sk += kk;
+    sv += vv;
+  }
+  const float inv = 1.f / float(t1 - t0);
+  kc[o] = sk * inv;
+  vc[o] = sv * inv;
+}
+
+ssa_status pool_rows(const Ctx& c, bool bf16, const void* k, const void* v, float* kc, float* vc, cudaStream_t st) {
+  if (c.n_blk[SSA_LEVEL_CMP] == 0) return SSA_OK;
+  dim3 grid(c.n_blk[SSA_LEVEL_CMP], c.h_kv);
+  if (bf16)
+    k_pool_rows<__nv_bfloat16><<<grid, c.D, 0, st>>>(c, static_cast<const __nv_bfloat16*>(k),
+                                                      static_cast<const __nv_bfloat16*>(v), c.row_base, kc, vc);
+  else
+    k_pool_rows<float><<<grid, c.D, 0, st>>>(c, static_cast<const float*>(k), static_cast<const float*>(v), c.row_base, kc, vc);
+  SSA_LAUNCH_CHECK("k_pool_rows");
   return SSA_OK;
 }
 

@@ -11,7 +11,9 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D);
 size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc);
 // forward after gather + pool: compression attention + scores + top-k, selection + window attention,
 // gated combine (writes c.out and the saved state).
-ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st);
+// kv_ev: wait for it before the first read of raw k / v; gather_keys_late: the key gather (k, v ->
+// internal layout) has not been done yet and runs after the wait (pooled keys supplied by the caller)
+ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev = nullptr, bool gather_keys_late = false);
 // backward after gather + prologue + inverse CSR: fills dq_acc, dk_acc, dv_acc, dkc, dvc.
 ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st);
 }  // namespace ssa

@@ -61,6 +61,32 @@ __device__ __forceinline__ uint4 f32x8_to_h(const float* f, float s) {
   return make_uint4(h2_sat(f[0] * s, f[1] * s), h2_sat(f[2] * s, f[3] * s), h2_sat(f[4] * s, f[5] * s),
                     h2_sat(f[6] * s, f[7] * s));
 }
+// Power-of-two scale of the fp16 dO operands (a loss averaged over ~1e5 tokens gives dO of
+// ~1e-6 and below, where an unscaled fp16 copy loses bits or flushes to zero). s = 2^(2 - e) for
+// max|dO| in [2^e, 2^(e+1)) brings max|s dO| into [4, 8): every bf16 dO value with |x| >= 2^-20 max|dO|
+// converts exactly, and dP = (s dO) V^T keeps the fp16 headroom of unit-variance data. dO, w dO and
+// D_c are scaled by s in the row prologue; dq / dk / dv (and the compressed-key partials) are
+// multiplied by 1/s where they leave TMEM. s = 1 for a zero or non-finite maximum.
+__device__ __forceinline__ float do_pow2(const uint32_t* amax, bool inverse) {
+  const uint32_t bits = *amax;
+  const int e = int((bits >> 23) & 0xffu) - 127;
+  if (bits == 0u || e > 120 || e < -120) return 1.f;
+  const int k = inverse ? e - 2 : 2 - e;
+  return __int_as_float((k + 127) << 23);
+}
+// max |dO| over the caller's dout (bf16, 8 elements per thread; non-negative floats order as uint32)
+__global__ void k_do_absmax(const __nv_bfloat16* dout, int64_t n8, uint32_t* amax) {
+  uint32_t m = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(dout)[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m = max(m, max((w[j] << 16) & 0x7fff0000u, w[j] & 0x7fff0000u));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(amax, m);
+}
 // one thread per 8 consecutive elements (16-byte loads and stores; every count is a multiple of 64)
 // Row prologue of the backward, one pass over the query rows: 8 lanes per row (g, p, s) in plan order,
 // 8 elements each. Gathers q and dO straight from the caller's order (bf16), writes the fp16 MMA
@@ -75,12 +101,16 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
   const int rr = valid ? row : 0;
   const int s = rr % c.h_s, p = (rr / c.h_s) % c.N, g = rr / (c.h_s * c.N);
   const int h = g * c.h_s + s;
+  const bool owned = valid && p >= c.row_lo && p < c.row_hi;   // rows of other shards are never touched
   const int src_p = c.sorted_input ? p : c.perm[p];
   const int64_t so = (int64_t(src_p) * c.H + h) * kD + sub * 8, io = int64_t(rr) * kD + sub * 8;
-  float fq[8], fd[8];
-  bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.q) + so), fq);
-  bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dout) + so), fd);
+  float fq[8] = {}, fd[8] = {};
+  if (owned) {
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.q) + so), fq);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dout) + so), fd);
+  }
   const float* w = c.gs + int64_t(rr) * 3;
+  const float ds = do_pow2(c.do_amax, false);
   float acc[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
@@ -88,21 +118,21 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
     const float4 x = o[0], y = o[1];
     acc[b] = fd[0] * x.x + fd[1] * x.y + fd[2] * x.z + fd[3] * x.w + fd[4] * y.x + fd[5] * y.y + fd[6] * y.z + fd[7] * y.w;
   }
-  if (valid) {
+  if (owned) {
     *reinterpret_cast<uint4*>(q16 + io) = f32x8_to_h(fq, 1.f);
-    *reinterpret_cast<uint4*>(do16 + io) = f32x8_to_h(fd, 1.f);
+    *reinterpret_cast<uint4*>(do16 + io) = f32x8_to_h(fd, ds);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) *reinterpret_cast<uint4*>(dow + int64_t(b) * nrows * kD + io) = f32x8_to_h(fd, w[b]);
+    for (int b = 0; b < 3; ++b) *reinterpret_cast<uint4*>(dow + int64_t(b) * nrows * kD + io) = f32x8_to_h(fd, w[b] * ds);
   }
 #pragma unroll
   for (int o = 4; o; o >>= 1)
 #pragma unroll
     for (int b = 0; b < 3; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-  if (!valid || sub != 0) return;
+  if (!owned || sub != 0) return;
   if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;   // rows of other shards
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
-    c.Dd[b][rr] = w[b] * acc[b];
+    c.Dd[b][rr] = w[b] * acc[b] * ds;
     static_cast<__nv_bfloat16*>(c.dgates)[(int64_t(src_p) * c.H + h) * 3 + b] = __float2bfloat16_rn(acc[b]);
   }
 }
@@ -506,14 +536,15 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       tc_fence_before();
       mbar_arrive(&S->dq_empty[wg]);
       if (rvalid) {
+        const float osc = c.scale * do_pow2(c.do_amax, true);
         const int tok = t0 + r / c.h_s, hs = r % c.h_s;
         const int dst = c.sorted_input ? tok : c.perm[tok];
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
 #pragma unroll
         for (int e = 0; e < kD; e += 8)
           *reinterpret_cast<uint4*>(o + e) =
-              make_uint4(pack_bf16(v[e] * c.scale, v[e + 1] * c.scale), pack_bf16(v[e + 2] * c.scale, v[e + 3] * c.scale),
-                         pack_bf16(v[e + 4] * c.scale, v[e + 5] * c.scale), pack_bf16(v[e + 6] * c.scale, v[e + 7] * c.scale));
+              make_uint4(pack_bf16(v[e] * osc, v[e + 1] * osc), pack_bf16(v[e + 2] * osc, v[e + 3] * osc),
+                         pack_bf16(v[e + 4] * osc, v[e + 5] * osc), pack_bf16(v[e + 6] * osc, v[e + 7] * osc));
       }
     }
   }
@@ -964,7 +995,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
           o = (wg == 0 ? c.kv_part_k : c.kv_part_v) + idx;
         }
         const bool none = n_tiles == 0;
-        const float sc = wg == 0 ? c.scale : 1.f;
+        const float sc = (wg == 0 ? c.scale : 1.f) * do_pow2(c.do_amax, true);
 #pragma unroll
         for (int e = 0; e < kD; e += 4) {
           float4 v4;
@@ -1035,7 +1066,7 @@ static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T) {
 
 size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc) {
   // fp16 copies: q, dO, 3 x gate-scaled dO (rows), k, v (keys), K^cmp, V^cmp (n_cmp <= N)
-  size_t b = (size_t(5) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 7 * 256;
+  size_t b = (size_t(5) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 8 * 256;
   const int64_t nkeys = int64_t(n_slc) * h_kv;
   b += size_t(2 * nkeys + 2) * 4 + 512 + scan_ws_bytes(nkeys + 1);                  // item counts / offsets
   b += size_t(2) * kv_items_bound(n_slc, n_q, h_kv, T) * max_fill_slc * D * 4 + 512;  // partials
@@ -1062,6 +1093,15 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T);
   c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
+  uint32_t* amax = cw.take<uint32_t>(1);
+  c.do_amax = amax;
+  SSA_CUDA_TRY(cudaMemsetAsync(amax, 0, 4, st));
+  {
+    const int64_t n8 = int64_t(c.N) * c.H * kD / 8;
+    const unsigned blocks = unsigned(std::min<int64_t>((n8 + 255) / 256, 148 * 8));
+    k_do_absmax<<<std::max(1u, blocks), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(c.dout), n8, amax);
+    SSA_LAUNCH_CHECK("k_do_absmax");
+  }
   k_tc_bwd_rows<<<unsigned((int64_t(c.N) * c.H * 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow);
   SSA_LAUNCH_CHECK("k_tc_bwd_rows");
   const int64_t n = int64_t(krows) * kD;   // >= h_kv * n_cmp * kD

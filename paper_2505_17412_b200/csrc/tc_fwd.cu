@@ -80,12 +80,13 @@ struct TcArgs {
 };
 
 // K^cmp -> bf16 hi/lo pair, V^cmp -> fp16 (P.V runs in fp16), raw V -> fp16 copy (exact for bf16)
-__global__ void k_tc_prep(Ctx c, __nv_bfloat16* kc_hi, __nv_bfloat16* kc_lo, __half* vc16, __half* vs16) {
+// part: 1 = pooled keys only (K^cmp hi/lo, V^cmp fp16), 2 = raw values only (V fp16), 3 = both
+__global__ void k_tc_prep(Ctx c, __nv_bfloat16* kc_hi, __nv_bfloat16* kc_lo, __half* vc16, __half* vs16, int part) {
   // 4 elements per thread (every array is a multiple of 64 long and 256-B aligned)
   const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   const int64_t n = int64_t(c.h_kv) * c.n_blk[SSA_LEVEL_CMP] * kD;
   const int64_t nv = int64_t(c.h_kv) * c.N * kD;
-  if (i < n) {
+  if ((part & 1) && i < n) {
     const float4 k = *reinterpret_cast<const float4*>(static_cast<const float*>(c.kc) + i);
     const float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(c.vc) + i);
     const float kk[4] = {k.x, k.y, k.z, k.w};
@@ -100,7 +101,7 @@ __global__ void k_tc_prep(Ctx c, __nv_bfloat16* kc_hi, __nv_bfloat16* kc_lo, __h
     const __half2 v01 = __floats2half2_rn(v.x, v.y), v23 = __floats2half2_rn(v.z, v.w);
     *reinterpret_cast<uint2*>(vc16 + i) = make_uint2(*reinterpret_cast<const uint32_t*>(&v01), *reinterpret_cast<const uint32_t*>(&v23));
   }
-  if (i < nv) {
+  if ((part & 2) && i < nv) {
     const uint2 b = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(c.vs) + i);
     const __nv_bfloat162 b01 = *reinterpret_cast<const __nv_bfloat162*>(&b.x), b23 = *reinterpret_cast<const __nv_bfloat162*>(&b.y);
     const float2 f01 = __bfloat1622float2(b01), f23 = __bfloat1622float2(b23);
@@ -961,7 +962,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       tc_fence_before();
       mbar_arrive(&S->o_empty[wg]);
       if (rvalid) {
-        c.lse[1][row] = lse_slc;
+        if (n_slc_tiles > 0) c.lse[1][row] = lse_slc;   // window-only: keep the "no keys" sentinel (api.cu)
         c.lse[2][row] = m + lg2(l);
       }
       __syncwarp();
@@ -1022,7 +1023,7 @@ bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
          (info.max_fill[SSA_LEVEL_SLC] + 127) / 128 <= 4 * 64 + 8;
 }
 
-ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
+ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev, bool gather_keys_late) {
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
   Carve cw(ws, tc_fwd_ws_bytes(c.N, c.H, c.h_kv, c.D));
   __nv_bfloat16* kc_hi = cw.take<__nv_bfloat16>(size_t(c.h_kv) * n_cmp * kD);
@@ -1030,7 +1031,15 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
   __half* vc = cw.take<__half>(size_t(c.h_kv) * n_cmp * kD);
   __half* vs16 = cw.take<__half>(size_t(c.h_kv) * c.N * kD);
   const int64_t n = int64_t(c.h_kv) * c.N * kD;   // >= h_kv * n_cmp * kD
-  k_tc_prep<<<unsigned((n / 4 + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16);
+  // raw k / v pending (cfg.kv_event, sharded mode 2): only the pooled keys are prepared before the
+  // compression kernel; the wait, the key gather and the V conversion follow it
+  const bool split = kv_ev != nullptr || gather_keys_late;
+  if (split) {
+    const int64_t nc = int64_t(c.h_kv) * n_cmp * kD;
+    k_tc_prep<<<unsigned(std::max<int64_t>(1, (nc / 4 + 255) / 256)), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16, 1);
+  } else {
+    k_tc_prep<<<unsigned((n / 4 + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16, 3);
+  }
   SSA_LAUNCH_CHECK("k_tc_prep");
   CUtensorMap tmQ, tmKh, tmKl, tmVc;
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
@@ -1049,6 +1058,15 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st) {
       k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
       SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
     }
+  }
+  if (split) {
+    if (kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
+    if (gather_keys_late) {
+      ssa_status s = gather_inputs(c, true, st, false, /*rows=*/false, /*keys=*/true, /*gates=*/false);
+      if (s != SSA_OK) return s;
+    }
+    k_tc_prep<<<unsigned((n / 4 + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16, 2);
+    SSA_LAUNCH_CHECK("k_tc_prep(v)");
   }
   {
     const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);

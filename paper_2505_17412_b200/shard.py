@@ -1,9 +1,13 @@
-"""Host-side multi-GPU orchestration for SSA (no data-path collective).
+"""Host-side multi-GPU orchestration for SSA.
 
-SSA has no parameters and the shapes of a batch never interact (SURVEY §8e mode 1), so N GPUs process
-disjoint subsets of the shapes; torch.distributed is used only for the timing barrier and the
-max-over-ranks reduction. Shapes are dealt by LPT on a cost model ~ n_tokens^2 (the compression
-branch dominates and is quadratic in the token count).
+Mode 1 (batch of shapes): SSA has no parameters and the shapes of a batch never interact, so N GPUs
+process disjoint subsets of the shapes with no data-path collective; torch.distributed is used only for
+the timing barrier and the max-over-ranks reduction. Shapes are dealt by LPT on a cost model
+~ n_tokens^2 (the compression branch dominates and is quadratic in the token count).
+Mode 2 (one large shape): query blocks sharded over ranks (ssa_step_sharded) with the path's real
+exchange steps: pooled-key all-reduce, K/V all-gather (overlapped with the compression branch) and the
+dK/dV reduce-scatter.
+Hybrid (C4 at scale): hybrid_plan splits the largest shapes of a batch over sub-groups of ranks.
 """
 from __future__ import annotations
 
@@ -60,40 +64,171 @@ def balanced_q_ranges(q_offsets, world: int):
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
-def ssa_step_sharded(plan, cfg, q_sorted, k_local, v_local, gates_sorted, dout_sorted, tok_ranges, rank, group=None):
-    """Forward + backward of one shape sharded by query blocks (NCCL / any torch.distributed group).
+def _backend(group):
+    import torch.distributed as dist
+    return dist.get_backend(group) if dist.is_initialized() else "none"
 
-    Inputs are in plan (block-sorted) order. k_local / v_local hold this rank's token range
-    tok_ranges[rank] (padded to the largest range); q / gates / dout are full-size buffers of which only
-    the owned rows are read. Returns (out, dq, dk_local, dv_local, dgates): out / dq / dgates are valid on
-    the owned rows, dk_local / dv_local are this rank's tokens' complete gradients.
-    Collectives: one all-gather of K and V (forward), one all-reduce of the dK / dV partials (backward).
-    """
-    import dataclasses
+
+def all_gather_rows(full, local, tok_ranges, rank, group=None):
+    """full[a_r:b_r] = rank r's `local` rows for every rank r (one padded all-gather; gloo groups stage
+    through host memory). full: [N, ...] on local's device."""
     import torch
     import torch.distributed as dist
-    from . import ssa
     world = len(tok_ranges)
     pad = max(b - a for a, b in tok_ranges)
-    shape = (world * pad,) + tuple(k_local.shape[1:])
-    k_all = torch.empty(shape, dtype=k_local.dtype, device=k_local.device)
-    v_all = torch.empty_like(k_all)
-    if world == 1:
-        k_all.copy_(k_local)
-        v_all.copy_(v_local)
-    else:
-        dist.all_gather_into_tensor(k_all, k_local.contiguous(), group=group)
-        dist.all_gather_into_tensor(v_all, v_local.contiguous(), group=group)
-    k = torch.cat([k_all[r * pad: r * pad + (b - a)] for r, (a, b) in enumerate(tok_ranges)])
-    v = torch.cat([v_all[r * pad: r * pad + (b - a)] for r, (a, b) in enumerate(tok_ranges)])
-    qo = plan.offsets(ssa.LEVEL_Q).cpu().tolist()
-    qb = [qo.index(a) for a, _ in tok_ranges] + [len(qo) - 1]
-    c2 = dataclasses.replace(cfg, flags=cfg.flags | ssa.SSA_INPUT_SORTED | ssa.SSA_KV_GRAD_FP32,
-                             q_begin=qb[rank], q_end=qb[rank + 1])
-    out, saved = ssa.ssa_forward(plan, c2, q_sorted, k, v, gates_sorted)
-    dq, dk, dv, dg = ssa.ssa_backward(plan, c2, saved, q_sorted, k, v, gates_sorted, dout_sorted)
-    if world > 1:
-        dist.all_reduce(dk, group=group)      # fp32 partials (SSA_KV_GRAD_FP32)
-        dist.all_reduce(dv, group=group)
     a, b = tok_ranges[rank]
-    return out, dq, dk[a:b].to(k_local.dtype), dv[a:b].to(k_local.dtype), dg
+    if world == 1:
+        full[a:b].copy_(local)
+        return full
+    send = torch.zeros((pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    send[:b - a] = local
+    if _backend(group) == "nccl":
+        got = torch.empty((world * pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(got, send, group=group)
+    else:
+        parts = [torch.empty_like(send, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, send.cpu(), group=group)
+        got = torch.cat(parts).to(local.device)
+    for r, (x, y) in enumerate(tok_ranges):
+        full[x:y] = got[r * pad: r * pad + (y - x)]
+    return full
+
+
+def reduce_scatter_rows(full, tok_ranges, rank, group=None):
+    """Sum over ranks of full[a_r:b_r] for this rank's range (one padded reduce-scatter; gloo groups stage
+    through host memory with an all-reduce)."""
+    import torch
+    import torch.distributed as dist
+    world = len(tok_ranges)
+    a, b = tok_ranges[rank]
+    if world == 1:
+        return full[a:b].clone()
+    pad = max(y - x for x, y in tok_ranges)
+    send = torch.zeros((world * pad,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+    for r, (x, y) in enumerate(tok_ranges):
+        send[r * pad: r * pad + (y - x)] = full[x:y]
+    if _backend(group) == "nccl":
+        out = torch.empty((pad,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+        dist.reduce_scatter_tensor(out, send, group=group)
+    else:
+        h = send.cpu()
+        dist.all_reduce(h, group=group)
+        out = h[rank * pad:(rank + 1) * pad].to(full.device)
+    return out[:b - a]
+
+
+def all_reduce_sum(t, group=None):
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return t
+    if _backend(group) == "nccl":
+        dist.all_reduce(t, group=group)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    return t
+
+
+def shard_ranges(plan, world: int):
+    """(query-block ranges, token ranges) of the `world` shards of one plan (every rank computes the
+    same from the same plan)."""
+    qo = plan.q_offsets_host()
+    rng = balanced_q_ranges(qo, world)
+    return rng, [(int(qo[a]), int(qo[b])) for a, b in rng]
+
+
+def ssa_step_sharded(plan, cfg, q_loc, k_loc, v_loc, gates_loc, dout_loc, rank, world, group=None,
+                     comm_stream=None, q_ranges=None):
+    """Forward + backward of ONE shape with its query blocks sharded over `world` ranks (SURVEY §8e
+    mode 2). Every rank built the same plan; rank r holds only its own rows (plan order, tokens
+    shard_ranges(plan, world)[1][r]) of q, k, v, gates, dout. Data path:
+      1. ssa_pool of the owned compression blocks (compression blocks nest in query blocks), summed
+         over ranks (all-reduce, 2 x h_kv x n_cmp x d fp32 — 5 MB at C3);
+      2. raw K/V all-gather on `comm_stream`, recorded in an event the forward waits on right before
+         the selection / window branch, so the exchange overlaps the compression attention (a4/a5);
+      3. forward and backward for the owned rows only (SSA_LOCAL_ROWS); dk, dv come back as fp32
+         partials over every token (SSA_KV_GRAD_FP32) and are reduce-scattered to their owners.
+    q_ranges: optional explicit query-block range of every rank of the group (hybrid_plan); default
+    balanced by tokens. Returns (out, dq, dk, dv, dgates) for the owned rows (dk, dv in k_loc's dtype)."""
+    import dataclasses
+    import torch
+    from . import ssa
+    if q_ranges is None:
+        q_rng, tok = shard_ranges(plan, world)
+    else:
+        qo = plan.q_offsets_host()
+        q_rng = [tuple(x) for x in q_ranges]
+        tok = [(int(qo[a]), int(qo[b])) for a, b in q_rng]
+    qb, qe = q_rng[rank]
+    c2 = dataclasses.replace(cfg, flags=cfg.flags | ssa.SSA_INPUT_SORTED | ssa.SSA_KV_GRAD_FP32 | ssa.SSA_LOCAL_ROWS,
+                             q_begin=qb, q_end=qe)
+    dev = q_loc.device
+    cur = torch.cuda.current_stream(dev)
+    kc, vc = ssa.ssa_pool(plan, c2, k_loc, v_loc)
+    all_reduce_sum(kc, group)
+    all_reduce_sum(vc, group)
+    comm = comm_stream or torch.cuda.Stream(dev)
+    comm.wait_stream(cur)                          # k_loc / v_loc are ready
+    ev = torch.cuda.Event()
+    with torch.cuda.stream(comm):
+        k = torch.empty((plan.n,) + tuple(k_loc.shape[1:]), dtype=k_loc.dtype, device=dev)
+        v = torch.empty_like(k)
+        all_gather_rows(k, k_loc, tok, rank, group)
+        all_gather_rows(v, v_loc, tok, rank, group)
+        ev.record(comm)
+    k.record_stream(cur)
+    v.record_stream(cur)
+    cf = dataclasses.replace(c2, kc_in=kc, vc_in=vc, kv_event=ev)
+    out, saved = ssa.ssa_forward(plan, cf, q_loc, k, v, gates_loc)
+    dq, dk, dv, dg = ssa.ssa_backward(plan, c2, saved, q_loc, k, v, gates_loc, dout_loc)
+    dk_loc = reduce_scatter_rows(dk, tok, rank, group)
+    dv_loc = reduce_scatter_rows(dv, tok, rank, group)
+    return out, dq, dk_loc.to(k_loc.dtype), dv_loc.to(k_loc.dtype), dg
+
+
+# ---------------------------------------------------------------------------------------------------
+# Hybrid placement (SURVEY §8e: "near-linear scaling to 8 needs hybrid splitting"). The query blocks of
+# all shapes of the batch are laid end to end on one cost line (a query block of shape b costs
+# ~ tokens(Q) * n_b: its rows against the n_b / m_cmp^3 compressed keys of its shape, the dominant
+# compression branch) and the line is cut into `world` contiguous pieces of equal cost. A rank whose
+# piece covers a shape entirely runs it whole (mode 1, no collective); a shape cut by one or more
+# piece boundaries is sharded by query blocks (mode 2, ssa_step_sharded) over the contiguous sub-group
+# of ranks that hold a piece of it, with unequal ranges.
+# ---------------------------------------------------------------------------------------------------
+def hybrid_plan(q_tokens, world: int):
+    """q_tokens: per shape, the token counts of its query blocks (plan order). Returns one list per rank
+    of (shape, q_begin, q_end, group) with group = the ascending tuple of ranks that share the shape
+    (length 1: the shape runs whole on this rank). Deterministic: every rank computes the same plan."""
+    import numpy as np
+    n_tok = [int(np.sum(t)) for t in q_tokens]
+    w = [np.asarray(t, np.float64) * n for t, n in zip(q_tokens, n_tok)]
+    total = float(sum(x.sum() for x in w))
+    out = [[] for _ in range(world)]
+    if world <= 1 or total <= 0:
+        out[0] = [(s, 0, len(t), (0,)) for s, t in enumerate(q_tokens)]
+        return out
+    pieces = {}          # shape -> {rank: [q_begin, q_end)}
+    acc = 0.0
+    for s, ws in enumerate(w):
+        for Q, x in enumerate(ws):
+            r = min(world - 1, int((acc + 0.5 * x) / total * world))   # rank of the block's cost midpoint
+            acc += x
+            rng = pieces.setdefault(s, {}).setdefault(r, [Q, Q + 1])
+            rng[1] = Q + 1
+        if not len(ws):
+            pieces.setdefault(s, {})[min(world - 1, int(acc / total * world))] = [0, 0]
+    for s in range(len(q_tokens)):
+        grp = tuple(sorted(pieces[s]))
+        for r in grp:
+            a, b = pieces[s][r]
+            out[r].append((s, a, b, grp))
+    return out
+
+
+def hybrid_makespan(q_tokens, plan):
+    """Modelled cost (same model as hybrid_plan) of the busiest rank of a plan."""
+    import numpy as np
+    n_tok = [int(np.sum(t)) for t in q_tokens]
+    return max((sum(float(np.sum(np.asarray(q_tokens[s][a:b], np.float64))) * n_tok[s] for s, a, b, _ in items)
+                for items in plan), default=0.0)

@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa_b200.so"))   # SSA_LIB: debug builds only
 
 SSA_F32, SSA_BF16 = 0, 1
-SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32, SSA_WINDOW_ONLY = 1, 2, 4, 8, 16
+SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32, SSA_WINDOW_ONLY, SSA_LOCAL_ROWS = 1, 2, 4, 8, 16, 32
 LEVEL_CMP, LEVEL_SLC, LEVEL_WIN, LEVEL_Q = 0, 1, 2, 3
 STATUS = ["SSA_OK", "SSA_ERR_ARG", "SSA_ERR_DUP_COORD", "SSA_ERR_COORD_RANGE", "SSA_ERR_HIERARCHY",
           "SSA_ERR_BAD_STATE", "SSA_ERR_WORKSPACE", "SSA_ERR_UNSUPPORTED", "SSA_ERR_CUDA"]
@@ -49,7 +49,8 @@ class AttnCfgC(ctypes.Structure):
     _fields_ = [("h_q", ctypes.c_int32), ("h_kv", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p),
-                ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32)]
+                ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32), ("kc_in", ctypes.c_void_p),
+                ("vc_in", ctypes.c_void_p), ("kv_event", ctypes.c_void_p)]
 
 
 class SavedView(ctypes.Structure):
@@ -77,6 +78,7 @@ SIGNATURES = {
     "ssa_backward_size": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _SZ]),
     "ssa_backward": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P, _P,
                                     _P, _P, _P, ctypes.c_size_t, _P]),
+    "ssa_pool": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P]),
     "ssa_saved_state": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, ctypes.c_size_t,
                                        ctypes.POINTER(SavedView)]),
     "ssa_status_str": (ctypes.c_char_p, [ctypes.c_int]),
@@ -165,6 +167,12 @@ class Plan:
     def offsets(self, level: int):
         return self._i32(self.info.offsets[level], self.n_blocks[level] + 1)
 
+    def q_offsets_host(self):
+        """Query-block token offsets on the host (cached; one device read)."""
+        if getattr(self, "_q_off", None) is None:
+            self._q_off = self.offsets(LEVEL_Q).cpu().numpy()
+        return self._q_off
+
     def block_coords(self, level: int):
         return self._i32(self.info.block_coords[level], 4 * self.n_blocks[level]).view(-1, 4)
 
@@ -214,11 +222,17 @@ class AttnCfg:
     pe_v: torch.Tensor | None = None
     q_begin: int = 0            # query-block shard [q_begin, q_end) in plan order; q_end <= 0: all
     q_end: int = 0
+    kc_in: torch.Tensor | None = None    # caller-supplied pooled keys / values, fp32 [h_kv, n_cmp, d]
+    vc_in: torch.Tensor | None = None
+    kv_event: torch.cuda.Event | None = None   # raw k / v ready (recorded after a K/V all-gather)
 
     def c(self) -> AttnCfgC:
+        def ptr(t):
+            return t.data_ptr() if t is not None else None
+        ev = self.kv_event.cuda_event if self.kv_event is not None else None
         return AttnCfgC(self.h_q, self.h_kv, self.d, self.top_k, float(self.scale), _dtype_code(self.dtype),
-                        int(self.flags), self.pe_k.data_ptr() if self.pe_k is not None else None,
-                        self.pe_v.data_ptr() if self.pe_v is not None else None, int(self.q_begin), int(self.q_end))
+                        int(self.flags), ptr(self.pe_k), ptr(self.pe_v), int(self.q_begin), int(self.q_end),
+                        ptr(self.kc_in), ptr(self.vc_in), ev)
 
 
 class Saved:
@@ -264,11 +278,22 @@ class Saved:
                 self._slice(self.view.v_cmp, self.cfg.h_kv * nc * self.cfg.d, torch.float32).view(self.cfg.h_kv, nc, self.cfg.d))
 
 
+def owned_rows(plan: Plan, cfg: AttnCfg):
+    """(first, end) plan-order rows of cfg's query-block range (all rows without a range)."""
+    if cfg.q_end <= 0:
+        return 0, plan.n
+    off = plan.q_offsets_host()
+    return int(off[cfg.q_begin]), int(off[cfg.q_end])
+
+
 def _check_inputs(plan: Plan, cfg: AttnCfg, q, k, v, gates):
     n = plan.n
-    if tuple(q.shape) != (n, cfg.h_q, cfg.d) or tuple(k.shape) != (n, cfg.h_kv, cfg.d) or \
-            tuple(v.shape) != (n, cfg.h_kv, cfg.d) or tuple(gates.shape) != (n, cfg.h_q, 3):
-        raise ValueError("shape mismatch: q [N,h_q,d], k/v [N,h_kv,d], gates [N,h_q,3]")
+    a, b = owned_rows(plan, cfg) if cfg.flags & SSA_LOCAL_ROWS else (0, n)
+    nr = b - a
+    if tuple(q.shape) != (nr, cfg.h_q, cfg.d) or tuple(k.shape) != (n, cfg.h_kv, cfg.d) or \
+            tuple(v.shape) != (n, cfg.h_kv, cfg.d) or tuple(gates.shape) != (nr, cfg.h_q, 3):
+        raise ValueError("shape mismatch: q [N,h_q,d], k/v [N,h_kv,d], gates [N,h_q,3] "
+                         "(q, gates: owned rows only with SSA_LOCAL_ROWS)")
     for t in (q, k, v, gates):
         if t.dtype != cfg.dtype:
             raise ValueError(f"tensor dtype {t.dtype} != cfg.dtype {cfg.dtype}")
@@ -290,7 +315,11 @@ _default_ws = {}
 
 
 def _ws(device, key):
-    return _default_ws.setdefault((str(device), key), Workspace())
+    """Per (device, stream) scratch: calls on different streams never share (or free) each other's
+    buffer, and a buffer replaced on growth was only ever used on its own stream, so the caching
+    allocator's stream-ordered reuse is safe."""
+    sid = torch.cuda.current_stream(device).cuda_stream
+    return _default_ws.setdefault((str(device), sid, key), Workspace())
 
 
 def ssa_forward(plan: Plan, cfg: AttnCfg, q, k, v, gates, out=None, saved: Saved | None = None,
@@ -311,6 +340,20 @@ def ssa_forward(plan: Plan, cfg: AttnCfg, q, k, v, gates, out=None, saved: Saved
                          _dev(gates, "gates"), _dev(out, "out"), ctypes.c_void_p(saved.buf.data_ptr()),
                          saved.buf.numel(), ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_forward")
     return out, saved
+
+
+def ssa_pool(plan: Plan, cfg: AttnCfg, k, v, kc=None, vc=None):
+    """C: ssa_pool. Pooled keys / values (Eq. 7) fp32 [h_kv, n_cmp, d] of the compression blocks inside
+    the owned rows (all blocks without a query-block range); other blocks are 0. k, v in plan order
+    (SSA_INPUT_SORTED), the owned rows only with SSA_LOCAL_ROWS."""
+    nc = plan.n_blocks[LEVEL_CMP]
+    if kc is None:
+        kc = torch.empty(cfg.h_kv, nc, cfg.d, dtype=torch.float32, device=k.device)
+        vc = torch.empty_like(kc)
+    cc = cfg.c()
+    _check(lib().ssa_pool(plan.handle, ctypes.byref(cc), _dev(k, "k"), _dev(v, "v"), _dev(kc, "kc"), _dev(vc, "vc"),
+                          _stream(k.device)), "ssa_pool")
+    return kc, vc
 
 
 def ssa_backward(plan: Plan, cfg: AttnCfg, saved: Saved, q, k, v, gates, dout, grads=None,

@@ -27,3 +27,16 @@ def random_coords(rng, n, G, batch=1):
 @pytest.fixture
 def rng():
     return np.random.Generator(np.random.PCG64(1234))
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the per-tensor parity report (tests/gpu_util.REPORT) when SSA_PARITY_REPORT is set."""
+    path = os.environ.get("SSA_PARITY_REPORT")
+    mod = sys.modules.get("gpu_util")
+    if not path or mod is None or not mod.REPORT:
+        return
+    import json
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump({"metric": "max|x-ref|/rms(ref), undiscounted; LSE: max|x-ref| (natural log)",
+                   "rows": mod.REPORT}, f, indent=1)

@@ -13,19 +13,34 @@ def to_dev(x, dtype):
     return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype=dtype)
 
 
-def rel_err(x, ref, u=0.0):
-    """max(|x - ref| - u*|ref|) / rms(ref) — SURVEY §8c parity metric (relative to unit-variance data).
-
-    u is the unit roundoff of the OUTPUT format (2^-8 for bf16 round-to-nearest, 0 for fp32): a bf16
-    output cannot be closer to the exact value than its own rounding, so that part of the difference
-    is not charged to the kernel's arithmetic (reading R16)."""
+def rel_err(x, ref):
+    """max|x - ref| / rms(ref) — SURVEY §8c parity metric, the north star's "max-abs error relative to
+    unit-variance data", with no discount: the bf16 rounding of the kernel's own output is charged to
+    the kernel. A reference that is analytically zero (rms < 1e-6) is compared in absolute terms."""
     x = np.asarray(x, np.float64)
     ref = np.asarray(ref, np.float64)
     if not ref.size:
         return 0.0
     rms = float(np.sqrt(np.mean(ref * ref)))
-    err = float(np.max(np.maximum(np.abs(x - ref) - u * np.abs(ref), 0.0)))
-    return err / rms if rms > 1e-6 else err        # an (analytically) zero reference: absolute error
+    err = float(np.max(np.abs(x - ref)))
+    return err / rms if rms > 1e-6 else err
+
+
+# Per-tensor parity report (undiscounted): every comparison made through `record` is kept here and
+# written as JSON at the end of the session when SSA_PARITY_REPORT names a file (tests/conftest.py).
+REPORT = []
+
+
+def record(test, name, x, ref, tol, **extra):
+    """rel_err + a report row {test, tensor, max_abs, rms_ref, rel, tol, pass}; returns rel."""
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    rel = rel_err(x, ref)
+    REPORT.append(dict(test=test, tensor=name, n=int(ref.size),
+                       max_abs=float(np.max(np.abs(x - ref))) if ref.size else 0.0,
+                       rms_ref=float(np.sqrt(np.mean(ref * ref))) if ref.size else 0.0,
+                       rel=rel, tol=tol, ok=bool(rel <= tol), **extra))
+    return rel
 
 
 def internal_to_orig(t_internal: torch.Tensor, perm: np.ndarray):

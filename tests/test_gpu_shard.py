@@ -49,3 +49,124 @@ def test_virtual_ranks(force_simt):
         # fp32 summation-order differences
         err = ((got - ref).abs() - 2.0 ** -8 * ref.abs()).clamp_min(0).max().item() / ref.pow(2).mean().sqrt().item()
         assert err < 1e-3, err
+
+
+def _c2_sorted(seed=11):
+    import torch
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import config_coords, make_inputs
+    c, grid, batch = config_coords("C2")
+    inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=seed)
+    dev = torch.device("cuda")
+    plan = ssa.ssa_build_blocks(torch.from_numpy(c).to(dev), grid, batch, 4, 8, 8, 8)
+    perm = plan.perm().cpu().numpy()
+    t = [torch.from_numpy(x[perm]).to(dev, dtype=torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
+    return plan, t
+
+
+def test_local_rows_pool_and_kv_event():
+    """Mode-2 data path on one GPU with virtual ranks, exactly as ssa_step_sharded drives it but with the
+    collectives replaced by sums / concatenation: ssa_pool of each rank's own rows (SSA_LOCAL_ROWS), the
+    pooled keys summed over ranks and passed as kc_in / vc_in, the raw K/V produced on a side stream and
+    signalled through kv_event, forward + backward on local row tensors. Owned rows of out / dq / dgates
+    are bit-identical to the unsharded run; the summed dk / dv partials match it up to fp32 order."""
+    import dataclasses
+    import torch
+    from paper_2505_17412_b200 import ssa
+    from paper_2505_17412_b200.shard import shard_ranges
+    plan, (q, k, v, g, do) = _c2_sorted()
+    base = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=ssa.SSA_INPUT_SORTED)
+    out0, saved0 = ssa.ssa_forward(plan, base, q, k, v, g)
+    ref = [x.clone() for x in ssa.ssa_backward(plan, base, saved0, q, k, v, g, do)]
+    out0 = out0.clone()
+    q_rng, tok = shard_ranges(plan, 3)
+    flags = base.flags | ssa.SSA_KV_GRAD_FP32 | ssa.SSA_LOCAL_ROWS
+    cfgs = [dataclasses.replace(base, flags=flags, q_begin=a, q_end=b) for a, b in q_rng]
+    kc = torch.zeros(2, plan.n_blocks[ssa.LEVEL_CMP], 64, device="cuda")
+    vc = torch.zeros_like(kc)
+    for cr, (a, b) in zip(cfgs, tok):
+        pk, pv = ssa.ssa_pool(plan, cr, k[a:b].contiguous(), v[a:b].contiguous())
+        kc += pk
+        vc += pv
+    kc0, vc0 = saved0.k_cmp()
+    assert torch.equal(kc, kc0) and torch.equal(vc, vc0)          # same summation order as the full pool
+    dk = torch.zeros(k.shape, dtype=torch.float32, device="cuda")
+    dv = torch.zeros_like(dk)
+    side = torch.cuda.Stream()
+    for cr, (a, b) in zip(cfgs, tok):
+        ev = torch.cuda.Event()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):                              # "all-gather" of K/V on a side stream
+            kk, vv = k.clone(), v.clone()
+            ev.record(side)
+        kk.record_stream(torch.cuda.current_stream())
+        vv.record_stream(torch.cuda.current_stream())
+        cf = dataclasses.replace(cr, kc_in=kc, vc_in=vc, kv_event=ev)
+        o, sv = ssa.ssa_forward(plan, cf, q[a:b].contiguous(), kk, vv, g[a:b].contiguous())
+        gq, gk, gv, gg = ssa.ssa_backward(plan, cr, sv, q[a:b].contiguous(), kk, vv, g[a:b].contiguous(),
+                                          do[a:b].contiguous())
+        assert torch.equal(o, out0[a:b]) and torch.equal(gq, ref[0][a:b]) and torch.equal(gg, ref[3][a:b])
+        dk += gk
+        dv += gv
+    for got, want in ((dk, ref[1].float()), (dv, ref[2].float())):
+        err = ((got - want).abs() - 2.0 ** -8 * want.abs()).clamp_min(0).max().item() / want.pow(2).mean().sqrt().item()
+        assert err < 1e-3, err
+
+
+def _proc(rank, world, port, path):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_17412_b200.shard import shard_ranges, ssa_step_sharded
+    from paper_2505_17412_b200 import ssa
+    plan, (q, k, v, g, do) = _c2_sorted()
+    cfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16)
+    _, tok = shard_ranges(plan, world)
+    a, b = tok[rank]
+    loc = [x[a:b].contiguous() for x in (q, k, v, g, do)]
+    res = ssa_step_sharded(plan, cfg, *loc, rank=rank, world=world)
+    torch.cuda.synchronize()
+    torch.save([x.cpu() for x in res] + [torch.tensor([a, b])], f"{path}/r{rank}.pt")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_process_sharded_step(tmp_path):
+    """ssa_step_sharded end to end in two processes (gloo on one GPU; the driver's boxes have one GPU):
+    per-rank inputs (own rows of q, k, v, gates, dO only), pooled-key all-reduce, K/V all-gather on a side
+    stream overlapping the compression branch, dK/dV reduce-scatter. Each rank's out / dq / dgates equal
+    the unsharded run's rows bit for bit; its dk / dv rows match up to fp32 summation order."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2505_17412_b200 import ssa
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    ps = [ctx.Process(target=_proc, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    plan, (q, k, v, g, do) = _c2_sorted()
+    base = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=ssa.SSA_INPUT_SORTED)
+    out0, saved0 = ssa.ssa_forward(plan, base, q, k, v, g)
+    ref = ssa.ssa_backward(plan, base, saved0, q, k, v, g, do)
+    torch.cuda.synchronize()
+    covered = 0
+    for r in range(2):
+        o, dq, dk, dv, dg, ab = torch.load(f"{tmp_path}/r{r}.pt")
+        a, b = ab.tolist()
+        covered += b - a
+        assert torch.equal(o, out0[a:b].cpu()) and torch.equal(dq, ref[0][a:b].cpu()) and torch.equal(dg, ref[3][a:b].cpu())
+        for got, want in ((dk, ref[1][a:b].cpu()), (dv, ref[2][a:b].cpu())):
+            got, want = got.float(), want.float()
+            # both sides rounded to bf16 from fp32 sums taken in different orders: one bf16 ulp
+            assert bool(((got - want).abs() <= 2.0 ** -7 * want.abs() + 1e-4 * want.pow(2).mean().sqrt()).all())
+    assert covered == plan.n

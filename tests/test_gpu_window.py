@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import oracle as O
-from gpu_util import rel_err, to_dev
+from gpu_util import record, to_dev
 from paper_2505_17412_b200 import ssa
 from ssa_workload import batch_coords, make_inputs, sphere_shell
 
@@ -50,8 +50,8 @@ def test_window_attention(shift, window_only):
     dq, dk, dv = ssa.window_attention_backward(ctx, q, k, v, do)
     torch.cuda.synchronize()
     ref = _reference(coords, inp.q, inp.k, inp.v, inp.dout, 2, 8, shift)
-    u = 2.0 ** -8
-    errs = {n: rel_err(x.float().cpu().numpy().astype(np.float64), r, u)
+    test = f"test_window_attention[shift={shift},window_only={window_only}]"
+    errs = {n: record(test, n, x.float().cpu().numpy().astype(np.float64), r, 2e-2)
             for n, x, r in zip(("out", "dq", "dk", "dv"), (out, dq, dk, dv), ref)}
     assert all(e <= 2e-2 for e in errs.values()), errs
 
@@ -68,7 +68,8 @@ def test_window_covering_grid_is_full_attention():
     ref = np.zeros_like(inp.q)
     for h in range(H):
         ref[:, h] = O.dense_attention(inp.q[:, h], inp.k[:, h // 4], inp.v[:, h // 4], 1.0 / math.sqrt(d))[0]
-    assert rel_err(out.float().cpu().numpy().astype(np.float64), ref, 2.0 ** -8) <= 2e-2
+    assert record("test_window_covering_grid_is_full_attention", "out", out.float().cpu().numpy().astype(np.float64),
+                  ref, 2e-2) <= 2e-2
 
 
 def test_window_only_skips_branches_and_matches_composition():
@@ -91,4 +92,7 @@ def test_window_only_skips_branches_and_matches_composition():
     assert res[False][1] == {"tc_cmp_fwd": 1, "tc_bwd_cmp_kv": 1}
     assert res[True][1] == {"tc_cmp_fwd": 0, "tc_bwd_cmp_kv": 0}
     for a, b in zip(res[True][0], res[False][0]):
-        assert torch.equal(a, b) or rel_err(a.float().cpu().numpy(), b.float().cpu().numpy().astype(np.float64), 2.0 ** -8) <= 1e-3
+        # GPU vs GPU (same kernels; the window-only run may differ by one bf16 ulp where a skipped
+        # branch's exact zero changes an fp32 rounding): |a - b| <= 2^-8 |b| element-wise
+        a, b = a.float(), b.float()
+        assert torch.equal(a, b) or bool(((a - b).abs() <= 2.0 ** -8 * b.abs()).all())

@@ -225,3 +225,96 @@ def test_window_locality(rng):
     q2[outside] = 0
     f2 = O.ssa_forward(c, (8, 8, 8), 1, q2, k2, v2, gates, **kw)
     assert np.allclose(f1.o["win"][t], f2.o["win"][t], atol=1e-14)
+
+
+def _blocks_from_coords(coords, m):
+    """Pure-python grouping of token indices by (b, x//m, y//m, z//m) — independent of block_build."""
+    groups = {}
+    for i, (b, x, y, z) in enumerate(np.asarray(coords).tolist()):
+        groups.setdefault((b, x // m, y // m, z // m), []).append(i)
+    return groups
+
+
+def test_eq8_triple_loop_multi_block(rng):
+    """Eq. 8 as a pure-python triple loop — sum over t in Q, over the h_s shared heads and
+    over the compression blocks whose coordinates lie inside each selection block — on inputs with 8
+    selection blocks of 2^3 compression blocks each ("random case -> naive triple loop").
+    Everything is derived from the coordinates here: the pooled keys (mean per compression cell), the
+    probabilities (math.exp softmax per (t, head)) and the containment cmp -> slc (bx_c // 2 == bx_s);
+    a compression block credited to the wrong selection block, a dropped head or a dropped token fails."""
+    m_cmp, m_slc, m_q, h_kv, h_s, d = 2, 4, 4, 2, 3, 5
+    c = random_coords(rng, 300, 8, 2)
+    N = len(c)
+    q = rng.standard_normal((N, h_kv * h_s, d))
+    k = rng.standard_normal((N, h_kv, d))
+    scale = 1.0 / math.sqrt(d)
+    plan = O.block_build(c, (8, 8, 8), 2, m_cmp, m_slc, m_slc, m_q)
+    P = plan.perm
+    k_cmp = O.compress(plan, k[P])
+    _, _, probs = O.compression_attention(plan, q[P], k_cmp, k_cmp, h_kv, scale)
+    scores = O.block_scores(plan, probs, h_kv)
+    cmp_groups = _blocks_from_coords(c, m_cmp)
+    slc_groups = _blocks_from_coords(c, m_slc)
+    q_groups = _blocks_from_coords(c, m_q)
+    ratio = m_slc // m_cmp
+    n_checked = 0
+    for qkey, qtoks in q_groups.items():
+        b = qkey[0]
+        ckeys = sorted(kk for kk in cmp_groups if kk[0] == b)
+        skeys = sorted(kk for kk in slc_groups if kk[0] == b)
+        for g in range(h_kv):
+            kbar = {kk: [math.fsum(k[i][g][e] for i in cmp_groups[kk]) / len(cmp_groups[kk]) for e in range(d)]
+                    for kk in ckeys}
+            want = {sk: 0.0 for sk in skeys}
+            for t in qtoks:                                            # sum over t in Q
+                for s in range(h_s):                                   # sum over the shared heads
+                    h = g * h_s + s
+                    logit = {kk: scale * math.fsum(q[t][h][e] * kbar[kk][e] for e in range(d)) for kk in ckeys}
+                    mx = max(logit.values())
+                    den = math.fsum(math.exp(x - mx) for x in logit.values())
+                    for kk in ckeys:                                   # sum over cmp blocks in the slc block
+                        sk = (b, kk[1] // ratio, kk[2] // ratio, kk[3] // ratio)
+                        want[sk] += math.exp(logit[kk] - mx) / den
+            # oracle's query block / selection block numbering: sorted block coordinates of the plan
+            Q = int(plan.tok_block["q"][plan.inv_perm[qtoks[0]]])
+            s0 = int(plan.batch_blocks["slc"][b])
+            got = scores[(Q, g)]
+            assert len(got) == len(skeys) >= 3
+            for j, sk in enumerate(skeys):
+                assert tuple(plan.block_coords["slc"][s0 + j]) == sk
+                assert abs(got[j] - want[sk]) <= 1e-12 * max(1.0, want[sk])
+            n_checked += 1
+    assert n_checked >= 8
+    assert max(len([kk for kk in cmp_groups if (kk[0], kk[1] // 2, kk[2] // 2, kk[3] // 2) == sk])
+               for sk in slc_groups) >= 4                              # several cmp blocks per slc block
+
+
+def test_compress_pe_pins(rng):
+    """Eq. 7 with the intra-block PE: with k = 0, k^cmp of a block is the mean
+    of the PE rows at the local offsets (x % m, y % m, z % m) of its ACTIVE tokens; with k != 0 it is the
+    naive per-block mean of k_j + PE[local(j)] (PE added before pooling). Grouping and local offsets are
+    computed here from the coordinates."""
+    m, h_kv, d = 4, 2, 3
+    c = random_coords(rng, 200, 16, 2)
+    N = len(c)
+    pe = rng.standard_normal((m ** 3, h_kv, d))
+    plan = O.block_build(c, (16, 16, 16), 2, m, 2 * m, 2 * m, 2 * m)
+    groups = _blocks_from_coords(c, m)
+    kc0 = O.compress(plan, np.zeros((N, h_kv, d)), pe)
+    k = rng.standard_normal((N, h_kv, d))
+    kc1 = O.compress(plan, k[plan.perm], pe)
+    for j, bc in enumerate(plan.block_coords["cmp"].tolist()):
+        toks = groups[tuple(bc)]
+        loc = [((c[i][1] % m) * m + c[i][2] % m) * m + c[i][3] % m for i in toks]
+        want0 = np.mean([pe[l] for l in loc], axis=0)
+        want1 = np.mean([k[i] + pe[l] for i, l in zip(toks, loc)], axis=0)
+        assert np.allclose(kc0[j], want0, rtol=0, atol=1e-14)
+        assert np.allclose(kc1[j], want1, rtol=0, atol=1e-14)
+    # a PE that depends only on z % m: swapping the x and y offsets of the table changes nothing,
+    # swapping x and z does (the table is indexed (x*m + y)*m + z)
+    pz = np.zeros((m, m, m, h_kv, d))
+    pz[:, :, 1] = 1.0
+    a = O.compress(plan, np.zeros((N, h_kv, d)), pz.reshape(m ** 3, h_kv, d))
+    b = O.compress(plan, np.zeros((N, h_kv, d)), np.swapaxes(pz, 0, 1).reshape(m ** 3, h_kv, d))
+    cz = O.compress(plan, np.zeros((N, h_kv, d)), np.swapaxes(pz, 0, 2).reshape(m ** 3, h_kv, d))
+    assert np.array_equal(a, b) and not np.array_equal(a, cz)

@@ -78,3 +78,28 @@ def test_gradient_sparsity(rng):
         for t in range(len(c)):
             if t not in used:
                 assert np.all(dk[t, g] == 0) and np.all(dv[t, g] == 0)
+
+
+def test_block_kv_grad_equals_full_backward(rng):
+    """The per-block gradient functions used for full-size parity (block_kv_grad = raw_kv_grad_block +
+    compression_kv_grad pool share) equal ssa_backward's dk / dv on every selection block of a ragged
+    two-item problem (so they inherit its finite-difference pins); chunking and threads do not matter."""
+    c, q, k, v, gates, dout = _problem(rng, n=90, H=6, d=4)
+    kw = dict(KW, T=3)
+    f = O.ssa_forward(c, (8, 8, 8), 2, q, k, v, gates, **kw)
+    dq, dk, dv, dg = O.ssa_backward(f, q, k, v, gates, dout, h_kv=2)
+    plan = f.plan
+    P = plan.perm
+    scale = 1.0 / math.sqrt(q.shape[2])
+    C = plan.offsets["slc"]
+    res = O.block_kv_grad(plan, q[P], k[P], v[P], f.k_cmp, f.v_cmp, gates[P], dout[P], f.I, 2, scale,
+                          range(plan.n_blocks("slc")), workers=3)
+    for B, (gk, gv) in res.items():
+        assert np.allclose(gk, dk[P][C[B]:C[B + 1]], rtol=0, atol=1e-12)
+        assert np.allclose(gv, dv[P][C[B]:C[B + 1]], rtol=0, atol=1e-12)
+    b = 1
+    c0, c1 = int(plan.batch_blocks["cmp"][b]), int(plan.batch_blocks["cmp"][b + 1])
+    cols = np.arange(c0, c1)
+    a = O.compression_kv_grad(plan, q[P], f.k_cmp, f.v_cmp, gates[P], dout[P], 2, scale, b, cols, chunk=5)
+    z = O.compression_kv_grad(plan, q[P], f.k_cmp, f.v_cmp, gates[P], dout[P], 2, scale, b, cols, chunk=10 ** 6)
+    assert np.allclose(a[0], z[0], rtol=0, atol=1e-12) and np.allclose(a[1], z[1], rtol=0, atol=1e-12)

@@ -16,7 +16,7 @@ t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v
 cc = torch.from_numpy(c).cuda()
 for m_q in (8, 1):
     plan = ssa.ssa_build_blocks(cc, grid, batch, 4, 8, 8, m_q)
-    acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16)
+    acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=0 if m_q == 8 else ssa.SSA_FORCE_SIMT)
     for i in range(4):
         if i == 1:
             torch.cuda.synchronize()
