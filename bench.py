@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-full", action="store_true", help="skip the full-attention comparator")
     ap.add_argument("--no-window", action="store_true", help="skip the window-only (SSA_WINDOW_ONLY) context timing")
+    ap.add_argument("--no-learned", action="store_true", help="skip the learned-delta / gate-projection context timing")
     ap.add_argument("--force-simt", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: validate the N>1 logic with several ranks on one GPU)")
@@ -489,6 +490,49 @@ def main():
         win = {"impl": "SSA_WINDOW_ONLY (sparse 3D window attention alone, fwd+bwd, same tokens and windows)",
                "fwd_bwd_ms": round(float(np.mean([a.elapsed_time(b) for a, b in wt])) / batch, 4)}
 
+    # ---- context: the learned delta (R17) + gate projection (R18) variant of the same step, C = 1024
+    # input features (the DiT width); random weights (trained ones are out of scope) ----
+    learned_ctx = None
+    if rank == 0 and used_tc and not sharded and not hybrid and not args.no_learned:
+        C = 1024
+        gen = torch.Generator(device=dev).manual_seed(5)
+        m3 = cfg["m_cmp"] ** 3
+        eye = torch.eye(d, device=dev)
+        Wk = eye + 0.05 * torch.randn(m3, h_kv, d, d, device=dev, generator=gen)
+        Wv = eye + 0.05 * torch.randn(m3, h_kv, d, d, device=dev, generator=gen)
+        bk = torch.zeros(h_kv, d, device=dev)
+        xf = torch.randn(q.shape[0], C, device=dev, generator=gen).to(tdt)
+        Wg = torch.randn(C, 3 * H, device=dev, generator=gen) / math.sqrt(C)
+        bg = torch.zeros(3 * H, device=dev)
+        lcfg = ssa.AttnCfg(h_q=H, h_kv=h_kv, d=d, top_k=T, dtype=tdt, learned=ssa.Learned(
+            conv_k_w=Wk, conv_k_b=bk, conv_v_w=Wv, conv_v_b=bk, x=xf, gate_w=Wg, gate_b=bg))
+        lt = []
+        ssa.profile_reset()
+        ssa.profile_enable(True)
+        for i in range(8):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan_l = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+            _, sv = ssa.ssa_forward(plan_l, lcfg, q, k, v, None, out=out)
+            ssa.ssa_backward(plan_l, lcfg, sv, q, k, v, None, do)
+            e1.record(st)
+            if i >= 3:
+                lt.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        ssa.profile_enable(False)
+        lk = {}
+        for kn in ("k_pool_learned", "k_gate_proj"):
+            t_, n_ = ssa.profile_read(kn)
+            if n_:
+                lk[kn] = round(t_ / n_, 4)
+        ssa.profile_reset()
+        l_ms = float(np.mean([a.elapsed_time(b) for a, b in lt]))
+        learned_ctx = {"impl": "learned delta (sparse conv kernel = stride = m_cmp + mean pool, R17) and gate "
+                               "projection from C = 1024 features (R18), fwd+bwd incl. weight gradients",
+                       "fwd_bwd_ms": round(l_ms / batch, 4), "extra_ms_vs_plain": round((l_ms - ms_per_step) / batch, 4),
+                       "kernel_ms": lk}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, cfg, coords, grid, batch, inp, value)
@@ -517,6 +561,8 @@ def main():
         }
         if win:
             line["window_attention"] = win
+        if learned_ctx:
+            line["learned_delta_gates"] = learned_ctx
         if hybrid_info:
             line["config"]["hybrid_plan"] = hybrid_info["plan"]
         if full:

@@ -144,6 +144,38 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
 #define SSA_WINDOW_ONLY 16u   /* window branch only (sparse 3D window attention)                   */
 #define SSA_LOCAL_ROWS 32u    /* q / gates / dout / out / dq / dgates hold only the owned rows       */
 
+/* ------------------------------------------------------------------------------------------------
+ * Learned compression delta and gate projection (readings R17, R18).
+ *   Eq. 7: k^cmp_B = (1/n_B) sum_{t in B} W_k[loc(t), g] (k_t + PE_k[loc(t), g]) + b_k[g] —
+ *     a sparse 3D convolution with kernel = stride = m_cmp over the active tokens of each compression
+ *     block (one d x d matrix per intra-block offset loc = ((x%m)*m + y%m)*m + z%m, grouped per kv head,
+ *     applied as W x) followed by the sparse mean pooling. W [m_cmp^3][h_kv][d][d], b [h_kv][d], fp32,
+ *     device. NULL conv_k_w: the masked mean pool (R4). V likewise with W_v, b_v.
+ *   Eq. 6 gates: omega = sigmoid(x W_g + b_g) from the input features x [n][c] (dtype, caller
+ *     order; SSA_LOCAL_ROWS: owned rows), W_g [c][3 h_q] (column h*3 + branch), b_g [3 h_q] fp32.
+ *     NULL x: the gates are the `gates` input. The computed gates are kept in the saved state.
+ *   Gradient outputs (written by ssa_backward where non-NULL): d_conv_* fp32 like their weights;
+ *   dx [n][c] dtype; d_gate_w, d_gate_b fp32. tcgen05 / SIMT paths alike; d == 64 only.
+ *   The pointers of this struct must be the same in the forward and the backward of one step.
+ * ----------------------------------------------------------------------------------------------*/
+typedef struct {
+  const float* conv_k_w;
+  const float* conv_k_b;
+  const float* conv_v_w;
+  const float* conv_v_b;
+  const void* x;
+  int32_t c;
+  const float* gate_w;
+  const float* gate_b;
+  float* d_conv_k_w;
+  float* d_conv_k_b;
+  float* d_conv_v_w;
+  float* d_conv_v_b;
+  void* dx;
+  float* d_gate_w;
+  float* d_gate_b;
+} ssa_learned;
+
 typedef struct {
   int32_t h_q, h_kv, d, top_k;
   float scale;
@@ -172,6 +204,7 @@ typedef struct {
   const void* kc_in;
   const void* vc_in;
   void* kv_event;
+  const ssa_learned* learned;   /* NULL: delta = mean pool, gates are inputs (see ssa_learned) */
 } ssa_attn_cfg;
 
 /* ------------------------------------------------------------------------------------------------

@@ -500,7 +500,8 @@ def compression_kv_grad(plan: BlockPlan, q_sorted, k_cmp, v_cmp, gates_sorted, d
         starts = list(range(0, R.shape[0], chunk))
         if workers > 1:
             from concurrent.futures import ThreadPoolExecutor
-            with ThreadPoolExecutor(workers) as ex:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(1), ThreadPoolExecutor(workers) as ex:   # no BLAS oversubscription
                 parts = list(ex.map(one, starts))
         else:
             parts = [one(r0) for r0 in starts]
@@ -510,50 +511,74 @@ def compression_kv_grad(plan: BlockPlan, q_sorted, k_cmp, v_cmp, gates_sorted, d
     return dk, dv
 
 
-def raw_kv_grad_block(plan: BlockPlan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv: int,
-                      scale: float, B: int, g: int):
-    """dk, dv [n_B, d] of the raw tokens of selection block B for kv group g from the selection branch
-    (every (Q, g) with B in I[Q, g], attention over all of Q's selected tokens, Alg. 1 / O6) and the
-    window branch (every window holding a token of B, O7) — everything but the compression pool share."""
+def raw_kv_grad_blocks(plan: BlockPlan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv: int,
+                       scale: float, blocks, workers: int = 1) -> dict:
+    """{B: (dk, dv) [n_B, h_kv, d]}: gradients of the raw tokens of each selection block B from the
+    selection branch (every (Q, g) with B in I[Q, g]: attention over all of Q's selected tokens, Alg. 1 /
+    O6) and the window branch (every window holding a token of B, O7) — everything but the compression
+    pool share. Each (Q, g) / (window, g) problem is evaluated once for all requested blocks; `workers`
+    > 1 evaluates the problems on a thread pool (BLAS single-threaded); contributions are summed in
+    problem order."""
     N, H, d = q_sorted.shape
     h_s = H // h_kv
     C = plan.offsets["slc"]
-    b0, b1 = int(C[B]), int(C[B + 1])
     gs = np.asarray(gates_sorted, np.float64)
     dos = np.asarray(dout_sorted, np.float64)
-    dk = np.zeros((b1 - b0, d))
-    dv = np.zeros((b1 - b0, v_sorted.shape[2]))
-    Cq = plan.offsets["q"]
+    do_slc, do_win = gs[..., 1:2] * dos, gs[..., 2:3] * dos          # omega_c dO per branch (Eq. 6)
+    want = set(int(B) for B in blocks)
+    out = {B: (np.zeros((int(C[B + 1] - C[B]), h_kv, d)), np.zeros((int(C[B + 1] - C[B]), h_kv, v_sorted.shape[2])))
+           for B in sorted(want)}
+    Cq, Cw = plan.offsets["q"], plan.offsets["win"]
+    tasks = []
     for Q in range(len(Cq) - 1):
-        if B not in set(int(x) for x in I[Q, g]):
-            continue
-        t0, t1 = int(Cq[Q]), int(Cq[Q + 1])
-        kt = _selected_tokens(plan, I, Q, g)
+        for g in range(h_kv):
+            hit = sorted(want & set(int(x) for x in I[Q, g]))
+            if hit:
+                tasks.append(("slc", Q, g, hit))
+    wins = sorted(set(int(x) for B in want for x in plan.tok_block["win"][int(C[B]):int(C[B + 1])]))
+    for w in wins:
+        for g in range(h_kv):
+            tasks.append(("win", w, g, None))
+
+    def run(task):
+        kind, a, g, hit = task
+        if kind == "slc":
+            t0, t1 = int(Cq[a]), int(Cq[a + 1])
+            kt = _selected_tokens(plan, I, a, g)
+            dor = _rows(do_slc, t0, t1, g, h_s)
+        else:
+            t0, t1 = int(Cw[a]), int(Cw[a + 1])
+            kt = np.arange(t0, t1)
+            dor = _rows(do_win, t0, t1, g, h_s)
         rows = _rows(q_sorted, t0, t1, g, h_s)
-        dor = _rows(gs[..., 1:2] * dos, t0, t1, g, h_s)
         o, _, p = dense_attention(rows, k_sorted[kt, g], v_sorted[kt, g], scale)
-        m = (kt >= b0) & (kt < b1)
-        _, dkr, dvr = dense_attention_backward(rows, k_sorted[kt[m], g], v_sorted[kt[m], g], p[:, m], o, dor, scale)
-        dk[kt[m] - b0] += dkr
-        dv[kt[m] - b0] += dvr
-    Cw = plan.offsets["win"]
-    for w in sorted(set(int(x) for x in plan.tok_block["win"][b0:b1])):
-        t0, t1 = int(Cw[w]), int(Cw[w + 1])
-        kt = np.arange(t0, t1)
-        rows = _rows(q_sorted, t0, t1, g, h_s)
-        dor = _rows(gs[..., 2:3] * dos, t0, t1, g, h_s)
-        o, _, p = dense_attention(rows, k_sorted[kt, g], v_sorted[kt, g], scale)
-        m = (kt >= b0) & (kt < b1)
-        _, dkr, dvr = dense_attention_backward(rows, k_sorted[kt[m], g], v_sorted[kt[m], g], p[:, m], o, dor, scale)
-        dk[kt[m] - b0] += dkr
-        dv[kt[m] - b0] += dvr
-    return dk, dv
+        res = []
+        for B in (hit if hit is not None else sorted(want)):
+            m = (kt >= C[B]) & (kt < C[B + 1])
+            if not m.any():
+                continue
+            _, dkr, dvr = dense_attention_backward(rows, k_sorted[kt[m], g], v_sorted[kt[m], g], p[:, m], o, dor, scale)
+            res.append((B, g, kt[m] - int(C[B]), dkr, dvr))
+        return res
+
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1), ThreadPoolExecutor(workers) as ex:
+            results = list(ex.map(run, tasks))
+    else:
+        results = [run(t) for t in tasks]
+    for res in results:
+        for B, g, idx, dkr, dvr in res:
+            out[B][0][idx, g] += dkr
+            out[B][1][idx, g] += dvr
+    return out
 
 
 def block_kv_grad(plan: BlockPlan, q_sorted, k_sorted, v_sorted, k_cmp, v_cmp, gates_sorted, dout_sorted, I,
                   h_kv: int, scale: float, blocks, workers: int = 1) -> dict:
     """{B: (dk, dv) [n_B, h_kv, d]}: total gradients of the tokens of each selection block B (sorted
-    order) = raw-key part (raw_kv_grad_block) + the mean-pool share dk^cmp_c / n_c of every compression
+    order) = raw-key part (raw_kv_grad_blocks) + the mean-pool share dk^cmp_c / n_c of every compression
     block c inside B (Eq. 7 backward with delta = mean, R4). One compression_kv_grad pass per batch item
     covers all requested blocks of that item."""
     C = plan.offsets["slc"]
@@ -568,15 +593,11 @@ def block_kv_grad(plan: BlockPlan, q_sorted, k_sorted, v_sorted, k_cmp, v_cmp, g
         dkc, dvc = compression_kv_grad(plan, q_sorted, k_cmp, v_cmp, gates_sorted, dout_sorted, h_kv, scale, bi,
                                        np.array(cols, np.int64), workers=workers)
         col_of = {c: i for i, c in enumerate(cols)}
+        raw = raw_kv_grad_blocks(plan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv, scale, Bs,
+                                 workers=workers)
         for B in Bs:
             b0, b1 = int(C[B]), int(C[B + 1])
-            dk = np.zeros((b1 - b0, h_kv, d))
-            dv = np.zeros((b1 - b0, h_kv, v_sorted.shape[2]))
-            for g in range(h_kv):
-                rk, rv = raw_kv_grad_block(plan, q_sorted, k_sorted, v_sorted, gates_sorted, dout_sorted, I, h_kv,
-                                           scale, B, g)
-                dk[:, g] += rk
-                dv[:, g] += rv
+            dk, dv = raw[B]
             for c in sorted(set(int(x) for x in plan.tok_block["cmp"][b0:b1])):
                 a, e = int(Cc[c]), int(Cc[c + 1])
                 dk[a - b0:e - b0] += dkc[col_of[c]] / (e - a)
@@ -740,3 +761,18 @@ def ssa_backward_learned(fwd: ForwardResult, q, k, v, x, gates, dout, *, conv_k,
     inv = plan.inv_perm
     dx, dWg, dbg = gate_projection_backward(x, gate[0], gate[1], dgates[inv])
     return dq[inv], dk[inv], dv[inv], dx, dWk, dbk, dWv, dbv, dWg, dbg
+
+
+# --------------------------------------------------------------------------------------------------
+# NSA-1D blocking ("treating latent tokens z as a 1D sequence and partitioning it into
+# fixed-length blocks based on token indices, analogous to NSA"; the ablation arm of P:394).
+# READING R19: block lengths l = m^3 tokens (the token count of the corresponding 3D block), runs of
+# consecutive indices per batch item (the last run of an item is shorter), windows non-overlapping.
+# --------------------------------------------------------------------------------------------------
+def block_offsets_1d(lengths, l: int) -> np.ndarray:
+    """C of fixed-length 1D blocks of l tokens over the concatenated batch items (index order)."""
+    starts, base = [], 0
+    for n in lengths:
+        starts += list(range(base, base + int(n), l))
+        base += int(n)
+    return np.array(starts + [base], dtype=np.int64)

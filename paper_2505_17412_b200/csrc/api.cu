@@ -136,6 +136,10 @@ void carve_saved(Carve& c, const Dims& d, const ssa_attn_cfg* cfg, Ctx* x) {
   x->I = c.take<int32_t>(size_t(d.n_q) * d.h_kv * d.T);
   x->scores = (cfg->flags & SSA_SAVE_SCORES) ? c.take<float>(size_t(d.n_q) * d.h_kv * std::max(d.max_slc_b, 1)) : nullptr;
 }
+// gates computed by the projection (ssa_learned.x) are part of the saved state, [h_kv][N][h_s][3] fp32
+float* carve_saved_gates(Carve& c, const Dims& d, const ssa_attn_cfg* cfg) {
+  return (cfg->learned && cfg->learned->x) ? c.take<float>(size_t(d.N) * d.H * 3) : nullptr;
+}
 
 void carve_inputs(Carve& c, const Dims& d, Ctx* x, bool with_dout) {
   const int64_t rows = d.N * d.H, keys = d.N * d.h_kv;
@@ -230,6 +234,12 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->row_lo = ranged ? p->h_q_offsets[x->q_begin] : 0;
   x->row_hi = ranged ? p->h_q_offsets[x->q_end] : int32_t(d.N);
   x->row_base = (cfg->flags & SSA_LOCAL_ROWS) ? x->row_lo : 0;
+  if (const ssa_learned* L = cfg->learned) {
+    x->conv_kw = L->conv_k_w; x->conv_kb = L->conv_k_b; x->conv_vw = L->conv_v_w; x->conv_vb = L->conv_v_b;
+    x->conv_dkw = L->d_conv_k_w; x->conv_dkb = L->d_conv_k_b; x->conv_dvw = L->d_conv_v_w; x->conv_dvb = L->d_conv_v_b;
+    x->gx = L->x; x->gC = L->c; x->gw = L->gate_w; x->gb = L->gate_b;
+    x->gdx = L->dx; x->gdw = L->d_gate_w; x->gdb = L->d_gate_b;
+  }
 }
 
 // SSA_LOCAL_ROWS: the caller's row tensors start at row row_base; kernels index rows by their plan
@@ -253,10 +263,12 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   Ctx x{};
   Carve cs(nullptr, 0);
   carve_saved(cs, d, cfg, &x);
+  carve_saved_gates(cs, d, cfg);
   *saved_bytes = cs.used + 256;
   Carve cw(nullptr, 0);
   carve_inputs(cw, d, &x, false);
-  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + 512;
+  fill_common(&x, p, d, cfg);
+  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + 1024;
   return SSA_OK;
 }
 
@@ -267,7 +279,8 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   Dims d;
   ssa_status s = check_cfg(p, cfg, &d);
   if (s != SSA_OK) return s;
-  if (!q || !k || !v || !gates || !out || !saved || !ws) { set_error("null tensor pointer"); return SSA_ERR_ARG; }
+  const bool lgates = cfg->learned && cfg->learned->x;
+  if (!q || !k || !v || !(gates || lgates) || !out || !saved || !ws) { set_error("null tensor pointer"); return SSA_ERR_ARG; }
   size_t need_ws, need_saved;
   s = ssa_forward_size(plan, cfg, &need_ws, &need_saved);
   if (s != SSA_OK) return s;
@@ -282,11 +295,15 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   x.gates = rows_at(gates, x, int64_t(d.H) * 3, d.esz);
   x.out = rows_at(out, x, int64_t(d.H) * d.D, d.esz);
   x.k = k; x.v = v;
+  if ((s = learned_checks(x)) != SSA_OK) return s;
   Carve cs(saved, saved_bytes);
   carve_saved(cs, d, cfg, &x);
+  float* saved_gates = carve_saved_gates(cs, d, cfg);
   Carve cw(ws, ws_bytes);
   carve_inputs(cw, d, &x, false);
   void* tc_ws = cw.take<char>(tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
+  void* l_ws = cw.take<char>(learned_fwd_ws_bytes(x));
+  if (lgates) x.gs = saved_gates;
   const bool bf16 = cfg->dtype == SSA_BF16;
   // caller-supplied pooled keys (mode 2): no pooling; raw k / v are first read by the selection /
   // window branch, after cfg.kv_event (tcgen05 path) — the compression branch overlaps the K/V exchange
@@ -297,12 +314,17 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
     SSA_CUDA_TRY(cudaMemcpyAsync(x.kc, cfg->kc_in, kc_bytes, cudaMemcpyDeviceToDevice, st));
     SSA_CUDA_TRY(cudaMemcpyAsync(x.vc, cfg->vc_in, kc_bytes, cudaMemcpyDeviceToDevice, st));
     if (!tc && kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
-    if ((s = gather_inputs(x, bf16, st, false, true, /*keys=*/!tc)) != SSA_OK) return s;
+    if ((s = gather_inputs(x, bf16, st, false, true, /*keys=*/!tc, /*gates=*/!lgates)) != SSA_OK) return s;
   } else {
     if (kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
-    if ((s = gather_inputs(x, bf16, st, false)) != SSA_OK) return s;
-    if ((s = pool_forward(x, bf16, st)) != SSA_OK) return s;
+    if ((s = gather_inputs(x, bf16, st, false, true, true, /*gates=*/!lgates)) != SSA_OK) return s;
+    if (x.conv_kw) {
+      if ((s = learned_pool_forward(x, bf16, l_ws, st)) != SSA_OK) return s;
+    } else if ((s = pool_forward(x, bf16, st)) != SSA_OK) {
+      return s;
+    }
   }
+  if (lgates && (s = gate_proj_forward(x, bf16, st)) != SSA_OK) return s;
   if (x.win_only) {
     // skipped branches: O = 0, indices -1 (no selected blocks), LSE huge (p = exp2(s - LSE) = 0 anywhere)
     const int64_t rows = int64_t(d.N) * d.H;
@@ -332,6 +354,7 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q);
+  if (cfg->learned && cfg->learned->x) scan += learned_bwd_ws_bytes(d.N, d.H, d.h_kv, cfg->learned->c);
   *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]) + 1024;
   return SSA_OK;
 }
@@ -344,7 +367,8 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   Dims d;
   ssa_status s = check_cfg(p, cfg, &d);
   if (s != SSA_OK) return s;
-  if (!q || !k || !v || !gates || !saved || !dout || !dq || !dk || !dv || !dgates || !ws) {
+  const bool lgates = cfg->learned && cfg->learned->x;
+  if (!q || !k || !v || !(gates || lgates) || !saved || !dout || !dq || !dk || !dv || !dgates || !ws) {
     set_error("null tensor pointer");
     return SSA_ERR_ARG;
   }
@@ -364,17 +388,25 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   x.dq = rows_at(dq, x, int64_t(d.H) * d.D, d.esz);
   x.dgates = rows_at(dgates, x, int64_t(d.H) * 3, d.esz);
   x.k = k; x.v = v; x.dk = dk; x.dv = dv;
+  if ((s = learned_checks(x)) != SSA_OK) return s;
   Carve cs(const_cast<void*>(saved), saved_bytes);
   carve_saved(cs, d, cfg, &x);
+  float* saved_gates = carve_saved_gates(cs, d, cfg);
   Carve cw(ws, ws_bytes);
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
   void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
+  void* part_ws = nullptr;
+  if (lgates) {
+    x.gs = saved_gates;
+    x.dz = cw.take<float>(size_t(d.N) * d.H * 3);
+    part_ws = cw.take<float>(size_t((d.N + 1023) / 1024 + 1) * cfg->learned->c * 3 * d.H);
+  }
   const bool bf16 = cfg->dtype == SSA_BF16;
   const bool tc = use_tc_bwd(d, cfg, p);
   // the tcgen05 backward gathers the q / dO rows and computes D_c, dgates in its own row prologue
-  if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc)) != SSA_OK) return s;
+  if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc, true, /*gates=*/!lgates)) != SSA_OK) return s;
   if (!tc && (s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
   if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
   if (tc) {
@@ -388,7 +420,10 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   } else {
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
   }
-  return bwd_epilogue(x, bf16, st, /*skip_q=*/tc);
+  if (x.conv_kw && (s = learned_pool_backward_params(x, bf16, st)) != SSA_OK) return s;
+  if ((s = bwd_epilogue(x, bf16, st, /*skip_q=*/tc)) != SSA_OK) return s;
+  if (lgates && (s = gate_proj_backward(x, bf16, part_ws, st)) != SSA_OK) return s;
+  return SSA_OK;
 }
 
 extern "C" ssa_status ssa_pool(ssa_plan plan, const ssa_attn_cfg* cfg, const void* k, const void* v, void* kc, void* vc,

@@ -73,7 +73,16 @@ struct Ctx {
   float *dkc, *dvc;               // fp32 [h_kv][n_cmp][D]
   float *dkc_part, *dvc_part;     // fp32 [n_chunk][h_kv][n_cmp][D]
   int32_t n_chunk;
-  const uint32_t* do_amax;        // tcgen05 backward: max |dO| (float bits) -> power-of-two operand scale
+  const uint32_t* do_amax;
+  // §8f row 2 (learned.cu): learned compression delta (R17) and gate projection (R18)
+  const float *conv_kw, *conv_kb, *conv_vw, *conv_vb;   // [m^3][h_kv][D][D], [h_kv][D]; null = mean pool
+  float *conv_dkw, *conv_dkb, *conv_dvw, *conv_dvb;     // their gradients (backward outputs)
+  const void* gx;                 // [N][gC] input features (caller order, dtype); null = gates are inputs
+  int32_t gC;
+  const float *gw, *gb;           // W_g [gC][3H], b_g [3H]
+  void* gdx;                      // dx (dtype), dW_g, db_g (fp32) — backward outputs
+  float *gdw, *gdb;
+  float* dz;                      // [h_kv][N][h_s][3] gradients of the gate logits (row prologue)        // tcgen05 backward: max |dO| (float bits) -> power-of-two operand scale
   int32_t *inv_off, *inv_list, *inv_cnt;   // inverse selection CSR over (slc block, g)
   int32_t *cmp_tiles;             // [n_cmp_tiles][2] (batch item, first cmp block) for the KV-outer cmp kernels
   int32_t n_cmp_tiles;
@@ -88,6 +97,14 @@ ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
 // rows = false: only keys and gates are gathered (the tcgen05 backward reads q / dO rows itself)
 ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows = true, bool keys = true,
                          bool gates = true);
+// learned.cu
+size_t learned_fwd_ws_bytes(const Ctx& c);
+size_t learned_bwd_ws_bytes(int64_t N, int H, int h_kv, int C);
+ssa_status learned_checks(const Ctx& c);
+ssa_status learned_pool_forward(const Ctx& c, bool bf16, void* ws, cudaStream_t st);
+ssa_status gate_proj_forward(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status gate_proj_backward(const Ctx& c, bool bf16, void* part_ws, cudaStream_t st);
+ssa_status learned_pool_backward_params(const Ctx& c, bool bf16, cudaStream_t st);
 // ssa_pool's kernel: pooled keys of the owned compression blocks from caller-layout (sorted) k, v
 ssa_status pool_rows(const Ctx& c, bool bf16, const void* k, const void* v, float* kc, float* vc, cudaStream_t st);
 ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);

@@ -395,7 +395,9 @@ __global__ void k_bwd_pre(Ctx c) {
   const int dst = c.sorted_input ? p : c.perm[p];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
-    c.Dd[b][row] = c.gs[row * 3 + b] * acc[b];
+    const float wb = c.gs[row * 3 + b];
+    if (c.dz) c.dz[row * 3 + b] = acc[b] * wb * (1.f - wb);   // gate projection backward (R18)
+    c.Dd[b][row] = wb * acc[b];
     st(static_cast<T*>(c.dgates) + (int64_t(dst) * c.H + h) * 3 + b, acc[b]);
   }
 }
@@ -807,7 +809,27 @@ __global__ void k_bwd_final_kv(Ctx c) {
   const int dst = c.sorted_input ? p : c.perm[p];
   const int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
   const float4 ak = *reinterpret_cast<const float4*>(c.dk_acc + ki), av = *reinterpret_cast<const float4*>(c.dv_acc + ki);
-  const float4 ck = *reinterpret_cast<const float4*>(c.dkc + ci), cv = *reinterpret_cast<const float4*>(c.dvc + ci);
+  float4 ck = *reinterpret_cast<const float4*>(c.dkc + ci), cv = *reinterpret_cast<const float4*>(c.dvc + ci);
+  if (c.conv_kw) {
+    // learned delta (R17): d(k_t) = W[loc(t), g]^T dk^cmp_B / n_B (the 1/n_B is applied below)
+    const int m = c.m_cmp;
+    const int4 cc = reinterpret_cast<const int4*>(c.sorted_coords)[p];
+    const int loc = ((cc.y % m) * m + (cc.z % m)) * m + (cc.w % m);
+    const float* wk = c.conv_kw + (int64_t(loc) * c.h_kv + g) * c.D * c.D + e;
+    const float* wv = c.conv_vw + (int64_t(loc) * c.h_kv + g) * c.D * c.D + e;
+    const float* yk = c.dkc + (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D;
+    const float* yv = c.dvc + (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D;
+    float4 sk = make_float4(0.f, 0.f, 0.f, 0.f), sv = sk;
+    for (int r = 0; r < c.D; ++r) {
+      const float4 a = *reinterpret_cast<const float4*>(wk + int64_t(r) * c.D);
+      const float4 b = *reinterpret_cast<const float4*>(wv + int64_t(r) * c.D);
+      const float y1 = yk[r], y2 = yv[r];
+      sk.x += a.x * y1; sk.y += a.y * y1; sk.z += a.z * y1; sk.w += a.w * y1;
+      sv.x += b.x * y2; sv.y += b.y * y2; sv.z += b.z * y2; sv.w += b.w * y2;
+    }
+    ck = sk;
+    cv = sv;
+  }
   const float gk[4] = {ak.x + ck.x * inv, ak.y + ck.y * inv, ak.z + ck.z * inv, ak.w + ck.w * inv};
   const float gv[4] = {av.x + cv.x * inv, av.y + cv.y * inv, av.z + cv.z * inv, av.w + cv.w * inv};
   if (c.kv_grad_f32) {

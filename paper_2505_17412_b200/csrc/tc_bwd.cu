@@ -132,6 +132,7 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
   if (p < c.off[SSA_LEVEL_Q][c.q_begin] || p >= c.off[SSA_LEVEL_Q][c.q_end]) return;   // rows of other shards
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
+    if (c.dz) c.dz[int64_t(rr) * 3 + b] = acc[b] * w[b] * (1.f - w[b]);   // gate projection backward (R18)
     c.Dd[b][rr] = w[b] * acc[b] * ds;
     static_cast<__nv_bfloat16*>(c.dgates)[(int64_t(src_p) * c.H + h) * 3 + b] = __float2bfloat16_rn(acc[b]);
   }

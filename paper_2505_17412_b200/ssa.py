@@ -45,12 +45,20 @@ class PlanInfo(ctypes.Structure):
                 ("cmp_to_slc", ctypes.c_void_p)]
 
 
+class LearnedC(ctypes.Structure):
+    _fields_ = [("conv_k_w", ctypes.c_void_p), ("conv_k_b", ctypes.c_void_p), ("conv_v_w", ctypes.c_void_p),
+                ("conv_v_b", ctypes.c_void_p), ("x", ctypes.c_void_p), ("c", ctypes.c_int32),
+                ("gate_w", ctypes.c_void_p), ("gate_b", ctypes.c_void_p), ("d_conv_k_w", ctypes.c_void_p),
+                ("d_conv_k_b", ctypes.c_void_p), ("d_conv_v_w", ctypes.c_void_p), ("d_conv_v_b", ctypes.c_void_p),
+                ("dx", ctypes.c_void_p), ("d_gate_w", ctypes.c_void_p), ("d_gate_b", ctypes.c_void_p)]
+
+
 class AttnCfgC(ctypes.Structure):
     _fields_ = [("h_q", ctypes.c_int32), ("h_kv", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p),
                 ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32), ("kc_in", ctypes.c_void_p),
-                ("vc_in", ctypes.c_void_p), ("kv_event", ctypes.c_void_p)]
+                ("vc_in", ctypes.c_void_p), ("kv_event", ctypes.c_void_p), ("learned", ctypes.POINTER(LearnedC))]
 
 
 class SavedView(ctypes.Structure):
@@ -118,7 +126,9 @@ def _stream(device: torch.device):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
-def _dev(t: torch.Tensor, name: str):
+def _dev(t: torch.Tensor, name: str, optional: bool = False):
+    if t is None and optional:
+        return None
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
     if not t.is_contiguous():
@@ -210,6 +220,41 @@ def ssa_build_blocks(coords: torch.Tensor, grid, batch: int, m_cmp: int, m_slc: 
 
 
 @dataclass
+class Learned:
+    """Learned compression delta (Eq. 7, reading R17) and gate projection (Eq. 6 / P:153, reading R18):
+    conv_*_w fp32 [m_cmp^3, h_kv, d, d], conv_*_b fp32 [h_kv, d]; x [N, C] (dtype, caller order),
+    gate_w fp32 [C, 3 h_q], gate_b fp32 [3 h_q]. ssa_backward fills `grads` (same names with a d_ prefix;
+    dx in x's dtype)."""
+    conv_k_w: torch.Tensor | None = None
+    conv_k_b: torch.Tensor | None = None
+    conv_v_w: torch.Tensor | None = None
+    conv_v_b: torch.Tensor | None = None
+    x: torch.Tensor | None = None
+    gate_w: torch.Tensor | None = None
+    gate_b: torch.Tensor | None = None
+    grads: dict | None = None
+
+    def c(self, grads: dict | None = None) -> LearnedC:
+        def ptr(t):
+            return t.data_ptr() if t is not None else None
+        g = grads or {}
+        return LearnedC(ptr(self.conv_k_w), ptr(self.conv_k_b), ptr(self.conv_v_w), ptr(self.conv_v_b), ptr(self.x),
+                        int(self.x.shape[1]) if self.x is not None else 0, ptr(self.gate_w), ptr(self.gate_b),
+                        ptr(g.get("d_conv_k_w")), ptr(g.get("d_conv_k_b")), ptr(g.get("d_conv_v_w")),
+                        ptr(g.get("d_conv_v_b")), ptr(g.get("dx")), ptr(g.get("d_gate_w")), ptr(g.get("d_gate_b")))
+
+    def alloc_grads(self) -> dict:
+        g = {}
+        for name in ("conv_k_w", "conv_k_b", "conv_v_w", "conv_v_b", "gate_w", "gate_b"):
+            t = getattr(self, name)
+            if t is not None:
+                g["d_" + name] = torch.zeros_like(t, dtype=torch.float32)
+        if self.x is not None:
+            g["dx"] = torch.empty_like(self.x)
+        return g
+
+
+@dataclass
 class AttnCfg:
     h_q: int
     h_kv: int
@@ -225,14 +270,18 @@ class AttnCfg:
     kc_in: torch.Tensor | None = None    # caller-supplied pooled keys / values, fp32 [h_kv, n_cmp, d]
     vc_in: torch.Tensor | None = None
     kv_event: torch.cuda.Event | None = None   # raw k / v ready (recorded after a K/V all-gather)
+    learned: Learned | None = None
 
-    def c(self) -> AttnCfgC:
+    def c(self, learned_grads: dict | None = None) -> AttnCfgC:
         def ptr(t):
             return t.data_ptr() if t is not None else None
         ev = self.kv_event.cuda_event if self.kv_event is not None else None
-        return AttnCfgC(self.h_q, self.h_kv, self.d, self.top_k, float(self.scale), _dtype_code(self.dtype),
-                        int(self.flags), ptr(self.pe_k), ptr(self.pe_v), int(self.q_begin), int(self.q_end),
-                        ptr(self.kc_in), ptr(self.vc_in), ev)
+        lc = self.learned.c(learned_grads) if self.learned is not None else None
+        cc = AttnCfgC(self.h_q, self.h_kv, self.d, self.top_k, float(self.scale), _dtype_code(self.dtype),
+                      int(self.flags), ptr(self.pe_k), ptr(self.pe_v), int(self.q_begin), int(self.q_end),
+                      ptr(self.kc_in), ptr(self.vc_in), ev, ctypes.pointer(lc) if lc is not None else None)
+        cc._keep = lc          # the struct the pointer refers to lives as long as cc
+        return cc
 
 
 class Saved:
@@ -290,12 +339,15 @@ def _check_inputs(plan: Plan, cfg: AttnCfg, q, k, v, gates):
     n = plan.n
     a, b = owned_rows(plan, cfg) if cfg.flags & SSA_LOCAL_ROWS else (0, n)
     nr = b - a
+    lg = cfg.learned is not None and cfg.learned.x is not None
+    if gates is None and not lg:
+        raise ValueError("gates are required unless cfg.learned.x supplies the gate projection input")
     if tuple(q.shape) != (nr, cfg.h_q, cfg.d) or tuple(k.shape) != (n, cfg.h_kv, cfg.d) or \
-            tuple(v.shape) != (n, cfg.h_kv, cfg.d) or tuple(gates.shape) != (nr, cfg.h_q, 3):
+            tuple(v.shape) != (n, cfg.h_kv, cfg.d) or (gates is not None and tuple(gates.shape) != (nr, cfg.h_q, 3)):
         raise ValueError("shape mismatch: q [N,h_q,d], k/v [N,h_kv,d], gates [N,h_q,3] "
                          "(q, gates: owned rows only with SSA_LOCAL_ROWS)")
-    for t in (q, k, v, gates):
-        if t.dtype != cfg.dtype:
+    for t in (q, k, v, gates, cfg.learned.x if lg else None):
+        if t is not None and t.dtype != cfg.dtype:
             raise ValueError(f"tensor dtype {t.dtype} != cfg.dtype {cfg.dtype}")
 
 
@@ -337,7 +389,7 @@ def ssa_forward(plan: Plan, cfg: AttnCfg, q, k, v, gates, out=None, saved: Saved
         saved = Saved(plan, cfg, torch.empty(svb.value, dtype=torch.uint8, device=dev))
     w = (ws or _ws(dev, "fwd")).get(wsb.value, dev)
     _check(L.ssa_forward(plan.handle, ctypes.byref(cc), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
-                         _dev(gates, "gates"), _dev(out, "out"), ctypes.c_void_p(saved.buf.data_ptr()),
+                         _dev(gates, "gates", optional=True), _dev(out, "out"), ctypes.c_void_p(saved.buf.data_ptr()),
                          saved.buf.numel(), ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_forward")
     return out, saved
 
@@ -363,20 +415,23 @@ def ssa_backward(plan: Plan, cfg: AttnCfg, saved: Saved, q, k, v, gates, dout, g
     _check_inputs(plan, cfg, q, k, v, gates)
     if tuple(dout.shape) != tuple(q.shape) or dout.dtype != cfg.dtype:
         raise ValueError("dout must match q")
-    cc = cfg.c()
+    lgrads = cfg.learned.alloc_grads() if cfg.learned is not None else None
+    cc = cfg.c(lgrads)
     wsb = ctypes.c_size_t()
     _check(L.ssa_backward_size(plan.handle, ctypes.byref(cc), ctypes.byref(wsb)), "ssa_backward_size")
     dev = q.device
     if grads is None:
         kvd = torch.float32 if cfg.flags & SSA_KV_GRAD_FP32 else k.dtype
         grads = (torch.empty_like(q), torch.empty_like(k, dtype=kvd), torch.empty_like(v, dtype=kvd),
-                 torch.empty_like(gates))
+                 torch.empty(q.shape[0], cfg.h_q, 3, dtype=q.dtype, device=q.device))
     dq, dk, dv, dg = grads
     w = (ws or _ws(dev, "bwd")).get(wsb.value, dev)
     _check(L.ssa_backward(plan.handle, ctypes.byref(cc), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
-                          _dev(gates, "gates"), ctypes.c_void_p(saved.buf.data_ptr()), saved.buf.numel(),
+                          _dev(gates, "gates", optional=True), ctypes.c_void_p(saved.buf.data_ptr()), saved.buf.numel(),
                           _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"), _dev(dg, "dgates"),
                           ctypes.c_void_p(w.data_ptr()), w.numel(), _stream(dev)), "ssa_backward")
+    if lgrads is not None:
+        cfg.learned.grads = lgrads
     return dq, dk, dv, dg
 
 
@@ -459,3 +514,31 @@ class SSAFunction(torch.autograd.Function):
 
 def default_scale(d: int) -> float:
     return 1.0 / math.sqrt(d)
+
+
+def nsa1d_coords(lengths, m_cmp: int, m_slc: int):
+    """The NSA-1D blocking arm ("treating latent tokens as a 1D sequence and partitioning it into
+    fixed-length blocks based on token indices, analogous to NSA"; the paper's ablation baseline):
+    coordinates whose spatial blocks ARE runs of consecutive token indices, so ssa_build_blocks + the
+    unchanged SSA kernels compute NSA-style 1D block attention. Token i of a batch item gets
+    x = 8 * (i // m_slc^3) ... such that compression blocks = l_cmp = m_cmp^3 consecutive tokens,
+    selection blocks (and windows, query blocks with m_win = m_q = m_slc) = l_slc = m_slc^3 consecutive
+    tokens, and the plan order is the index order. Index arithmetic only (no method arithmetic).
+    lengths: tokens per batch item. Returns (coords int32 [N, 4] on the host, grid (3,))."""
+    import numpy as np
+    if m_slc % m_cmp:
+        raise ValueError("m_slc must be a multiple of m_cmp")
+    r = m_slc // m_cmp
+    l_cmp, l_slc = m_cmp ** 3, m_slc ** 3
+    out = []
+    for b, n in enumerate(int(x) for x in lengths):
+        i = np.arange(n, dtype=np.int64)
+        B, rem = i // l_slc, i % l_slc
+        c, v = rem // l_cmp, rem % l_cmp                       # cmp sub-block in the slc block, voxel
+        cx, cy, cz = c // (r * r), (c // r) % r, c % r
+        vx, vy, vz = v // (m_cmp * m_cmp), (v // m_cmp) % m_cmp, v % m_cmp
+        out.append(np.stack([np.full(n, b), B * m_slc + cx * m_cmp + vx, cy * m_cmp + vy, cz * m_cmp + vz], 1))
+    coords = np.concatenate(out).astype(np.int32) if out else np.zeros((0, 4), np.int32)
+    n_max = max([int(x) for x in lengths] + [1])
+    grid = (-(-n_max // l_slc) * m_slc, m_slc, m_slc)
+    return coords, grid

@@ -99,7 +99,7 @@ def _check_blocks(inp, kw, r, plan_o, blocks, test):
                 refs[name].append(ref)
                 gots[name].append(gpu)
     for name in refs:
-        errs[name] = record(test, name, np.concatenate(gots[name]), np.concatenate(refs[name]), 2e-2)
+        errs[name] = record(test, name, np.concatenate(gots[name]), np.concatenate(refs[name]), 2e-2, stored_bf16=True)
     REPORT.append(dict(test=test, tensor="scores", rel=score_worst, tol=1e-4, ok=bool(score_worst <= 1e-4),
                        metric="max|score_gpu - score_ref| / (T-th largest ref score), per (Q, g)"))
     errs["scores"] = score_worst / 1e-4 * 2e-2       # scaled so the common 2e-2 bound applies
@@ -146,8 +146,10 @@ def _check_kv_blocks(inp, kw, r, plan_o, kv_blocks, test):
         got_v.append(dv_g[a:b].reshape(-1))
         ref_k.append(rk.reshape(-1))
         ref_v.append(rv.reshape(-1))
-    return {"dk": record(test, "dk", np.concatenate(got_k), np.concatenate(ref_k), 2e-2, blocks=list(map(int, kv_blocks))),
-            "dv": record(test, "dv", np.concatenate(got_v), np.concatenate(ref_v), 2e-2, blocks=list(map(int, kv_blocks)))}
+    return {"dk": record(test, "dk", np.concatenate(got_k), np.concatenate(ref_k), 2e-2, stored_bf16=True,
+                         blocks=list(map(int, kv_blocks))),
+            "dv": record(test, "dv", np.concatenate(got_v), np.concatenate(ref_v), 2e-2, stored_bf16=True,
+                         blocks=list(map(int, kv_blocks)))}
 
 
 def _identities(inp, r, h_kv):

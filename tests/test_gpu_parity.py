@@ -32,7 +32,8 @@ def _errors(test, inp, r, f, grads, tol, backward=True, gates=None):
     the parity report. LSEs (saved log2-domain, converted to natural log) are compared in absolute
     terms against the same tolerance."""
     from gpu_util import internal_to_orig, record
-    errs = {"out": record(test, "out", r["out"], f.out, tol)}
+    b16 = inp.dtype == "bf16"                      # out / dq / dk / dv / dgates are stored in the input dtype
+    errs = {"out": record(test, "out", r["out"], f.out, tol, stored_bf16=b16)}
     for b, name in enumerate(("cmp", "slc", "win")):
         o, lse = r["saved"].branch(b)
         errs["o_" + name] = record(test, "o_" + name, internal_to_orig(o, r["perm"]), f.o[name], tol)
@@ -44,7 +45,7 @@ def _errors(test, inp, r, f, grads, tol, backward=True, gates=None):
         errs["lse_" + name] = err
     if backward:
         for name, g, ref in zip(("dq", "dk", "dv", "dgates"), (r["dq"], r["dk"], r["dv"], r["dgates"]), grads):
-            errs[name] = record(test, name, g, ref, tol)
+            errs[name] = record(test, name, g, ref, tol, stored_bf16=b16)
     return errs
 
 
@@ -280,3 +281,20 @@ def test_negative_controls():
     j = int(unsel[0]) - s0
     sc[Q, g, j] = sc[Q, g, :s1 - s0].max() * 2
     assert topk_isolated_check(plan_o, sc, r["I"], kw["T"]) >= 1
+
+
+def test_nsa1d_arm():
+    """The NSA-1D blocking arm (reading R19): fixed-length 1D blocks of 64 / 512 consecutive
+    tokens through ssa.nsa1d_coords on the unchanged tcgen05 kernels — plan = the oracle's 1D partition,
+    parity of the whole step against the oracle on the same (embedded) coordinates."""
+    import oracle as O
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import make_inputs
+    lengths = [3000, 1700]
+    c, grid = ssa.nsa1d_coords(lengths, 4, 8)
+    inp = make_inputs(c, grid, 2, 16, 2, 64, "bf16", seed=23)
+    kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    r, _ = _check_all(inp, kw, expect_tc=True, test="test_nsa1d_arm")
+    assert np.array_equal(r["perm"], np.arange(sum(lengths)))
+    assert np.array_equal(r["plan"].offsets(ssa.LEVEL_CMP).cpu().numpy(), O.block_offsets_1d(lengths, 64))
+    assert np.array_equal(r["plan"].offsets(ssa.LEVEL_SLC).cpu().numpy(), O.block_offsets_1d(lengths, 512))

@@ -51,7 +51,7 @@ def test_window_attention(shift, window_only):
     torch.cuda.synchronize()
     ref = _reference(coords, inp.q, inp.k, inp.v, inp.dout, 2, 8, shift)
     test = f"test_window_attention[shift={shift},window_only={window_only}]"
-    errs = {n: record(test, n, x.float().cpu().numpy().astype(np.float64), r, 2e-2)
+    errs = {n: record(test, n, x.float().cpu().numpy().astype(np.float64), r, 2e-2, stored_bf16=True)
             for n, x, r in zip(("out", "dq", "dk", "dv"), (out, dq, dk, dv), ref)}
     assert all(e <= 2e-2 for e in errs.values()), errs
 
@@ -69,7 +69,7 @@ def test_window_covering_grid_is_full_attention():
     for h in range(H):
         ref[:, h] = O.dense_attention(inp.q[:, h], inp.k[:, h // 4], inp.v[:, h // 4], 1.0 / math.sqrt(d))[0]
     assert record("test_window_covering_grid_is_full_attention", "out", out.float().cpu().numpy().astype(np.float64),
-                  ref, 2e-2) <= 2e-2
+                  ref, 2e-2, stored_bf16=True) <= 2e-2
 
 
 def test_window_only_skips_branches_and_matches_composition():

@@ -89,3 +89,19 @@ def test_errors(rng):
         block_build(np.array([[0, 1, 0, 0]]), (8, 8, 8), 1, 4, 6, 6, 6)   # 6 not multiple of 4
     with pytest.raises(OracleError):
         block_build(np.array([[0, 1, 0, 0]]), (8, 8, 8), 1, 4, 8, 6, 8)   # 6 breaks the chain
+
+
+def test_nsa1d_embedding_is_fixed_length_1d_blocking():
+    """The NSA-1D arm (reading R19) runs on the 3D kernels through a coordinate embedding
+    (paper_2505_17412_b200.ssa.nsa1d_coords, index arithmetic only). Pinned against the oracle's direct
+    1D partition: the block build of the embedded coordinates keeps the index order and its blocks are
+    the fixed-length runs of l_cmp = m_cmp^3 / l_slc = m_slc^3 tokens of every batch item."""
+    import oracle as O
+    from paper_2505_17412_b200.ssa import nsa1d_coords
+    for lengths in ([1000, 700], [512], [1, 64, 65, 1537]):
+        c, grid = nsa1d_coords(lengths, 4, 8)
+        plan = O.block_build(c, grid, len(lengths), 4, 8, 8, 8)
+        assert np.array_equal(plan.perm, np.arange(sum(lengths)))
+        assert np.array_equal(plan.offsets["cmp"], O.block_offsets_1d(lengths, 64))
+        for lvl in ("slc", "win", "q"):
+            assert np.array_equal(plan.offsets[lvl], O.block_offsets_1d(lengths, 512))
