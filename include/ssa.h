@@ -136,6 +136,15 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *                                     skipped branches are 0). With gates (0, 0, 1) this is sparse 3D
  *                                     window attention (the SS-VAE layer). tcgen05 path only
  *                                     (bf16, d = 64, m_win == m_slc == m_q); SSA_ERR_UNSUPPORTED otherwise.
+ *                  SSA_NO_WINDOW    — the window branch is skipped (saved O_win = 0, LSE sentinel):
+ *                                     out = omega_cmp O_cmp + omega_slc O_slc; dgates_win = 0.
+ *                  SSA_ACCUMULATE   — out (forward) and dq, dk, dv, dgates (backward) are added to
+ *                                     what the caller's buffers hold instead of overwriting them.
+ *                                     Together: SSA with SHIFTED windows = one
+ *                                     SSA_NO_WINDOW call on the plan of the coordinates, then one
+ *                                     SSA_WINDOW_ONLY | SSA_ACCUMULATE call on the plan of the shifted
+ *                                     coordinates (whose aligned windows are the shifted windows) with
+ *                                     the same tensors (ssa.py: shifted_window_ssa). tcgen05 path only.
  * ----------------------------------------------------------------------------------------------*/
 #define SSA_INPUT_SORTED 1u
 #define SSA_FORCE_SIMT 2u
@@ -143,6 +152,8 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
 #define SSA_KV_GRAD_FP32 8u   /* dk / dv are written as fp32 (partials of a query-block shard)    */
 #define SSA_WINDOW_ONLY 16u   /* window branch only (sparse 3D window attention)                   */
 #define SSA_LOCAL_ROWS 32u    /* q / gates / dout / out / dq / dgates hold only the owned rows       */
+#define SSA_NO_WINDOW 64u     /* window branch skipped: O_win = 0 (its gate term vanishes)          */
+#define SSA_ACCUMULATE 128u   /* out, dq, dk, dv, dgates are ADDED to the caller's buffers          */
 
 /* ------------------------------------------------------------------------------------------------
  * Learned compression delta and gate projection (readings R17, R18).

@@ -776,3 +776,66 @@ def block_offsets_1d(lengths, l: int) -> np.ndarray:
         starts += list(range(base, base + int(n), l))
         base += int(n)
     return np.array(starts + [base], dtype=np.int64)
+
+
+# --------------------------------------------------------------------------------------------------
+# SSA with shifted sparse 3D windows (§8f row 3): the window branch of Eq. 6 over the non-overlapping
+# m_win^3 windows of the SHIFTED coordinates (x + s, y + s, z + s) — the Swin-style alternation the
+# SS-VAE uses for its sparse window attention, applied to SSA's window module;
+# compression and selection unchanged. READING R20: s is added to all three axes; windows are formed
+# per batch item by floor((coord + s) / m_win).
+# --------------------------------------------------------------------------------------------------
+def _shifted_windows(coords, m_win: int, shift: int):
+    """-> list of ORIGINAL token index arrays, one per non-empty shifted window (python grouping)."""
+    groups = {}
+    for i, (b, x, y, z) in enumerate(np.asarray(coords).tolist()):
+        groups.setdefault((b, (x + shift) // m_win, (y + shift) // m_win, (z + shift) // m_win), []).append(i)
+    return [np.array(groups[k], dtype=np.int64) for k in sorted(groups)]
+
+
+def ssa_forward_shifted(coords, grid, batch, q, k, v, gates, *, shift, h_kv, T, m_cmp, m_slc, m_win, m_q,
+                        I_override=None):
+    """SSA (Eq. 6) with the window branch on shifted windows. Returns a ForwardResult (original order)
+    whose o['win'] / lse['win'] are the shifted-window branch."""
+    f = ssa_forward(coords, grid, batch, q, k, v, gates, h_kv=h_kv, T=T, m_cmp=m_cmp, m_slc=m_slc, m_win=m_win,
+                    m_q=m_q, I_override=I_override)
+    q = np.asarray(q, np.float64)
+    N, H, d = q.shape
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    o_w, l_w = np.zeros((N, H, d)), np.zeros((N, H))
+    for t in _shifted_windows(coords, m_win, shift):
+        for g in range(h_kv):
+            rows = q[t, g * h_s:(g + 1) * h_s].reshape(-1, d)
+            oo, ll, _ = dense_attention(rows, np.asarray(k, np.float64)[t, g], np.asarray(v, np.float64)[t, g], scale)
+            o_w[t, g * h_s:(g + 1) * h_s] = oo.reshape(len(t), h_s, d)
+            l_w[t, g * h_s:(g + 1) * h_s] = ll.reshape(len(t), h_s)
+    f.o["win"], f.lse["win"] = o_w, l_w
+    f.out = gate_combine(f.o["cmp"], f.o["slc"], o_w, gates)
+    return f
+
+
+def ssa_backward_shifted(fwd: ForwardResult, coords, q, k, v, gates, dout, *, shift, m_win, h_kv):
+    """Gradients (dq, dk, dv, dgates) of ssa_forward_shifted (indices constant, R15): the compression
+    and selection branches as in ssa_backward (its window term removed by a zero window gate), plus
+    the shifted-window branch."""
+    g0 = np.asarray(gates, np.float64).copy()
+    g0[..., 2] = 0.0
+    dq, dk, dv, dg = ssa_backward(fwd, q, k, v, g0, dout, h_kv=h_kv)
+    q = np.asarray(q, np.float64)
+    N, H, d = q.shape
+    h_s = H // h_kv
+    scale = 1.0 / math.sqrt(d)
+    do = np.asarray(dout, np.float64)
+    dg[..., 2] = (do * fwd.o["win"]).sum(axis=2)
+    dow = np.asarray(gates, np.float64)[..., 2:3] * do
+    for t in _shifted_windows(coords, m_win, shift):
+        for g in range(h_kv):
+            rows = q[t, g * h_s:(g + 1) * h_s].reshape(-1, d)
+            kk, vv = np.asarray(k, np.float64)[t, g], np.asarray(v, np.float64)[t, g]
+            oo, _, pp = dense_attention(rows, kk, vv, scale)
+            gq, gk, gv = dense_attention_backward(rows, kk, vv, pp, oo, dow[t, g * h_s:(g + 1) * h_s].reshape(-1, d), scale)
+            dq[t, g * h_s:(g + 1) * h_s] += gq.reshape(len(t), h_s, d)
+            dk[t, g] += gk
+            dv[t, g] += gv
+    return dq, dk, dv, dg

@@ -112,8 +112,12 @@ const char* tc_reason(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
 // (100-500x slower) SIMT kernels with SSA_FORCE_SIMT — no silent fallback.
 ssa_status choose_path(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p, bool* tc) {
   *tc = use_tc(d, cfg, p);
-  if (cfg->flags & SSA_WINDOW_ONLY) {
-    if (!*tc) { set_error("SSA_WINDOW_ONLY needs the tcgen05 path (bf16, d = 64, m_win == m_slc == m_q)"); return SSA_ERR_UNSUPPORTED; }
+  if ((cfg->flags & SSA_WINDOW_ONLY) && (cfg->flags & SSA_NO_WINDOW)) { set_error("SSA_WINDOW_ONLY and SSA_NO_WINDOW exclude each other"); return SSA_ERR_ARG; }
+  if (cfg->flags & (SSA_WINDOW_ONLY | SSA_NO_WINDOW | SSA_ACCUMULATE)) {
+    if (!*tc) {
+      set_error("SSA_WINDOW_ONLY / SSA_NO_WINDOW / SSA_ACCUMULATE need the tcgen05 path (bf16, d = 64, m_win == m_slc == m_q)");
+      return SSA_ERR_UNSUPPORTED;
+    }
     return SSA_OK;
   }
   if (cfg->dtype == SSA_BF16 && !*tc && !(cfg->flags & SSA_FORCE_SIMT)) {
@@ -211,6 +215,8 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.D));
   x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
   x->win_only = (cfg->flags & SSA_WINDOW_ONLY) ? 1 : 0;
+  x->no_win = (cfg->flags & SSA_NO_WINDOW) ? 1 : 0;
+  x->accumulate = (cfg->flags & SSA_ACCUMULATE) ? 1 : 0;
   x->save_scores = (cfg->flags & SSA_SAVE_SCORES) ? 1 : 0;
   x->kv_grad_f32 = (cfg->flags & SSA_KV_GRAD_FP32) ? 1 : 0;
   x->perm = p->perm;
@@ -333,6 +339,11 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
       SSA_CUDA_TRY(cudaMemsetAsync(x.lse[b], 0x7f, size_t(rows) * 4, st));
     }
     SSA_CUDA_TRY(cudaMemsetAsync(x.I, 0xff, size_t(d.n_q) * d.h_kv * d.T * 4, st));
+  }
+  if (x.no_win) {   // skipped window branch: O_win = 0, LSE sentinel
+    const int64_t rows = int64_t(d.N) * d.H;
+    SSA_CUDA_TRY(cudaMemsetAsync(x.o[2], 0, size_t(rows) * d.D * 4, st));
+    SSA_CUDA_TRY(cudaMemsetAsync(x.lse[2], 0x7f, size_t(rows) * 4, st));
   }
   if (tc) {
     if ((s = tc_forward(x, tc_ws, st, ext_kc ? kv_ev : nullptr, ext_kc)) != SSA_OK) return s;

@@ -45,6 +45,8 @@ struct Ctx {
   float scale;                    // softmax scale (natural)
   int32_t sorted_input;
   int32_t win_only;                   // SSA_WINDOW_ONLY: compression / selection branches skipped
+  int32_t no_win;                     // SSA_NO_WINDOW: the window branch skipped (O_win = 0)
+  int32_t accumulate;                 // SSA_ACCUMULATE: out / dq / dk / dv / dgates += instead of =
   int32_t q_begin, q_end;         // owned query blocks [q_begin, q_end) (plan order)
   int32_t tok_begin, tok_end;     // their token range
   int32_t row_lo, row_hi;         // rows (plan order) whose caller row tensors may be touched: the owned

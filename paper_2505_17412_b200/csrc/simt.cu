@@ -833,13 +833,21 @@ __global__ void k_bwd_final_kv(Ctx c) {
   const float gk[4] = {ak.x + ck.x * inv, ak.y + ck.y * inv, ak.z + ck.z * inv, ak.w + ck.w * inv};
   const float gv[4] = {av.x + cv.x * inv, av.y + cv.y * inv, av.z + cv.z * inv, av.w + cv.w * inv};
   if (c.kv_grad_f32) {
-    *reinterpret_cast<float4*>(static_cast<float*>(c.dk) + o) = make_float4(gk[0], gk[1], gk[2], gk[3]);
-    *reinterpret_cast<float4*>(static_cast<float*>(c.dv) + o) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+    float4* pk = reinterpret_cast<float4*>(static_cast<float*>(c.dk) + o);
+    float4* pv = reinterpret_cast<float4*>(static_cast<float*>(c.dv) + o);
+    float4 ak4 = make_float4(gk[0], gk[1], gk[2], gk[3]), av4 = make_float4(gv[0], gv[1], gv[2], gv[3]);
+    if (c.accumulate) {
+      const float4 a = *pk, b = *pv;
+      ak4.x += a.x; ak4.y += a.y; ak4.z += a.z; ak4.w += a.w;
+      av4.x += b.x; av4.y += b.y; av4.z += b.z; av4.w += b.w;
+    }
+    *pk = ak4;
+    *pv = av4;
   } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      st(static_cast<T*>(c.dk) + o + u, gk[u]);
-      st(static_cast<T*>(c.dv) + o + u, gv[u]);
+    for (int u = 0; u < 4; ++u) {   // SSA_ACCUMULATE: add to the caller's dk / dv
+      st(static_cast<T*>(c.dk) + o + u, c.accumulate ? gk[u] + ld(static_cast<const T*>(c.dk) + o + u) : gk[u]);
+      st(static_cast<T*>(c.dv) + o + u, c.accumulate ? gv[u] + ld(static_cast<const T*>(c.dv) + o + u) : gv[u]);
     }
   }
 }

@@ -134,7 +134,8 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
   for (int b = 0; b < 3; ++b) {
     if (c.dz) c.dz[int64_t(rr) * 3 + b] = acc[b] * w[b] * (1.f - w[b]);   // gate projection backward (R18)
     c.Dd[b][rr] = w[b] * acc[b] * ds;
-    static_cast<__nv_bfloat16*>(c.dgates)[(int64_t(src_p) * c.H + h) * 3 + b] = __float2bfloat16_rn(acc[b]);
+    __nv_bfloat16* dg = static_cast<__nv_bfloat16*>(c.dgates) + (int64_t(src_p) * c.H + h) * 3 + b;
+    *dg = __float2bfloat16_rn(c.accumulate ? acc[b] + __bfloat162float(*dg) : acc[b]);
   }
 }
 
@@ -299,8 +300,8 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
     for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], 1);   // (unselected: empty range)
     if (n <= kMaxKT && n > 0 && S->tile_br[n - 1] != 0) flush();
     pos = kKT;                                    // the window starts a fresh tile
-    add_block(t0, t1, 2);
-    if (n <= kMaxKT) flush();
+    if (!c.no_win) add_block(t0, t1, 2);          // SSA_NO_WINDOW: no window tiles
+    if (n <= kMaxKT && n > 0) flush();
     n = min(n, kMaxKT);
     S->tile_seg[n] = ns;
     S->n_tiles = n;
@@ -542,10 +543,23 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         const int dst = c.sorted_input ? tok : c.perm[tok];
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
 #pragma unroll
-        for (int e = 0; e < kD; e += 8)
-          *reinterpret_cast<uint4*>(o + e) =
-              make_uint4(pack_bf16(v[e] * osc, v[e + 1] * osc), pack_bf16(v[e + 2] * osc, v[e + 3] * osc),
-                         pack_bf16(v[e + 4] * osc, v[e + 5] * osc), pack_bf16(v[e + 6] * osc, v[e + 7] * osc));
+        for (int e = 0; e < kD; e += 8) {
+          float y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) y[u] = v[e + u] * osc;
+          if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's dq
+            const uint4 old = *reinterpret_cast<const uint4*>(o + e);
+            const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float2 f = unpack_bf16(ow[u]);
+              y[2 * u] += f.x;
+              y[2 * u + 1] += f.y;
+            }
+          }
+          *reinterpret_cast<uint4*>(o + e) = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                                                        pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+        }
       }
     }
   }
@@ -655,7 +669,7 @@ __device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
   const int l0 = c.inv_off[key], l1 = c.inv_off[key + 1];
   it->li = min(l1, l0 + it->chunk * kQBlocksPerItem);
   it->le = min(l1, it->li + kQBlocksPerItem);
-  it->with_win = it->chunk == nch - 1 && it->kblock >= c.q_begin && it->kblock < c.q_end;  // window = block
+  it->with_win = !c.no_win && it->chunk == nch - 1 && it->kblock >= c.q_begin && it->kblock < c.q_end;  // window = block
   it->first = it->chunk == 0;
   it->part_slot = id;
   it->ra = it->re = 0;

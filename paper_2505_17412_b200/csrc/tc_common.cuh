@@ -203,6 +203,10 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // ------------------------------------------------------------------------------------------------
 // manual writes into SWIZZLE_128B bf16 tiles (region base 1024-B aligned)
 // ------------------------------------------------------------------------------------------------
+// bf16x2 word -> two floats (element lo in the low half)
+__device__ __forceinline__ float2 unpack_bf16(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);

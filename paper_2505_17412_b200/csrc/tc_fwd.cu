@@ -671,7 +671,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j]);   // (unselected: empty range)
     S->n_slc_tiles = min(n, kMaxTiles);
     pos = kTile;                                  // the window starts a fresh tile
-    add_block(t0, t1);
+    if (!c.no_win) add_block(t0, t1);             // SSA_NO_WINDOW: no window tile
     if (n <= kMaxTiles) flush();
     n = min(n, kMaxTiles);
     S->tile_seg[n] = ns;
@@ -936,7 +936,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         for (int ii = 0; ii < 8; ++ii) {
           const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
           const int64_t grow = qrow0 + rr;
-          e_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 4 * ch);
+          if (!c.no_win) e_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 4 * ch);
           e_cm[ii] = *reinterpret_cast<const float4*>(ocm_g + grow * kD + 4 * ch);
           e_w[ii][0] = c.gs[grow * 3];
           e_w[ii][1] = c.gs[grow * 3 + 1];
@@ -962,12 +962,14 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       tc_fence_before();
       mbar_arrive(&S->o_empty[wg]);
       if (rvalid) {
-        if (n_slc_tiles > 0) c.lse[1][row] = lse_slc;   // window-only: keep the "no keys" sentinel (api.cu)
-        c.lse[2][row] = m + lg2(l);
+        // window-only: keep the "no keys" sentinel of the selection LSE (api.cu); no-window: the O in
+        // TMEM is the selection branch's (its tiles were the last ones)
+        if (n_slc_tiles > 0 && !c.no_win) c.lse[1][row] = lse_slc;
+        c.lse[c.no_win ? 1 : 2][row] = m + lg2(l);
       }
       __syncwarp();
       if (warp == 0) TRACE_SW(2, 0, pr);
-      float* ow = static_cast<float*>(c.o[2]);
+      float* ow = static_cast<float*>(c.o[c.no_win ? 1 : 2]);
 #pragma unroll
       for (int bt = 0; bt < 2; ++bt) {
         if (bt == 1) epi_load(1);
@@ -977,13 +979,20 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = wrow0 + rl;
           if (rr < rows) {
             const int64_t grow = qrow0 + rr;
-            const float4 wn = staged_chunk(wbuf, rl, ch), sl = e_sl[ii], cm = e_cm[ii];
-            const float w0 = e_w[ii][0], w1 = e_w[ii][1], w2 = e_w[ii][2];
+            const float4 wn = staged_chunk(wbuf, rl, ch), cm = e_cm[ii];
+            const float4 sl = c.no_win ? wn : e_sl[ii];
+            const float w0 = e_w[ii][0], w1 = e_w[ii][1], w2 = c.no_win ? 0.f : e_w[ii][2];
             *reinterpret_cast<float4*>(ow + grow * kD + 4 * ch) = wn;
             __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) +
                                  (int64_t(e_dst[ii]) * c.H + g * c.h_s + rr % c.h_s) * kD + 4 * ch;
-            *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y),
-                                                        pack_bf16(w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w));
+            float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
+                                   w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w);
+            if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's out (e.g. the shifted-window pass)
+              const uint2 old = *reinterpret_cast<const uint2*>(out);
+              const float2 a = unpack_bf16(old.x), b = unpack_bf16(old.y);
+              y.x += a.x; y.y += a.y; y.z += b.x; y.w += b.y;
+            }
+            *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
           }
         }
       }

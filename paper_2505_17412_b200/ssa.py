@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa_b200.so"))   # 
 
 SSA_F32, SSA_BF16 = 0, 1
 SSA_INPUT_SORTED, SSA_FORCE_SIMT, SSA_SAVE_SCORES, SSA_KV_GRAD_FP32, SSA_WINDOW_ONLY, SSA_LOCAL_ROWS = 1, 2, 4, 8, 16, 32
+SSA_NO_WINDOW, SSA_ACCUMULATE = 64, 128
 LEVEL_CMP, LEVEL_SLC, LEVEL_WIN, LEVEL_Q = 0, 1, 2, 3
 STATUS = ["SSA_OK", "SSA_ERR_ARG", "SSA_ERR_DUP_COORD", "SSA_ERR_COORD_RANGE", "SSA_ERR_HIERARCHY",
           "SSA_ERR_BAD_STATE", "SSA_ERR_WORKSPACE", "SSA_ERR_UNSUPPORTED", "SSA_ERR_CUDA"]
@@ -458,6 +459,34 @@ def window_attention(coords: torch.Tensor, grid, batch: int, m_win: int, q, k, v
     gates[..., 2] = 1
     out, saved = ssa_forward(plan, cfg, q, k, v, gates)
     return out, (plan, cfg, saved, gates)
+
+
+def shifted_window_ssa(coords: torch.Tensor, grid, batch: int, m_cmp: int, m_slc: int, shift: int, cfg: AttnCfg,
+                       q, k, v, gates):
+    """SSA with SHIFTED sparse 3D windows (the SS-VAE's Swin-style alternation, P:87-88,
+    applied to SSA's window branch): compression and selection on the blocks of `coords`, the
+    window branch on the aligned m_slc^3 windows of coords + shift. Composition over the C ABI (no
+    arithmetic here): ssa_forward with SSA_NO_WINDOW on the plan of coords, then ssa_forward with
+    SSA_WINDOW_ONLY | SSA_ACCUMULATE on the plan of the shifted coordinates (grid + shift), which adds
+    omega_win * O_win(shifted) into the same `out`. Returns (out, ctx) for shifted_window_ssa_backward."""
+    import dataclasses
+    plan0 = ssa_build_blocks(coords, grid, batch, m_cmp, m_slc, m_slc, m_slc)
+    cs = coords.clone()
+    cs[:, 1:] += int(shift)
+    plan1 = ssa_build_blocks(cs, tuple(int(x) + int(shift) for x in grid), batch, m_cmp, m_slc, m_slc, m_slc)
+    c0 = dataclasses.replace(cfg, flags=cfg.flags | SSA_NO_WINDOW)
+    c1 = dataclasses.replace(cfg, flags=cfg.flags | SSA_WINDOW_ONLY | SSA_ACCUMULATE)
+    out, s0 = ssa_forward(plan0, c0, q, k, v, gates)
+    out, s1 = ssa_forward(plan1, c1, q, k, v, gates, out=out)
+    return out, (plan0, plan1, c0, c1, s0, s1)
+
+
+def shifted_window_ssa_backward(ctx, q, k, v, gates, dout):
+    """(dq, dk, dv, dgates) of shifted_window_ssa: the SSA_NO_WINDOW backward, then the shifted
+    window-only backward accumulated into the same buffers (SSA_ACCUMULATE)."""
+    plan0, plan1, c0, c1, s0, s1 = ctx
+    grads = ssa_backward(plan0, c0, s0, q, k, v, gates, dout)
+    return ssa_backward(plan1, c1, s1, q, k, v, gates, dout, grads=grads)
 
 
 def window_attention_backward(ctx, q, k, v, dout):

@@ -264,7 +264,7 @@ def test_negative_controls():
     inp2 = replace(inp, gates=inp.gates[..., [1, 0, 2]].copy())
     f2, g2 = _oracle(inp2, r["I"], kw)
     e2 = _errors("negctl:gates", inp, r, f2, g2, tol)
-    assert e2["out"] > tol and e2["dgates"] > tol, e2
+    assert e2["out"] > tol and e2["dq"] > tol, e2        # (dgates = <dO, O_c> does not involve the gates)
     # (3) perturbed saved LSE (selection branch, one query block's rows, +0.25 in log2 units) -> GPU backward
     o_slc, lse_slc = r["saved"].branch(1)
     a, e = int(plan_o.offsets["q"][Q]), int(plan_o.offsets["q"][Q + 1])

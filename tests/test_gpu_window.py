@@ -96,3 +96,36 @@ def test_window_only_skips_branches_and_matches_composition():
         # branch's exact zero changes an fp32 rounding): |a - b| <= 2^-8 |b| element-wise
         a, b = a.float(), b.float()
         assert torch.equal(a, b) or bool(((a - b).abs() <= 2.0 ** -8 * b.abs()).all())
+
+
+@pytest.mark.parametrize("shift", [0, 4])
+def test_shifted_window_ssa(shift):
+    """SSA with shifted windows (reading R20): ssa.shifted_window_ssa = SSA_NO_WINDOW on
+    the plan of the coordinates + SSA_WINDOW_ONLY | SSA_ACCUMULATE on the plan of the shifted ones,
+    against oracle.ssa_forward_shifted / ssa_backward_shifted (GPU indices fed to the oracle). shift 0
+    must also reproduce the plain step."""
+    coords = batch_coords([sphere_shell(32, 13.0, 2.0), sphere_shell(32, 9.0, 2.0)])
+    grid = (32, 32, 32)
+    inp = make_inputs(coords, grid, 2, 16, 2, 64, "bf16", seed=15)
+    q, k, v, g, do = (to_dev(x, torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout))
+    cfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=4, dtype=torch.bfloat16)
+    c = torch.from_numpy(coords).cuda()
+    out, ctx = ssa.shifted_window_ssa(c, grid, 2, 4, 8, shift, cfg, q, k, v, g)
+    dq, dk, dv, dg = ssa.shifted_window_ssa_backward(ctx, q, k, v, g, do)
+    torch.cuda.synchronize()
+    I = ctx[4].indices().cpu().numpy().astype(np.int64)
+    kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
+    f = O.ssa_forward_shifted(coords, grid, 2, inp.q, inp.k, inp.v, inp.gates, shift=shift, I_override=I, **kw)
+    ref = O.ssa_backward_shifted(f, coords, inp.q, inp.k, inp.v, inp.gates, inp.dout, shift=shift, m_win=8, h_kv=2)
+    test = f"test_shifted_window_ssa[{shift}]"
+    errs = {n: record(test, n, x.float().cpu().numpy().astype(np.float64), r, 2e-2, stored_bf16=True)
+            for n, x, r in zip(("out", "dq", "dk", "dv", "dgates"), (out, dq, dk, dv, dg), (f.out,) + tuple(ref))}
+    assert all(e <= 2e-2 for e in errs.values()), errs
+    if shift == 0:
+        plan = ssa.ssa_build_blocks(c, grid, 2, 4, 8, 8, 8)
+        o0, s0 = ssa.ssa_forward(plan, cfg, q, k, v, g)
+        r0 = ssa.ssa_backward(plan, cfg, s0, q, k, v, g, do)
+        torch.cuda.synchronize()
+        for a, b in zip((out, dq, dk, dv, dg), (o0,) + tuple(r0)):
+            a, b = a.float(), b.float()      # two bf16 roundings (pass sum) vs one: 1 ulp + fp32 order
+            assert bool(((a - b).abs() <= 2.0 ** -7 * b.abs() + 1e-3 * b.pow(2).mean().sqrt()).all())

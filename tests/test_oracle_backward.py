@@ -103,3 +103,39 @@ def test_block_kv_grad_equals_full_backward(rng):
     a = O.compression_kv_grad(plan, q[P], f.k_cmp, f.v_cmp, gates[P], dout[P], 2, scale, b, cols, chunk=5)
     z = O.compression_kv_grad(plan, q[P], f.k_cmp, f.v_cmp, gates[P], dout[P], 2, scale, b, cols, chunk=10 ** 6)
     assert np.allclose(a[0], z[0], rtol=0, atol=1e-12) and np.allclose(a[1], z[1], rtol=0, atol=1e-12)
+
+
+def test_shifted_window_ssa(rng):
+    """Shifted-window SSA (reading R20): shift 0 is plain SSA; with shift 2 the output differs only in
+    the window term (cmp / slc branches unchanged) and the analytic gradients match central finite
+    differences of the shifted forward (indices frozen)."""
+    c, q, k, v, gates, dout = _problem(rng)
+    f0 = O.ssa_forward(c, (8, 8, 8), 2, q, k, v, gates, **KW)
+    fs0 = O.ssa_forward_shifted(c, (8, 8, 8), 2, q, k, v, gates, shift=0, **KW)
+    assert np.allclose(fs0.out, f0.out, rtol=0, atol=1e-14)
+    g_plain = O.ssa_backward(f0, q, k, v, gates, dout, h_kv=2)
+    g_s0 = O.ssa_backward_shifted(fs0, c, q, k, v, gates, dout, shift=0, m_win=4, h_kv=2)
+    for a, b in zip(g_plain, g_s0):
+        assert np.allclose(a, b, rtol=0, atol=1e-12)
+    fs = O.ssa_forward_shifted(c, (8, 8, 8), 2, q, k, v, gates, shift=2, **KW)
+    assert np.allclose(fs.o["cmp"], f0.o["cmp"]) and np.allclose(fs.o["slc"], f0.o["slc"])
+    assert not np.allclose(fs.o["win"], f0.o["win"])
+    grads = O.ssa_backward_shifted(fs, c, q, k, v, gates, dout, shift=2, m_win=4, h_kv=2)
+
+    def loss():
+        f = O.ssa_forward_shifted(c, (8, 8, 8), 2, q, k, v, gates, shift=2, I_override=fs.I, **KW)
+        return float((f.out * dout).sum())
+
+    h = 1e-5
+    sel = np.random.Generator(np.random.PCG64(9))
+    for arr, grad in zip((q, k, v, gates), grads):
+        flat, gflat = arr.reshape(-1), grad.reshape(-1)
+        for idx in sel.choice(flat.size, size=10, replace=False):
+            orig = flat[idx]
+            flat[idx] = orig + h
+            lp = loss()
+            flat[idx] = orig - h
+            lm = loss()
+            flat[idx] = orig
+            fd = (lp - lm) / (2 * h)
+            assert abs(fd - gflat[idx]) <= 1e-5 * max(1.0, abs(fd))
