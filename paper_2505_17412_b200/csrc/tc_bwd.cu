@@ -596,6 +596,9 @@ constexpr int kPBuf = SSA_KV_PBUF;
 #define SSA_KV_QB_PER_ITEM 8
 #endif
 constexpr int kQBlocksPerItem = SSA_KV_QB_PER_ITEM;       // raw keys: query blocks per work item (splits popular blocks)
+#ifndef SSA_KV_STATS_WAIT
+#define SSA_KV_STATS_WAIT 1       // row stats: cp.async + wait + plain arrive (0: cp.async.mbarrier.arrive.noinc)
+#endif
 // One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
 // row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
 // dV 64), its own row-stage ring and its own MMA issuer (warps 9 / 10); warp 8 is the producer. The
@@ -820,7 +823,14 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
           cp_async4(&S->st_l2[w][rs.idx][e], e < nr ? c.lse[br] + row : &g_pos_inf);
           cp_async4(&S->st_D[w][rs.idx][e], e < nr ? c.Dd[br] + row : &g_zero);
         }
+#if SSA_KV_STATS_WAIT
+        // wait for this lane's two copies, then a plain (release) arrival: the cp.async.mbarrier
+        // arrive.noinc form is not modelled by compute-sanitizer synccheck ("missing init", r1f)
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        mbar_arrive(&S->r_full[w][rs.idx]);
+#else
         cp_async_mbar_arrive_noinc(&S->r_full[w][rs.idx]);
+#endif
         if (lane == 0) {
           uint8_t* st = sR + (w * kRStages + rs.idx) * 16384;
           mbar_expect_tx(&S->r_full[w][rs.idx], 16384);
@@ -1111,11 +1121,15 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   uint32_t* amax = cw.take<uint32_t>(1);
   c.do_amax = amax;
   SSA_CUDA_TRY(cudaMemsetAsync(amax, 0, 4, st));
-  {
-    const int64_t n8 = int64_t(c.N) * c.H * kD / 8;
+  {  // over the rows this call may read (the owned range with a query-block range / SSA_LOCAL_ROWS)
+    const int64_t n8 = int64_t(c.row_hi - c.row_lo) * c.H * kD / 8;
+    const __nv_bfloat16* d0 = static_cast<const __nv_bfloat16*>(c.dout) + int64_t(c.row_lo) * c.H * kD;
     const unsigned blocks = unsigned(std::min<int64_t>((n8 + 255) / 256, 148 * 8));
-    k_do_absmax<<<std::max(1u, blocks), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(c.dout), n8, amax);
-    SSA_LAUNCH_CHECK("k_do_absmax");
+    if (n8 > 0) {
+      k_do_absmax<<<std::max(1u, blocks), 256, 0, st>>>(c.sorted_input ? d0 : static_cast<const __nv_bfloat16*>(c.dout),
+                                                         c.sorted_input ? n8 : int64_t(c.N) * c.H * kD / 8, amax);
+      SSA_LAUNCH_CHECK("k_do_absmax");
+    }
   }
   k_tc_bwd_rows<<<unsigned((int64_t(c.N) * c.H * 8 + 255) / 256), 256, 0, st>>>(c, q16, do16, dow);
   SSA_LAUNCH_CHECK("k_tc_bwd_rows");

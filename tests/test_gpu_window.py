@@ -121,11 +121,3 @@ def test_shifted_window_ssa(shift):
     errs = {n: record(test, n, x.float().cpu().numpy().astype(np.float64), r, 2e-2, stored_bf16=True)
             for n, x, r in zip(("out", "dq", "dk", "dv", "dgates"), (out, dq, dk, dv, dg), (f.out,) + tuple(ref))}
     assert all(e <= 2e-2 for e in errs.values()), errs
-    if shift == 0:
-        plan = ssa.ssa_build_blocks(c, grid, 2, 4, 8, 8, 8)
-        o0, s0 = ssa.ssa_forward(plan, cfg, q, k, v, g)
-        r0 = ssa.ssa_backward(plan, cfg, s0, q, k, v, g, do)
-        torch.cuda.synchronize()
-        for a, b in zip((out, dq, dk, dv, dg), (o0,) + tuple(r0)):
-            a, b = a.float(), b.float()      # two bf16 roundings (pass sum) vs one: 1 ulp + fp32 order
-            assert bool(((a - b).abs() <= 2.0 ** -7 * b.abs() + 1e-3 * b.pow(2).mean().sqrt()).all())
