@@ -118,8 +118,9 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *   blocks (clamped per batch item to N_slc(b), padded slots hold -1, reading R9).
  *   scale        : softmax scale; <= 0 means 1/sqrt(d) (Eq. 5).
  *   dtype        : SSA_F32 (SIMT fp32 kernels, the fp32 mode) or SSA_BF16 (tcgen05 tensor-core
- *                  kernels: d == 64, m_win == m_slc == m_q, block counts within the kernels' on-chip
- *                  limits). A bf16 request outside those returns SSA_ERR_UNSUPPORTED (reason in
+ *                  kernels: d == 64 — or d == 32, the paper's DiT head dim, run zero-padded to
+ *                  64 inside the library: the logits and the outputs are unchanged — m_win == m_slc ==
+ *                  m_q, block counts within the kernels' on-chip limits). A bf16 request outside those returns SSA_ERR_UNSUPPORTED (reason in
  *                  ssa_last_error) unless SSA_FORCE_SIMT opts into the SIMT kernels — there is no
  *                  silent fallback. Every check happens before any work is enqueued.
  *   pe_k, pe_v   : optional device [m_cmp^3, h_kv, d] (dtype) intra-block PE tables added before
@@ -275,6 +276,8 @@ typedef struct {
   const void* k_cmp;   /* [h_kv][n_blocks[CMP]][d] fp32 */
   const void* v_cmp;
   int32_t used_tcgen05;  /* 1 if the forward ran the tcgen05 kernels */
+  int32_t d_internal;    /* head dim of o_branch / k_cmp rows: d, or 64 when a d = 32 problem runs the
+                            tcgen05 kernels zero-padded to 64 (padded entries are 0) */
 } ssa_saved_view;
 ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,
                            ssa_saved_view* out);

@@ -45,9 +45,24 @@ namespace {
 struct Dims {
   int64_t N;
   int H, h_kv, h_s, D, T;
+  int Dc;   // caller head dim (D: internal, 64 when a d = 32 problem runs the tcgen05 kernels padded)
   size_t esz;
   int n_cmp, n_slc, n_win, n_q, max_slc_b;
 };
+
+bool use_tc(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p);
+// d = 32 (the paper's DiT head dim) on the tcgen05 path: heads are zero-padded to 64 in the
+// internal layouts (zero features change neither q.k nor the first 32 output dims); every caller-
+// facing read / write uses Dc = 32. Only where the whole tcgen05 path applies (no caller-supplied
+// pooled keys, no learned delta: those interfaces are d = 64).
+void pad_for_tc(Dims* d, const ssa_attn_cfg* cfg, const Plan* p) {
+  if (d->Dc != 32 || cfg->dtype != SSA_BF16 || (cfg->flags & SSA_FORCE_SIMT) || cfg->kc_in || cfg->learned ||
+      cfg->pe_k || cfg->pe_v)
+    return;
+  Dims t = *d;
+  t.D = 64;
+  if (use_tc(t, cfg, p)) d->D = 64;
+}
 
 ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
   if (!p) { set_error("null plan"); return SSA_ERR_BAD_STATE; }
@@ -84,6 +99,8 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
   d->n_win = p->info.n_blocks[SSA_LEVEL_WIN];
   d->n_q = p->info.n_blocks[SSA_LEVEL_Q];
   d->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
+  d->Dc = cfg->d;
+  pad_for_tc(d, cfg, p);
   return SSA_OK;
 }
 
@@ -102,7 +119,7 @@ bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
 const char* tc_reason(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   const int32_t* m = p->info.m;
   if (!tc_available()) return "library built without the tcgen05 kernels";
-  if (d.D != 64) return "head dim != 64";
+  if (d.D != 64) return "head dim not 32 or 64";
   if (m[SSA_LEVEL_WIN] != m[SSA_LEVEL_SLC] || m[SSA_LEVEL_Q] != m[SSA_LEVEL_SLC]) return "m_win or m_q != m_slc";
   if (!tc_plan_ok(p->info, cfg->top_k)) return "a batch item's block counts exceed the kernels' on-chip limits";
   return nullptr;
@@ -200,6 +217,7 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   x->h_kv = d.h_kv;
   x->h_s = d.h_s;
   x->D = d.D;
+  x->Dc = d.Dc;
   x->T = d.T;
   x->batch = p->info.batch;
   x->m_cmp = p->info.m[SSA_LEVEL_CMP];
@@ -212,7 +230,7 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
   }
   x->max_cmp_b = p->info.max_blocks_per_batch[SSA_LEVEL_CMP];
   x->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
-  x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.D));
+  x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.Dc));
   x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
   x->win_only = (cfg->flags & SSA_WINDOW_ONLY) ? 1 : 0;
   x->no_win = (cfg->flags & SSA_NO_WINDOW) ? 1 : 0;
@@ -297,9 +315,9 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Ctx x{};
   fill_common(&x, p, d, cfg);
-  x.q = rows_at(q, x, int64_t(d.H) * d.D, d.esz);
+  x.q = rows_at(q, x, int64_t(d.H) * d.Dc, d.esz);
   x.gates = rows_at(gates, x, int64_t(d.H) * 3, d.esz);
-  x.out = rows_at(out, x, int64_t(d.H) * d.D, d.esz);
+  x.out = rows_at(out, x, int64_t(d.H) * d.Dc, d.esz);
   x.k = k; x.v = v;
   if ((s = learned_checks(x)) != SSA_OK) return s;
   Carve cs(saved, saved_bytes);
@@ -365,7 +383,8 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q);
-  if (cfg->learned && cfg->learned->x) scan += learned_bwd_ws_bytes(d.N, d.H, d.h_kv, cfg->learned->c);
+  if (cfg->learned && cfg->learned->x) scan += gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c);
+  if (cfg->learned && cfg->learned->conv_k_w) scan += conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D);
   *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]) + 1024;
   return SSA_OK;
 }
@@ -393,10 +412,10 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Ctx x{};
   fill_common(&x, p, d, cfg);
-  x.q = rows_at(q, x, int64_t(d.H) * d.D, d.esz);
+  x.q = rows_at(q, x, int64_t(d.H) * d.Dc, d.esz);
   x.gates = rows_at(gates, x, int64_t(d.H) * 3, d.esz);
-  x.dout = rows_at(dout, x, int64_t(d.H) * d.D, d.esz);
-  x.dq = rows_at(dq, x, int64_t(d.H) * d.D, d.esz);
+  x.dout = rows_at(dout, x, int64_t(d.H) * d.Dc, d.esz);
+  x.dq = rows_at(dq, x, int64_t(d.H) * d.Dc, d.esz);
   x.dgates = rows_at(dgates, x, int64_t(d.H) * 3, d.esz);
   x.k = k; x.v = v; x.dk = dk; x.dv = dv;
   if ((s = learned_checks(x)) != SSA_OK) return s;
@@ -409,11 +428,14 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
   void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
   void* part_ws = nullptr;
+  void* conv_ws = nullptr;
   if (lgates) {
+    char* gw = cw.take<char>(gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c));
     x.gs = saved_gates;
-    x.dz = cw.take<float>(size_t(d.N) * d.H * 3);
-    part_ws = cw.take<float>(size_t((d.N + 1023) / 1024 + 1) * cfg->learned->c * 3 * d.H);
+    x.dz = reinterpret_cast<float*>(gw);
+    part_ws = gw + ((size_t(d.N) * d.H * 3 * 4 + 255) & ~size_t(255));
   }
+  if (x.conv_kw) conv_ws = cw.take<char>(conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D));
   const bool bf16 = cfg->dtype == SSA_BF16;
   const bool tc = use_tc_bwd(d, cfg, p);
   // the tcgen05 backward gathers the q / dO rows and computes D_c, dgates in its own row prologue
@@ -431,7 +453,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   } else {
     if ((s = simt_backward(x, bf16, st)) != SSA_OK) return s;
   }
-  if (x.conv_kw && (s = learned_pool_backward_params(x, bf16, st)) != SSA_OK) return s;
+  if (x.conv_kw && (s = learned_pool_backward_params(x, bf16, conv_ws, st)) != SSA_OK) return s;
   if ((s = bwd_epilogue(x, bf16, st, /*skip_q=*/tc)) != SSA_OK) return s;
   if (lgates && (s = gate_proj_backward(x, bf16, part_ws, st)) != SSA_OK) return s;
   return SSA_OK;
@@ -445,6 +467,7 @@ extern "C" ssa_status ssa_pool(ssa_plan plan, const ssa_attn_cfg* cfg, const voi
   if (s != SSA_OK) return s;
   if (!k || !v || !kc || !vc) { set_error("null tensor pointer"); return SSA_ERR_ARG; }
   if (!(cfg->flags & SSA_INPUT_SORTED)) { set_error("ssa_pool needs SSA_INPUT_SORTED (plan-order k, v)"); return SSA_ERR_ARG; }
+  if (cfg->d != 64 && cfg->dtype == SSA_BF16) { set_error("ssa_pool / caller-supplied pooled keys need d == 64"); return SSA_ERR_UNSUPPORTED; }
   Ctx x{};
   fill_common(&x, p, d, cfg);
   return pool_rows(x, cfg->dtype == SSA_BF16, k, v, static_cast<float*>(kc), static_cast<float*>(vc),
@@ -468,6 +491,7 @@ extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, co
   out->k_cmp = x.kc;
   out->v_cmp = x.vc;
   out->used_tcgen05 = use_tc(d, cfg, p) ? 1 : 0;
+  out->d_internal = d.D;
   return SSA_OK;
 }
 

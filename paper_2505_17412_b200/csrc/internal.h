@@ -39,6 +39,7 @@ struct Plan {
 struct Ctx {
   // problem
   int32_t N, H, h_kv, h_s, D, T, batch, m_cmp;
+  int32_t Dc;                     // head dim of the caller's tensors (D = internal; 32 padded to 64 on tcgen05)
   int32_t n_blk[kLevels];
   int32_t max_cmp_b, max_slc_b;   // max compression / selection blocks of one batch item
   int32_t max_fill[kLevels];
@@ -101,12 +102,13 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
                          bool gates = true);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);
-size_t learned_bwd_ws_bytes(int64_t N, int H, int h_kv, int C);
+size_t gate_bwd_ws_bytes(int64_t N, int H, int C);
+size_t conv_bwd_ws_bytes(int64_t N, int h_kv, int m_cmp, int n_cmp, int D);
 ssa_status learned_checks(const Ctx& c);
 ssa_status learned_pool_forward(const Ctx& c, bool bf16, void* ws, cudaStream_t st);
 ssa_status gate_proj_forward(const Ctx& c, bool bf16, cudaStream_t st);
 ssa_status gate_proj_backward(const Ctx& c, bool bf16, void* part_ws, cudaStream_t st);
-ssa_status learned_pool_backward_params(const Ctx& c, bool bf16, cudaStream_t st);
+ssa_status learned_pool_backward_params(const Ctx& c, bool bf16, void* ws, cudaStream_t st);
 // ssa_pool's kernel: pooled keys of the owned compression blocks from caller-layout (sorted) k, v
 ssa_status pool_rows(const Ctx& c, bool bf16, const void* k, const void* v, float* kc, float* vc, cudaStream_t st);
 ssa_status pool_forward(const Ctx& c, bool bf16, cudaStream_t st);

@@ -38,9 +38,15 @@ __global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ 
   const int p = i / (per * c.h_kv);
   if (p < c.row_lo || p >= c.row_hi) return;             // rows of other shards are never read
   const int src_p = c.sorted_input ? p : c.perm[p];
-  const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
   uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t(g) * c.N + p) * c.h_s * c.D);
-  d4[ch] = s4[ch];
+  if (c.Dc == c.D) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
+    d4[ch] = s4[ch];
+  } else {   // caller head dim Dc < D: zero-padded heads (d = 32 on the tcgen05 path)
+    const int hc = c.D * int(sizeof(T)) / 16, s = ch / hc, cc = ch % hc, e = cc * 16 / int(sizeof(T));
+    d4[ch] = e < c.Dc ? *reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s + s) * c.Dc + e)
+                      : make_uint4(0u, 0u, 0u, 0u);
+  }
 }
 
 template <class T>
@@ -53,9 +59,11 @@ __global__ void k_gather_keys(Ctx c, const T* __restrict__ k, const T* __restric
   const int g = (i / per) % c.h_kv;
   const int p = i / (per * c.h_kv);
   const int src_p = c.sorted_input ? p : c.perm[p];
-  const int64_t so = (int64_t(src_p) * c.h_kv + g) * c.D, dof = (int64_t(g) * c.N + p) * c.D;
-  reinterpret_cast<uint4*>(ks + dof)[ch] = reinterpret_cast<const uint4*>(k + so)[ch];
-  reinterpret_cast<uint4*>(vs + dof)[ch] = reinterpret_cast<const uint4*>(v + so)[ch];
+  const int64_t so = (int64_t(src_p) * c.h_kv + g) * c.Dc, dof = (int64_t(g) * c.N + p) * c.D;
+  const int e = ch * 16 / int(sizeof(T));
+  const bool in = e < c.Dc;                      // zero-padded heads when Dc < D (d = 32 on tcgen05)
+  reinterpret_cast<uint4*>(ks + dof)[ch] = in ? *reinterpret_cast<const uint4*>(k + so + e) : make_uint4(0u, 0u, 0u, 0u);
+  reinterpret_cast<uint4*>(vs + dof)[ch] = in ? *reinterpret_cast<const uint4*>(v + so + e) : make_uint4(0u, 0u, 0u, 0u);
 }
 
 template <class T>
@@ -807,7 +815,8 @@ __global__ void k_bwd_final_kv(Ctx c) {
   const int64_t ki = (int64_t(g) * c.N + p) * c.D + e;
   const int64_t ci = (int64_t(g) * c.n_blk[SSA_LEVEL_CMP] + j) * c.D + e;
   const int dst = c.sorted_input ? p : c.perm[p];
-  const int64_t o = (int64_t(dst) * c.h_kv + g) * c.D + e;
+  if (e >= c.Dc) return;                         // zero-padded head dims (d = 32 on tcgen05) are not output
+  const int64_t o = (int64_t(dst) * c.h_kv + g) * c.Dc + e;
   const float4 ak = *reinterpret_cast<const float4*>(c.dk_acc + ki), av = *reinterpret_cast<const float4*>(c.dv_acc + ki);
   float4 ck = *reinterpret_cast<const float4*>(c.dkc + ci), cv = *reinterpret_cast<const float4*>(c.dvc + ci);
   if (c.conv_kw) {

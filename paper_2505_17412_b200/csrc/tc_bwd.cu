@@ -103,9 +103,9 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
   const int h = g * c.h_s + s;
   const bool owned = valid && p >= c.row_lo && p < c.row_hi;   // rows of other shards are never touched
   const int src_p = c.sorted_input ? p : c.perm[p];
-  const int64_t so = (int64_t(src_p) * c.H + h) * kD + sub * 8, io = int64_t(rr) * kD + sub * 8;
+  const int64_t so = (int64_t(src_p) * c.H + h) * c.Dc + sub * 8, io = int64_t(rr) * kD + sub * 8;
   float fq[8] = {}, fd[8] = {};
-  if (owned) {
+  if (owned && sub * 8 < c.Dc) {                 // (Dc = 32: dims 32..63 are the zero padding)
     bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.q) + so), fq);
     bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.dout) + so), fd);
   }
@@ -541,9 +541,10 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         const float osc = c.scale * do_pow2(c.do_amax, true);
         const int tok = t0 + r / c.h_s, hs = r % c.h_s;
         const int dst = c.sorted_input ? tok : c.perm[tok];
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * kD;
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * c.Dc;
 #pragma unroll
         for (int e = 0; e < kD; e += 8) {
+          if (e >= c.Dc) break;                  // zero-padded head dims are not output
           float y[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) y[u] = v[e + u] * osc;
@@ -1122,12 +1123,12 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   c.do_amax = amax;
   SSA_CUDA_TRY(cudaMemsetAsync(amax, 0, 4, st));
   {  // over the rows this call may read (the owned range with a query-block range / SSA_LOCAL_ROWS)
-    const int64_t n8 = int64_t(c.row_hi - c.row_lo) * c.H * kD / 8;
-    const __nv_bfloat16* d0 = static_cast<const __nv_bfloat16*>(c.dout) + int64_t(c.row_lo) * c.H * kD;
+    const int64_t n8 = int64_t(c.row_hi - c.row_lo) * c.H * c.Dc / 8;
+    const __nv_bfloat16* d0 = static_cast<const __nv_bfloat16*>(c.dout) + int64_t(c.row_lo) * c.H * c.Dc;
     const unsigned blocks = unsigned(std::min<int64_t>((n8 + 255) / 256, 148 * 8));
     if (n8 > 0) {
       k_do_absmax<<<std::max(1u, blocks), 256, 0, st>>>(c.sorted_input ? d0 : static_cast<const __nv_bfloat16*>(c.dout),
-                                                         c.sorted_input ? n8 : int64_t(c.N) * c.H * kD / 8, amax);
+                                                         c.sorted_input ? n8 : int64_t(c.N) * c.H * c.Dc / 8, amax);
       SSA_LAUNCH_CHECK("k_do_absmax");
     }
   }

@@ -984,9 +984,10 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             const float w0 = e_w[ii][0], w1 = e_w[ii][1], w2 = c.no_win ? 0.f : e_w[ii][2];
             *reinterpret_cast<float4*>(ow + grow * kD + 4 * ch) = wn;
             __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) +
-                                 (int64_t(e_dst[ii]) * c.H + g * c.h_s + rr % c.h_s) * kD + 4 * ch;
+                                 (int64_t(e_dst[ii]) * c.H + g * c.h_s + rr % c.h_s) * c.Dc + 4 * ch;
             float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
                                    w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w);
+            if (4 * ch >= c.Dc) continue;        // zero-padded head dims (d = 32) are not output
             if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's out (e.g. the shifted-window pass)
               const uint2 old = *reinterpret_cast<const uint2*>(out);
               const float2 a = unpack_bf16(old.x), b = unpack_bf16(old.y);

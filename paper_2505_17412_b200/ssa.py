@@ -65,7 +65,7 @@ class AttnCfgC(ctypes.Structure):
 class SavedView(ctypes.Structure):
     _fields_ = [("idx", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("o_branch", ctypes.c_void_p * 3),
                 ("lse_branch", ctypes.c_void_p * 3), ("k_cmp", ctypes.c_void_p), ("v_cmp", ctypes.c_void_p),
-                ("used_tcgen05", ctypes.c_int32)]
+                ("used_tcgen05", ctypes.c_int32), ("d_internal", ctypes.c_int32)]
 
 
 _lib = None
@@ -296,6 +296,7 @@ class Saved:
                                      ctypes.byref(v)), "ssa_saved_state")
         self.view = v
         self.used_tcgen05 = bool(v.used_tcgen05)
+        self.d_internal = int(v.d_internal)     # 64 when a d = 32 problem ran the tcgen05 kernels padded
 
     def _slice(self, ptr, count, dtype):
         es = torch.tensor([], dtype=dtype).element_size()
@@ -317,15 +318,16 @@ class Saved:
 
     def branch(self, b: int):
         """(o, lse) of branch b (0 cmp, 1 slc, 2 win), internal layout [h_kv][N][h_s][d], sorted order."""
-        n, hk, hs, d = self.plan.n, self.cfg.h_kv, self.cfg.h_q // self.cfg.h_kv, self.cfg.d
+        n, hk, hs, d = self.plan.n, self.cfg.h_kv, self.cfg.h_q // self.cfg.h_kv, self.d_internal
         o = self._slice(self.view.o_branch[b], n * self.cfg.h_q * d, torch.float32).view(hk, n, hs, d)
         lse = self._slice(self.view.lse_branch[b], n * self.cfg.h_q, torch.float32).view(hk, n, hs)
         return o, lse
 
     def k_cmp(self):
         nc = self.plan.n_blocks[LEVEL_CMP]
-        return (self._slice(self.view.k_cmp, self.cfg.h_kv * nc * self.cfg.d, torch.float32).view(self.cfg.h_kv, nc, self.cfg.d),
-                self._slice(self.view.v_cmp, self.cfg.h_kv * nc * self.cfg.d, torch.float32).view(self.cfg.h_kv, nc, self.cfg.d))
+        d = self.d_internal
+        return (self._slice(self.view.k_cmp, self.cfg.h_kv * nc * d, torch.float32).view(self.cfg.h_kv, nc, d),
+                self._slice(self.view.v_cmp, self.cfg.h_kv * nc * d, torch.float32).view(self.cfg.h_kv, nc, d))
 
 
 def owned_rows(plan: Plan, cfg: AttnCfg):

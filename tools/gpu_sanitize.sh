@@ -1,7 +1,14 @@
-# compute-sanitizer memcheck / racecheck / synccheck of tools/sanitize_case.py; usage: bash tools/gpu_sanitize.sh <tag>
+# compute-sanitizer memcheck / racecheck / synccheck of tools/sanitize_case.py, one case per run (see
+# the case list in the script); usage: bash tools/gpu_sanitize.sh <tag> [tools] [cases]
 T=${1:-r2}
-for tool in memcheck racecheck synccheck; do
-  echo "# compute-sanitizer --tool $tool python tools/sanitize_case.py ($T)" > gpurun_out/sanitize_${tool}_$T.txt
-  timeout 900 compute-sanitizer --tool $tool python tools/sanitize_case.py >> gpurun_out/sanitize_${tool}_$T.txt 2>&1
-  tail -1 gpurun_out/sanitize_${tool}_$T.txt
+TOOLS=${2:-"memcheck racecheck synccheck"}
+CASES=${3:-"0 1 4 5 2 3"}
+for tool in $TOOLS; do
+  out=gpurun_out/sanitize_${tool}_$T.txt
+  echo "# compute-sanitizer --tool $tool python tools/sanitize_case.py <case> ($T), cases: $CASES" > $out
+  for cs in $CASES; do
+    echo "## case $cs" >> $out
+    timeout 400 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_case.py $cs >> $out 2>&1
+    tail -1 $out
+  done
 done
