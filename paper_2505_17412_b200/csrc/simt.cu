@@ -556,6 +556,12 @@ __device__ __forceinline__ void kv_rows_tile(KvAcc<D>& a, bool kvalid, int half,
                                              const float* st_lse2, const float* st_w, const float* st_D, int nr,
                                              float scale) {
   const float l2s = scale * kLog2e;
+  // two-level summation: the tile's rows are summed into fresh registers, then added to the running
+  // totals once per tile (fp32 error growth ~ rows/tile + tiles instead of all rows of a popular key
+  // block — the fp32 mode's 1e-4 bound at C2, where a key collects ~3e5 row terms)
+  float tdk[D / 2], tdv[D / 2];
+#pragma unroll
+  for (int e = 0; e < D / 2; ++e) tdk[e] = tdv[e] = 0.f;
   for (int rr = 0; rr < nr; ++rr) {
     float x = 0.f, dp = 0.f;
 #pragma unroll
@@ -572,9 +578,14 @@ __device__ __forceinline__ void kv_rows_tile(KvAcc<D>& a, bool kvalid, int half,
     const float pw = p * w;
 #pragma unroll
     for (int e = 0; e < D / 2; ++e) {
-      a.dv[e] += pw * Ot[rr * D + half * (D / 2) + e];
-      a.dk[e] += ds * Qt[rr * D + half * (D / 2) + e];
+      tdv[e] += pw * Ot[rr * D + half * (D / 2) + e];
+      tdk[e] += ds * Qt[rr * D + half * (D / 2) + e];
     }
+  }
+#pragma unroll
+  for (int e = 0; e < D / 2; ++e) {
+    a.dv[e] += tdv[e];
+    a.dk[e] += tdk[e];
   }
 }
 

@@ -597,8 +597,12 @@ constexpr int kPBuf = SSA_KV_PBUF;
 #define SSA_KV_QB_PER_ITEM 8
 #endif
 constexpr int kQBlocksPerItem = SSA_KV_QB_PER_ITEM;       // raw keys: query blocks per work item (splits popular blocks)
+#ifndef SSA_BWD_FORK
+#define SSA_BWD_FORK 1
+#endif
+constexpr bool kBwdFork = SSA_BWD_FORK;   // dQ and the KV-outer launches on two streams (see tc_backward)
 #ifndef SSA_KV_STATS_WAIT
-#define SSA_KV_STATS_WAIT 1       // row stats: cp.async + wait + plain arrive (0: cp.async.mbarrier.arrive.noinc)
+#define SSA_KV_STATS_WAIT 0       // 1: cp.async + wait_all + plain arrive (synccheck unchanged, 0.8 ms slower at C3)
 #endif
 // One CTA per SM, 352 threads: warpgroups 0 / 1 (warps 0-3 / 4-7, thread = key = TMEM lane) split the
 // row tiles of the item (even / odd), each with its own 256 TMEM columns (S^T 64 | dP^T 64 | dK 64 |
@@ -1148,6 +1152,26 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
       !make_tmap_bf16_2d(&tmKc128, kc, crows, 128) || !make_tmap_bf16_2d(&tmVc128, vc, crows, 128) ||
       !make_tmap_bf16_2d(&tmK128, k16, krows, 128) || !make_tmap_bf16_2d(&tmV128, v16, krows, 128))
     return SSA_ERR_CUDA;
+  // The Q-outer dQ kernel and the KV-outer dK/dV kernels read the same operands and write disjoint
+  // outputs: with SSA_BWD_FORK the KV-outer launches go to an internal stream forked from (and joined
+  // back into) the caller's stream, so each kernel's last partial wave overlaps the other's work.
+  cudaStream_t kst = st;
+  cudaEvent_t ev_join = nullptr;
+  if (kBwdFork) {
+    static cudaStream_t side[16] = {};
+    int dev = 0;
+    SSA_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 16) {
+      if (!side[dev]) SSA_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+      cudaEvent_t ev_fork;
+      SSA_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      SSA_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      SSA_CUDA_TRY(cudaEventRecord(ev_fork, st));
+      SSA_CUDA_TRY(cudaStreamWaitEvent(side[dev], ev_fork, 0));
+      cudaEventDestroy(ev_fork);      // released once the recorded work completes
+      kst = side[dev];
+    }
+  }
   {
     const size_t smem = 1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem);
     static_assert(1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem) <= 232448, "dQ shared memory");
@@ -1160,24 +1184,29 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   if (smem > 232448) { set_error("KV-outer shared memory exceeds 227 KB"); return SSA_ERR_UNSUPPORTED; }
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
-    k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, st>>>(c, item_cnt);
+    k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, kst>>>(c, item_cnt);
     SSA_LAUNCH_CHECK("k_kv_item_count");
-    ssa_status s = exclusive_scan(item_cnt, c.kv_item_off, nkeys, c.kv_item_off + nkeys, scan_ws, st);
+    ssa_status s = exclusive_scan(item_cnt, c.kv_item_off, nkeys, c.kv_item_off + nkeys, scan_ws, kst);
     if (s != SSA_OK) return s;
-    ProfScope ps("tc_bwd_kv", st);
-    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, st>>>(c, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
+    ProfScope ps("tc_bwd_kv", kst);
+    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, kst>>>(c, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
   }
   {
     const int64_t nk = int64_t(c.N) * c.h_kv * (kD / 4);
-    k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, st>>>(c);
+    k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, kst>>>(c);
     SSA_LAUNCH_CHECK("k_kv_reduce");
   }
   if (!c.win_only) {
-    ProfScope ps("tc_bwd_cmp_kv", st);
-    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, st>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
-                                                                              tmVc128);
+    ProfScope ps("tc_bwd_cmp_kv", kst);
+    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, kst>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
+                                                                               tmVc128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(cmp)");
+  }
+  if (ev_join) {   // join: the caller's stream continues after the KV-outer work
+    SSA_CUDA_TRY(cudaEventRecord(ev_join, kst));
+    SSA_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
+    cudaEventDestroy(ev_join);
   }
   return SSA_OK;
 }
