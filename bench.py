@@ -580,7 +580,8 @@ def main():
 
 def full_attention_time(torch, dev, n, H, h_kv, d, dt):
     """Dense non-causal attention over all n tokens, fwd+bwd, GQA (context only, SURVEY 8d comparators):
-    torch SDPA default dispatch, SDPA pinned to the cuDNN backend, and flash_attn (FA2) when it runs here."""
+    torch SDPA default dispatch, SDPA pinned to the cuDNN backend, flash_attn (FA2) and the FA4 CuTe-DSL
+    sm100 kernels (vllm.vllm_flash_attn.cute) when they run here."""
     import torch.nn.functional as F
     q = torch.randn(1, H, n, d, device=dev, dtype=dt, requires_grad=True)
     k = torch.randn(1, h_kv, n, d, device=dev, dtype=dt, requires_grad=True)
@@ -625,6 +626,20 @@ def full_attention_time(torch, dev, n, H, h_kv, d, dt):
         others["flash_attn2_ms"] = timed(lambda: flash_attn_func(qf, kf, vf).backward(gof))
     except Exception as ex:
         others["flash_attn2_error"] = str(ex)[:160]
+    try:
+        # FA4 (CuTe DSL, sm100: tcgen05 / TMEM), vendored by vllm — the strongest full-attention kernel here
+        from vllm.vllm_flash_attn.cute.interface import flash_attn_func as fa4
+        q4 = q.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        k4 = k.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        v4 = v.detach().transpose(1, 2).contiguous().requires_grad_(True)
+        go4 = go.transpose(1, 2).contiguous()
+
+        def fa4_step():
+            o4 = fa4(q4, k4, v4, causal=False)
+            (o4[0] if isinstance(o4, tuple) else o4).backward(go4)
+        others["flash_attn4_cute_ms"] = timed(fa4_step)
+    except Exception as ex:
+        others["flash_attn4_cute_error"] = str(ex)[:160]
     res["others"] = others
     return res
 
