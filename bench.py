@@ -533,6 +533,32 @@ def main():
                        "fwd_bwd_ms": round(l_ms / batch, 4), "extra_ms_vs_plain": round((l_ms - ms_per_step) / batch, 4),
                        "kernel_ms": lk}
 
+    # ---- context: the paper's DiT attention layout (2 kv groups x 16 heads, head dim 32) on the
+    # same tokens (tcgen05 kernels, heads zero-padded to 64 inside the library) ----
+    paper_ctx = None
+    if rank == 0 and used_tc and not sharded and not hybrid and not args.no_learned:
+        gen = torch.Generator(device=dev).manual_seed(6)
+        Hp, dp = 32, 32
+        tp = [torch.randn(q.shape[0], hh, dp, device=dev, generator=gen).to(tdt) for hh in (Hp, h_kv, h_kv)]
+        gp = torch.sigmoid(torch.randn(q.shape[0], Hp, 3, device=dev, generator=gen)).to(tdt)
+        dop = torch.randn(q.shape[0], Hp, dp, device=dev, generator=gen).to(tdt)
+        pcfg = ssa.AttnCfg(h_q=Hp, h_kv=h_kv, d=dp, top_k=T, dtype=tdt)
+        pt = []
+        for i in range(6):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan_p = ssa.ssa_build_blocks(c_d, grid, batch, *ms)
+            _, sv = ssa.ssa_forward(plan_p, pcfg, *tp, gp)
+            ssa.ssa_backward(plan_p, pcfg, sv, *tp, gp, dop)
+            e1.record(st)
+            if i >= 2:
+                pt.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        paper_ctx = {"impl": "paper DiT layout H = 32 (h_kv = 2), d = 32 (P:272), same tokens, tcgen05 (d padded to 64)",
+                     "fwd_bwd_ms": round(float(np.mean([a.elapsed_time(b) for a, b in pt])) / batch, 4),
+                     "path": "tcgen05" if sv.used_tcgen05 else "simt"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, cfg, coords, grid, batch, inp, value)
@@ -563,6 +589,8 @@ def main():
             line["window_attention"] = win
         if learned_ctx:
             line["learned_delta_gates"] = learned_ctx
+        if paper_ctx:
+            line["paper_layout_d32"] = paper_ctx
         if hybrid_info:
             line["config"]["hybrid_plan"] = hybrid_info["plan"]
         if full:
