@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-window", action="store_true", help="skip the window-only (SSA_WINDOW_ONLY) context timing")
     ap.add_argument("--no-learned", action="store_true", help="skip the learned-delta / gate-projection context timing")
     ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "fetch"],
+                    help="C5 / hybrid K/V exchange: bulk all-gather or one-sided fetch of the selected blocks")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: validate the N>1 logic with several ranks on one GPU)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="query blocks in the oracle sample (0: 4 per core)")
@@ -244,7 +246,7 @@ def main():
             a, b = tok[rank]
             rows = plan.perm()[a:b].long()
             loc = [x[rows] for x in (qq, kk, vv, gg, dd)]
-            ssa_step_sharded(plan, acfg, *loc, rank=rank, world=world, comm_stream=comm)
+            ssa_step_sharded(plan, acfg, *loc, rank=rank, world=world, comm_stream=comm, exchange=args.exchange)
             return plan, None
         o, saved = ssa.ssa_forward(plan, acfg, qq, kk, vv, gg, out=o_)
         ssa.ssa_backward(plan, acfg, saved, qq, kk, vv, gg, dd, grads=gr_)

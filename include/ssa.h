@@ -217,7 +217,26 @@ typedef struct {
   const void* vc_in;
   void* kv_event;
   const ssa_learned* learned;   /* NULL: delta = mean pool, gates are inputs (see ssa_learned) */
+  /* One-sided fetch of the selected K/V blocks (mode 2 without the bulk all-gather):
+   * n_peer > 0 ranks own contiguous plan-order token ranges [peer_tok[r], peer_tok[r+1]) of one
+   * shape; peer_k[r] / peer_v[r] are device pointers (local, or peer mappings opened with
+   * ssa_ipc_open — NVLink P2P on a multi-GPU node) to rank r's rows, layout [rows][h_kv][d].
+   * Needs kc_in / vc_in. The forward then copies into the caller's full-size k, v buffers (which hold
+   * this rank's own rows) exactly the rows of the selection blocks its owned query blocks selected —
+   * after the compression attention and top-k, before the selection branch — instead of waiting for
+   * a K/V all-gather; kv_event is not used. my_rank: this rank's index. */
+  int32_t n_peer, my_rank;
+  const void* peer_k[16];
+  const void* peer_v[16];
+  int32_t peer_tok[17];
 } ssa_attn_cfg;
+
+/* CUDA IPC helpers for the one-sided fetch: export a device allocation (base pointer) as a 64-byte
+ * handle; open another process's handle (peer mapping; on one GPU a second mapping of the same memory)
+ * and close it. Errors: SSA_ERR_ARG, SSA_ERR_CUDA. */
+ssa_status ssa_ipc_handle(const void* base, void* handle64);
+ssa_status ssa_ipc_open(const void* handle64, void** ptr);
+ssa_status ssa_ipc_close(void* ptr);
 
 /* ------------------------------------------------------------------------------------------------
  * ssa_pool — the compression pool alone (Eq. 7; delta = masked mean, reading R4, plus the

@@ -87,6 +87,21 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
     return SSA_ERR_ARG;
   }
   if ((cfg->kc_in == nullptr) != (cfg->vc_in == nullptr)) { set_error("kc_in and vc_in go together"); return SSA_ERR_ARG; }
+  if (cfg->n_peer != 0) {
+    if (cfg->n_peer < 1 || cfg->n_peer > 16 || cfg->my_rank < 0 || cfg->my_rank >= cfg->n_peer) {
+      set_error("n_peer must be in [1, 16] and my_rank in [0, n_peer)");
+      return SSA_ERR_ARG;
+    }
+    if (!cfg->kc_in || cfg->peer_tok[0] != 0 || cfg->peer_tok[cfg->n_peer] != p->info.n) {
+      set_error("the one-sided fetch needs kc_in / vc_in and peer_tok covering [0, n)");
+      return SSA_ERR_ARG;
+    }
+    for (int r = 0; r < cfg->n_peer; ++r)
+      if (!cfg->peer_k[r] || !cfg->peer_v[r] || cfg->peer_tok[r] > cfg->peer_tok[r + 1]) {
+        set_error("peer_k / peer_v / peer_tok invalid");
+        return SSA_ERR_ARG;
+      }
+  }
   d->N = p->info.n;
   d->H = cfg->h_q;
   d->h_kv = cfg->h_kv;
@@ -137,6 +152,7 @@ ssa_status choose_path(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p, bo
     }
     return SSA_OK;
   }
+  if (cfg->n_peer > 0 && !*tc) { set_error("the one-sided K/V fetch needs the tcgen05 path"); return SSA_ERR_UNSUPPORTED; }
   if (cfg->dtype == SSA_BF16 && !*tc && !(cfg->flags & SSA_FORCE_SIMT)) {
     set_error(std::string("bf16 request outside the tcgen05 kernels (") + tc_reason(d, cfg, p) +
               "); set SSA_FORCE_SIMT to run the SIMT kernels");
@@ -264,6 +280,10 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
     x->gx = L->x; x->gC = L->c; x->gw = L->gate_w; x->gb = L->gate_b;
     x->gdx = L->dx; x->gdw = L->d_gate_w; x->gdb = L->d_gate_b;
   }
+  x->n_peer = cfg->n_peer;
+  x->my_rank = cfg->my_rank;
+  for (int r = 0; r < 16; ++r) { x->peer_k[r] = cfg->peer_k[r]; x->peer_v[r] = cfg->peer_v[r]; }
+  for (int r = 0; r < 17; ++r) x->peer_tok[r] = cfg->peer_tok[r];
 }
 
 // SSA_LOCAL_ROWS: the caller's row tensors start at row row_base; kernels index rows by their plan
@@ -292,7 +312,7 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   Carve cw(nullptr, 0);
   carve_inputs(cw, d, &x, false);
   fill_common(&x, p, d, cfg);
-  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + 1024;
+  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 + 1024;
   return SSA_OK;
 }
 
@@ -327,6 +347,7 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   carve_inputs(cw, d, &x, false);
   void* tc_ws = cw.take<char>(tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
   void* l_ws = cw.take<char>(learned_fwd_ws_bytes(x));
+  x.fetch_mark = cw.take<int32_t>(size_t(d.n_slc) + 1);
   if (lgates) x.gs = saved_gates;
   const bool bf16 = cfg->dtype == SSA_BF16;
   // caller-supplied pooled keys (mode 2): no pooling; raw k / v are first read by the selection /
@@ -472,6 +493,24 @@ extern "C" ssa_status ssa_pool(ssa_plan plan, const ssa_attn_cfg* cfg, const voi
   fill_common(&x, p, d, cfg);
   return pool_rows(x, cfg->dtype == SSA_BF16, k, v, static_cast<float*>(kc), static_cast<float*>(vc),
                    static_cast<cudaStream_t>(stream));
+}
+
+extern "C" ssa_status ssa_ipc_handle(const void* base, void* handle64) {
+  if (!base || !handle64) { set_error("null argument"); return SSA_ERR_ARG; }
+  SSA_CUDA_TRY(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle64), const_cast<void*>(base)));
+  return SSA_OK;
+}
+extern "C" ssa_status ssa_ipc_open(const void* handle64, void** ptr) {
+  if (!handle64 || !ptr) { set_error("null argument"); return SSA_ERR_ARG; }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  SSA_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SSA_OK;
+}
+extern "C" ssa_status ssa_ipc_close(void* ptr) {
+  if (!ptr) { set_error("null argument"); return SSA_ERR_ARG; }
+  SSA_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return SSA_OK;
 }
 
 extern "C" ssa_status ssa_saved_state(ssa_plan plan, const ssa_attn_cfg* cfg, const void* saved, size_t saved_bytes,

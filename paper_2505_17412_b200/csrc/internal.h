@@ -85,7 +85,13 @@ struct Ctx {
   const float *gw, *gb;           // W_g [gC][3H], b_g [3H]
   void* gdx;                      // dx (dtype), dW_g, db_g (fp32) — backward outputs
   float *gdw, *gdb;
-  float* dz;                      // [h_kv][N][h_s][3] gradients of the gate logits (row prologue)        // tcgen05 backward: max |dO| (float bits) -> power-of-two operand scale
+  float* dz;                      // [h_kv][N][h_s][3] gradients of the gate logits (row prologue)
+  // one-sided fetch of the selected K/V blocks (cfg n_peer > 0)
+  int32_t n_peer, my_rank;
+  const void* peer_k[16];
+  const void* peer_v[16];
+  int32_t peer_tok[17];
+  int32_t* fetch_mark;            // [n_slc] needed selection blocks        // tcgen05 backward: max |dO| (float bits) -> power-of-two operand scale
   int32_t *inv_off, *inv_list, *inv_cnt;   // inverse selection CSR over (slc block, g)
   int32_t *cmp_tiles;             // [n_cmp_tiles][2] (batch item, first cmp block) for the KV-outer cmp kernels
   int32_t n_cmp_tiles;
@@ -100,6 +106,9 @@ ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st);
 // rows = false: only keys and gates are gathered (the tcgen05 backward reads q / dO rows itself)
 ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dout, bool rows = true, bool keys = true,
                          bool gates = true);
+// one-sided fetch (simt.cu): mark the selection blocks owned query blocks selected, copy the peer-owned
+// ones into the caller's full-size k / v (before the selection branch)
+ssa_status fetch_selected(const Ctx& c, bool bf16, cudaStream_t st);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);
 size_t gate_bwd_ws_bytes(int64_t N, int H, int C);

@@ -1128,4 +1128,54 @@ ssa_status simt_backward(const Ctx& c, bool bf16, cudaStream_t st) {
   return bf16 ? dispatch_d_bwd<__nv_bfloat16>(c, st) : dispatch_d_bwd<float>(c, st);
 }
 
+// ---------------------------------------------------------------------------------------------
+// One-sided fetch of the selected K/V blocks: k_fetch_mark flags every selection
+// block an owned query block selected; k_fetch_copy copies the flagged blocks owned by another rank
+// from that rank's rows (peer pointer) into the caller's full-size k / v. Blocks are contiguous in plan
+// order, [rows][h_kv][d]; one CTA per block, 16-byte vectors.
+// ---------------------------------------------------------------------------------------------
+namespace {
+__global__ void k_fetch_mark(Ctx c) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n = int64_t(c.q_end - c.q_begin) * c.h_kv * c.T;
+  if (i >= n) return;
+  const int B = c.I[int64_t(c.q_begin) * c.h_kv * c.T + i];
+  if (B >= 0) c.fetch_mark[B] = 1;
+}
+__global__ void k_fetch_copy(Ctx c, int esz) {
+  const int B = blockIdx.x;
+  if (!c.fetch_mark[B]) return;
+  const int t0 = c.off[SSA_LEVEL_SLC][B], t1 = c.off[SSA_LEVEL_SLC][B + 1];
+  int owner = 0;
+  while (owner + 1 < c.n_peer && c.peer_tok[owner + 1] <= t0) ++owner;
+  if (owner == c.my_rank) return;
+  const int64_t row_bytes = int64_t(c.h_kv) * c.Dc * esz;
+  const int64_t n16 = int64_t(t1 - t0) * row_bytes / 16;
+  const uint4* sk = reinterpret_cast<const uint4*>(static_cast<const char*>(c.peer_k[owner]) + (t0 - c.peer_tok[owner]) * row_bytes);
+  const uint4* sv = reinterpret_cast<const uint4*>(static_cast<const char*>(c.peer_v[owner]) + (t0 - c.peer_tok[owner]) * row_bytes);
+  uint4* dk = reinterpret_cast<uint4*>(static_cast<char*>(const_cast<void*>(c.k)) + int64_t(t0) * row_bytes);
+  uint4* dv = reinterpret_cast<uint4*>(static_cast<char*>(const_cast<void*>(c.v)) + int64_t(t0) * row_bytes);
+  for (int64_t j = threadIdx.x; j < n16; j += blockDim.x) {
+    dk[j] = sk[j];
+    dv[j] = sv[j];
+  }
+}
+}  // namespace
+
+ssa_status fetch_selected(const Ctx& c, bool bf16, cudaStream_t st) {
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC];
+  SSA_CUDA_TRY(cudaMemsetAsync(c.fetch_mark, 0, size_t(n_slc) * 4, st));
+  const int64_t n = int64_t(c.q_end - c.q_begin) * c.h_kv * c.T;
+  if (n > 0) {
+    k_fetch_mark<<<nblk(n, 256), 256, 0, st>>>(c);
+    SSA_LAUNCH_CHECK("k_fetch_mark");
+  }
+  if (n_slc > 0) {
+    ProfScope ps("k_fetch_copy", st);
+    k_fetch_copy<<<n_slc, 256, 0, st>>>(c, bf16 ? 2 : 4);
+    SSA_LAUNCH_CHECK("k_fetch_copy");
+  }
+  return SSA_OK;
+}
+
 }  // namespace ssa

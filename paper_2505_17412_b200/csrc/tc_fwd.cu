@@ -1071,6 +1071,10 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
   }
   if (split) {
     if (kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
+    if (c.n_peer > 0) {   // one-sided fetch of the selected blocks (needs this CTA grid's indices: done)
+      ssa_status s = fetch_selected(c, true, st);
+      if (s != SSA_OK) return s;
+    }
     if (gather_keys_late) {
       ssa_status s = gather_inputs(c, true, st, false, /*rows=*/false, /*keys=*/true, /*gates=*/false);
       if (s != SSA_OK) return s;

@@ -138,8 +138,35 @@ def shard_ranges(plan, world: int):
     return rng, [(int(qo[a]), int(qo[b])) for a, b in rng]
 
 
+def exchange_peer_pointers(k_loc, v_loc, rank, world, group=None):
+    """One-sided K/V access: every rank exports its own K/V rows as CUDA IPC handles,
+    all ranks exchange them, and each opens the others' (peer mappings: NVLink P2P on a multi-GPU node,
+    a second mapping of the same memory when the ranks share one GPU). Returns (peer_k, peer_v, bases
+    to close)."""
+    import torch.distributed as dist
+    from . import ssa
+    mine = (ssa.ipc_export(k_loc), ssa.ipc_export(v_loc))
+    allh = [None] * world
+    if world > 1:
+        dist.all_gather_object(allh, mine, group=group)
+    else:
+        allh = [mine]
+    pk, pv, bases = [], [], []
+    for r, ((hk, ok), (hv, ov)) in enumerate(allh):
+        if r == rank:
+            pk.append(k_loc.data_ptr())
+            pv.append(v_loc.data_ptr())
+            continue
+        bk, p1 = ssa.ipc_open(hk, ok)
+        bv, p2 = ssa.ipc_open(hv, ov)
+        pk.append(p1)
+        pv.append(p2)
+        bases += [bk, bv]
+    return pk, pv, bases
+
+
 def ssa_step_sharded(plan, cfg, q_loc, k_loc, v_loc, gates_loc, dout_loc, rank, world, group=None,
-                     comm_stream=None, q_ranges=None):
+                     comm_stream=None, q_ranges=None, exchange="allgather"):
     """Forward + backward of ONE shape with its query blocks sharded over `world` ranks (SURVEY §8e
     mode 2). Every rank built the same plan; rank r holds only its own rows (plan order, tokens
     shard_ranges(plan, world)[1][r]) of q, k, v, gates, dout. Data path:
@@ -150,7 +177,10 @@ def ssa_step_sharded(plan, cfg, q_loc, k_loc, v_loc, gates_loc, dout_loc, rank, 
       3. forward and backward for the owned rows only (SSA_LOCAL_ROWS); dk, dv come back as fp32
          partials over every token (SSA_KV_GRAD_FP32) and are reduce-scattered to their owners.
     q_ranges: optional explicit query-block range of every rank of the group (hybrid_plan); default
-    balanced by tokens. Returns (out, dq, dk, dv, dgates) for the owned rows (dk, dv in k_loc's dtype)."""
+    balanced by tokens. exchange="fetch" replaces step 2 by the one-sided fetch: the ranks exchange
+    CUDA IPC handles of their K/V rows and the forward copies only the selection blocks its query blocks
+    selected from their owners, after the compression attention and top-k (cfg.peers).
+    Returns (out, dq, dk, dv, dgates) for the owned rows (dk, dv in k_loc's dtype)."""
     import dataclasses
     import torch
     from . import ssa
@@ -168,19 +198,38 @@ def ssa_step_sharded(plan, cfg, q_loc, k_loc, v_loc, gates_loc, dout_loc, rank, 
     kc, vc = ssa.ssa_pool(plan, c2, k_loc, v_loc)
     all_reduce_sum(kc, group)
     all_reduce_sum(vc, group)
-    comm = comm_stream or torch.cuda.Stream(dev)
-    comm.wait_stream(cur)                          # k_loc / v_loc are ready
-    ev = torch.cuda.Event()
-    with torch.cuda.stream(comm):
+    if exchange == "fetch":
+        import torch.distributed as dist
         k = torch.empty((plan.n,) + tuple(k_loc.shape[1:]), dtype=k_loc.dtype, device=dev)
         v = torch.empty_like(k)
-        all_gather_rows(k, k_loc, tok, rank, group)
-        all_gather_rows(v, v_loc, tok, rank, group)
-        ev.record(comm)
-    k.record_stream(cur)
-    v.record_stream(cur)
-    cf = dataclasses.replace(c2, kc_in=kc, vc_in=vc, kv_event=ev)
-    out, saved = ssa.ssa_forward(plan, cf, q_loc, k, v, gates_loc)
+        a, b = tok[rank]
+        k[a:b] = k_loc
+        v[a:b] = v_loc
+        pk, pv, bases = exchange_peer_pointers(k_loc, v_loc, rank, world, group)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(group=group)              # every rank's K/V rows are in place
+        cf = dataclasses.replace(c2, kc_in=kc, vc_in=vc, peers=(pk, pv, [t[0] for t in tok] + [tok[-1][1]], rank))
+        out, saved = ssa.ssa_forward(plan, cf, q_loc, k, v, gates_loc)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(group=group)              # no rank frees rows another is still reading
+        for base in bases:
+            ssa.ipc_close(base)
+    else:
+        comm = comm_stream or torch.cuda.Stream(dev)
+        comm.wait_stream(cur)                          # k_loc / v_loc are ready
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(comm):
+            k = torch.empty((plan.n,) + tuple(k_loc.shape[1:]), dtype=k_loc.dtype, device=dev)
+            v = torch.empty_like(k)
+            all_gather_rows(k, k_loc, tok, rank, group)
+            all_gather_rows(v, v_loc, tok, rank, group)
+            ev.record(comm)
+        k.record_stream(cur)
+        v.record_stream(cur)
+        cf = dataclasses.replace(c2, kc_in=kc, vc_in=vc, kv_event=ev)
+        out, saved = ssa.ssa_forward(plan, cf, q_loc, k, v, gates_loc)
     dq, dk, dv, dg = ssa.ssa_backward(plan, c2, saved, q_loc, k, v, gates_loc, dout_loc)
     dk_loc = reduce_scatter_rows(dk, tok, rank, group)
     dv_loc = reduce_scatter_rows(dv, tok, rank, group)

@@ -59,7 +59,9 @@ class AttnCfgC(ctypes.Structure):
                 ("top_k", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("pe_k", ctypes.c_void_p), ("pe_v", ctypes.c_void_p),
                 ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32), ("kc_in", ctypes.c_void_p),
-                ("vc_in", ctypes.c_void_p), ("kv_event", ctypes.c_void_p), ("learned", ctypes.POINTER(LearnedC))]
+                ("vc_in", ctypes.c_void_p), ("kv_event", ctypes.c_void_p), ("learned", ctypes.POINTER(LearnedC)),
+                ("n_peer", ctypes.c_int32), ("my_rank", ctypes.c_int32), ("peer_k", ctypes.c_void_p * 16),
+                ("peer_v", ctypes.c_void_p * 16), ("peer_tok", ctypes.c_int32 * 17)]
 
 
 class SavedView(ctypes.Structure):
@@ -88,6 +90,9 @@ SIGNATURES = {
     "ssa_backward": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P, _P,
                                     _P, _P, _P, ctypes.c_size_t, _P]),
     "ssa_pool": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, _P, _P, _P, _P]),
+    "ssa_ipc_handle": (ctypes.c_int, [_P, _P]),
+    "ssa_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "ssa_ipc_close": (ctypes.c_int, [_P]),
     "ssa_saved_state": (ctypes.c_int, [_P, ctypes.POINTER(AttnCfgC), _P, ctypes.c_size_t,
                                        ctypes.POINTER(SavedView)]),
     "ssa_status_str": (ctypes.c_char_p, [ctypes.c_int]),
@@ -272,6 +277,8 @@ class AttnCfg:
     vc_in: torch.Tensor | None = None
     kv_event: torch.cuda.Event | None = None   # raw k / v ready (recorded after a K/V all-gather)
     learned: Learned | None = None
+    # one-sided fetch of the selected K/V blocks: (peer_k ptrs, peer_v ptrs, token offsets [world + 1], my rank)
+    peers: tuple | None = None
 
     def c(self, learned_grads: dict | None = None) -> AttnCfgC:
         def ptr(t):
@@ -282,6 +289,13 @@ class AttnCfg:
                       int(self.flags), ptr(self.pe_k), ptr(self.pe_v), int(self.q_begin), int(self.q_end),
                       ptr(self.kc_in), ptr(self.vc_in), ev, ctypes.pointer(lc) if lc is not None else None)
         cc._keep = lc          # the struct the pointer refers to lives as long as cc
+        if self.peers is not None:
+            pk, pv, tok, me = self.peers
+            cc.n_peer, cc.my_rank = len(pk), int(me)
+            for r in range(len(pk)):
+                cc.peer_k[r], cc.peer_v[r] = int(pk[r]), int(pv[r])
+            for r, t in enumerate(tok):
+                cc.peer_tok[r] = int(t)
         return cc
 
 
@@ -496,6 +510,27 @@ def window_attention_backward(ctx, q, k, v, dout):
     plan, cfg, saved, gates = ctx
     dq, dk, dv, _ = ssa_backward(plan, cfg, saved, q, k, v, gates, dout)
     return dq, dk, dv
+
+
+def ipc_export(t: torch.Tensor):
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t's data in it) — for ipc_open in
+    another process (the caching allocator sub-allocates, so the offset is carried separately)."""
+    st = t.untyped_storage()
+    info = st._share_cuda_()
+    handle, off = info[1], int(info[3])
+    return bytes(handle), off + (t.data_ptr() - st.data_ptr())
+
+
+def ipc_open(handle: bytes, offset: int) -> tuple:
+    """Open a peer's exported allocation: returns (mapped base, data pointer = base + offset)."""
+    p = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(handle, 64)
+    _check(lib().ssa_ipc_open(buf, ctypes.byref(p)), "ssa_ipc_open")
+    return p.value, p.value + offset
+
+
+def ipc_close(base: int):
+    _check(lib().ssa_ipc_close(ctypes.c_void_p(base)), "ssa_ipc_close")
 
 
 def launch_count() -> int:

@@ -113,7 +113,7 @@ def test_local_rows_pool_and_kv_event():
         assert err < 1e-3, err
 
 
-def _proc(rank, world, port, path):
+def _proc(rank, world, port, path, exchange="allgather"):
     import os
     import torch
     import torch.distributed as dist
@@ -127,17 +127,19 @@ def _proc(rank, world, port, path):
     _, tok = shard_ranges(plan, world)
     a, b = tok[rank]
     loc = [x[a:b].contiguous() for x in (q, k, v, g, do)]
-    res = ssa_step_sharded(plan, cfg, *loc, rank=rank, world=world)
+    res = ssa_step_sharded(plan, cfg, *loc, rank=rank, world=world, exchange=exchange)
     torch.cuda.synchronize()
     torch.save([x.cpu() for x in res] + [torch.tensor([a, b])], f"{path}/r{rank}.pt")
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_process_sharded_step(tmp_path):
+@pytest.mark.parametrize("exchange", ["allgather", "fetch"])
+def test_two_process_sharded_step(tmp_path, exchange):
     """ssa_step_sharded end to end in two processes (gloo on one GPU; the driver's boxes have one GPU):
     per-rank inputs (own rows of q, k, v, gates, dO only), pooled-key all-reduce, K/V all-gather on a side
-    stream overlapping the compression branch, dK/dV reduce-scatter. Each rank's out / dq / dgates equal
+    stream overlapping the compression branch (or, exchange="fetch", the one-sided fetch of only the
+    selected blocks through CUDA IPC peer mappings), dK/dV reduce-scatter. Each rank's out / dq / dgates equal
     the unsharded run's rows bit for bit; its dk / dv rows match up to fp32 summation order."""
     import socket
     import torch
@@ -148,7 +150,7 @@ def test_two_process_sharded_step(tmp_path):
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
-    ps = [ctx.Process(target=_proc, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    ps = [ctx.Process(target=_proc, args=(r, 2, port, str(tmp_path), exchange)) for r in range(2)]
     for p in ps:
         p.start()
     for p in ps:
