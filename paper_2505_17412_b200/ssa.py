@@ -517,8 +517,12 @@ def ipc_export(t: torch.Tensor):
     another process (the caching allocator sub-allocates, so the offset is carried separately)."""
     st = t.untyped_storage()
     info = st._share_cuda_()
-    handle, off = info[1], int(info[3])
-    return bytes(handle), off + (t.data_ptr() - st.data_ptr())
+    handle, off = bytes(info[1]), int(info[3])
+    # torch's shareable handle: [format version byte][allocation kind byte][cudaIpcMemHandle_t, 64 B]
+    # (a plain cudaMalloc'ed block; expandable segments are not IPC-exportable this way)
+    if len(handle) > 64:
+        handle = handle[-64:]
+    return handle, off + (t.data_ptr() - st.data_ptr())
 
 
 def ipc_open(handle: bytes, offset: int) -> tuple:
