@@ -133,59 +133,27 @@ def workload(config: str, rank: int, world: int):
     return cfg, batch_coords(shells), (cfg["G"],) * 3, len(shells)
 
 
-def hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world):
-    """C4 on N > 1 ranks (SURVEY §8e hybrid): the batch's query blocks on one cost line cut into N equal
-    pieces (shard.hybrid_plan). Shapes a rank holds entirely run whole as one batch plan (mode 1, no
-    collective); shapes cut by a piece boundary run ssa_step_sharded over their sub-group (mode 2).
+def hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world, exchange="allgather"):
+    """C4 on N > 1 ranks (SURVEY §8e hybrid, shard.HybridBatch): the batch's query blocks on one cost line
+    cut into N equal pieces; shapes a rank holds entirely run whole as one batch plan (mode 1, no
+    collective), shapes cut by a piece boundary run ssa_step_sharded over their sub-group (mode 2).
     Every rank holds the batch's inputs (identical seeds per shape); a step includes every block build
-    and the gather of the rank's own rows. Returns step()."""
-    import numpy as np
-    from paper_2505_17412_b200.shard import hybrid_plan, ssa_step_sharded
+    and the gather of the rank's own rows. Returns (step, info)."""
+    from paper_2505_17412_b200.shard import HybridBatch
     from ssa_workload import batch_coords, make_inputs, sphere_shell
     G = (cfg["G"],) * 3
     ms = (cfg["m_cmp"], cfg["m_slc"], cfg["m_win"], cfg["m_q"])
-    tdt = acfg.dtype
-    shells = [sphere_shell(*sh) for sh in cfg["shapes"]]
-    coords = [batch_coords([sh]) for sh in shells]
+    coords = [batch_coords([sphere_shell(*sh)]) for sh in cfg["shapes"]]
     tens = []
     for s, c in enumerate(coords):
         inp = make_inputs(c, G, 1, cfg["H"], cfg["h_kv"], cfg["d"], cfg["dtype"], seed=cfg["seed"] + s)
-        tens.append([torch.from_numpy(x).to(dev, dtype=tdt) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)])
-    cdev = [torch.from_numpy(c).to(dev) for c in coords]
-    qt = [np.diff(ssa.ssa_build_blocks(cd, G, 1, *ms).q_offsets_host()) for cd in cdev]
-    allp = hybrid_plan(qt, world)
-    groups, ranges = {}, {}
-    for s in range(len(shells)):                   # every rank creates every sub-group, in shape order
-        grp = next(g for items in allp for (ss, a, b, g) in items if ss == s)
-        if len(grp) > 1:
-            groups[s] = dist.new_group(list(grp))
-            ranges[s] = [next((a, b) for (ss, a, b, _) in allp[r] if ss == s) for r in grp]
-    mine = allp[rank]
-    whole = [s for (s, a, b, g) in mine if len(g) == 1]
-    split = [(s, g) for (s, a, b, g) in mine if len(g) > 1]
-    wb = None
-    if whole:
-        wc = batch_coords([shells[s] for s in whole])
-        wb = (torch.from_numpy(wc).to(dev), len(whole),
-              [torch.cat([tens[s][i] for s in whole]) for i in range(5)])
-    comm = torch.cuda.Stream(dev)
-    info = {"whole_shapes": whole, "split_shapes": [(s, list(g)) for s, g in split],
-            "plan": [[(s, a, b, len(g)) for (s, a, b, g) in items] for items in allp]}
+        tens.append([torch.from_numpy(x).to(dev, dtype=acfg.dtype) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)])
+    hb = HybridBatch(coords, G, ms, acfg, rank, world, dev, exchange=exchange)
+    info = {"whole_shapes": hb.whole, "split_shapes": [(s, list(g)) for s, g in hb.split],
+            "plan": [[(s, a, b, len(g)) for (s, a, b, g) in items] for items in hb.plan]}
 
     def step():
-        if wb is not None:
-            cd, nb, (q, k, v, g, do) = wb
-            plan = ssa.ssa_build_blocks(cd, G, nb, *ms)
-            _, saved = ssa.ssa_forward(plan, acfg, q, k, v, g)
-            ssa.ssa_backward(plan, acfg, saved, q, k, v, g, do)
-        for s, grp in split:
-            plan = ssa.ssa_build_blocks(cdev[s], G, 1, *ms)
-            qo = plan.q_offsets_host()
-            a, b = ranges[s][grp.index(rank)]
-            rows = plan.perm()[int(qo[a]):int(qo[b])].long()
-            loc = [x[rows] for x in tens[s]]
-            ssa_step_sharded(plan, acfg, *loc, rank=grp.index(rank), world=len(grp), group=groups[s],
-                             comm_stream=comm, q_ranges=ranges[s])
+        hb.step(tens)
         return None, None
     return step, info
 
@@ -229,7 +197,7 @@ def main():
     hybrid_info = None
     comm = torch.cuda.Stream(dev)
     if hybrid:
-        hstep, hybrid_info = hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world)
+        hstep, hybrid_info = hybrid_step(ssa, torch, dist, dev, cfg, acfg, rank, world, exchange=args.exchange)
 
     def step(qq=q, kk=k, vv=v, gg=g, dd=do, o_=out, gr_=grads, cc=c_d, after_build=None):
         if hybrid:

@@ -36,9 +36,12 @@ __global__ void k_gather_rows(Ctx c, const T* __restrict__ src, T* __restrict__ 
   const int ch = i % per;
   const int g = (i / per) % c.h_kv;
   const int p = i / (per * c.h_kv);
-  if (p < c.row_lo || p >= c.row_hi) return;             // rows of other shards are never read
-  const int src_p = c.sorted_input ? p : c.perm[p];
   uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t(g) * c.N + p) * c.h_s * c.D);
+  if (p < c.row_lo || p >= c.row_hi) {   // rows of other shards are never read; zeros keep the padded
+    d4[ch] = make_uint4(0u, 0u, 0u, 0u); // tail of a row tile finite (TMA loads whole 128-row tiles)
+    return;
+  }
+  const int src_p = c.sorted_input ? p : c.perm[p];
   if (c.Dc == c.D) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t(src_p) * c.H + g * c.h_s) * c.D);
     d4[ch] = s4[ch];
@@ -72,9 +75,13 @@ __global__ void k_gather_gates(Ctx c, const T* __restrict__ gates, float* __rest
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.N * c.H) return;
   const int h = i % c.H, p = i / c.H;
-  if (p < c.row_lo || p >= c.row_hi) return;             // rows of other shards are never read
-  const int src_p = c.sorted_input ? p : c.perm[p];
   const int g = h / c.h_s, s = h % c.h_s;
+  if (p < c.row_lo || p >= c.row_hi) {                   // rows of other shards are never read
+    float* z = gs + ((int64_t(g) * c.N + p) * c.h_s + s) * 3;
+    z[0] = z[1] = z[2] = 0.f;
+    return;
+  }
+  const int src_p = c.sorted_input ? p : c.perm[p];
   const T* src = gates + (int64_t(src_p) * c.H + h) * 3;
   float* dst = gs + ((int64_t(g) * c.N + p) * c.h_s + s) * 3;
   dst[0] = ld(src);

@@ -118,11 +118,12 @@ __global__ void k_tc_bwd_rows(Ctx c, __half* q16, __half* do16, __half* dow) {
     const float4 x = o[0], y = o[1];
     acc[b] = fd[0] * x.x + fd[1] * x.y + fd[2] * x.z + fd[3] * x.w + fd[4] * y.x + fd[5] * y.y + fd[6] * y.z + fd[7] * y.w;
   }
-  if (owned) {
+  if (valid) {   // rows of other shards: zeros (fq = fd = 0), so padded tile tails stay finite
     *reinterpret_cast<uint4*>(q16 + io) = f32x8_to_h(fq, 1.f);
     *reinterpret_cast<uint4*>(do16 + io) = f32x8_to_h(fd, ds);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) *reinterpret_cast<uint4*>(dow + int64_t(b) * nrows * kD + io) = f32x8_to_h(fd, w[b] * ds);
+    for (int b = 0; b < 3; ++b)
+      *reinterpret_cast<uint4*>(dow + int64_t(b) * nrows * kD + io) = f32x8_to_h(fd, owned ? w[b] * ds : 0.f);
   }
 #pragma unroll
   for (int o = 4; o; o >>= 1)

@@ -281,3 +281,68 @@ def hybrid_makespan(q_tokens, plan):
     n_tok = [int(np.sum(t)) for t in q_tokens]
     return max((sum(float(np.sum(np.asarray(q_tokens[s][a:b], np.float64))) * n_tok[s] for s, a, b, _ in items)
                 for items in plan), default=0.0)
+
+
+class HybridBatch:
+    """One rank's share of a batch of shapes under the hybrid placement (hybrid_plan):
+    the shapes this rank holds entirely run as ONE batch plan (mode 1, no collective), the shapes cut by
+    a piece boundary run ssa_step_sharded over their sub-group (mode 2). Every rank must construct it
+    with the same arguments (it creates the sub-groups with dist.new_group in shape order).
+
+    coords: list of host int32 [n_s, 4] arrays (batch index 0), one per shape; grid; ms = (m_cmp, m_slc,
+    m_win, m_q); cfg: AttnCfg. step(tensors) with tensors[s] = (q, k, v, gates, dout) of shape s in its
+    caller order returns {"whole": (shapes, out, dq, dk, dv, dgates) of the concatenated whole shapes or
+    None, "split": {s: (plan-order rows [a, b), out, dq, dk, dv, dgates) of this rank's rows}}."""
+
+    def __init__(self, coords, grid, ms, cfg, rank, world, device, exchange="allgather"):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        from . import ssa
+        self.ssa, self.cfg, self.rank, self.world, self.ms = ssa, cfg, rank, world, tuple(ms)
+        self.grid = tuple(grid)
+        self.exchange = exchange
+        self.cdev = [torch.from_numpy(np.ascontiguousarray(c)).to(device) for c in coords]
+        qt = [np.diff(ssa.ssa_build_blocks(cd, self.grid, 1, *self.ms).q_offsets_host()) for cd in self.cdev]
+        self.plan = hybrid_plan(qt, world)
+        self.groups, self.ranges = {}, {}
+        for s in range(len(coords)):                   # every rank creates every sub-group, in shape order
+            grp = next(g for items in self.plan for (ss, a, b, g) in items if ss == s)
+            if len(grp) > 1:
+                self.groups[s] = dist.new_group(list(grp)) if world > 1 else None
+                self.ranges[s] = [next((a, b) for (ss, a, b, _) in self.plan[r] if ss == s) for r in grp]
+        mine = self.plan[rank]
+        self.whole = [s for (s, a, b, g) in mine if len(g) == 1]
+        self.split = [(s, g) for (s, a, b, g) in mine if len(g) > 1]
+        self.wcoords = None
+        if self.whole:
+            parts = []
+            for i, s in enumerate(self.whole):
+                c = np.array(coords[s], copy=True)
+                c[:, 0] = i
+                parts.append(c)
+            self.wcoords = torch.from_numpy(np.concatenate(parts)).to(device)
+        self.comm = torch.cuda.Stream(device)
+
+    def step(self, tensors):
+        import torch
+        ssa = self.ssa
+        res = {"whole": None, "split": {}}
+        if self.whole:
+            q, k, v, g, do = (torch.cat([tensors[s][i] for s in self.whole]) for i in range(5))
+            plan = ssa.ssa_build_blocks(self.wcoords, self.grid, len(self.whole), *self.ms)
+            out, saved = ssa.ssa_forward(plan, self.cfg, q, k, v, g)
+            dq, dk, dv, dg = ssa.ssa_backward(plan, self.cfg, saved, q, k, v, g, do)
+            res["whole"] = (list(self.whole), out, dq, dk, dv, dg)
+        for s, grp in self.split:
+            plan = ssa.ssa_build_blocks(self.cdev[s], self.grid, 1, *self.ms)
+            qo = plan.q_offsets_host()
+            a, b = self.ranges[s][grp.index(self.rank)]
+            ta, tb = int(qo[a]), int(qo[b])
+            rows = plan.perm()[ta:tb].long()
+            loc = [x[rows] for x in tensors[s]]
+            out = ssa_step_sharded(plan, self.cfg, *loc, rank=grp.index(self.rank), world=len(grp),
+                                   group=self.groups[s], comm_stream=self.comm, q_ranges=self.ranges[s],
+                                   exchange=self.exchange)
+            res["split"][s] = ((ta, tb),) + tuple(out)
+        return res

@@ -172,3 +172,96 @@ def test_two_process_sharded_step(tmp_path, exchange):
             # both sides rounded to bf16 from fp32 sums taken in different orders: one bf16 ulp
             assert bool(((got - want).abs() <= 2.0 ** -7 * want.abs() + 1e-4 * want.pow(2).mean().sqrt()).all())
     assert covered == plan.n
+
+
+def _hybrid_shapes():
+    from ssa_workload import batch_coords, sphere_shell
+    return [batch_coords([sphere_shell(32, r, 2.0)]) for r in (9.0, 12.0, 14.0)]
+
+
+def _hybrid_proc(rank, world, port, path, exchange):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_17412_b200 import ssa
+    from paper_2505_17412_b200.shard import HybridBatch
+    from ssa_workload import make_inputs
+    shapes = _hybrid_shapes()
+    tens = []
+    for s, c in enumerate(shapes):
+        inp = make_inputs(c, (32, 32, 32), 1, 16, 2, 64, "bf16", seed=40 + s)
+        tens.append([torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)])
+    cfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=4, dtype=torch.bfloat16)
+    hb = HybridBatch(shapes, (32, 32, 32), (4, 8, 8, 8), cfg, rank, world, torch.device("cuda"), exchange=exchange)
+    res = hb.step(tens)
+    torch.cuda.synchronize()
+    w = res["whole"]
+    save = {"whole": None if w is None else (w[0],) + tuple(x.cpu() for x in w[1:]),
+            "split": {s: (v[0],) + tuple(x.cpu() for x in v[1:]) for s, v in res["split"].items()},
+            "plan": hb.plan}
+    torch.save(save, f"{path}/h{rank}.pt")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["allgather", "fetch"])
+def test_two_process_hybrid_batch(tmp_path, exchange):
+    """Hybrid placement of a 3-shape batch on 2 ranks (shard.HybridBatch, the C4 bench path
+    at N > 1): the cost-line cut splits the middle shape over both ranks (mode 2) while the others run
+    whole (mode 1). Every shape's out / dq / dgates equal a single-GPU run of that shape (whole shapes:
+    the batch plan computes each item independently; split shape: owned rows bit for bit); dk / dv
+    within one bf16 ulp (fp32 partial sums in another order)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2505_17412_b200 import ssa
+    from ssa_workload import make_inputs
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    ps = [ctx.Process(target=_hybrid_proc, args=(r, 2, port, str(tmp_path), exchange)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    res = [torch.load(f"{tmp_path}/h{r}.pt") for r in range(2)]
+    assert any(len(g) > 1 for items in res[0]["plan"] for (_, _, _, g) in items), "expected a split shape"
+    cfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=4, dtype=torch.bfloat16)
+    shapes = _hybrid_shapes()
+    ref = []
+    for s, c in enumerate(shapes):
+        inp = make_inputs(c, (32, 32, 32), 1, 16, 2, 64, "bf16", seed=40 + s)
+        t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
+        plan = ssa.ssa_build_blocks(torch.from_numpy(c).cuda(), (32, 32, 32), 1, 4, 8, 8, 8)
+        o, sv = ssa.ssa_forward(plan, cfg, *t[:4])
+        g = ssa.ssa_backward(plan, cfg, sv, *t)
+        torch.cuda.synchronize()
+        ref.append((plan.perm().cpu().long(), o.cpu(), *(x.cpu() for x in g)))
+
+    def close(a, b):
+        a, b = a.float(), b.float()
+        return bool(((a - b).abs() <= 2.0 ** -7 * b.abs() + 1e-4 * b.pow(2).mean().sqrt()).all())
+
+    seen = {s: 0 for s in range(len(shapes))}
+    for r in range(2):
+        w = res[r]["whole"]
+        if w is not None:
+            off = 0
+            for s in w[0]:
+                n = len(shapes[s])
+                for got, want in zip(w[1:], ref[s][1:]):
+                    assert close(got[off:off + n], want)
+                off += n
+                seen[s] += n
+        for s, (ab, out, dq, dk, dv, dg) in res[r]["split"].items():
+            perm = ref[s][0][ab[0]:ab[1]]
+            assert torch.equal(out, ref[s][1][perm]) and torch.equal(dq, ref[s][2][perm]) and torch.equal(dg, ref[s][5][perm])
+            assert close(dk, ref[s][3][perm]) and close(dv, ref[s][4][perm])
+            seen[s] += ab[1] - ab[0]
+    assert all(seen[s] == len(shapes[s]) for s in seen)
