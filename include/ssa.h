@@ -119,8 +119,9 @@ ssa_status ssa_get_plan_info(ssa_plan plan, ssa_plan_info* out);
  *   scale        : softmax scale; <= 0 means 1/sqrt(d) (Eq. 5).
  *   dtype        : SSA_F32 (SIMT fp32 kernels, the fp32 mode) or SSA_BF16 (tcgen05 tensor-core
  *                  kernels: d == 64 — or d == 32, the paper's DiT head dim, run zero-padded to
- *                  64 inside the library: the logits and the outputs are unchanged — m_win == m_slc ==
- *                  m_q, block counts within the kernels' on-chip limits). A bf16 request outside those returns SSA_ERR_UNSUPPORTED (reason in
+ *                  64 inside the library: the logits and the outputs are unchanged — m_win == m_slc,
+ *                  m_q dividing m_slc (m_q = 1: per-token selection, Alg. 1), block counts within the
+ *                  kernels' on-chip limits). A bf16 request outside those returns SSA_ERR_UNSUPPORTED (reason in
  *                  ssa_last_error) unless SSA_FORCE_SIMT opts into the SIMT kernels — there is no
  *                  silent fallback. Every check happens before any work is enqueued.
  *   pe_k, pe_v   : optional device [m_cmp^3, h_kv, d] (dtype) intra-block PE tables added before

@@ -124,7 +124,8 @@ ssa_status check_cfg(const Plan* p, const ssa_attn_cfg* cfg, Dims* d) {
 bool use_tc(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   const int32_t* m = p->info.m;
   return tc_available() && cfg->dtype == SSA_BF16 && d.D == 64 && !(cfg->flags & SSA_FORCE_SIMT) &&
-         m[SSA_LEVEL_WIN] == m[SSA_LEVEL_SLC] && m[SSA_LEVEL_Q] == m[SSA_LEVEL_SLC] && cfg->top_k <= 64 &&
+         m[SSA_LEVEL_WIN] == m[SSA_LEVEL_SLC] && m[SSA_LEVEL_Q] <= m[SSA_LEVEL_SLC] &&
+         m[SSA_LEVEL_SLC] % m[SSA_LEVEL_Q] == 0 && cfg->top_k <= 64 &&
          tc_plan_ok(p->info, cfg->top_k);
 }
 bool use_tc_bwd(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
@@ -135,7 +136,7 @@ const char* tc_reason(const Dims& d, const ssa_attn_cfg* cfg, const Plan* p) {
   const int32_t* m = p->info.m;
   if (!tc_available()) return "library built without the tcgen05 kernels";
   if (d.D != 64) return "head dim not 32 or 64";
-  if (m[SSA_LEVEL_WIN] != m[SSA_LEVEL_SLC] || m[SSA_LEVEL_Q] != m[SSA_LEVEL_SLC]) return "m_win or m_q != m_slc";
+  if (m[SSA_LEVEL_WIN] != m[SSA_LEVEL_SLC] || m[SSA_LEVEL_Q] > m[SSA_LEVEL_SLC]) return "m_win != m_slc or m_q > m_slc";
   if (!tc_plan_ok(p->info, cfg->top_k)) return "a batch item's block counts exceed the kernels' on-chip limits";
   return nullptr;
 }
@@ -245,6 +246,7 @@ void fill_common(Ctx* x, const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) 
     x->bb[l] = p->batch_blocks[l];
   }
   x->max_cmp_b = p->info.max_blocks_per_batch[SSA_LEVEL_CMP];
+  x->qb_per_item = tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q]);
   x->max_slc_b = p->info.max_blocks_per_batch[SSA_LEVEL_SLC];
   x->scale = cfg->scale > 0.f ? cfg->scale : 1.0f / std::sqrt(float(d.Dc));
   x->sorted_input = (cfg->flags & SSA_INPUT_SORTED) ? 1 : 0;
@@ -406,7 +408,8 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q);
   if (cfg->learned && cfg->learned->x) scan += gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c);
   if (cfg->learned && cfg->learned->conv_k_w) scan += conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D);
-  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]) + 1024;
+  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC],
+                                               tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q])) + 1024;
   return SSA_OK;
 }
 
@@ -447,7 +450,8 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, d, p, &x);
   void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
-  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
+  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC],
+                                              x.qb_per_item));
   void* part_ws = nullptr;
   void* conv_ws = nullptr;
   if (lgates) {

@@ -76,6 +76,7 @@ struct Ctx {
   float *dkc, *dvc;               // fp32 [h_kv][n_cmp][D]
   float *dkc_part, *dvc_part;     // fp32 [n_chunk][h_kv][n_cmp][D]
   int32_t n_chunk;
+  int32_t qb_per_item;            // raw-key KV-outer work item size in query blocks (tc_qb_per_item)
   const uint32_t* do_amax;
   // §8f row 2 (learned.cu): learned compression delta (R17) and gate projection (R18)
   const float *conv_kw, *conv_kb, *conv_vw, *conv_vb;   // [m^3][h_kv][D][D], [h_kv][D]; null = mean pool

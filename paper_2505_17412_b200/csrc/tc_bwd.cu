@@ -301,7 +301,10 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
     for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], 1);   // (unselected: empty range)
     if (n <= kMaxKT && n > 0 && S->tile_br[n - 1] != 0) flush();
     pos = kKT;                                    // the window starts a fresh tile
-    if (!c.no_win) add_block(t0, t1, 2);          // SSA_NO_WINDOW: no window tiles
+    if (!c.no_win) {                              // the window holding the query block (SSA_NO_WINDOW: none)
+      const int wb = c.tok_block[SSA_LEVEL_WIN][t0];
+      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1], 2);
+    }
     if (n <= kMaxKT && n > 0) flush();
     n = min(n, kMaxKT);
     S->tile_seg[n] = ns;
@@ -676,8 +679,8 @@ __device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
   it->kblock = key / c.h_kv;
   it->g = key % c.h_kv;
   const int l0 = c.inv_off[key], l1 = c.inv_off[key + 1];
-  it->li = min(l1, l0 + it->chunk * kQBlocksPerItem);
-  it->le = min(l1, it->li + kQBlocksPerItem);
+  it->li = min(l1, l0 + it->chunk * c.qb_per_item);
+  it->le = min(l1, it->li + c.qb_per_item);
   it->with_win = !c.no_win && it->chunk == nch - 1 && it->kblock >= c.q_begin && it->kblock < c.q_end;  // window = block
   it->first = it->chunk == 0;
   it->part_slot = id;
@@ -702,8 +705,11 @@ struct RowWalk {
   __device__ bool next_range() {
     if (it.mode == 0) return false;
     if (li < it.le) {
-      const int Qb = c->inv_list[li++];
+      int Qb = c->inv_list[li++];
       cur = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_Q][Qb]) * c->h_s;
+      // consecutive query blocks in the (ascending) list are contiguous rows: one range, so 64-row
+      // tiles are not cut at every query block (small query blocks, e.g. per-token selection)
+      while (li < it.le && c->inv_list[li] == Qb + 1) Qb = c->inv_list[li++];
       end = (int64_t(it.g) * c->N + c->off[SSA_LEVEL_Q][Qb + 1]) * c->h_s;
       br = 1;
       return true;
@@ -1056,7 +1062,7 @@ __global__ void k_kv_item_count(Ctx c, int32_t* cnt) {
   const int key = blockIdx.x * blockDim.x + threadIdx.x;
   if (key >= c.n_blk[SSA_LEVEL_SLC] * c.h_kv) return;
   const int len = c.inv_off[key + 1] - c.inv_off[key];
-  cnt[key] = max(1, (len + kQBlocksPerItem - 1) / kQBlocksPerItem);
+  cnt[key] = max(1, (len + c.qb_per_item - 1) / c.qb_per_item);
 }
 // fold the partials of items 1.. of every (block, g) into dk_acc / dv_acc, in item order
 __global__ void k_kv_reduce(Ctx c) {
@@ -1091,16 +1097,21 @@ __global__ void k_kv_reduce(Ctx c) {
 
 bool tc_bwd_available() { return true; }
 
-static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T) {
-  return int64_t(n_slc) * h_kv + (int64_t(n_q) * h_kv * T + kQBlocksPerItem - 1) / kQBlocksPerItem + 1;
+static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T, int qbpi) {
+  return int64_t(n_slc) * h_kv + (int64_t(n_q) * h_kv * T + qbpi - 1) / qbpi + 1;
 }
 
-size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc) {
+int tc_qb_per_item(int m_slc, int m_q) {
+  const int r = m_q > 0 && m_slc % m_q == 0 ? m_slc / m_q : 1;
+  return kQBlocksPerItem * r * r * r;
+}
+
+size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, int T, int max_fill_slc, int qb_per_item) {
   // fp16 copies: q, dO, 3 x gate-scaled dO (rows), k, v (keys), K^cmp, V^cmp (n_cmp <= N)
   size_t b = (size_t(5) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 8 * 256;
   const int64_t nkeys = int64_t(n_slc) * h_kv;
   b += size_t(2 * nkeys + 2) * 4 + 512 + scan_ws_bytes(nkeys + 1);                  // item counts / offsets
-  b += size_t(2) * kv_items_bound(n_slc, n_q, h_kv, T) * max_fill_slc * D * 4 + 512;  // partials
+  b += size_t(2) * kv_items_bound(n_slc, n_q, h_kv, T, qb_per_item) * max_fill_slc * D * 4 + 512;  // partials
   return b;
 }
 
@@ -1108,7 +1119,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   Ctx c = c_in;
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
   const int n_slc = c.n_blk[SSA_LEVEL_SLC];
-  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D, n_slc, c.n_blk[SSA_LEVEL_Q], c.T, c.max_fill[SSA_LEVEL_SLC]));
+  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D, n_slc, c.n_blk[SSA_LEVEL_Q], c.T, c.max_fill[SSA_LEVEL_SLC], c.qb_per_item));
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
   __half* q16 = cw.take<__half>(qrows * kD);
   __half* do16 = cw.take<__half>(qrows * kD);
@@ -1121,7 +1132,7 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   int32_t* item_cnt = cw.take<int32_t>(nkeys + 1);
   c.kv_item_off = cw.take<int32_t>(nkeys + 1);
   void* scan_ws = cw.take<char>(scan_ws_bytes(nkeys + 1));
-  const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T);
+  const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T, c.qb_per_item);
   c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   uint32_t* amax = cw.take<uint32_t>(1);

@@ -671,7 +671,10 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j]);   // (unselected: empty range)
     S->n_slc_tiles = min(n, kMaxTiles);
     pos = kTile;                                  // the window starts a fresh tile
-    if (!c.no_win) add_block(t0, t1);             // SSA_NO_WINDOW: no window tile
+    if (!c.no_win) {                              // the window holding the query block (SSA_NO_WINDOW: none)
+      const int wb = c.tok_block[SSA_LEVEL_WIN][t0];
+      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1]);
+    }
     if (n <= kMaxTiles) flush();
     n = min(n, kMaxTiles);
     S->tile_seg[n] = ns;

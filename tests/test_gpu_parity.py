@@ -139,7 +139,7 @@ def test_small_cases(dtype, case):
         c = c[rng.permutation(len(c))[: len(c) - 37]]             # ragged batch items, shuffled order
     inp = make_inputs(c, (G, G, G), batch, H, h_kv, d, dtype, seed=7)
     flags = 0
-    if dtype == "bf16" and case in ("mq1_pertoken", "win_lt_q"):
+    if dtype == "bf16" and case == "win_lt_q":
         # outside the tcgen05 kernels: bf16 needs the explicit SIMT opt-in (no silent fallback) ...
         from paper_2505_17412_b200 import ssa
         with pytest.raises(ssa.SSAError, match="SSA_ERR_UNSUPPORTED"):
@@ -324,3 +324,16 @@ def test_paper_head_layout_d32():
     kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=8)
     r, _ = _check_all(inp, kw, expect_tc=True, test="test_paper_head_layout_d32")
     assert r["saved"].d_internal == 64
+
+
+@pytest.mark.parametrize("m_q", [1, 2, 4])
+def test_tc_small_query_blocks(m_q):
+    """Query blocks smaller than the selection blocks on the tcgen05 kernels — m_q = 1 is the paper's
+    per-token selection, I in R^{N x h_kv x T} (Alg. 1): every token's
+    Eq. 8 score is its own (8 heads), its top-T its own; the window is the m_win^3 block holding the
+    query block. Parity (top-k isolated / end to end, every output and gradient) against the oracle."""
+    from ssa_workload import batch_coords, make_inputs, sphere_shell
+    c = batch_coords([sphere_shell(32, 13.0, 2.0)])
+    inp = make_inputs(c, (32, 32, 32), 1, 16, 2, 64, "bf16", seed=25)
+    kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=m_q)
+    _check_all(inp, kw, expect_tc=True, test=f"test_tc_small_query_blocks[{m_q}]")

@@ -1,5 +1,5 @@
-"""Per-token selection (m_q = 1, the paper's exact Alg. 1 granularity) runs on the SIMT kernels; time it
-at C2 next to the tensor-core query-block path (m_q = m_slc) for context."""
+"""Per-token selection (m_q = 1, the paper's exact Alg. 1 granularity) on the tcgen05 kernels at C2, next
+to the query-block path (m_q = m_slc), with the per-kernel split of the per-token step."""
 import os
 import sys
 
@@ -14,9 +14,9 @@ c, grid, batch = config_coords("C2")
 inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=1)
 t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
 cc = torch.from_numpy(c).cuda()
-for m_q in (8, 1):
+for m_q in (8, 4, 1):
     plan = ssa.ssa_build_blocks(cc, grid, batch, 4, 8, 8, m_q)
-    acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=0 if m_q == 8 else ssa.SSA_FORCE_SIMT)
+    acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=0)
     for i in range(4):
         if i == 1:
             torch.cuda.synchronize()
@@ -35,7 +35,8 @@ out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
 ssa.ssa_backward(plan, acfg, saved, *t)
 torch.cuda.synchronize()
 ssa.profile_enable(False)
-for kn in ("k_cmp_fwd", "k_attn_fwd(slc)", "k_attn_fwd(win)", "k_dq", "k_slc_dkdv", "k_win_bwd", "k_cmp_dkdv"):
+for kn in ("tc_cmp_fwd", "tc_slc_win_fwd", "tc_bwd_dq", "tc_bwd_kv", "tc_bwd_cmp_kv",
+           "k_cmp_fwd", "k_attn_fwd(slc)", "k_attn_fwd(win)", "k_dq", "k_slc_dkdv", "k_win_bwd", "k_cmp_dkdv"):
     ms, n = ssa.profile_read(kn)
     if n:
         print(f"  {kn}: {ms:.2f} ms")
