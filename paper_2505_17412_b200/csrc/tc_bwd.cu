@@ -14,6 +14,7 @@
 //             (mode 0): a 1/n_chunk share of the batch item's rows -> per-chunk partials reduced in a
 //             fixed order (deterministic).
 #include <cfloat>
+#include <mutex>
 
 #include "internal.h"
 #include "tc.h"
@@ -1171,10 +1172,14 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   cudaEvent_t ev_join = nullptr;
   if (kBwdFork) {
     static cudaStream_t side[16] = {};
+    static std::mutex side_mu;
     int dev = 0;
     SSA_CUDA_TRY(cudaGetDevice(&dev));
     if (dev < 16) {
-      if (!side[dev]) SSA_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+      {
+        std::lock_guard<std::mutex> lk(side_mu);   // one internal stream per device, created once
+        if (!side[dev]) SSA_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+      }
       cudaEvent_t ev_fork;
       SSA_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       SSA_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
