@@ -1,6 +1,8 @@
 // api.cu — the C ABI of libssa_b200 (include/ssa.h): size queries, caller-buffer carving and the
 // forward / backward orchestration. Every step of the path runs in this library's kernels.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -211,6 +213,48 @@ int pick_chunks(const Plan* p, int h_kv) {
   return best;
 }
 
+// query blocks smaller than the selection blocks on the tcgen05 path run the selection / window, dQ and
+// KV-outer kernels on a virtual query level (pertoken.cu): its block count bound and 64 union slots
+// S = query blocks per sub-group: enough for about SSA_VQ_ROWS (default 128, one tile) query rows at the
+// plan's mean tokens per query block, at most 64 / T; 0 = no virtual level (m_q == m_slc, query blocks
+// that fill a tile on their own, or a query-block range / SSA_LOCAL_ROWS, which the virtual level does
+// not cut)
+double env_or(const char* name, double dflt) {
+  const char* e = getenv(name);
+  const double x = e ? atof(e) : 0.0;
+  return x > 0.0 ? x : dflt;
+}
+double q_rows(const Dims& d) { return d.n_q > 0 ? double(d.N) / d.n_q * (d.H / d.h_kv) : 0.0; }
+int vq_group(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
+  if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32) return 0;
+  if (cfg->q_end > 0 && (cfg->q_begin > 0 || cfg->q_end < d.n_q)) return 0;
+  const double target = env_or("SSA_VQ_ROWS", 128.0);
+  const int S = std::min(64 / d.T, std::max(1, int(target / q_rows(d) + 0.5)));
+  return S >= 2 ? S : 0;
+}
+// The virtual level of the backward: dQ always runs on it (when S > 0); the KV-outer kernel only when
+// query blocks are shorter than SSA_VQ_KV_ROWS (default 16) rows, since its row walk already merges
+// consecutive selecting query blocks into full tiles and the union only adds masked rows.
+struct VqBwd {
+  int S = 0;
+  bool kv = false;
+  Dims dkv;        // sizes of the inverse CSR / KV-outer work items
+  int qbpi = 0;    // KV-outer work-item size
+};
+VqBwd vq_backward(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg, bool tc) {
+  VqBwd v;
+  v.S = tc ? vq_group(p, d, cfg) : 0;
+  const double kv_rows = env_or("SSA_VQ_KV_ROWS", 16.0);
+  v.kv = v.S > 0 && q_rows(d) < kv_rows;
+  v.dkv = d;
+  if (v.kv) {
+    v.dkv.n_q = int(vq_bound(d.n_slc, d.n_q, v.S));
+    v.dkv.T = vq_slots(v.S, d.T);
+  }
+  v.qbpi = v.kv ? vq_qb_per_item() : tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q]);
+  return v;
+}
+
 void carve_bwd(Carve& c, const Dims& d, const Plan* p, Ctx* x) {
   const int64_t rows = d.N * d.H, keys = d.N * d.h_kv;
   for (int b = 0; b < 3; ++b) x->Dd[b] = c.take<float>(rows);
@@ -314,7 +358,8 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   Carve cw(nullptr, 0);
   carve_inputs(cw, d, &x, false);
   fill_common(&x, p, d, cfg);
-  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 + 1024;
+  *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 +
+              (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T) : 0) + 2048;
   return SSA_OK;
 }
 
@@ -350,6 +395,8 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   void* tc_ws = cw.take<char>(tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D));
   void* l_ws = cw.take<char>(learned_fwd_ws_bytes(x));
   x.fetch_mark = cw.take<int32_t>(size_t(d.n_slc) + 1);
+  x.vq_S = tc ? vq_group(p, d, cfg) : 0;
+  x.vq_ws = x.vq_S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, x.vq_S, d.T)) : nullptr;
   if (lgates) x.gs = saved_gates;
   const bool bf16 = cfg->dtype == SSA_BF16;
   // caller-supplied pooled keys (mode 2): no pooling; raw k / v are first read by the selection /
@@ -403,13 +450,14 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   if (!ws_bytes) { set_error("null size pointer"); return SSA_ERR_ARG; }
   Ctx x{};
   Carve cw(nullptr, 0);
+  const VqBwd vq = vq_backward(p, d, cfg, use_tc_bwd(d, cfg, p));
   carve_inputs(cw, d, &x, true);
-  carve_bwd(cw, d, p, &x);
-  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q);
+  carve_bwd(cw, vq.dkv, p, &x);
+  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q) + (vq.S ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T) : 0);
   if (cfg->learned && cfg->learned->x) scan += gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c);
   if (cfg->learned && cfg->learned->conv_k_w) scan += conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D);
-  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC],
-                                               tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q])) + 1024;
+  *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, vq.dkv.n_q, vq.dkv.T,
+                                               p->info.max_fill[SSA_LEVEL_SLC], vq.qbpi) + 1024;
   return SSA_OK;
 }
 
@@ -447,11 +495,13 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   carve_saved(cs, d, cfg, &x);
   float* saved_gates = carve_saved_gates(cs, d, cfg);
   Carve cw(ws, ws_bytes);
+  const VqBwd vq = vq_backward(p, d, cfg, tc_path);
   carve_inputs(cw, d, &x, true);
-  carve_bwd(cw, d, p, &x);
-  void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, d.n_q));
-  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, d.n_q, d.T, p->info.max_fill[SSA_LEVEL_SLC],
-                                              x.qb_per_item));
+  carve_bwd(cw, vq.dkv, p, &x);
+  void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q));
+  void* vq_ws = vq.S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T)) : nullptr;
+  void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, vq.dkv.n_q, vq.dkv.T,
+                                              p->info.max_fill[SSA_LEVEL_SLC], vq.qbpi));
   void* part_ws = nullptr;
   void* conv_ws = nullptr;
   if (lgates) {
@@ -466,9 +516,12 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   // the tcgen05 backward gathers the q / dO rows and computes D_c, dgates in its own row prologue
   if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc, true, /*gates=*/!lgates)) != SSA_OK) return s;
   if (!tc && (s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
-  if ((s = build_inverse_csr(x, scan_ws, st)) != SSA_OK) return s;
+  Ctx xq = x;                                      // the dQ context (virtual level for small m_q)
+  if (vq.S && (s = build_virtual_level(x, vq.S, vq_ws, st, &xq)) != SSA_OK) return s;
+  Ctx& xk = vq.kv ? xq : x;                        // the KV-outer context
+  if ((s = build_inverse_csr(xk, scan_ws, st)) != SSA_OK) return s;
   if (tc) {
-    if ((s = tc_backward(x, tc_ws, st)) != SSA_OK) return s;
+    if ((s = tc_backward(xq, xk, tc_ws, st)) != SSA_OK) return s;
     if (x.win_only) {   // no compressed-key gradients: the pool backward adds zeros
       SSA_CUDA_TRY(cudaMemsetAsync(x.dkc, 0, size_t(d.h_kv) * d.n_cmp * d.D * 4, st));
       SSA_CUDA_TRY(cudaMemsetAsync(x.dvc, 0, size_t(d.h_kv) * d.n_cmp * d.D * 4, st));

@@ -77,6 +77,14 @@ struct Ctx {
   float *dkc_part, *dvc_part;     // fp32 [n_chunk][h_kv][n_cmp][D]
   int32_t n_chunk;
   int32_t qb_per_item;            // raw-key KV-outer work item size in query blocks (tc_qb_per_item)
+  // query blocks smaller than the selection blocks on tcgen05 (pertoken.cu): the virtual-level context
+  // carries the per-token slot masks and, for the KV-outer row masks, the per-query-block selections
+  const unsigned long long* umask;  // [N][h_kv] union-slot mask of every token, null on the plain path
+  const int32_t* tok_I;             // [n_q][h_kv][tok_T] per-query-block selections
+  int32_t tok_T;
+  const int32_t* tok_qb;            // token -> query block
+  void* vq_ws;                      // scratch of the virtual level (forward), null when it is not used
+  int32_t vq_S;                     // its sub-group size in query blocks
   const uint32_t* do_amax;
   // §8f row 2 (learned.cu): learned compression delta (R17) and gate projection (R18)
   const float *conv_kw, *conv_kb, *conv_vw, *conv_vb;   // [m^3][h_kv][D][D], [h_kv][D]; null = mean pool
@@ -110,6 +118,13 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
 // one-sided fetch (simt.cu): mark the selection blocks owned query blocks selected, copy the peer-owned
 // ones into the caller's full-size k / v (before the selection branch)
 ssa_status fetch_selected(const Ctx& c, bool bf16, cudaStream_t st);
+// pertoken.cu: the virtual query level of small query blocks (m_q < m_slc)
+int vq_slots(int S, int T);
+int vq_qb_per_item();
+bool vq_enabled();
+int64_t vq_bound(int n_slc, int n_q, int S);
+size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T);
+ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);
 size_t gate_bwd_ws_bytes(int64_t N, int H, int C);

@@ -1,0 +1,184 @@
+// pertoken.cu — query blocks smaller than the selection blocks (m_q | m_slc, m_q < m_slc; m_q = 1 is the
+// paper's per-token selection, I in R^{N x h_kv x T}, Alg. 1 P:182 / P:188) on the tcgen05 kernels.
+//
+// The compression kernel runs per query block (its Eq. 8 scores and top-k ARE per query block). The
+// selection / window and dQ / KV-outer kernels would then see one query block's few rows per 128-row
+// tile, so they run on a "virtual" query level instead: each selection block's query blocks are cut
+// into sub-groups of S consecutive query blocks (contiguous rows; S chosen on the host so that a sub-group
+// fills about one 128-row tile, S * T <= 64); a sub-group's key set is the union of its query blocks'
+// selections (<= S * T blocks), and every row keeps
+// only its own query block's blocks through a 64-bit slot mask (umask[token][g]): the softmax loops set
+// the other granules' logits to -inf (forward, dQ), the KV-outer producer gives the rows of query
+// blocks that did not select the key block an LSE of +inf (p = 0). Same arithmetic per row as the
+// query-block path; only the row / key grouping changes.
+#include <climits>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace ssa {
+namespace {
+
+inline unsigned nb(int64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+// query-block range [qa, qe) of selection block B
+__device__ __forceinline__ void slc_qblocks(const Ctx& c, int B, int* qa, int* qe) {
+  const int t0 = c.off[SSA_LEVEL_SLC][B], t1 = c.off[SSA_LEVEL_SLC][B + 1];
+  *qa = c.tok_block[SSA_LEVEL_Q][t0];
+  *qe = c.tok_block[SSA_LEVEL_Q][t1 - 1] + 1;
+}
+
+__global__ void k_vq_count(Ctx c, int S, int32_t* __restrict__ cnt) {
+  const int B = blockIdx.x * blockDim.x + threadIdx.x;
+  if (B >= c.n_blk[SSA_LEVEL_SLC]) return;
+  int qa, qe;
+  slc_qblocks(c, B, &qa, &qe);
+  cnt[B] = (qe - qa + S - 1) / S;
+}
+
+// sub-group v of selection block B covers query blocks [qa_v, qe_v): token offsets off_v, batch item,
+// identity work order; slots past the real count are empty (off = N) so their CTAs do nothing
+__global__ void k_vq_fill(Ctx c, int S, const int32_t* __restrict__ start, int32_t* __restrict__ off_v,
+                          int32_t* __restrict__ qrange, int32_t* __restrict__ batch_v, int32_t* __restrict__ order_v,
+                          int bound) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > bound) return;
+  const int total = start[c.n_blk[SSA_LEVEL_SLC]];
+  if (v < bound) order_v[v] = v;
+  if (v >= total) {
+    off_v[v] = c.N;
+    if (v < bound) { qrange[2 * v] = qrange[2 * v + 1] = 0; batch_v[v] = 0; }
+    return;
+  }
+  int lo = 0, hi = c.n_blk[SSA_LEVEL_SLC];      // selection block B with start[B] <= v < start[B + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (start[mid] <= v) lo = mid; else hi = mid;
+  }
+  const int B = lo;
+  int qa, qe;
+  slc_qblocks(c, B, &qa, &qe);
+  const int a = qa + (v - start[B]) * S, e = min(qe, a + S);
+  off_v[v] = c.off[SSA_LEVEL_Q][a];
+  qrange[2 * v] = a;
+  qrange[2 * v + 1] = e;
+  batch_v[v] = c.q_batch[a];
+}
+
+// union of the sub-group's selections (sorted, unique, -1 padded to S * T <= 64 slots) and the slot mask of every
+// token of the sub-group. One 32-thread CTA per (sub-group, kv group).
+__global__ void k_vq_union(Ctx c, int vT, const int32_t* __restrict__ qrange, int32_t* __restrict__ I_u,
+                           unsigned long long* __restrict__ umask) {
+  __shared__ int u[64];
+  __shared__ int nu;
+  const int v = blockIdx.x, g = blockIdx.y, lane = threadIdx.x;
+  const int a = qrange[2 * v], e = qrange[2 * v + 1];
+  int32_t* out = I_u + (int64_t(v) * c.h_kv + g) * vT;
+  if (lane == 0) {
+    int n = 0;
+    for (int q = a; q < e; ++q)
+      for (int j = 0; j < c.T; ++j) {
+        const int B = c.I[(int64_t(q) * c.h_kv + g) * c.T + j];
+        if (B < 0) continue;
+        int k = n;                                   // insertion into the sorted unique list
+        bool dup = false;
+        while (k > 0 && u[k - 1] >= B) {
+          if (u[k - 1] == B) { dup = true; break; }
+          --k;
+        }
+        if (dup) continue;
+        for (int m = n; m > k; --m) u[m] = u[m - 1];
+        u[k] = B;
+        ++n;                                         // <= (e - a) * T <= S * T <= 64
+      }
+    nu = n;
+  }
+  __syncwarp();
+  const int n = nu;
+  for (int j = lane; j < vT; j += 32) out[j] = j < n ? u[j] : -1;
+  for (int q = a + lane; q < e; q += 32) {
+    unsigned long long m = 0ull;
+    for (int j = 0; j < c.T; ++j) {
+      const int B = c.I[(int64_t(q) * c.h_kv + g) * c.T + j];
+      if (B < 0) continue;
+      int lo = 0, hi = n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (u[mid] < B) lo = mid + 1; else hi = mid;
+      }
+      m |= 1ull << lo;
+    }
+    for (int t = c.off[SSA_LEVEL_Q][q]; t < c.off[SSA_LEVEL_Q][q + 1]; ++t) umask[int64_t(t) * c.h_kv + g] = m;
+  }
+}
+
+}  // namespace
+
+// KV-outer work-item size on the virtual level, in virtual query blocks (build knob SSA_VQ_QB_PER_ITEM;
+// the partial-sum buffers scale with 1 / this)
+// (knobs are read per call, so a test can switch them between calls)
+int vq_qb_per_item() {
+  const char* e = getenv("SSA_VQ_QB_PER_ITEM");
+  const int x = e ? atoi(e) : 0;
+  return x > 0 ? x : 128;
+}
+// the virtual level can be switched off (A/B knob SSA_VQ=0: the query-block tiles run as they are)
+bool vq_enabled() {
+  const char* e = getenv("SSA_VQ");
+  return !(e && atoi(e) == 0);
+}
+
+int vq_slots(int S, int T) { return S * T; }
+int64_t vq_bound(int n_slc, int n_q, int S) { return int64_t(n_slc) + (int64_t(n_q) + S - 1) / S; }
+size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T) {
+  const int64_t bound = vq_bound(n_slc, n_q, S);
+  return size_t(n_slc + 2) * 4 * 2 + scan_ws_bytes(n_slc + 1) + size_t(bound + 2) * 4 * 5 +
+         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 16 * 256;
+}
+
+// Build the virtual query level (see the header) with sub-groups of S query blocks from the per-query-
+// block selections c.I and return in *v the context the selection / window, dQ and KV-outer kernels run
+// with.
+ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v) {
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
+  const int vT = vq_slots(S, c.T);
+  if (S < 2 || vT > 64) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
+  const int64_t bound = vq_bound(n_slc, n_q, S);
+  Carve cw(ws, vq_ws_bytes(c.N, c.h_kv, n_slc, n_q, S, c.T));
+  int32_t* cnt = cw.take<int32_t>(n_slc + 1);
+  int32_t* start = cw.take<int32_t>(n_slc + 1);
+  void* sws = cw.take<char>(scan_ws_bytes(n_slc + 1));
+  int32_t* off_v = cw.take<int32_t>(bound + 1);
+  int32_t* qrange = cw.take<int32_t>(2 * bound + 2);
+  int32_t* batch_v = cw.take<int32_t>(bound + 1);
+  int32_t* order_v = cw.take<int32_t>(bound + 1);
+  int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
+  unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv);
+  if (n_slc > 0) {
+    k_vq_count<<<nb(n_slc, 256), 256, 0, st>>>(c, S, cnt);
+    SSA_LAUNCH_CHECK("k_vq_count");
+  }
+  ssa_status s = exclusive_scan(cnt, start, n_slc, start + n_slc, sws, st);
+  if (s != SSA_OK) return s;
+  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, S, start, off_v, qrange, batch_v, order_v, int(bound));
+  SSA_LAUNCH_CHECK("k_vq_fill");
+  k_vq_union<<<dim3(unsigned(bound), c.h_kv), 32, 0, st>>>(c, vT, qrange, I_u, umask);
+  SSA_LAUNCH_CHECK("k_vq_union");
+  *v = c;
+  v->tok_I = c.I;            // the per-query-block selections (KV-outer row masks)
+  v->tok_T = c.T;
+  v->tok_qb = c.tok_block[SSA_LEVEL_Q];
+  v->off[SSA_LEVEL_Q] = off_v;
+  v->n_blk[SSA_LEVEL_Q] = int32_t(bound);
+  v->q_order = order_v;
+  v->q_batch = batch_v;
+  v->q_begin = 0;
+  v->q_end = int32_t(bound);
+  v->I = I_u;
+  v->T = vT;
+  v->umask = umask;
+  v->qb_per_item = vq_qb_per_item();     // KV-outer work items in virtual query blocks (bounds the partial buffers)
+  return SSA_OK;
+}
+
+}  // namespace ssa

@@ -17,6 +17,7 @@ int tc_qb_per_item(int m_slc, int m_q);
 // kv_ev: wait for it before the first read of raw k / v; gather_keys_late: the key gather (k, v ->
 // internal layout) has not been done yet and runs after the wait (pooled keys supplied by the caller)
 ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev = nullptr, bool gather_keys_late = false);
-// backward after gather + prologue + inverse CSR: fills dq_acc, dk_acc, dv_acc, dkc, dvc.
-ssa_status tc_backward(const Ctx& c, void* ws, cudaStream_t st);
+// backward after gather + prologue + inverse CSR: fills dq_acc, dk_acc, dv_acc, dkc, dvc. c: row prologue,
+// dQ and compressed-key KV-outer; c_kv: raw-key KV-outer (its query level carries the inverse CSR).
+ssa_status tc_backward(const Ctx& c, const Ctx& c_kv, void* ws, cudaStream_t st);
 }  // namespace ssa

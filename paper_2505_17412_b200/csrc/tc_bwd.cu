@@ -209,11 +209,14 @@ struct DqSmem {
   int seg_dst_len[kMaxSegDq];             // destination slot << 8 | rows
   int blk_a0[kMaxBlkDq], blk_a1[kMaxBlkDq];   // key ranges of the selected blocks
   int8_t tile_br[kMaxKT];
+  uint8_t seg_slot[kMaxSegDq];            // selection slot of every segment (0xff: window)
 #ifdef SSA_TRACE
   unsigned long long trace[3][128];
 #endif
 };
 
+// kMask: per-row union-slot masks of small query blocks (pertoken.cu), a separate instantiation
+template <bool kMask>
 __global__ void __launch_bounds__(kDqThreads, 1)
 k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
         __grid_constant__ const CUtensorMap tmKc, __grid_constant__ const CUtensorMap tmVc,
@@ -230,6 +233,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
   if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  if (t1 <= t0) return;                               // empty virtual query block (uniform per CTA)
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + 127) / 128;
   const int n_pair = (n_rt + 1) / 2;
@@ -280,7 +284,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       ++n;
     }
     auto flush = [&]() { for (int w = 0; w < 3; ++w) S->tile_mask[n - 1][w] = mk[w]; };
-    auto add_block = [&](int a0, int a1, int br) {
+    auto add_block = [&](int a0, int a1, int br, int slot) {
       const int len = a1 - a0, l8 = (len + 7) & ~7;
       for (int x = 0; x < l8 && n <= kMaxKT;) {
         if (pos == kKT) {
@@ -293,18 +297,23 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           pos = 0;
         }
         const int take = min(l8 - x, kKT - pos), valid = max(0, min(take, len - x));
-        if (ns < kMaxSegDq) { S->seg_row[ns] = g * c.N + a0 + x; S->seg_dst_len[ns] = (pos << 8) | take; ++ns; }
+        if (ns < kMaxSegDq) {
+          S->seg_row[ns] = g * c.N + a0 + x;
+          S->seg_dst_len[ns] = (pos << 8) | take;
+          S->seg_slot[ns] = uint8_t(slot);
+          ++ns;
+        }
         set_bits(pos, pos + valid);
         pos += take;
         x += take;
       }
     };
-    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], 1);   // (unselected: empty range)
+    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], 1, j);   // (unselected: empty range)
     if (n <= kMaxKT && n > 0 && S->tile_br[n - 1] != 0) flush();
     pos = kKT;                                    // the window starts a fresh tile
     if (!c.no_win) {                              // the window holding the query block (SSA_NO_WINDOW: none)
       const int wb = c.tok_block[SSA_LEVEL_WIN][t0];
-      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1], 2);
+      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1], 2, 0xff);
     }
     if (n <= kMaxKT && n > 0) flush();
     n = min(n, kMaxKT);
@@ -471,6 +480,8 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         wgt[br] = c.gs[row * 3 + br];
         Dv[br] = c.Dd[br][row];
       }
+      // small query blocks (virtual level): the selection slots this row's query block selected
+      const unsigned long long rmask = (kMask && rvalid) ? c.umask[int64_t(t0 + r / c.h_s) * c.h_kv + g] : ~0ull;
       for (int j = 0; j < n_tiles; ++j) {
         const int br = S->tile_br[j];
         const uint32_t mk0 = S->tile_mask[j][0], mk1 = S->tile_mask[j][1], mk2 = S->tile_mask[j][2];
@@ -478,6 +489,15 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         const float l2 = br == 0 ? lse2[0] : (br == 1 ? lse2[1] : lse2[2]);
         const float wb = br == 0 ? wgt[0] : (br == 1 ? wgt[1] : wgt[2]);
         const float Db = br == 0 ? Dv[0] : (br == 1 ? Dv[1] : Dv[2]);
+        uint32_t umk = 0u;                             // virtual level: granules this row must not see
+        if (kMask && br == 1)
+          for (int q = S->tile_seg[j]; q < S->tile_seg[j + 1]; ++q) {
+            const uint32_t slot = S->seg_slot[q];
+            if (slot < 64u && !((rmask >> slot) & 1ull)) {
+              const int dst = S->seg_dst_len[q] >> 8, len = S->seg_dst_len[q] & 0xff;
+              umk |= ((1u << (len / 8)) - 1u) << (dst / 8);
+            }
+          }
         mbar_wait(&S->s_full[wg], sb.ph);
         if (warp == 0) TRACE_R(2, 7, j);
         tc_fence_after();
@@ -504,6 +524,14 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
                 for (int i = 0; i < 8; ++i) s[8 * gr + i] = (bits >> i) & 1u ? s[8 * gr + i] : -INFINITY;
               }
             }
+          }
+          if (kMask && umk) {                        // granules of blocks this row's query block did not select
+#pragma unroll
+            for (int gr = 0; gr < 4; ++gr)
+              if ((umk >> (c0 / 8 + gr)) & 1u) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s[8 * gr + i] = -INFINITY;
+              }
           }
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -833,7 +861,15 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         for (int h = 0; h < 2; ++h) {
           const int e = lane + 32 * h;
           const int64_t row = r0 + e;
-          cp_async4(&S->st_l2[w][rs.idx][e], e < nr ? c.lse[br] + row : &g_pos_inf);
+          bool keep = e < nr;
+          if (keep && br == 1 && c.umask) {   // virtual level: rows whose query block did not select the key block
+            const int tok = int(row / c.h_s) - it.g * c.N;
+            const int32_t* sel = c.tok_I + (int64_t(c.tok_qb[tok]) * c.h_kv + it.g) * c.tok_T;
+            bool hit = false;
+            for (int jj = 0; jj < c.tok_T; ++jj) hit |= sel[jj] == it.kblock;
+            keep = hit;
+          }
+          cp_async4(&S->st_l2[w][rs.idx][e], keep ? c.lse[br] + row : &g_pos_inf);
           cp_async4(&S->st_D[w][rs.idx][e], e < nr ? c.Dd[br] + row : &g_zero);
         }
 #if SSA_KV_STATS_WAIT
@@ -1116,11 +1152,12 @@ size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, in
   return b;
 }
 
-ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
-  Ctx c = c_in;
+ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t st) {
+  Ctx c = c_in;     // row prologue, dQ, compressed-key KV-outer
+  Ctx ck = ck_in;   // raw-key KV-outer (its own query level: inverse CSR, work items)
   const int n_cmp = c.n_blk[SSA_LEVEL_CMP];
   const int n_slc = c.n_blk[SSA_LEVEL_SLC];
-  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D, n_slc, c.n_blk[SSA_LEVEL_Q], c.T, c.max_fill[SSA_LEVEL_SLC], c.qb_per_item));
+  Carve cw(ws, tc_bwd_ws_bytes(c.N, c.H, c.h_kv, c.D, n_slc, ck.n_blk[SSA_LEVEL_Q], ck.T, c.max_fill[SSA_LEVEL_SLC], ck.qb_per_item));
   const uint64_t qrows = uint64_t(c.h_kv) * c.N * c.h_s, crows = uint64_t(c.h_kv) * n_cmp, krows = uint64_t(c.h_kv) * c.N;
   __half* q16 = cw.take<__half>(qrows * kD);
   __half* do16 = cw.take<__half>(qrows * kD);
@@ -1131,13 +1168,14 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   __half* vc = cw.take<__half>(crows * kD);
   const int64_t nkeys = int64_t(n_slc) * c.h_kv;
   int32_t* item_cnt = cw.take<int32_t>(nkeys + 1);
-  c.kv_item_off = cw.take<int32_t>(nkeys + 1);
+  ck.kv_item_off = cw.take<int32_t>(nkeys + 1);
   void* scan_ws = cw.take<char>(scan_ws_bytes(nkeys + 1));
-  const int64_t bound = kv_items_bound(n_slc, c.n_blk[SSA_LEVEL_Q], c.h_kv, c.T, c.qb_per_item);
-  c.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
-  c.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
+  const int64_t bound = kv_items_bound(n_slc, ck.n_blk[SSA_LEVEL_Q], c.h_kv, ck.T, ck.qb_per_item);
+  ck.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
+  ck.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   uint32_t* amax = cw.take<uint32_t>(1);
   c.do_amax = amax;
+  ck.do_amax = amax;
   SSA_CUDA_TRY(cudaMemsetAsync(amax, 0, 4, st));
   {  // over the rows this call may read (the owned range with a query-block range / SSA_LOCAL_ROWS)
     const int64_t n8 = int64_t(c.row_hi - c.row_lo) * c.H * c.Dc / 8;
@@ -1192,26 +1230,28 @@ ssa_status tc_backward(const Ctx& c_in, void* ws, cudaStream_t st) {
   {
     const size_t smem = 1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem);
     static_assert(1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem) <= 232448, "dQ shared memory");
-    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_bwd_dq", st);
-    k_tc_dq<<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
+    if (c.umask) k_tc_dq<true><<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
+    else k_tc_dq<false><<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     SSA_LAUNCH_CHECK("k_tc_dq");
   }
   const size_t smem = 1024 + 32768 + 2 * kRStages * 16384 + 2 * kPBuf * 32768 + sizeof(KvSmem);
   if (smem > 232448) { set_error("KV-outer shared memory exceeds 227 KB"); return SSA_ERR_UNSUPPORTED; }
   SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   {
-    k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, kst>>>(c, item_cnt);
+    k_kv_item_count<<<unsigned((nkeys + 255) / 256), 256, 0, kst>>>(ck, item_cnt);
     SSA_LAUNCH_CHECK("k_kv_item_count");
-    ssa_status s = exclusive_scan(item_cnt, c.kv_item_off, nkeys, c.kv_item_off + nkeys, scan_ws, kst);
+    ssa_status s = exclusive_scan(item_cnt, ck.kv_item_off, nkeys, ck.kv_item_off + nkeys, scan_ws, kst);
     if (s != SSA_OK) return s;
     ProfScope ps("tc_bwd_kv", kst);
-    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, kst>>>(c, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
+    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, kst>>>(ck, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
   }
   {
     const int64_t nk = int64_t(c.N) * c.h_kv * (kD / 4);
-    k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, kst>>>(c);
+    k_kv_reduce<<<unsigned((nk + 255) / 256), 256, 0, kst>>>(ck);
     SSA_LAUNCH_CHECK("k_kv_reduce");
   }
   if (!c.win_only) {

@@ -573,6 +573,7 @@ struct SwSmem {
   int seg_row[kMaxSegs];
   int seg_dst_len[kMaxSegs];
   int blk_a0[kMaxTiles], blk_a1[kMaxTiles];   // key ranges of the selected blocks (T <= kMaxTiles)
+  alignas(16) uint8_t gran_slot[kMaxTiles][16];   // selection slot of every 8-key granule (0xff: none / window)
 };
 
 // Per-warp staging of 32 rows x 64 fp32 (8 KB): the thread that owns a row (TMEM lane) writes it with
@@ -592,6 +593,9 @@ __device__ __forceinline__ float4 staged_chunk(const float* wbuf, int rl, int ch
   return *reinterpret_cast<const float4*>(wbuf + rl * 64 + 4 * (ch ^ (rl & 15)));
 }
 
+// kMask: the per-row union-slot masks of small query blocks (pertoken.cu); a separate instantiation so
+// the query-block path carries none of its registers
+template <bool kMask>
 __global__ void __launch_bounds__(kSwThreads, 1)
 k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const TmapSet4 tmK,
                 __grid_constant__ const TmapSet4 tmV) {
@@ -609,6 +613,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   const unsigned long long stamp0 = gtimer();
 #endif
   const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  if (t1 <= t0) return;                               // empty virtual query block (uniform per CTA)
   const int rows = (t1 - t0) * c.h_s;
   const int n_rt = (rows + kTile - 1) / kTile;
   const int n_pair = (n_rt + 1) / 2;
@@ -646,7 +651,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     auto flush = [&]() {
       if (n > 0) for (int w = 0; w < 4; ++w) S->tile_mask[n - 1][w] = mk[w];
     };
-    auto add_block = [&](int a0, int a1) {
+    auto add_block = [&](int a0, int a1, int slot) {
       const int len = a1 - a0, l8 = (len + 7) & ~7;
       for (int x = 0; x < l8 && n <= kMaxTiles;) {
         if (pos == kTile) {
@@ -654,10 +659,12 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           if (n == kMaxTiles) { n = kMaxTiles + 1; break; }
           S->tile_seg[n] = ns;
           mk[0] = mk[1] = mk[2] = mk[3] = 0u;
+          for (int gq = 0; gq < 16; ++gq) S->gran_slot[n][gq] = 0xffu;
           ++n;
           pos = 0;
         }
         const int take = min(l8 - x, kTile - pos), valid = max(0, min(take, len - x));
+        for (int gq = pos / 8; gq < (pos + take) / 8; ++gq) S->gran_slot[n - 1][gq] = uint8_t(slot);
         if (ns < kMaxSegs) { S->seg_row[ns] = a0 + x; S->seg_dst_len[ns] = (pos << 8) | take; ++ns; }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {              // bits [pos, pos + valid) of the 128-bit mask
@@ -668,12 +675,12 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         x += take;
       }
     };
-    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j]);   // (unselected: empty range)
+    for (int j = 0; j < c.T; ++j) add_block(S->blk_a0[j], S->blk_a1[j], j);   // (unselected: empty range)
     S->n_slc_tiles = min(n, kMaxTiles);
     pos = kTile;                                  // the window starts a fresh tile
     if (!c.no_win) {                              // the window holding the query block (SSA_NO_WINDOW: none)
       const int wb = c.tok_block[SSA_LEVEL_WIN][t0];
-      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1]);
+      add_block(c.off[SSA_LEVEL_WIN][wb], c.off[SSA_LEVEL_WIN][wb + 1], 0xff);
     }
     if (n <= kMaxTiles) flush();
     n = min(n, kMaxTiles);
@@ -825,6 +832,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       }
       float lse_slc = 0.f;
       float m = -1e30f, l = 0.f;
+      // small query blocks (virtual level): the selection slots this row's query block selected
+      const unsigned long long rmask = (kMask && rvalid) ? c.umask[int64_t(t0 + r / c.h_s) * c.h_kv + g] : ~0ull;
       for (int j = 0; j < n_tiles; ++j) {
         const bool fresh = j == 0 || j == n_slc_tiles;
         const bool closed = j == n_slc_tiles && j > 0;
@@ -878,12 +887,26 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             }
           }
         }
+        if (kMask && j < n_slc_tiles) {   // granules of blocks this row's query block did not select
+          const uint4 gs4 = *reinterpret_cast<const uint4*>(&S->gran_slot[j][0]);
+          const uint32_t gw[4] = {gs4.x, gs4.y, gs4.z, gs4.w};
+#pragma unroll
+          for (int gr = 0; gr < kTile / 8; ++gr) {
+            const uint32_t slot = (gw[gr >> 2] >> (8 * (gr & 3))) & 0xffu;
+            if (slot < 64u && !((rmask >> slot) & 1ull)) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * gr + i] = -INFINITY;
+            }
+          }
+        }
         if (!closed) {   // P.V(j-1) complete: O is up to date and P may be rewritten
           mbar_wait(&S->p_free[wg], fph);
           fph ^= 1u;
           tc_fence_after();
         }
-        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
+        // (a tile may hold no key of this row at all under a per-row mask: keep the max finite)
+        const float mx0 = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
+        const float mx = kMask ? fmaxf(mx0, -1e30f) : mx0;
         const bool bump = fresh || mx > m + kRescale;
         const float m_new = bump ? mx : m;
         const float alpha = ex2(m - m_new);           // 1 when the reference does not move
@@ -1085,15 +1108,23 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
     k_tc_prep<<<unsigned((n / 4 + 255) / 256), 256, 0, st>>>(c, kc_hi, kc_lo, vc, vs16, 2);
     SSA_LAUNCH_CHECK("k_tc_prep(v)");
   }
+  Ctx cv = c;   // query blocks smaller than the selection blocks: the virtual level (pertoken.cu)
+  if (c.vq_ws) {
+    ssa_status s = build_virtual_level(c, c.vq_S, c.vq_ws, st, &cv);
+    if (s != SSA_OK) return s;
+  }
   {
+    const int nq = cv.n_blk[SSA_LEVEL_Q];
     const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);
-    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_slc_win_fwd", st);
     TmapSet4 tk, tv;
     for (int b = 0; b < 4; ++b)
       if (!make_tmap_bf16_2d(&tk.m[b], c.ks, krows, 64u >> b) || !make_tmap_bf16_2d(&tv.m[b], vs16, krows, 64u >> b))
         return SSA_ERR_CUDA;
-    k_tc_slcwin_fwd<<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(c, tmQ, tk, tv);
+    if (cv.umask) k_tc_slcwin_fwd<true><<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(cv, tmQ, tk, tv);
+    else k_tc_slcwin_fwd<false><<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(cv, tmQ, tk, tv);
     SSA_LAUNCH_CHECK("k_tc_slcwin_fwd");
   }
   return SSA_OK;

@@ -326,14 +326,29 @@ def test_paper_head_layout_d32():
     assert r["saved"].d_internal == 64
 
 
+# query-level choices of the tcgen05 path for m_q < m_slc (pertoken.cu knobs): the plan's own choice,
+# the query-block tiles as they are, the virtual level for dQ / selection only, and for the KV-outer too
+_VQ_MODES = {
+    "auto": {},
+    "direct": {"SSA_VQ": "0"},
+    "vq_dq": {"SSA_VQ_ROWS": "100000", "SSA_VQ_KV_ROWS": "0.001"},
+    "vq_all": {"SSA_VQ_ROWS": "100000", "SSA_VQ_KV_ROWS": "100000", "SSA_VQ_QB_PER_ITEM": "3"},
+}
+
+
+@pytest.mark.parametrize("mode", list(_VQ_MODES))
 @pytest.mark.parametrize("m_q", [1, 2, 4])
-def test_tc_small_query_blocks(m_q):
+def test_tc_small_query_blocks(m_q, mode, monkeypatch):
     """Query blocks smaller than the selection blocks on the tcgen05 kernels — m_q = 1 is the paper's
     per-token selection, I in R^{N x h_kv x T} (Alg. 1): every token's
     Eq. 8 score is its own (8 heads), its top-T its own; the window is the m_win^3 block holding the
-    query block. Parity (top-k isolated / end to end, every output and gradient) against the oracle."""
+    query block. Parity (top-k isolated / end to end, every output and gradient) against the oracle, for
+    each query-level choice of the kernels (same arithmetic per row, only the row / key grouping differs;
+    vq_all also splits every key's rows into many KV-outer work items)."""
     from ssa_workload import batch_coords, make_inputs, sphere_shell
+    for k, v in _VQ_MODES[mode].items():
+        monkeypatch.setenv(k, v)
     c = batch_coords([sphere_shell(32, 13.0, 2.0)])
     inp = make_inputs(c, (32, 32, 32), 1, 16, 2, 64, "bf16", seed=25)
     kw = dict(h_kv=2, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=m_q)
-    _check_all(inp, kw, expect_tc=True, test=f"test_tc_small_query_blocks[{m_q}]")
+    _check_all(inp, kw, expect_tc=True, test=f"test_tc_small_query_blocks[{m_q},{mode}]")

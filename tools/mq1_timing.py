@@ -14,7 +14,7 @@ c, grid, batch = config_coords("C2")
 inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=1)
 t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
 cc = torch.from_numpy(c).cuda()
-for m_q in (8, 4, 1):
+for m_q in [int(x) for x in (sys.argv[1:] or ['8', '4', '1'])]:
     plan = ssa.ssa_build_blocks(cc, grid, batch, 4, 8, 8, m_q)
     acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=0)
     for i in range(4):
@@ -26,7 +26,15 @@ for m_q in (8, 4, 1):
         ssa.ssa_backward(plan, acfg, saved, *t)
     e1.record()
     torch.cuda.synchronize()
-    print(f"C2 m_q={m_q}: {e0.elapsed_time(e1) / 3:.2f} ms fwd+bwd ({'tcgen05' if saved.used_tcgen05 else 'SIMT'})", flush=True)
+    print(f"C2 m_q={m_q}: {e0.elapsed_time(e1) / 3:.2f} ms fwd+bwd ({'tcgen05' if saved.used_tcgen05 else 'SIMT'}), "
+          f"bwd ws {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB peak, N={c.shape[0]}", flush=True)
+    ssa.profile_reset()
+    ssa.profile_enable(True)
+    out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
+    ssa.ssa_backward(plan, acfg, saved, *t)
+    torch.cuda.synchronize()
+    ssa.profile_enable(False)
+    print("   ", {kn: round(ssa.profile_read(kn)[0], 3) for kn in ("tc_cmp_fwd", "tc_slc_win_fwd", "tc_bwd_dq", "tc_bwd_kv", "tc_bwd_cmp_kv")}, flush=True)
 
 # per-kernel split of the per-token (SIMT) step
 ssa.profile_reset()
