@@ -359,7 +359,8 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   carve_inputs(cw, d, &x, false);
   fill_common(&x, p, d, cfg);
   *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 +
-              (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T) : 0) + 2048;
+              (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T) : 0) +
+              tok_cmp_ws_bytes(d.n_q, p->info.batch, tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s), d.max_slc_b) + 2048;
   return SSA_OK;
 }
 
@@ -397,6 +398,8 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   x.fetch_mark = cw.take<int32_t>(size_t(d.n_slc) + 1);
   x.vq_S = tc ? vq_group(p, d, cfg) : 0;
   x.vq_ws = x.vq_S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, x.vq_S, d.T)) : nullptr;
+  x.tok_cmp = tc ? tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s) : 0;
+  x.tok_ws = x.tok_cmp ? cw.take<char>(tok_cmp_ws_bytes(d.n_q, p->info.batch, x.tok_cmp, d.max_slc_b)) : nullptr;
   if (lgates) x.gs = saved_gates;
   const bool bf16 = cfg->dtype == SSA_BF16;
   // caller-supplied pooled keys (mode 2): no pooling; raw k / v are first read by the selection /

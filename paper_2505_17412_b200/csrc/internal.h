@@ -85,6 +85,11 @@ struct Ctx {
   const int32_t* tok_qb;            // token -> query block
   void* vq_ws;                      // scratch of the virtual level (forward), null when it is not used
   int32_t vq_S;                     // its sub-group size in query blocks
+  // per-token compression (m_q = 1, tc_fwd.cu k_tc_cmp_fwd<h_s>): tok_cmp = h_s when used, else 0
+  int32_t tok_cmp;
+  void* tok_ws;                     // its scratch (tok_cmp_ws_bytes), carved by tc_forward into:
+  const int32_t* tok_cg;            // [bound][2] query-block range of each token group
+  float* tok_sc;                    // [kTokSlots][2 * 128 / h_s][max_slc_b] per-SM selection-score scratch
   const uint32_t* do_amax;
   // §8f row 2 (learned.cu): learned compression delta (R17) and gate projection (R18)
   const float *conv_kw, *conv_kb, *conv_vw, *conv_vb;   // [m^3][h_kv][D][D], [h_kv][D]; null = mean pool
@@ -120,6 +125,9 @@ ssa_status gather_inputs(const Ctx& c, bool bf16, cudaStream_t st, bool with_dou
 ssa_status fetch_selected(const Ctx& c, bool bf16, cudaStream_t st);
 // pertoken.cu: the virtual query level of small query blocks (m_q < m_slc)
 int vq_slots(int S, int T);
+constexpr int kTokSlots = 256;      // per-SM scratch slots of the per-token compression kernel (>= %nsmid)
+int tok_cmp_hs(int m_q, int h_s);   // h_s when the per-token compression kernel applies, else 0
+size_t tok_cmp_ws_bytes(int n_q, int batch, int h_s, int max_slc_b);
 int vq_qb_per_item();
 bool vq_enabled();
 int64_t vq_bound(int n_slc, int n_q, int S);

@@ -16,6 +16,8 @@
 // producer, warp 5 MMA issuer (one elected lane) + TMEM owner.
 #include <cfloat>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "tc.h"
 #include "tc_common.cuh"
@@ -165,6 +167,12 @@ __device__ __forceinline__ float4 ld_shared_f4(const float* p) {
   return r;
 }
 
+// kTok = 0: CTA per query block (any m_q), Eq. 8 column sums and selection scores in shared memory.
+// kTok = h_s (per-token selection, m_q = 1): CTA per group of 256 / h_s consecutive tokens of one batch
+// item (tc_tok_groups), two full row tiles; pass 2 sums each key's column per token (h_s rows) and folds
+// the sums into per-token selection-block scores tile by tile (fixed order: keys of a block in key
+// order, then tile order) in an L2-resident per-SM scratch; top-k per token by one warp each.
+template <int kTok>
 __global__ void __launch_bounds__(kCmpThreads, 1)
 k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmKh,
              __grid_constant__ const CUtensorMap tmKl, __grid_constant__ const CUtensorMap tmV) {
@@ -178,11 +186,30 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   float* sc_cmp0 = reinterpret_cast<float*>(S + 1);  // [max_cmp_b] Eq. 8 column sums, per warpgroup
   float* sc_cmp1 = sc_cmp0 + c.max_cmp_b;
   float* sc_slc = sc_cmp1 + c.max_cmp_b;             // [max_slc_b]
+  constexpr int kGT = kTok > 0 ? kTile / kTok : 1;   // tokens per row tile (per-token mode)
+  float* tbuf = reinterpret_cast<float*>(S + 1);     // per-token mode: [2 wg][2 parity][kGT][129] tile sums
+  int* tchosen = reinterpret_cast<int*>(tbuf + 4 * kGT * 129);   // [8 warps][64]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
-  if (Q < c.q_begin || Q >= c.q_end) return;          // not owned by this shard (uniform per CTA)
-  const int t0 = c.off[SSA_LEVEL_Q][Q], t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  const int g = blockIdx.y;
+  int Q, t0, t1;
+  float* tok_scr = nullptr;   // per-token mode: [2 kGT tokens][max_slc_b] scores of this CTA (per-SM slot)
+  if constexpr (kTok > 0) {
+    const int qa = c.tok_cg[2 * blockIdx.x], qe = c.tok_cg[2 * blockIdx.x + 1];
+    if (qe <= qa) return;                             // past the last group (uniform per CTA)
+    Q = qa;
+    t0 = c.off[SSA_LEVEL_Q][qa];
+    t1 = c.off[SSA_LEVEL_Q][qe];
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= unsigned(kTokSlots)) __trap();
+    tok_scr = c.tok_sc + size_t(smid) * (2 * kGT) * c.max_slc_b;   // one resident CTA per SM (smem)
+  } else {
+    Q = c.q_order[blockIdx.x];
+    if (Q < c.q_begin || Q >= c.q_end) return;        // not owned by this shard (uniform per CTA)
+    t0 = c.off[SSA_LEVEL_Q][Q];
+    t1 = c.off[SSA_LEVEL_Q][Q + 1];
+  }
   const int b = c.q_batch[Q];
   const int c0 = c.bb[SSA_LEVEL_CMP][b], nk = c.bb[SSA_LEVEL_CMP][b + 1] - c0;
   const int s0 = c.bb[SSA_LEVEL_SLC][b], ns = c.bb[SSA_LEVEL_SLC][b + 1] - s0;
@@ -213,7 +240,8 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   }
   if (warp == 8 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmKh); tma_prefetch(&tmKl); tma_prefetch(&tmV); }
   if (warp == 9) tmem_alloc<512>(&S->tmem);
-  for (int i = tid; i < nk; i += kCmpThreads) { sc_cmp0[i] = 0.f; sc_cmp1[i] = 0.f; }
+  if constexpr (kTok == 0)
+    for (int i = tid; i < nk; i += kCmpThreads) { sc_cmp0[i] = 0.f; sc_cmp1[i] = 0.f; }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -460,6 +488,57 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       lse_s[t] = lse2;
       named_bar_sync(1 + wg, 128);
       // ---- pass 2: thread = key; exact fp32 Eq. 8 column sums of exp2(S^T c - LSE)
+      if constexpr (kTok > 0) {
+        // per token (kTok consecutive rows): column sums -> tile buffer -> selection-block scores
+        float* gsc = tok_scr + size_t(wg * kGT) * c.max_slc_b;
+        int Bcur = 0;   // first selection block intersecting the current key tile (uniform)
+        for (int kt = 0; kt < n_kt; ++kt) {
+          const int k0 = kt * kTile, k1 = min(nk, k0 + kTile);
+          const bool kvalid = k0 + t < nk;
+          mbar_wait(&S->s_full[wg], sb.ph);
+          tc_fence_after();
+          float cs[kGT];
+#pragma unroll
+          for (int j = 0; j < kGT; ++j) cs[j] = 0.f;
+#pragma unroll
+          for (int c00 = 0; c00 < kTile; c00 += 32) {
+            float v[32];
+            tmem_ld32(s_base + c00, v);
+            tmem_wait_ld();
+            if (c00 == kTile - 32) {
+              tc_fence_before();
+              mbar_arrive(&S->s_empty[wg]);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 L = ld_shared_f4(&lse_s[c00 + i]);
+              cs[(c00 + i) / kTok] += ex2(fmaf(v[i], cl2, -L.x));
+              cs[(c00 + i + 1) / kTok] += ex2(fmaf(v[i + 1], cl2, -L.y));
+              cs[(c00 + i + 2) / kTok] += ex2(fmaf(v[i + 2], cl2, -L.z));
+              cs[(c00 + i + 3) / kTok] += ex2(fmaf(v[i + 3], cl2, -L.w));
+            }
+          }
+          sb.next();
+          float* bw = tbuf + (wg * 2 + (kt & 1)) * (kGT * 129);
+#pragma unroll
+          for (int j = 0; j < kGT; ++j) bw[j * 129 + t] = kvalid ? cs[j] : 0.f;
+          named_bar_sync(1 + wg, 128);   // (also orders the previous tile's score updates)
+          while (Bcur + 1 < ns && c.slc_cmp_begin[s0 + Bcur + 1] - c0 <= k0) ++Bcur;
+          for (int pi = t;; pi += 128) {
+            const int B = Bcur + pi / kGT, j = pi % kGT;
+            if (B >= ns) break;
+            const int a0 = c.slc_cmp_begin[s0 + B] - c0;
+            if (a0 >= k1) break;
+            const int e0 = c.slc_cmp_begin[s0 + B + 1] - c0;
+            const int lo = max(a0, k0) - k0, hi = min(e0, k1) - k0;
+            float sum = 0.f;
+            for (int k = lo; k < hi; ++k) sum += bw[j * 129 + k];
+            float* dst = gsc + size_t(j) * c.max_slc_b + B;
+            if (a0 >= k0) *dst = sum;      // first tile of block B
+            else *dst += sum;              // B continues from the previous tile
+          }
+        }
+      } else
       for (int kt = 0; kt < n_kt; ++kt) {
         const bool kvalid = kt * kTile + t < nk;
         mbar_wait(&S->s_full[wg], sb.ph);
@@ -490,6 +569,55 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         if (kvalid) sc_cmp[kt * kTile + t] += (cs[0] + cs[1]) + (cs[2] + cs[3]);
       }
     }
+    if constexpr (kTok > 0) {
+      // ---- per-token top-k: warp w takes tokens w, w + 8, ... (scores copied to shared memory when
+      // they fit the freed tile buffers, else read in place from the scratch)
+      __threadfence_block();
+      named_bar_sync(3, 256);
+      constexpr int kPerWarp = 4 * kGT * 129 / 8;
+      float* wrow = tbuf + warp * kPerWarp;
+      int* wch = tchosen + warp * 64;
+      const int ntok = t1 - t0;
+      const int Teff = min(c.T, ns);
+      for (int j = warp; j < ntok; j += 8) {
+        float* src = tok_scr + size_t(j) * c.max_slc_b;
+        const int64_t qj = int64_t(Q + j) * c.h_kv + g;   // query block of token j (m_q = 1)
+        if (c.save_scores)
+          for (int B = lane; B < ns; B += 32) c.scores[qj * c.max_slc_b + B] = src[B];
+        float* row = src;
+        if (ns <= kPerWarp) {
+          for (int B = lane; B < ns; B += 32) wrow[B] = src[B];
+          row = wrow;
+        }
+        __syncwarp();
+        for (int it = 0; it < Teff; ++it) {
+          float best = -2.f;
+          int bidx = 0x7fffffff;
+          for (int B = lane; B < ns; B += 32) {
+            const float v = row[B];
+            if (v > best) { best = v; bidx = B; }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+            if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+          }
+          if (lane == 0) { wch[it] = bidx; row[bidx] = -1.f; }
+          __syncwarp();
+        }
+        if (lane == 0)
+          for (int i = 1; i < Teff; ++i) {
+            const int v = wch[i];
+            int k = i - 1;
+            while (k >= 0 && wch[k] > v) { wch[k + 1] = wch[k]; --k; }
+            wch[k + 1] = v;
+          }
+        __syncwarp();
+        for (int jj = lane; jj < c.T; jj += 32) c.I[qj * c.T + jj] = jj < Teff ? s0 + wch[jj] : -1;
+        __syncwarp();
+      }
+    } else {
     // ---- Eq. 8 selection-block scores and top-k (both softmax warpgroups, 256 threads)
     named_bar_sync(3, 256);
     for (int B = tid; B < ns; B += 256) {
@@ -536,6 +664,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
     }
     named_bar_sync(3, 256);
     for (int j = tid; j < c.T; j += 256) c.I[(int64_t(Q) * c.h_kv + g) * c.T + j] = j < Teff ? s0 + S->chosen[j] : -1;
+    }
   }
 #ifdef SSA_TRACE
   if (TRACE_ON && (warp == 8 || warp == 9 || warp == 0)) {
@@ -1050,6 +1179,64 @@ size_t tc_fwd_ws_bytes(int64_t N, int H, int h_kv, int D) {
   return size_t(4) * size_t(h_kv) * size_t(N) * size_t(D) * 2 + 4 * 256;
 }
 
+// groups of GS consecutive query blocks (one token each, m_q = 1) of one batch item, inside the owned
+// range [q_begin, q_end): cg[v] = [qa, qe), empty past the last group. One CTA.
+__global__ void k_tok_groups(Ctx c, int GS, int32_t* __restrict__ pref, int32_t* __restrict__ cg, int bound) {
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < c.batch; ++b) {
+      pref[b] = acc;
+      const int qa = max(c.bb[SSA_LEVEL_Q][b], c.q_begin), qe = min(c.bb[SSA_LEVEL_Q][b + 1], c.q_end);
+      acc += qe > qa ? (qe - qa + GS - 1) / GS : 0;
+    }
+    pref[c.batch] = acc;
+  }
+  __syncthreads();
+  const int total = pref[c.batch];
+  for (int v = threadIdx.x; v < bound; v += blockDim.x) {
+    if (v >= total) { cg[2 * v] = cg[2 * v + 1] = 0; continue; }
+    int lo = 0, hi = c.batch;   // last item b with pref[b] <= v (non-empty: pref[b + 1] > v)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pref[mid] <= v) lo = mid; else hi = mid;
+    }
+    const int qb0 = max(c.bb[SSA_LEVEL_Q][lo], c.q_begin), qb1 = min(c.bb[SSA_LEVEL_Q][lo + 1], c.q_end);
+    const int qa = qb0 + (v - pref[lo]) * GS;
+    cg[2 * v] = qa;
+    cg[2 * v + 1] = min(qa + GS, qb1);
+  }
+}
+
+int tok_cmp_hs(int m_q, int h_s) {
+  const char* e = getenv("SSA_TOK_CMP");       // A/B knob: 0 = CTA per query block also at m_q = 1
+  if (e && atoi(e) == 0) return 0;
+  return m_q == 1 && (h_s == 4 || h_s == 8 || h_s == 16) ? h_s : 0;
+}
+static int tok_bound(int n_q, int batch, int h_s) { return n_q / (2 * kTile / h_s) + batch + 1; }
+size_t tok_cmp_ws_bytes(int n_q, int batch, int h_s, int max_slc_b) {
+  if (h_s <= 0) return 0;
+  return size_t(batch + 1) * 4 + 256 + size_t(tok_bound(n_q, batch, h_s)) * 8 + 256 +
+         size_t(kTokSlots) * (2 * kTile / h_s) * max_slc_b * 4 + 256;
+}
+template <int kTok>
+static size_t cmp_smem_bytes(const Ctx& c) {
+  const size_t base = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16;
+  if (kTok == 0) return base + (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
+  // tile buffers + chosen lists; at least 120 KB so that one CTA is resident per SM (per-SM scratch slot)
+  return std::max<size_t>(base + (4 * (kTile / std::max(kTok, 1)) * 129 + 8 * 64) * 4, 120 * 1024);
+}
+template <int kTok>
+static ssa_status launch_cmp(const Ctx& c, const TcArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmKh,
+                             const CUtensorMap& tmKl, const CUtensorMap& tmVc, int grid, cudaStream_t st) {
+  const size_t smem = cmp_smem_bytes<kTok>(c);
+  if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
+  SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd<kTok>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ProfScope ps("tc_cmp_fwd", st);
+  k_tc_cmp_fwd<kTok><<<dim3(grid, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
+  SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
+  return SSA_OK;
+}
+
 bool tc_plan_ok(const ssa_plan_info& info, int top_k) {
   const size_t smem = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16 +
                       (2 * size_t(info.max_blocks_per_batch[SSA_LEVEL_CMP]) + info.max_blocks_per_batch[SSA_LEVEL_SLC]) * 4;
@@ -1084,16 +1271,24 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
     return SSA_ERR_CUDA;
   TcArgs a{c, kc_hi, kc_lo, vc};
   const int nq = c.n_blk[SSA_LEVEL_Q];
-  {
-    const size_t smem = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16 +
-                        (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
-    if (smem > 232448) { set_error("compression tile state exceeds shared memory"); return SSA_ERR_UNSUPPORTED; }
-    SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_cmp_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    if (!c.win_only) {
-      ProfScope ps("tc_cmp_fwd", st);
-      k_tc_cmp_fwd<<<dim3(nq, c.h_kv), kCmpThreads, smem, st>>>(a, tmQ, tmKh, tmKl, tmVc);
-      SSA_LAUNCH_CHECK("k_tc_cmp_fwd");
+  if (!c.win_only) {
+    ssa_status s = SSA_OK;
+    if (c.tok_cmp) {   // per-token compression: token groups, per-SM score scratch
+      Carve tw(c.tok_ws, tok_cmp_ws_bytes(nq, c.batch, c.tok_cmp, c.max_slc_b));
+      int32_t* pref = tw.take<int32_t>(c.batch + 1);
+      const int bound = tok_bound(nq, c.batch, c.tok_cmp);
+      int32_t* cg = tw.take<int32_t>(size_t(bound) * 2);
+      a.c.tok_cg = cg;
+      a.c.tok_sc = tw.take<float>(size_t(kTokSlots) * (2 * kTile / c.tok_cmp) * c.max_slc_b);
+      k_tok_groups<<<1, 256, 0, st>>>(c, 2 * kTile / c.tok_cmp, pref, cg, bound);
+      SSA_LAUNCH_CHECK("k_tok_groups");
+      if (c.tok_cmp == 4) s = launch_cmp<4>(c, a, tmQ, tmKh, tmKl, tmVc, bound, st);
+      else if (c.tok_cmp == 8) s = launch_cmp<8>(c, a, tmQ, tmKh, tmKl, tmVc, bound, st);
+      else s = launch_cmp<16>(c, a, tmQ, tmKh, tmKl, tmVc, bound, st);
+    } else {
+      s = launch_cmp<0>(c, a, tmQ, tmKh, tmKl, tmVc, nq, st);
     }
+    if (s != SSA_OK) return s;
   }
   if (split) {
     if (kv_ev) SSA_CUDA_TRY(cudaStreamWaitEvent(st, kv_ev, 0));
