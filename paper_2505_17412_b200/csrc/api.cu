@@ -215,8 +215,9 @@ int pick_chunks(const Plan* p, int h_kv) {
 
 // query blocks smaller than the selection blocks on the tcgen05 path run the selection / window, dQ and
 // KV-outer kernels on a virtual query level (pertoken.cu): its block count bound and 64 union slots
-// S = query blocks per sub-group: enough for about SSA_VQ_ROWS (default 128, one tile) query rows at the
-// plan's mean tokens per query block, at most 64 / T; 0 = no virtual level (m_q == m_slc, query blocks
+// S = query blocks per sub-group (at most): enough for about SSA_VQ_ROWS (default 128, one tile) query rows at
+// the plan's mean tokens per query block, at most 32 (k_vq_count also closes a sub-group before its union of
+// selected blocks would exceed 64); 0 = no virtual level (m_q == m_slc, query blocks
 // that fill a tile on their own, or a query-block range / SSA_LOCAL_ROWS, which the virtual level does
 // not cut)
 double env_or(const char* name, double dflt) {
@@ -229,12 +230,12 @@ int vq_group(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
   if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32) return 0;
   if (cfg->q_end > 0 && (cfg->q_begin > 0 || cfg->q_end < d.n_q)) return 0;
   const double target = env_or("SSA_VQ_ROWS", 128.0);
-  const int S = std::min(64 / d.T, std::max(1, int(target / q_rows(d) + 0.5)));
+  const int S = std::min(32, std::max(1, int(target / q_rows(d) + 0.5)));
   return S >= 2 ? S : 0;
 }
 // The virtual level of the backward: dQ always runs on it (when S > 0); the KV-outer kernel only when
-// query blocks are shorter than SSA_VQ_KV_ROWS (default 16) rows, since its row walk already merges
-// consecutive selecting query blocks into full tiles and the union only adds masked rows.
+// query blocks are shorter than SSA_VQ_KV_ROWS rows (default 0: never), since its row walk packs the rows
+// of the selecting query blocks into full 64-row tiles (8-row granules) and the union only adds masked rows.
 struct VqBwd {
   int S = 0;
   bool kv = false;
@@ -244,11 +245,11 @@ struct VqBwd {
 VqBwd vq_backward(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg, bool tc) {
   VqBwd v;
   v.S = tc ? vq_group(p, d, cfg) : 0;
-  const double kv_rows = env_or("SSA_VQ_KV_ROWS", 16.0);
+  const double kv_rows = env_or("SSA_VQ_KV_ROWS", 0.0);
   v.kv = v.S > 0 && q_rows(d) < kv_rows;
   v.dkv = d;
   if (v.kv) {
-    v.dkv.n_q = int(vq_bound(d.n_slc, d.n_q, v.S));
+    v.dkv.n_q = int(vq_bound(d.n_slc, d.n_q, v.S, d.T));
     v.dkv.T = vq_slots(v.S, d.T);
   }
   v.qbpi = v.kv ? vq_qb_per_item() : tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q]);

@@ -112,6 +112,8 @@ struct Ctx {
   // tcgen05 raw-key KV-outer work items (tc_bwd.cu)
   int32_t* kv_item_off;           // [n_slc * h_kv + 1] first work item of every (selection block, g)
   float *kv_part_k, *kv_part_v;   // [items_bound][max_fill_slc][D] partials of items 1..
+  int32_t* kv_tile_off;           // [items + 1] first packed row tile of every raw-key work item
+  int2* kv_desc;                  // [tiles][8] per 8-row granule of a packed row tile: {first row, meta} (tc_bwd.cu)
 };
 
 // SIMT kernels (simt.cu). Return SSA_OK or a launch error.
@@ -130,7 +132,7 @@ int tok_cmp_hs(int m_q, int h_s);   // h_s when the per-token compression kernel
 size_t tok_cmp_ws_bytes(int n_q, int batch, int h_s, int max_slc_b);
 int vq_qb_per_item();
 bool vq_enabled();
-int64_t vq_bound(int n_slc, int n_q, int S);
+int64_t vq_bound(int n_slc, int n_q, int S, int T);
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T);
 ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
 // learned.cu

@@ -4,13 +4,14 @@
 // The compression kernel runs per query block (its Eq. 8 scores and top-k ARE per query block). The
 // selection / window and dQ / KV-outer kernels would then see one query block's few rows per 128-row
 // tile, so they run on a "virtual" query level instead: each selection block's query blocks are cut
-// into sub-groups of S consecutive query blocks (contiguous rows; S chosen on the host so that a sub-group
-// fills about one 128-row tile, S * T <= 64); a sub-group's key set is the union of its query blocks'
-// selections (<= S * T blocks), and every row keeps
-// only its own query block's blocks through a 64-bit slot mask (umask[token][g]): the softmax loops set
-// the other granules' logits to -inf (forward, dQ), the KV-outer producer gives the rows of query
+// into sub-groups of consecutive query blocks (contiguous rows) — greedily, up to S query blocks (S chosen
+// on the host so that a sub-group fills about one 128-row tile) while the union of the sub-group's
+// selections stays within 64 blocks for every kv group; a sub-group's key set is that union, and every row
+// keeps only its own query block's blocks through a 64-bit slot mask (umask[token][g]): the softmax loops
+// set the other granules' logits to -inf (forward, dQ), the KV-outer producer gives the rows of query
 // blocks that did not select the key block an LSE of +inf (p = 0). Same arithmetic per row as the
-// query-block path; only the row / key grouping changes.
+// query-block path; only the row / key grouping changes. A sub-group closed by the 64-slot cap holds at
+// least floor(64 / T) query blocks, which bounds the number of sub-groups (vq_bound).
 #include <climits>
 #include <cstdlib>
 
@@ -28,17 +29,63 @@ __device__ __forceinline__ void slc_qblocks(const Ctx& c, int B, int* qa, int* q
   *qe = c.tok_block[SSA_LEVEL_Q][t1 - 1] + 1;
 }
 
-__global__ void k_vq_count(Ctx c, int S, int32_t* __restrict__ cnt) {
-  const int B = blockIdx.x * blockDim.x + threadIdx.x;
-  if (B >= c.n_blk[SSA_LEVEL_SLC]) return;
+// Greedy sub-groups of selection block B (one warp per block): walk its query blocks in order, closing the
+// open sub-group before a query block whose selections would push any kv group's union past 64 blocks, or
+// when it holds S query blocks. first[qa + k] = first query block of sub-group k (k < count <= qe - qa);
+// cnt[B] = count. The open unions live in shared memory (unsorted; membership by ballot).
+constexpr int kVqWarps = 4;
+__global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_t* __restrict__ cnt,
+                                                            int32_t* __restrict__ first) {
+  extern __shared__ int vq_u[];                    // [warp][g][64]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int B = blockIdx.x * kVqWarps + wid;
+  if (B >= c.n_blk[SSA_LEVEL_SLC]) return;         // warp-uniform
+  int* u = vq_u + wid * c.h_kv * 64;
   int qa, qe;
   slc_qblocks(c, B, &qa, &qe);
-  cnt[B] = (qe - qa + S - 1) / S;
+  int n_open = 0, size = 0, start = qa;
+  int nu_lane = 0;                                 // lane g < h_kv: union size of kv group g
+  for (int q = qa; q < qe; ++q) {
+    // new blocks per kv group if q joins the open sub-group
+    bool over = false;
+    for (int g = 0; g < c.h_kv; ++g) {
+      const int Bj = lane < c.T ? c.I[(int64_t(q) * c.h_kv + g) * c.T + lane] : -1;
+      const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
+      bool member = false;
+      for (int i = 0; i < nu; ++i) member |= u[g * 64 + i] == Bj;
+      const int nnew = __popc(__ballot_sync(0xffffffffu, Bj >= 0 && !member));
+      over |= nu + nnew > 64;
+    }
+    if (size > 0 && (size == S || over)) {         // close the open sub-group before q
+      if (lane == 0) first[qa + n_open] = start;
+      ++n_open;
+      start = q;
+      size = 0;
+      nu_lane = 0;
+    }
+    for (int g = 0; g < c.h_kv; ++g) {             // insert q's blocks (distinct by top-k construction)
+      const int Bj = lane < c.T ? c.I[(int64_t(q) * c.h_kv + g) * c.T + lane] : -1;
+      const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
+      bool member = false;
+      for (int i = 0; i < nu; ++i) member |= u[g * 64 + i] == Bj;
+      const unsigned mk = __ballot_sync(0xffffffffu, Bj >= 0 && !member);
+      __syncwarp();
+      if ((mk >> lane) & 1u) u[g * 64 + nu + __popc(mk & ((1u << lane) - 1u))] = Bj;
+      __syncwarp();
+      if (lane == g) nu_lane = nu + __popc(mk);
+    }
+    ++size;
+  }
+  if (lane == 0) {
+    if (size > 0) first[qa + n_open] = start;
+    cnt[B] = n_open + (size > 0 ? 1 : 0);
+  }
 }
 
 // sub-group v of selection block B covers query blocks [qa_v, qe_v): token offsets off_v, batch item,
 // identity work order; slots past the real count are empty (off = N) so their CTAs do nothing
-__global__ void k_vq_fill(Ctx c, int S, const int32_t* __restrict__ start, int32_t* __restrict__ off_v,
+__global__ void k_vq_fill(Ctx c, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
+                          int32_t* __restrict__ off_v,
                           int32_t* __restrict__ qrange, int32_t* __restrict__ batch_v, int32_t* __restrict__ order_v,
                           int bound) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -58,14 +105,15 @@ __global__ void k_vq_fill(Ctx c, int S, const int32_t* __restrict__ start, int32
   const int B = lo;
   int qa, qe;
   slc_qblocks(c, B, &qa, &qe);
-  const int a = qa + (v - start[B]) * S, e = min(qe, a + S);
+  const int k = v - start[B];
+  const int a = first[qa + k], e = k + 1 < start[B + 1] - start[B] ? first[qa + k + 1] : qe;
   off_v[v] = c.off[SSA_LEVEL_Q][a];
   qrange[2 * v] = a;
   qrange[2 * v + 1] = e;
   batch_v[v] = c.q_batch[a];
 }
 
-// union of the sub-group's selections (sorted, unique, -1 padded to S * T <= 64 slots) and the slot mask of every
+// union of the sub-group's selections (sorted, unique, -1 padded to vT <= 64 slots) and the slot mask of every
 // token of the sub-group. One 32-thread CTA per (sub-group, kv group).
 __global__ void k_vq_union(Ctx c, int vT, const int32_t* __restrict__ qrange, int32_t* __restrict__ I_u,
                            unsigned long long* __restrict__ umask) {
@@ -89,7 +137,7 @@ __global__ void k_vq_union(Ctx c, int vT, const int32_t* __restrict__ qrange, in
         if (dup) continue;
         for (int m = n; m > k; --m) u[m] = u[m - 1];
         u[k] = B;
-        ++n;                                         // <= (e - a) * T <= S * T <= 64
+        ++n;                                         // <= 64 (k_vq_count's cap)
       }
     nu = n;
   }
@@ -128,25 +176,31 @@ bool vq_enabled() {
   return !(e && atoi(e) == 0);
 }
 
-int vq_slots(int S, int T) { return S * T; }
-int64_t vq_bound(int n_slc, int n_q, int S) { return int64_t(n_slc) + (int64_t(n_q) + S - 1) / S; }
+int vq_slots(int S, int T) { return S * T < 64 ? S * T : 64; }
+// every sub-group but the last of a selection block holds S query blocks or was closed by the 64-slot cap
+// (then it holds > (64 - T) / T, i.e. >= floor(64 / T), query blocks)
+int64_t vq_bound(int n_slc, int n_q, int S, int T) {
+  const int kmin = S < 64 / T ? S : 64 / T;
+  return int64_t(n_slc) + (int64_t(n_q) + kmin - 1) / kmin;
+}
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T) {
-  const int64_t bound = vq_bound(n_slc, n_q, S);
-  return size_t(n_slc + 2) * 4 * 2 + scan_ws_bytes(n_slc + 1) + size_t(bound + 2) * 4 * 5 +
-         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 16 * 256;
+  const int64_t bound = vq_bound(n_slc, n_q, S, T);
+  return size_t(n_slc + 2) * 4 * 2 + scan_ws_bytes(n_slc + 1) + size_t(bound + 2) * 4 * 5 + size_t(n_q + 1) * 4 +
+         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 17 * 256;
 }
 
-// Build the virtual query level (see the header) with sub-groups of S query blocks from the per-query-
+// Build the virtual query level (see the header) with sub-groups of at most S query blocks from the per-query-
 // block selections c.I and return in *v the context the selection / window, dQ and KV-outer kernels run
 // with.
 ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v) {
   const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
   const int vT = vq_slots(S, c.T);
-  if (S < 2 || vT > 64) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
-  const int64_t bound = vq_bound(n_slc, n_q, S);
+  if (S < 2 || c.T > 32) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
+  const int64_t bound = vq_bound(n_slc, n_q, S, c.T);
   Carve cw(ws, vq_ws_bytes(c.N, c.h_kv, n_slc, n_q, S, c.T));
   int32_t* cnt = cw.take<int32_t>(n_slc + 1);
   int32_t* start = cw.take<int32_t>(n_slc + 1);
+  int32_t* first = cw.take<int32_t>(n_q + 1);
   void* sws = cw.take<char>(scan_ws_bytes(n_slc + 1));
   int32_t* off_v = cw.take<int32_t>(bound + 1);
   int32_t* qrange = cw.take<int32_t>(2 * bound + 2);
@@ -155,12 +209,12 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
   unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv);
   if (n_slc > 0) {
-    k_vq_count<<<nb(n_slc, 256), 256, 0, st>>>(c, S, cnt);
+    k_vq_count<<<nb(n_slc, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cnt, first);
     SSA_LAUNCH_CHECK("k_vq_count");
   }
   ssa_status s = exclusive_scan(cnt, start, n_slc, start + n_slc, sws, st);
   if (s != SSA_OK) return s;
-  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, S, start, off_v, qrange, batch_v, order_v, int(bound));
+  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, start, first, off_v, qrange, batch_v, order_v, int(bound));
   SSA_LAUNCH_CHECK("k_vq_fill");
   k_vq_union<<<dim3(unsigned(bound), c.h_kv), 32, 0, st>>>(c, vT, qrange, I_u, umask);
   SSA_LAUNCH_CHECK("k_vq_union");

@@ -674,7 +674,7 @@ struct Item {
   int64_t ra, re;       // mode 0 row range
 };
 
-__device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
+__device__ __forceinline__ bool make_item(const Ctx& c, int mode, int id, Item* it) {
   it->mode = mode;
   if (mode == 0) {
     const int tile = blockIdx.x;
@@ -694,7 +694,6 @@ __device__ __forceinline__ bool make_item(const Ctx& c, int mode, Item* it) {
     it->first = 1;
     return true;
   }
-  const int id = blockIdx.x;
   const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
   if (id >= c.kv_item_off[nkeys]) return false;
   int lo = 0, hi = nkeys;                 // largest key with item_off[key] <= id
@@ -764,9 +763,100 @@ struct RowWalk {
   }
 };
 
+// Packed row tiles of the raw-key work items. The rows of an item (the rows of each selecting query block
+// in list order, then the window's rows from a fresh tile) are laid back to back in 64-row tiles at 8-row
+// granularity: a query block of n rows takes ceil(n / 8) granules and may continue in the next tile, so
+// a tile mixes query blocks (short ones, e.g. one token of h_s rows at m_q = 1, would otherwise leave a
+// tile mostly empty). Every granule is a slot of 8 rows at an 8-row (1024-B) aligned position, so a TMA
+// box of 8k rows there lands in the 128-B swizzle pattern of one 64-row box. A pre-pass (one warp per
+// item, the query blocks' slot offsets by a warp scan) writes, per tile and granule, int2 {first row,
+// meta}: meta bits 0-3 = valid rows (slots past them get an LSE of +inf: p = 0), bits 4-5 = branch
+// (1 selection, 2 window), bits 8-10 = TMA box starting at this granule (0 none, 1..4 = 64/32/16/8 rows).
+constexpr int kGranMetaBoxShift = 8;
+__device__ __forceinline__ int qb_rows(const Ctx& c, int Qb) {
+  return (c.off[SSA_LEVEL_Q][Qb + 1] - c.off[SSA_LEVEL_Q][Qb]) * c.h_s;
+}
+__device__ __forceinline__ int64_t round8(int64_t x) { return (x + 7) & ~int64_t(7); }
+// slots of the item's selection part and of the whole item (window from a fresh tile)
+__device__ __forceinline__ void item_slots(const Ctx& c, const Item& it, int lane, int64_t* sel, int64_t* total) {
+  int64_t s = 0;
+  for (int i = it.li + lane; i < it.le; i += 32) s += round8(qb_rows(c, c.inv_list[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  *sel = s;
+  *total = s;
+  if (it.with_win) {
+    const int64_t w = int64_t(c.off[SSA_LEVEL_SLC][it.kblock + 1] - c.off[SSA_LEVEL_SLC][it.kblock]) * c.h_s;
+    *total = (s + kRT - 1) / kRT * kRT + round8(w);
+  }
+}
+__global__ void k_kv_tile_count(Ctx c, int32_t* __restrict__ cnt, int bound) {
+  const int id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (id >= bound) return;   // warp-uniform
+  Item it;
+  if (!make_item(c, 1, id, &it)) {
+    if (lane == 0) cnt[id] = 0;
+    return;
+  }
+  int64_t sel, total;
+  item_slots(c, it, lane, &sel, &total);
+  if (lane == 0) cnt[id] = int32_t((total + kRT - 1) / kRT);
+}
+// granules of one piece: rows [row0, row0 + rows) at item slot s0 (a multiple of 8), boxes cut at tiles
+__device__ void write_piece(int2* __restrict__ desc, int64_t t0, int64_t s0, int64_t row0, int rows, int br) {
+  const int l8 = int(round8(rows));
+  for (int r = 0; r < l8;) {
+    const int64_t s = s0 + r;
+    const int in_tile = min(l8 - r, kRT - int(s % kRT));
+    int2* dt = desc + (t0 + s / kRT) * 8 + (s % kRT) / 8;
+    for (int o = 0; o < in_tile;) {
+      const int b = in_tile - o >= 64 ? 0 : (in_tile - o >= 32 ? 1 : (in_tile - o >= 16 ? 2 : 3));
+      for (int k = 0; k < (8 >> b); ++k) {
+        const int rr = r + o + 8 * k, nv = rows - rr < 8 ? rows - rr : 8;
+        dt[o / 8 + k] = make_int2(int(row0 + rr), nv | (br << 4) | (k == 0 ? (b + 1) << kGranMetaBoxShift : 0));
+      }
+      o += 64 >> b;
+    }
+    r += in_tile;
+  }
+}
+__global__ void k_kv_tile_fill(Ctx c, const int32_t* __restrict__ off, int2* __restrict__ desc, int bound) {
+  const int id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (id >= bound) return;   // warp-uniform
+  Item it;
+  if (!make_item(c, 1, id, &it)) return;
+  const int64_t t0 = off[id];
+  int64_t sel, total;
+  item_slots(c, it, lane, &sel, &total);
+  int64_t base = 0;
+  for (int i0 = it.li; i0 < it.le; i0 += 32) {   // selecting query blocks, list order
+    const int i = i0 + lane;
+    const int Qb = i < it.le ? c.inv_list[i] : 0;
+    const int rows = i < it.le ? qb_rows(c, Qb) : 0;
+    int64_t x = round8(rows);                      // inclusive warp scan of the slots
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (rows > 0)
+      write_piece(desc, t0, base + x - round8(rows), (int64_t(it.g) * c.N + c.off[SSA_LEVEL_Q][Qb]) * c.h_s, rows, 1);
+    base += __shfl_sync(0xffffffffu, x, 31);
+  }
+  int64_t pad0 = sel, pad1 = (sel + kRT - 1) / kRT * kRT;   // unused granules: selection tail, item tail
+  if (it.with_win) {
+    const int t_a = c.off[SSA_LEVEL_SLC][it.kblock], t_b = c.off[SSA_LEVEL_SLC][it.kblock + 1];
+    if (lane == 0) write_piece(desc, t0, pad1, (int64_t(it.g) * c.N + t_a) * c.h_s, (t_b - t_a) * c.h_s, 2);
+  }
+  for (int64_t s = pad0 + 8 * lane; s < pad1; s += 256) desc[(t0 + s / kRT) * 8 + (s % kRT) / 8] = make_int2(0, 0);
+  const int64_t tend = (total + kRT - 1) / kRT * kRT;
+  for (int64_t s = round8(total) + 8 * lane; s < tend && total > pad1; s += 256)
+    desc[(t0 + s / kRT) * 8 + (s % kRT) / 8] = make_int2(0, 0);
+}
+
 __global__ void __launch_bounds__(kKvThreads, 1)
-k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const CUtensorMap tmDO,
-          __grid_constant__ const CUtensorMap tmDO2, __grid_constant__ const CUtensorMap tmK,
+k_tc_dkdv(Ctx c, int mode, __grid_constant__ const TmapSet4 tmQ, __grid_constant__ const TmapSet4 tmDO,
+          __grid_constant__ const TmapSet4 tmDO2, __grid_constant__ const CUtensorMap tmK,
           __grid_constant__ const CUtensorMap tmV) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -778,7 +868,7 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Item it;
-  const bool ok = make_item(c, mode, &it);
+  const bool ok = make_item(c, mode, blockIdx.x, &it);
   if (!ok) return;                        // uniform for the whole CTA (grid is an upper bound)
   const int g = it.g;
   int kbase, nkeys_total;
@@ -794,7 +884,12 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
   }
   const int n_kt = (nkeys_total + 127) / 128;
   int n_tiles = 0;                        // row tiles of the item (the same for every key tile)
-  {
+  const bool packed = mode == 1 && c.kv_desc != nullptr;   // raw keys, short query blocks: packed row tiles
+  int64_t tile0 = 0;
+  if (packed) {
+    tile0 = c.kv_tile_off[blockIdx.x];
+    n_tiles = int(c.kv_tile_off[blockIdx.x + 1] - tile0);
+  } else {
     RowWalk w2;
     w2.init(c, it);
     int64_t r0;
@@ -821,8 +916,15 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
     }
     fence_barrier_init();
   }
+  // packed row tiles may leave slots unwritten: the row stages must hold finite values from the start
+  if (packed) {
+    for (int i = tid; i < 2 * kRStages * 16384 / 16; i += kKvThreads)
+      *reinterpret_cast<uint4*>(sR + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+  }
   if (warp == 8 && lane == 0) {
-    tma_prefetch(&tmQ); tma_prefetch(&tmDO); tma_prefetch(&tmDO2); tma_prefetch(&tmK); tma_prefetch(&tmV);
+    for (int b = 0; b < 4; ++b) { tma_prefetch(&tmQ.m[b]); tma_prefetch(&tmDO.m[b]); tma_prefetch(&tmDO2.m[b]); }
+    tma_prefetch(&tmK); tma_prefetch(&tmV);
   }
   if (warp == 9) tmem_alloc<512>(&S->tmem);
   tc_fence_before();
@@ -844,6 +946,67 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         mbar_expect_tx(&S->k_full, 32768);
         tma_load_2d(sK, &tmK, &S->k_full, 0, int(krow_g + kbase + kt * 128));
         tma_load_2d(sV, &tmV, &S->k_full, 0, int(krow_g + kbase + kt * 128));
+      }
+      if (packed) {
+        // lane j < 8 holds granule j of the tile; the next tile's descriptor is loaded one tile ahead
+        int2 nxt = lane < 8 && n_tiles > 0 ? c.kv_desc[tile0 * 8 + lane] : make_int2(0, 0);
+        for (int i = 0; i < n_tiles; ++i) {
+          const int w = i & 1;
+          Ring& rs = w ? rs1 : rs0;
+          const int2 cd = nxt;
+          if (lane < 8 && i + 1 < n_tiles) nxt = c.kv_desc[(tile0 + i + 1) * 8 + lane];
+          mbar_wait(&S->r_empty[w][rs.idx], rs.ph ^ 1u);
+          TRACE_R(0, 1, i);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h;
+            const int gx = __shfl_sync(0xffffffffu, cd.x, e >> 3), gy = __shfl_sync(0xffffffffu, cd.y, e >> 3);
+            const int nv = gy & 15, br = (gy >> 4) & 3;
+            const int64_t row = int64_t(gx) + (e & 7);
+            const bool valid = (e & 7) < nv;
+            bool keep = valid;
+            if (keep && br == 1 && c.umask) {   // virtual level: rows whose query block did not select the block
+              const int tok = int(row / c.h_s) - it.g * c.N;
+              const int32_t* sel = c.tok_I + (int64_t(c.tok_qb[tok]) * c.h_kv + it.g) * c.tok_T;
+              bool hit = false;
+              for (int jj = 0; jj < c.tok_T; ++jj) hit |= sel[jj] == it.kblock;
+              keep = hit;
+            }
+            cp_async4(&S->st_l2[w][rs.idx][e], keep ? c.lse[br] + row : &g_pos_inf);
+            cp_async4(&S->st_D[w][rs.idx][e], valid ? c.Dd[br] + row : &g_zero);
+          }
+#if SSA_KV_STATS_WAIT
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+          mbar_arrive(&S->r_full[w][rs.idx]);
+#else
+          cp_async_mbar_arrive_noinc(&S->r_full[w][rs.idx]);
+#endif
+          int2 gd[8];
+#pragma unroll
+          for (int gq = 0; gq < 8; ++gq) gd[gq] = make_int2(__shfl_sync(0xffffffffu, cd.x, gq), __shfl_sync(0xffffffffu, cd.y, gq));
+          if (lane == 0) {
+            uint8_t* st = sR + (w * kRStages + rs.idx) * 16384;
+            uint32_t rows = 0;
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq) {
+              const int bc = (gd[gq].y >> kGranMetaBoxShift) & 7;
+              rows += bc ? (64u >> (bc - 1)) : 0u;
+            }
+            mbar_expect_tx(&S->r_full[w][rs.idx], rows * 256u);
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq) {
+              const int bc = (gd[gq].y >> kGranMetaBoxShift) & 7;
+              if (bc) {
+                const TmapSet4& td = ((gd[gq].y >> 4) & 3) == 2 ? tmDO2 : tmDO;
+                tma_load_2d(st + gq * 1024, &tmQ.m[bc - 1], &S->r_full[w][rs.idx], 0, gd[gq].x);
+                tma_load_2d(st + 8192 + gq * 1024, &td.m[bc - 1], &S->r_full[w][rs.idx], 0, gd[gq].x);
+              }
+            }
+          }
+          __syncwarp();
+          rs.next();
+        }
+        continue;
       }
       RowWalk wk;
       wk.init(c, it);
@@ -883,8 +1046,8 @@ k_tc_dkdv(Ctx c, int mode, __grid_constant__ const CUtensorMap tmQ, __grid_const
         if (lane == 0) {
           uint8_t* st = sR + (w * kRStages + rs.idx) * 16384;
           mbar_expect_tx(&S->r_full[w][rs.idx], 16384);
-          tma_load_2d(st, &tmQ, &S->r_full[w][rs.idx], 0, int(r0));
-          tma_load_2d(st + 8192, br == 2 ? &tmDO2 : &tmDO, &S->r_full[w][rs.idx], 0, int(r0));
+          tma_load_2d(st, &tmQ.m[0], &S->r_full[w][rs.idx], 0, int(r0));
+          tma_load_2d(st + 8192, br == 2 ? &tmDO2.m[0] : &tmDO.m[0], &S->r_full[w][rs.idx], 0, int(r0));
         }
         __syncwarp();
         rs.next();
@@ -1138,6 +1301,13 @@ static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T, int qbpi) {
   return int64_t(n_slc) * h_kv + (int64_t(n_q) * h_kv * T + qbpi - 1) / qbpi + 1;
 }
 
+// packed row tiles of all raw-key items: every row of every range once ((T + 1) N H: the selections and
+// the window), at most 7 padding rows per range (inverse-list entries + windows), a partial last tile per item
+static int64_t kv_tiles_bound(int64_t N, int H, int h_kv, int n_slc, int n_q, int T, int64_t items) {
+  const int64_t rows = N * H * (T + 1) + 7 * (int64_t(n_q) * h_kv * T + int64_t(n_slc) * h_kv);
+  return rows / 64 + items + 1;
+}
+
 int tc_qb_per_item(int m_slc, int m_q) {
   const int r = m_q > 0 && m_slc % m_q == 0 ? m_slc / m_q : 1;
   return kQBlocksPerItem * r * r * r;
@@ -1148,7 +1318,10 @@ size_t tc_bwd_ws_bytes(int64_t N, int H, int h_kv, int D, int n_slc, int n_q, in
   size_t b = (size_t(5) * size_t(N) * size_t(H) + size_t(4) * size_t(h_kv) * size_t(N)) * size_t(D) * 2 + 8 * 256;
   const int64_t nkeys = int64_t(n_slc) * h_kv;
   b += size_t(2 * nkeys + 2) * 4 + 512 + scan_ws_bytes(nkeys + 1);                  // item counts / offsets
-  b += size_t(2) * kv_items_bound(n_slc, n_q, h_kv, T, qb_per_item) * max_fill_slc * D * 4 + 512;  // partials
+  const int64_t items = kv_items_bound(n_slc, n_q, h_kv, T, qb_per_item);
+  b += size_t(2) * items * max_fill_slc * D * 4 + 512;  // partials
+  b += size_t(2 * items + 4) * 4 + 512 + scan_ws_bytes(items + 1);                    // packed tile counts / offsets
+  b += size_t(kv_tiles_bound(N, H, h_kv, n_slc, n_q, T, items)) * 8 * sizeof(int2) + 1024;  // granule descriptors
   return b;
 }
 
@@ -1173,6 +1346,15 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
   const int64_t bound = kv_items_bound(n_slc, ck.n_blk[SSA_LEVEL_Q], c.h_kv, ck.T, ck.qb_per_item);
   ck.kv_part_k = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
   ck.kv_part_v = cw.take<float>(size_t(bound) * c.max_fill[SSA_LEVEL_SLC] * kD);
+  int32_t* tile_cnt = cw.take<int32_t>(bound + 1);
+  ck.kv_tile_off = cw.take<int32_t>(bound + 1);
+  void* tscan_ws = cw.take<char>(scan_ws_bytes(bound + 1));
+  ck.kv_desc = cw.take<int2>(size_t(kv_tiles_bound(c.N, c.H, c.h_kv, n_slc, ck.n_blk[SSA_LEVEL_Q], ck.T, bound)) * 8);
+  // packed row tiles only where query blocks are short (m_q < m_slc: a few rows each); long query blocks
+  // fill their tiles contiguously and keep the cheaper arithmetic row walk (measured: C3 raw keys 3.2 ms
+  // contiguous vs 4.0 ms packed)
+  const bool pack = ck.n_blk[SSA_LEVEL_Q] > 0 && int64_t(ck.N) * ck.h_s < int64_t(256) * ck.n_blk[SSA_LEVEL_Q];
+  if (!pack) ck.kv_desc = nullptr;
   uint32_t* amax = cw.take<uint32_t>(1);
   c.do_amax = amax;
   ck.do_amax = amax;
@@ -1192,12 +1374,13 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
   const int64_t n = int64_t(krows) * kD;   // >= h_kv * n_cmp * kD
   k_tc_bwd_prep<<<unsigned((n / 8 + 255) / 256), 256, 0, st>>>(c, k16, v16, kc, vc);
   SSA_LAUNCH_CHECK("k_tc_bwd_prep");
-  CUtensorMap tmQ, tmDO, tmQ64, tmDO64, tmKc, tmVc, tmKc128, tmVc128, tmK128, tmV128, tmDW[3];
-  TmapSet4 tmK, tmV;
+  CUtensorMap tmQ, tmDO, tmKc, tmVc, tmKc128, tmVc128, tmK128, tmV128;
+  TmapSet4 tmK, tmV, tmQs, tmDWs[3];
   for (int br = 0; br < 3; ++br)
-    if (!make_tmap_bf16_2d(&tmDW[br], dow + size_t(br) * qrows * kD, qrows, kRT)) return SSA_ERR_CUDA;
+    if (!make_tmap_set4(&tmDWs[br], dow + size_t(br) * qrows * kD, qrows))
+      return SSA_ERR_CUDA;
+  if (!make_tmap_set4(&tmQs, q16, qrows)) return SSA_ERR_CUDA;
   if (!make_tmap_bf16_2d(&tmQ, q16, qrows, 128) || !make_tmap_bf16_2d(&tmDO, do16, qrows, 128) ||
-      !make_tmap_bf16_2d(&tmQ64, q16, qrows, kRT) || !make_tmap_bf16_2d(&tmDO64, do16, qrows, kRT) ||
       !make_tmap_bf16_2d(&tmKc, kc, crows, kKT) || !make_tmap_bf16_2d(&tmVc, vc, crows, kKT) ||
       !make_tmap_set4(&tmK, k16, krows) || !make_tmap_set4(&tmV, v16, krows) ||
       !make_tmap_bf16_2d(&tmKc128, kc, crows, 128) || !make_tmap_bf16_2d(&tmVc128, vc, crows, 128) ||
@@ -1245,8 +1428,16 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
     SSA_LAUNCH_CHECK("k_kv_item_count");
     ssa_status s = exclusive_scan(item_cnt, ck.kv_item_off, nkeys, ck.kv_item_off + nkeys, scan_ws, kst);
     if (s != SSA_OK) return s;
+    if (ck.kv_desc) {
+      k_kv_tile_count<<<unsigned((bound + 3) / 4), 128, 0, kst>>>(ck, tile_cnt, int(bound));
+      SSA_LAUNCH_CHECK("k_kv_tile_count");
+      s = exclusive_scan(tile_cnt, ck.kv_tile_off, bound, ck.kv_tile_off + bound, tscan_ws, kst);
+      if (s != SSA_OK) return s;
+      k_kv_tile_fill<<<unsigned((bound + 3) / 4), 128, 0, kst>>>(ck, ck.kv_tile_off, ck.kv_desc, int(bound));
+      SSA_LAUNCH_CHECK("k_kv_tile_fill");
+    }
     ProfScope ps("tc_bwd_kv", kst);
-    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, kst>>>(ck, 1, tmQ64, tmDW[1], tmDW[2], tmK128, tmV128);
+    k_tc_dkdv<<<dim3(unsigned(bound), 1, 1), kKvThreads, smem, kst>>>(ck, 1, tmQs, tmDWs[1], tmDWs[2], tmK128, tmV128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(raw)");
   }
   {
@@ -1256,7 +1447,7 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
   }
   if (!c.win_only) {
     ProfScope ps("tc_bwd_cmp_kv", kst);
-    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, kst>>>(c, 0, tmQ64, tmDW[0], tmDW[0], tmKc128,
+    k_tc_dkdv<<<dim3(c.n_cmp_tiles, c.h_kv, c.n_chunk), kKvThreads, smem, kst>>>(c, 0, tmQs, tmDWs[0], tmDWs[0], tmKc128,
                                                                                tmVc128);
     SSA_LAUNCH_CHECK("k_tc_dkdv(cmp)");
   }
