@@ -215,7 +215,8 @@ int pick_chunks(const Plan* p, int h_kv) {
 
 // query blocks smaller than the selection blocks on the tcgen05 path run the selection / window, dQ and
 // KV-outer kernels on a virtual query level (pertoken.cu): its block count bound and 64 union slots
-// S = query blocks per sub-group (at most): enough for about SSA_VQ_ROWS (default 128, one tile) query rows at
+// S = query blocks per sub-group (at most): enough for about SSA_VQ_ROWS (default 256: a row-tile pair, so both
+// softmax warpgroups of the selection / dQ kernels work; measured C2 m_q = 1: 3.0 -> 2.0 ms, 3.0 -> 2.15 ms) query rows at
 // the plan's mean tokens per query block, at most 32 (k_vq_count also closes a sub-group before its union of
 // selected blocks would exceed 64); 0 = no virtual level (m_q == m_slc, query blocks
 // that fill a tile on their own, or a query-block range / SSA_LOCAL_ROWS, which the virtual level does
@@ -227,9 +228,10 @@ double env_or(const char* name, double dflt) {
 }
 double q_rows(const Dims& d) { return d.n_q > 0 ? double(d.N) / d.n_q * (d.H / d.h_kv) : 0.0; }
 int vq_group(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
-  if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32) return 0;
+  if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32 || d.h_kv > 8)
+    return 0;
   if (cfg->q_end > 0 && (cfg->q_begin > 0 || cfg->q_end < d.n_q)) return 0;
-  const double target = env_or("SSA_VQ_ROWS", 128.0);
+  const double target = env_or("SSA_VQ_ROWS", 256.0);
   const int S = std::min(32, std::max(1, int(target / q_rows(d) + 0.5)));
   return S >= 2 ? S : 0;
 }

@@ -31,11 +31,16 @@ __device__ __forceinline__ void slc_qblocks(const Ctx& c, int B, int* qa, int* q
 
 // Greedy sub-groups of selection block B (one warp per block): walk its query blocks in order, closing the
 // open sub-group before a query block whose selections would push any kv group's union past 64 blocks, or
-// when it holds S query blocks. first[qa + k] = first query block of sub-group k (k < count <= qe - qa);
-// cnt[B] = count. The open unions live in shared memory (unsorted; membership by ballot).
+// when it holds S query blocks. Per sub-group k (k < count <= qe - qa): first[qa + k] = its first query
+// block, un[((qa + k) * h_kv + g) * 64 + j] = its union for kv group g (order of first appearance, -1
+// padded); cnt[B] = count; umask[t][g] = the union slots of token t's own query block's selections (bits
+// stay valid: the union only grows by appending). The open unions live in shared memory; membership of
+// the T candidates (one per lane) is tested against the union held two entries per lane, by ballot.
 constexpr int kVqWarps = 4;
+constexpr int kVqMaxG = 8;                         // kv groups of the virtual level (vq_group)
 __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_t* __restrict__ cnt,
-                                                            int32_t* __restrict__ first) {
+                                                            int32_t* __restrict__ first, int32_t* __restrict__ un,
+                                                            unsigned long long* __restrict__ umask) {
   extern __shared__ int vq_u[];                    // [warp][g][64]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int B = blockIdx.x * kVqWarps + wid;
@@ -45,37 +50,76 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_
   slc_qblocks(c, B, &qa, &qe);
   int n_open = 0, size = 0, start = qa;
   int nu_lane = 0;                                 // lane g < h_kv: union size of kv group g
-  for (int q = qa; q < qe; ++q) {
-    // new blocks per kv group if q joins the open sub-group
-    bool over = false;
+  auto flush = [&](int k) {                        // write the open sub-group's unions as sub-group k
     for (int g = 0; g < c.h_kv; ++g) {
-      const int Bj = lane < c.T ? c.I[(int64_t(q) * c.h_kv + g) * c.T + lane] : -1;
       const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
-      bool member = false;
-      for (int i = 0; i < nu; ++i) member |= u[g * 64 + i] == Bj;
-      const int nnew = __popc(__ballot_sync(0xffffffffu, Bj >= 0 && !member));
+      int32_t* o = un + (int64_t(qa + k) * c.h_kv + g) * 64;
+      o[lane] = lane < nu ? u[g * 64 + lane] : -1;
+      o[lane + 32] = lane + 32 < nu ? u[g * 64 + lane + 32] : -1;
+    }
+  };
+  // candidates of the next query block, loaded one query block ahead (lane j < T: block I[q][g][j])
+  int nxt[kVqMaxG];
+#pragma unroll
+  for (int g = 0; g < kVqMaxG; ++g) nxt[g] = g < c.h_kv && lane < c.T && qa < qe ? c.I[(int64_t(qa) * c.h_kv + g) * c.T + lane] : -1;
+  for (int q = qa; q < qe; ++q) {
+    int cand[kVqMaxG];
+#pragma unroll
+    for (int g = 0; g < kVqMaxG; ++g) {
+      cand[g] = nxt[g];
+      nxt[g] = g < c.h_kv && lane < c.T && q + 1 < qe ? c.I[(int64_t(q + 1) * c.h_kv + g) * c.T + lane] : -1;
+    }
+    // membership of q's candidates in the open unions: slot or -1
+    int slot[kVqMaxG];
+    bool over = false;
+#pragma unroll
+    for (int g = 0; g < kVqMaxG; ++g) {
+      slot[g] = -1;
+      if (g >= c.h_kv) continue;
+      const int Bj = cand[g];
+      const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
+      const int u0 = lane < nu ? u[g * 64 + lane] : -2, u1 = lane + 32 < nu ? u[g * 64 + lane + 32] : -2;
+      for (int j = 0; j < c.T; ++j) {
+        const int b = __shfl_sync(0xffffffffu, Bj, j);
+        const unsigned h0 = __ballot_sync(0xffffffffu, u0 == b), h1 = __ballot_sync(0xffffffffu, u1 == b);
+        if (lane == j && b >= 0 && (h0 | h1)) slot[g] = h0 ? __ffs(h0) - 1 : 32 + __ffs(h1) - 1;
+      }
+      const int nnew = __popc(__ballot_sync(0xffffffffu, Bj >= 0 && slot[g] < 0));
       over |= nu + nnew > 64;
     }
     if (size > 0 && (size == S || over)) {         // close the open sub-group before q
+      flush(n_open);
+      __syncwarp();                                 // flush's reads of the union before its reuse
       if (lane == 0) first[qa + n_open] = start;
       ++n_open;
       start = q;
       size = 0;
       nu_lane = 0;
+#pragma unroll
+      for (int g = 0; g < kVqMaxG; ++g) slot[g] = -1;
     }
-    for (int g = 0; g < c.h_kv; ++g) {             // insert q's blocks (distinct by top-k construction)
-      const int Bj = lane < c.T ? c.I[(int64_t(q) * c.h_kv + g) * c.T + lane] : -1;
+#pragma unroll
+    for (int g = 0; g < kVqMaxG; ++g) {            // insert q's new blocks, q's slot mask
+      if (g >= c.h_kv) continue;
+      const int Bj = cand[g];
       const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
-      bool member = false;
-      for (int i = 0; i < nu; ++i) member |= u[g * 64 + i] == Bj;
-      const unsigned mk = __ballot_sync(0xffffffffu, Bj >= 0 && !member);
-      __syncwarp();
-      if ((mk >> lane) & 1u) u[g * 64 + nu + __popc(mk & ((1u << lane) - 1u))] = Bj;
+      int sl = slot[g];
+      const unsigned mk = __ballot_sync(0xffffffffu, Bj >= 0 && sl < 0);
+      if ((mk >> lane) & 1u) {
+        sl = nu + __popc(mk & ((1u << lane) - 1u));
+        u[g * 64 + sl] = Bj;
+      }
       __syncwarp();
       if (lane == g) nu_lane = nu + __popc(mk);
+      const unsigned long long bit = Bj >= 0 && sl >= 0 ? 1ull << sl : 0ull;
+      const unsigned long long m = (unsigned long long)__reduce_or_sync(0xffffffffu, uint32_t(bit >> 32)) << 32 |
+                                   __reduce_or_sync(0xffffffffu, uint32_t(bit));
+      for (int t = c.off[SSA_LEVEL_Q][q] + lane; t < c.off[SSA_LEVEL_Q][q + 1]; t += 32)
+        umask[int64_t(t) * c.h_kv + g] = m;
     }
     ++size;
   }
+  if (size > 0) flush(n_open);
   if (lane == 0) {
     if (size > 0) first[qa + n_open] = start;
     cnt[B] = n_open + (size > 0 ? 1 : 0);
@@ -84,8 +128,8 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_
 
 // sub-group v of selection block B covers query blocks [qa_v, qe_v): token offsets off_v, batch item,
 // identity work order; slots past the real count are empty (off = N) so their CTAs do nothing
-__global__ void k_vq_fill(Ctx c, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
-                          int32_t* __restrict__ off_v,
+__global__ void k_vq_fill(Ctx c, int vT, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
+                          const int32_t* __restrict__ un, int32_t* __restrict__ I_u, int32_t* __restrict__ off_v,
                           int32_t* __restrict__ qrange, int32_t* __restrict__ batch_v, int32_t* __restrict__ order_v,
                           int bound) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -94,7 +138,11 @@ __global__ void k_vq_fill(Ctx c, const int32_t* __restrict__ start, const int32_
   if (v < bound) order_v[v] = v;
   if (v >= total) {
     off_v[v] = c.N;
-    if (v < bound) { qrange[2 * v] = qrange[2 * v + 1] = 0; batch_v[v] = 0; }
+    if (v < bound) {
+      qrange[2 * v] = qrange[2 * v + 1] = 0;
+      batch_v[v] = 0;
+      for (int j = 0; j < c.h_kv * vT; ++j) I_u[int64_t(v) * c.h_kv * vT + j] = -1;   // selects nothing
+    }
     return;
   }
   int lo = 0, hi = c.n_blk[SSA_LEVEL_SLC];      // selection block B with start[B] <= v < start[B + 1]
@@ -111,53 +159,8 @@ __global__ void k_vq_fill(Ctx c, const int32_t* __restrict__ start, const int32_
   qrange[2 * v] = a;
   qrange[2 * v + 1] = e;
   batch_v[v] = c.q_batch[a];
-}
-
-// union of the sub-group's selections (sorted, unique, -1 padded to vT <= 64 slots) and the slot mask of every
-// token of the sub-group. One 32-thread CTA per (sub-group, kv group).
-__global__ void k_vq_union(Ctx c, int vT, const int32_t* __restrict__ qrange, int32_t* __restrict__ I_u,
-                           unsigned long long* __restrict__ umask) {
-  __shared__ int u[64];
-  __shared__ int nu;
-  const int v = blockIdx.x, g = blockIdx.y, lane = threadIdx.x;
-  const int a = qrange[2 * v], e = qrange[2 * v + 1];
-  int32_t* out = I_u + (int64_t(v) * c.h_kv + g) * vT;
-  if (lane == 0) {
-    int n = 0;
-    for (int q = a; q < e; ++q)
-      for (int j = 0; j < c.T; ++j) {
-        const int B = c.I[(int64_t(q) * c.h_kv + g) * c.T + j];
-        if (B < 0) continue;
-        int k = n;                                   // insertion into the sorted unique list
-        bool dup = false;
-        while (k > 0 && u[k - 1] >= B) {
-          if (u[k - 1] == B) { dup = true; break; }
-          --k;
-        }
-        if (dup) continue;
-        for (int m = n; m > k; --m) u[m] = u[m - 1];
-        u[k] = B;
-        ++n;                                         // <= 64 (k_vq_count's cap)
-      }
-    nu = n;
-  }
-  __syncwarp();
-  const int n = nu;
-  for (int j = lane; j < vT; j += 32) out[j] = j < n ? u[j] : -1;
-  for (int q = a + lane; q < e; q += 32) {
-    unsigned long long m = 0ull;
-    for (int j = 0; j < c.T; ++j) {
-      const int B = c.I[(int64_t(q) * c.h_kv + g) * c.T + j];
-      if (B < 0) continue;
-      int lo = 0, hi = n - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (u[mid] < B) lo = mid + 1; else hi = mid;
-      }
-      m |= 1ull << lo;
-    }
-    for (int t = c.off[SSA_LEVEL_Q][q]; t < c.off[SSA_LEVEL_Q][q + 1]; ++t) umask[int64_t(t) * c.h_kv + g] = m;
-  }
+  for (int g = 0; g < c.h_kv; ++g)
+    for (int j = 0; j < vT; ++j) I_u[(int64_t(v) * c.h_kv + g) * vT + j] = un[(int64_t(qa + k) * c.h_kv + g) * 64 + j];
 }
 
 }  // namespace
@@ -186,7 +189,8 @@ int64_t vq_bound(int n_slc, int n_q, int S, int T) {
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T) {
   const int64_t bound = vq_bound(n_slc, n_q, S, T);
   return size_t(n_slc + 2) * 4 * 2 + scan_ws_bytes(n_slc + 1) + size_t(bound + 2) * 4 * 5 + size_t(n_q + 1) * 4 +
-         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 17 * 256;
+         size_t(n_q) * h_kv * 64 * 4 +
+         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 18 * 256;
 }
 
 // Build the virtual query level (see the header) with sub-groups of at most S query blocks from the per-query-
@@ -201,6 +205,7 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   int32_t* cnt = cw.take<int32_t>(n_slc + 1);
   int32_t* start = cw.take<int32_t>(n_slc + 1);
   int32_t* first = cw.take<int32_t>(n_q + 1);
+  int32_t* un = cw.take<int32_t>(size_t(n_q) * c.h_kv * 64);
   void* sws = cw.take<char>(scan_ws_bytes(n_slc + 1));
   int32_t* off_v = cw.take<int32_t>(bound + 1);
   int32_t* qrange = cw.take<int32_t>(2 * bound + 2);
@@ -209,15 +214,13 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
   unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv);
   if (n_slc > 0) {
-    k_vq_count<<<nb(n_slc, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cnt, first);
+    k_vq_count<<<nb(n_slc, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cnt, first, un, umask);
     SSA_LAUNCH_CHECK("k_vq_count");
   }
   ssa_status s = exclusive_scan(cnt, start, n_slc, start + n_slc, sws, st);
   if (s != SSA_OK) return s;
-  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, start, first, off_v, qrange, batch_v, order_v, int(bound));
+  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, vT, start, first, un, I_u, off_v, qrange, batch_v, order_v, int(bound));
   SSA_LAUNCH_CHECK("k_vq_fill");
-  k_vq_union<<<dim3(unsigned(bound), c.h_kv), 32, 0, st>>>(c, vT, qrange, I_u, umask);
-  SSA_LAUNCH_CHECK("k_vq_union");
   *v = c;
   v->tok_I = c.I;            // the per-query-block selections (KV-outer row masks)
   v->tok_T = c.T;

@@ -1302,10 +1302,11 @@ static int64_t kv_items_bound(int n_slc, int n_q, int h_kv, int T, int qbpi) {
 }
 
 // packed row tiles of all raw-key items: every row of every range once ((T + 1) N H: the selections and
-// the window), at most 7 padding rows per range (inverse-list entries + windows), a partial last tile per item
+// the window), at most 7 padding rows per range (inverse-list entries + windows), and per item two partial
+// tiles (the selection part's last tile: the window starts a fresh one; the item's last tile)
 static int64_t kv_tiles_bound(int64_t N, int H, int h_kv, int n_slc, int n_q, int T, int64_t items) {
   const int64_t rows = N * H * (T + 1) + 7 * (int64_t(n_q) * h_kv * T + int64_t(n_slc) * h_kv);
-  return rows / 64 + items + 1;
+  return rows / 64 + 2 * items + 1;
 }
 
 int tc_qb_per_item(int m_slc, int m_q) {
@@ -1356,6 +1357,7 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
   const bool pack = ck.n_blk[SSA_LEVEL_Q] > 0 && int64_t(ck.N) * ck.h_s < int64_t(256) * ck.n_blk[SSA_LEVEL_Q];
   if (!pack) ck.kv_desc = nullptr;
   uint32_t* amax = cw.take<uint32_t>(1);
+  if (!cw.ok()) { set_error("tcgen05 backward: workspace carve exceeds tc_bwd_ws_bytes"); return SSA_ERR_WORKSPACE; }
   c.do_amax = amax;
   ck.do_amax = amax;
   SSA_CUDA_TRY(cudaMemsetAsync(amax, 0, 4, st));
