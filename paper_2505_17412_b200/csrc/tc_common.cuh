@@ -62,9 +62,17 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef SSA_MBAR_POLL
+#define SSA_MBAR_POLL 0   // 1: spin on test_wait (non-suspending) instead of try_wait
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SSA_MBAR_POLL
+  while (!mbar_test(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ------------------------------------------------------------------------------------------------

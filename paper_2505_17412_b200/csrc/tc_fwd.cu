@@ -692,7 +692,7 @@ constexpr int kMaxSegs = 2 * kMaxTiles + 8;
 constexpr int kSwThreads = 352;
 struct SwSmem {
   uint64_t q_full[2], q_empty[2], kv_full[kStages], kv_empty[kStages], s_full[2], s_empty[2], p_full[2], p_free[2],
-      o_full[2], o_empty[2];
+      o_full[2], o_empty[2], p_half[2];
   uint32_t tmem;
   int n_tiles, n_slc_tiles;
   // packed key tiles: tile j = segments [tile_seg[j], tile_seg[j + 1]); segment = 8-row-aligned run of one
@@ -766,6 +766,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       mbar_init(&S->s_full[i], 1);
       mbar_init(&S->s_empty[i], 128);
       mbar_init(&S->p_full[i], 128);
+      mbar_init(&S->p_half[i], 128);
       mbar_init(&S->p_free[i], 1);
       mbar_init(&S->o_full[i], 1);
       mbar_init(&S->o_empty[i], 128);
@@ -917,14 +918,23 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           oph ^= 1u;
           for (int j = 0; j < n_tiles; ++j) {
             if (j + 1 < n_tiles) issue_s();
-            mbar_wait(&S->p_full[w], pph);
-            pph ^= 1u;
-            tc_fence_after();
             const uint32_t sv = smem_u32(sKV + kv_pv.idx * 32768 + 16384);
             const bool fresh = j == 0 || j == n_slc_tiles;   // first tile of a branch: O restarts
+            // P.V in two halves: keys 0-63 as soon as the softmax has stored them (mid-turn), keys 64-127
+            // after the turn, so only the second half's MMAs sit between the turn and p_free
+            mbar_wait(&S->p_half[w], pph);
+            if (w == 0) TRACE_SW(1, 14, j);
+            tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < 4; ++k)
               umma_ts(tO, tP + k * 8, desc_sw128(sv + k * 2048, 0, 1024), idO, (!fresh || k > 0) ? 1u : 0u);
+            mbar_wait(&S->p_full[w], pph);
+            if (w == 0) TRACE_SW(1, 13, j);
+            pph ^= 1u;
+            tc_fence_after();
+#pragma unroll
+            for (int k = 4; k < 8; ++k)
+              umma_ts(tO, tP + k * 8, desc_sw128(sv + k * 2048, 0, 1024), idO, 1u);
             umma_commit(&S->p_free[w]);
             if (w == 0) TRACE_SW(1, 5, j);
             umma_commit(&S->kv_empty[kv_pv.idx]);
@@ -967,7 +977,6 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         const bool fresh = j == 0 || j == n_slc_tiles;
         const bool closed = j == n_slc_tiles && j > 0;
         if (closed) {             // close the selection branch -> saved O_slc (fp32), after P.V(j-1)
-          if (warp == 0) TRACE_SW(2, 12, j);
           mbar_wait(&S->p_free[wg], fph);
           fph ^= 1u;
           tc_fence_after();
@@ -1002,6 +1011,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         tmem_ld32(tS + 64, v + 64);
         tmem_ld32(tS + 96, v + 96);
         tmem_wait_ld();
+        if (warp == 0) TRACE_SW(2, 11, j);
         tc_fence_before();
         mbar_arrive(&S->s_empty[wg]);
         sb.next();
@@ -1033,6 +1043,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           fph ^= 1u;
           tc_fence_after();
         }
+        if (warp == 0) TRACE_SW(2, 12, j);
         // (a tile may hold no key of this row at all under a per-row mask: keep the max finite)
         const float mx0 = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
         const float mx = kMask ? fmaxf(mx0, -1e30f) : mx0;
@@ -1042,6 +1053,9 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         l *= alpha;
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        // the reference max moved inside a branch (rare): this warp rescales its rows of O after the turn and
+        // only then releases the first P.V half, which reads O (P.V(j-1) has completed: p_free)
+        const bool rescale = __any_sync(0xffffffffu, bump && !fresh);
         if (warp == 0) TRACE_SW(2, 8, j);
         if (kSwPingPong && duo) named_bar_sync(4 + wg, 256);
         if (warp == 0) TRACE_SW(2, 9, j);
@@ -1054,13 +1068,17 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             acc[(i >> 1) & 3] += p0 + p1;
             pk[i >> 1] = pack_f16(p0, p1);
           }
+          if (cc == 64 && !rescale) {   // keys 0-63 stored (their stores completed while these exps ran)
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&S->p_half[wg]);
+          }
           tmem_st16(tP + cc / 2, pk);
         }
         if (kSwPingPong && duo) named_bar_arrive(5 - wg, 256);
         if (warp == 0) TRACE_SW(2, 10, j);
         l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        // the reference max moved inside a branch: rescale O (P.V(j-1) has completed: p_free)
-        if (__any_sync(0xffffffffu, bump && !fresh)) {
+        if (rescale) {
 #pragma unroll
           for (int cc = 0; cc < kD; cc += 16) {
             float o[16];
@@ -1071,8 +1089,12 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             for (int i = 0; i < 16; ++i) ou[i] = __float_as_uint(fresh ? o[i] : o[i] * alpha);
             tmem_st16(tO + cc, ou);
           }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&S->p_half[wg]);
         }
         tmem_wait_st();
+        if (warp == 0) TRACE_SW(2, 15, j);
         tc_fence_before();
         mbar_arrive(&S->p_full[wg]);
       }

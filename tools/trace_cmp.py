@@ -39,7 +39,7 @@ if which == "kv":
              11: "S P written"}
 if which == "sw":
     names = {0: "S epi staged", 2: "S epi batch0", 4: "S epi batch1", 1: "P Q load", 3: "M S issued", 5: "M PV issued", 6: "S wait S", 7: "S S-ready", 8: "S turn-wait",
-             9: "S turn-in", 10: "S turn-out", 12: "S close", 13: "S epi wait O", 14: "S epi O-ready", 15: "S epi done"}
+             9: "S turn-in", 10: "S turn-out", 11: "S S-loaded", 12: "S p_free", 13: "S epi wait O", 14: "S epi O-ready", 15: "S epi done"}
 print("events", n)
 for i in order[:1600]:
     print(f"{clk[i]-t0:10d} {names.get(code[i], code[i]):14s} j={j[i]}")
