@@ -529,6 +529,29 @@ def main():
                      "fwd_bwd_ms": round(float(np.mean([a.elapsed_time(b) for a, b in pt])) / batch, 4),
                      "path": "tcgen05" if sv.used_tcgen05 else "simt"}
 
+    # ---- context: the paper's exact per-token selection (Alg. 1, I in R^{N x h_kv x T}, P:182 / P:188): the
+    # same tokens with query blocks of one token (m_q = 1) on the tcgen05 kernels ----
+    tok_ctx = None
+    if rank == 0 and used_tc and not sharded and not hybrid and not args.no_learned:
+        ms1 = tuple(ms[:3]) + (1,)
+        tt = []
+        for i in range(6):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan_t = ssa.ssa_build_blocks(c_d, grid, batch, *ms1)
+            _, sv = ssa.ssa_forward(plan_t, acfg, q, k, v, g, out=out)
+            ssa.ssa_backward(plan_t, acfg, sv, q, k, v, g, do)
+            e1.record(st)
+            if i >= 2:
+                tt.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        t_ms = float(np.mean([a.elapsed_time(b) for a, b in tt])) / batch
+        tok_ctx = {"impl": "per-token selection m_q = 1 (Alg. 1 granularity), same tokens and heads, tcgen05 "
+                           "(virtual query level for selection/window and dQ, packed KV-outer row tiles)",
+                   "fwd_bwd_ms": round(t_ms, 4), "ratio_vs_query_block_path": round(t_ms / ms_per_step, 2),
+                   "path": "tcgen05" if sv.used_tcgen05 else "simt"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, cfg, coords, grid, batch, inp, value)
@@ -561,6 +584,8 @@ def main():
             line["learned_delta_gates"] = learned_ctx
         if paper_ctx:
             line["paper_layout_d32"] = paper_ctx
+        if tok_ctx:
+            line["per_token_m_q1"] = tok_ctx
         if hybrid_info:
             line["config"]["hybrid_plan"] = hybrid_info["plan"]
         if full:

@@ -362,7 +362,7 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   carve_inputs(cw, d, &x, false);
   fill_common(&x, p, d, cfg);
   *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 +
-              (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T) : 0) +
+              (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T, p->info.max_fill[SSA_LEVEL_SLC]) : 0) +
               tok_cmp_ws_bytes(d.n_q, p->info.batch, tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s), d.max_slc_b) + 2048;
   return SSA_OK;
 }
@@ -400,7 +400,7 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   void* l_ws = cw.take<char>(learned_fwd_ws_bytes(x));
   x.fetch_mark = cw.take<int32_t>(size_t(d.n_slc) + 1);
   x.vq_S = tc ? vq_group(p, d, cfg) : 0;
-  x.vq_ws = x.vq_S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, x.vq_S, d.T)) : nullptr;
+  x.vq_ws = x.vq_S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, x.vq_S, d.T, p->info.max_fill[SSA_LEVEL_SLC])) : nullptr;
   x.tok_cmp = tc ? tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s) : 0;
   x.tok_ws = x.tok_cmp ? cw.take<char>(tok_cmp_ws_bytes(d.n_q, p->info.batch, x.tok_cmp, d.max_slc_b)) : nullptr;
   if (lgates) x.gs = saved_gates;
@@ -459,7 +459,7 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   const VqBwd vq = vq_backward(p, d, cfg, use_tc_bwd(d, cfg, p));
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, vq.dkv, p, &x);
-  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q) + (vq.S ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T) : 0);
+  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q) + (vq.S ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T, p->info.max_fill[SSA_LEVEL_SLC]) : 0);
   if (cfg->learned && cfg->learned->x) scan += gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c);
   if (cfg->learned && cfg->learned->conv_k_w) scan += conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D);
   *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, vq.dkv.n_q, vq.dkv.T,
@@ -505,7 +505,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, vq.dkv, p, &x);
   void* scan_ws = cw.take<char>(inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q));
-  void* vq_ws = vq.S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T)) : nullptr;
+  void* vq_ws = vq.S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T, p->info.max_fill[SSA_LEVEL_SLC])) : nullptr;
   void* tc_ws = cw.take<char>(tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, vq.dkv.n_q, vq.dkv.T,
                                               p->info.max_fill[SSA_LEVEL_SLC], vq.qbpi));
   void* part_ws = nullptr;

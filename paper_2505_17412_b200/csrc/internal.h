@@ -133,7 +133,7 @@ size_t tok_cmp_ws_bytes(int n_q, int batch, int h_s, int max_slc_b);
 int vq_qb_per_item();
 bool vq_enabled();
 int64_t vq_bound(int n_slc, int n_q, int S, int T);
-size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T);
+size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc);
 ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);

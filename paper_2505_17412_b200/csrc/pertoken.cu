@@ -29,25 +29,34 @@ __device__ __forceinline__ void slc_qblocks(const Ctx& c, int B, int* qa, int* q
   *qe = c.tok_block[SSA_LEVEL_Q][t1 - 1] + 1;
 }
 
-// Greedy sub-groups of selection block B (one warp per block): walk its query blocks in order, closing the
-// open sub-group before a query block whose selections would push any kv group's union past 64 blocks, or
-// when it holds S query blocks. Per sub-group k (k < count <= qe - qa): first[qa + k] = its first query
-// block, un[((qa + k) * h_kv + g) * 64 + j] = its union for kv group g (order of first appearance, -1
-// padded); cnt[B] = count; umask[t][g] = the union slots of token t's own query block's selections (bits
+// Greedy sub-groups of chunk ch (2 S consecutive query blocks) of selection block B (one warp per chunk):
+// walk its query blocks in order, closing the open sub-group before a query block whose selections would
+// push any kv group's union past 64 blocks, or when it holds S query blocks. With qa = the chunk's first
+// query block, per sub-group k (k < count <= its query blocks): first[qa + k] = its first query block,
+// un[((qa + k) * h_kv + g) * 64 + j] = its union for kv group g (order of first appearance, -1 padded);
+// cnt[B * cmax + ch] = count; umask[t][g] = the union slots of token t's own query block's selections (bits
 // stay valid: the union only grows by appending). The open unions live in shared memory; membership of
 // the T candidates (one per lane) is tested against the union held two entries per lane, by ballot.
 constexpr int kVqWarps = 4;
 constexpr int kVqMaxG = 8;                         // kv groups of the virtual level (vq_group)
-__global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_t* __restrict__ cnt,
+__global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cmax, int32_t* __restrict__ cnt,
                                                             int32_t* __restrict__ first, int32_t* __restrict__ un,
                                                             unsigned long long* __restrict__ umask) {
   extern __shared__ int vq_u[];                    // [warp][g][64]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int B = blockIdx.x * kVqWarps + wid;
+  const int w = blockIdx.x * kVqWarps + wid;       // (selection block, chunk of 2 S query blocks)
+  const int B = w / cmax, ch = w % cmax;
   if (B >= c.n_blk[SSA_LEVEL_SLC]) return;         // warp-uniform
   int* u = vq_u + wid * c.h_kv * 64;
   int qa, qe;
   slc_qblocks(c, B, &qa, &qe);
+  // chunks are walked independently (a sub-group never spans two): the serial walk is at most 2 S long
+  qa += ch * 2 * S;
+  if (qa >= qe) {
+    if (lane == 0) cnt[w] = 0;
+    return;
+  }
+  qe = min(qe, qa + 2 * S);
   int n_open = 0, size = 0, start = qa;
   int nu_lane = 0;                                 // lane g < h_kv: union size of kv group g
   auto flush = [&](int k) {                        // write the open sub-group's unions as sub-group k
@@ -62,6 +71,7 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_
   int nxt[kVqMaxG];
 #pragma unroll
   for (int g = 0; g < kVqMaxG; ++g) nxt[g] = g < c.h_kv && lane < c.T && qa < qe ? c.I[(int64_t(qa) * c.h_kv + g) * c.T + lane] : -1;
+  int nxt_t = c.off[SSA_LEVEL_Q][qa];               // token range of the next query block, also one ahead
   for (int q = qa; q < qe; ++q) {
     int cand[kVqMaxG];
 #pragma unroll
@@ -69,6 +79,9 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_
       cand[g] = nxt[g];
       nxt[g] = g < c.h_kv && lane < c.T && q + 1 < qe ? c.I[(int64_t(q + 1) * c.h_kv + g) * c.T + lane] : -1;
     }
+    const int tq0 = nxt_t;
+    nxt_t = c.off[SSA_LEVEL_Q][q + 1];
+    const int tq1 = nxt_t;
     // membership of q's candidates in the open unions: slot or -1
     int slot[kVqMaxG];
     bool over = false;
@@ -114,27 +127,26 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int32_
       const unsigned long long bit = Bj >= 0 && sl >= 0 ? 1ull << sl : 0ull;
       const unsigned long long m = (unsigned long long)__reduce_or_sync(0xffffffffu, uint32_t(bit >> 32)) << 32 |
                                    __reduce_or_sync(0xffffffffu, uint32_t(bit));
-      for (int t = c.off[SSA_LEVEL_Q][q] + lane; t < c.off[SSA_LEVEL_Q][q + 1]; t += 32)
-        umask[int64_t(t) * c.h_kv + g] = m;
+      for (int t = tq0 + lane; t < tq1; t += 32) umask[int64_t(t) * c.h_kv + g] = m;
     }
     ++size;
   }
   if (size > 0) flush(n_open);
   if (lane == 0) {
     if (size > 0) first[qa + n_open] = start;
-    cnt[B] = n_open + (size > 0 ? 1 : 0);
+    cnt[w] = n_open + (size > 0 ? 1 : 0);
   }
 }
 
 // sub-group v of selection block B covers query blocks [qa_v, qe_v): token offsets off_v, batch item,
 // identity work order; slots past the real count are empty (off = N) so their CTAs do nothing
-__global__ void k_vq_fill(Ctx c, int vT, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
+__global__ void k_vq_fill(Ctx c, int vT, int S, int cmax, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
                           const int32_t* __restrict__ un, int32_t* __restrict__ I_u, int32_t* __restrict__ off_v,
                           int32_t* __restrict__ qrange, int32_t* __restrict__ batch_v, int32_t* __restrict__ order_v,
                           int bound) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > bound) return;
-  const int total = start[c.n_blk[SSA_LEVEL_SLC]];
+  const int total = start[c.n_blk[SSA_LEVEL_SLC] * cmax];
   if (v < bound) order_v[v] = v;
   if (v >= total) {
     off_v[v] = c.N;
@@ -145,16 +157,18 @@ __global__ void k_vq_fill(Ctx c, int vT, const int32_t* __restrict__ start, cons
     }
     return;
   }
-  int lo = 0, hi = c.n_blk[SSA_LEVEL_SLC];      // selection block B with start[B] <= v < start[B + 1]
+  int lo = 0, hi = c.n_blk[SSA_LEVEL_SLC] * cmax;   // chunk w with start[w] <= v < start[w + 1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (start[mid] <= v) lo = mid; else hi = mid;
   }
-  const int B = lo;
+  const int w = lo, B = w / cmax, ch = w % cmax;
   int qa, qe;
   slc_qblocks(c, B, &qa, &qe);
-  const int k = v - start[B];
-  const int a = first[qa + k], e = k + 1 < start[B + 1] - start[B] ? first[qa + k + 1] : qe;
+  qa += ch * 2 * S;
+  qe = min(qe, qa + 2 * S);
+  const int k = v - start[w];
+  const int a = first[qa + k], e = k + 1 < start[w + 1] - start[w] ? first[qa + k + 1] : qe;
   off_v[v] = c.off[SSA_LEVEL_Q][a];
   qrange[2 * v] = a;
   qrange[2 * v + 1] = e;
@@ -184,11 +198,16 @@ int vq_slots(int S, int T) { return S * T < 64 ? S * T : 64; }
 // (then it holds > (64 - T) / T, i.e. >= floor(64 / T), query blocks)
 int64_t vq_bound(int n_slc, int n_q, int S, int T) {
   const int kmin = S < 64 / T ? S : 64 / T;
-  return int64_t(n_slc) + (int64_t(n_q) + kmin - 1) / kmin;
+  // + one short sub-group per chunk of 2 S query blocks (chunks: at most n_q / (2 S) + n_slc)
+  return int64_t(n_slc) * 2 + int64_t(n_q) / (2 * S) + (int64_t(n_q) + kmin - 1) / kmin + 1;
 }
-size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T) {
+// chunks of 2 S query blocks per selection block (a selection block holds at most max_fill_slc of them,
+// its most-populated one exactly that many tokens); the (selection block, chunk) grid is n_slc x cmax
+static int vq_cmax(int max_fill_slc, int S) { return (max_fill_slc + 2 * S - 1) / (2 * S); }
+size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc) {
   const int64_t bound = vq_bound(n_slc, n_q, S, T);
-  return size_t(n_slc + 2) * 4 * 2 + scan_ws_bytes(n_slc + 1) + size_t(bound + 2) * 4 * 5 + size_t(n_q + 1) * 4 +
+  const int64_t chunks = int64_t(n_slc) * vq_cmax(max_fill_slc, S);
+  return size_t(chunks + 2) * 4 * 2 + scan_ws_bytes(chunks + 1) + size_t(bound + 2) * 4 * 5 + size_t(n_q + 1) * 4 +
          size_t(n_q) * h_kv * 64 * 4 +
          size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 18 * 256;
 }
@@ -201,12 +220,14 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   const int vT = vq_slots(S, c.T);
   if (S < 2 || c.T > 32) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
   const int64_t bound = vq_bound(n_slc, n_q, S, c.T);
-  Carve cw(ws, vq_ws_bytes(c.N, c.h_kv, n_slc, n_q, S, c.T));
-  int32_t* cnt = cw.take<int32_t>(n_slc + 1);
-  int32_t* start = cw.take<int32_t>(n_slc + 1);
+  Carve cw(ws, vq_ws_bytes(c.N, c.h_kv, n_slc, n_q, S, c.T, c.max_fill[SSA_LEVEL_SLC]));
+  const int cmax = vq_cmax(c.max_fill[SSA_LEVEL_SLC], S);
+  const int64_t nw = int64_t(n_slc) * cmax;
+  int32_t* cnt = cw.take<int32_t>(nw + 1);
+  int32_t* start = cw.take<int32_t>(nw + 1);
   int32_t* first = cw.take<int32_t>(n_q + 1);
   int32_t* un = cw.take<int32_t>(size_t(n_q) * c.h_kv * 64);
-  void* sws = cw.take<char>(scan_ws_bytes(n_slc + 1));
+  void* sws = cw.take<char>(scan_ws_bytes(nw + 1));
   int32_t* off_v = cw.take<int32_t>(bound + 1);
   int32_t* qrange = cw.take<int32_t>(2 * bound + 2);
   int32_t* batch_v = cw.take<int32_t>(bound + 1);
@@ -214,12 +235,12 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
   unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv);
   if (n_slc > 0) {
-    k_vq_count<<<nb(n_slc, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cnt, first, un, umask);
+    k_vq_count<<<nb(nw, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cmax, cnt, first, un, umask);
     SSA_LAUNCH_CHECK("k_vq_count");
   }
-  ssa_status s = exclusive_scan(cnt, start, n_slc, start + n_slc, sws, st);
+  ssa_status s = exclusive_scan(cnt, start, nw, start + nw, sws, st);
   if (s != SSA_OK) return s;
-  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, vT, start, first, un, I_u, off_v, qrange, batch_v, order_v, int(bound));
+  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, vT, S, cmax, start, first, un, I_u, off_v, qrange, batch_v, order_v, int(bound));
   SSA_LAUNCH_CHECK("k_vq_fill");
   *v = c;
   v->tok_I = c.I;            // the per-query-block selections (KV-outer row masks)

@@ -17,16 +17,18 @@ cc = torch.from_numpy(c).cuda()
 for m_q in [int(x) for x in (sys.argv[1:] or ['8', '4', '1'])]:
     plan = ssa.ssa_build_blocks(cc, grid, batch, 4, 8, 8, m_q)
     acfg = ssa.AttnCfg(h_q=16, h_kv=2, d=64, top_k=8, dtype=torch.bfloat16, flags=0)
-    for i in range(4):
-        if i == 1:
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+    ts = []
+    for i in range(13):              # 3 warm-up steps, then the median of 10 (each bracketed by events)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         out, saved = ssa.ssa_forward(plan, acfg, *t[:4])
         ssa.ssa_backward(plan, acfg, saved, *t)
-    e1.record()
-    torch.cuda.synchronize()
-    print(f"C2 m_q={m_q}: {e0.elapsed_time(e1) / 3:.2f} ms fwd+bwd ({'tcgen05' if saved.used_tcgen05 else 'SIMT'}), "
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    print(f"C2 m_q={m_q}: {ts[len(ts) // 2]:.2f} ms fwd+bwd (median of 10; {'tcgen05' if saved.used_tcgen05 else 'SIMT'}), "
           f"bwd ws {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB peak, N={c.shape[0]}", flush=True)
     ssa.profile_reset()
     ssa.profile_enable(True)
