@@ -231,14 +231,23 @@ __device__ __forceinline__ float lg2(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// max / sum of 32 values with 8 independent chains (breaks the 32-deep dependency chain)
-__device__ __forceinline__ float max32(const float* v) {
+// three-input max (FMNMX3, sm_100): NaN-ignoring like fmaxf; the result is exact (no rounding)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// max of 128 values: 8 independent chains of three-input maxes (67 FMNMX3 instead of 127 FMNMX)
+__device__ __forceinline__ float max128(const float* v) {
   float m[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m[i] = fmaxf(v[i], v[i + 8]);
+  for (int i = 0; i < 8; ++i) {
+    m[i] = fmax3f(v[i], v[i + 8], v[i + 16]);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], fmaxf(v[i + 16], v[i + 24]));
-  return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+    for (int t = 3; t < 15; t += 2) m[i] = fmax3f(m[i], v[i + 8 * t], v[i + 8 * t + 8]);
+    m[i] = fmaxf(m[i], v[i + 120]);
+  }
+  return fmax3f(fmax3f(m[0], m[1], m[2]), fmax3f(m[3], m[4], m[5]), fmaxf(m[6], m[7]));
 }
 __device__ __forceinline__ uint32_t pack_f16(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);

@@ -29,10 +29,15 @@ using namespace tc;
 constexpr int kD = 64;
 constexpr int kTile = 128;
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef SSA_SW_EPI_HALF
+#define SSA_SW_EPI_HALF 1   // epilogue staged 32 columns at a time (4 KB per warp): room for a 4th K/V stage
+#endif
+constexpr bool kEpiHalf = SSA_SW_EPI_HALF;
 #ifndef SSA_SW_STAGES
-#define SSA_SW_STAGES 3
+#define SSA_SW_STAGES (SSA_SW_EPI_HALF ? 4 : 3)
 #endif
 constexpr int kStages = SSA_SW_STAGES;   // K/V stages of the selection+window kernel
+constexpr int kEpiBytes = kEpiHalf ? 32768 : 65536;   // epilogue staging, all 8 softmax warps
 #ifndef SSA_SW_PINGPONG
 #define SSA_SW_PINGPONG 1
 #endif
@@ -418,7 +423,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 #pragma unroll
           for (int i = 0; i < 128; ++i) v[i] = i < nv ? v[i] : -INFINITY;   // padded keys: p = 0
         }
-        const float mx = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
+        const float mx = max128(v) * cl2;
         const bool bump = mx > m + kRescale;
         const float m_new = bump ? mx : m;
         const float alpha = ex2(m - m_new);           // 1 when the reference does not move
@@ -721,6 +726,17 @@ __device__ __forceinline__ void stage_row(float* wbuf, int lane, const float* v,
 __device__ __forceinline__ float4 staged_chunk(const float* wbuf, int rl, int ch) {
   return *reinterpret_cast<const float4*>(wbuf + rl * 64 + 4 * (ch ^ (rl & 15)));
 }
+// half-width staging (kEpiHalf): 32 rows x 32 fp32 (4 KB) per warp, chunks XOR-swizzled by row & 7; read back
+// four rows per instruction (lanes 8i..8i+7 take row 4k+i), every global access a 128-B row segment
+__device__ __forceinline__ void stage_row_h(float* wbuf, int lane, const float* v, float scale) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 4)
+    *reinterpret_cast<float4*>(wbuf + lane * 32 + 4 * ((j >> 2) ^ (lane & 7))) =
+        make_float4(v[j] * scale, v[j + 1] * scale, v[j + 2] * scale, v[j + 3] * scale);
+}
+__device__ __forceinline__ float4 staged_h(const float* wbuf, int rl, int ch) {
+  return *reinterpret_cast<const float4*>(wbuf + rl * 32 + 4 * (ch ^ (rl & 7)));
+}
 
 // kMask: the per-row union-slot masks of small query blocks (pertoken.cu); a separate instantiation so
 // the query-block path carries none of its registers
@@ -732,8 +748,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;                          // 2 x 16 KB (row tiles of the pair)
   uint8_t* sKV = sm + 32768;                 // kStages x {K, V} 32 KB
-  uint8_t* sEpi = sKV + kStages * 32768;     // epilogue operands: 8 KB per softmax warp
-  SwSmem* S = reinterpret_cast<SwSmem*>(sEpi + 65536);
+  uint8_t* sEpi = sKV + kStages * 32768;     // epilogue staging: kEpiBytes / 8 per softmax warp
+  SwSmem* S = reinterpret_cast<SwSmem*>(sEpi + kEpiBytes);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = c.q_order[blockIdx.x], g = blockIdx.y;
@@ -962,7 +978,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       const bool rvalid = r < rows;
       const int64_t row = qrow0 + (rvalid ? r : 0);
       const int wrow0 = rt * kTile + (warp & 3) * 32;   // first row of this warp
-      float* wbuf = reinterpret_cast<float*>(sEpi + wg * 32768 + (warp & 3) * 8192);
+      float* wbuf = reinterpret_cast<float*>(sEpi + wg * (kEpiBytes / 2) + (warp & 3) * (kEpiBytes / 8));
       if (wrow0 + lane < rows) {
         // pull this warp's O_cmp rows (HBM) and gates toward L2 now; the epilogue reads them a pair later
         const char* pc = reinterpret_cast<const char*>(static_cast<const float*>(c.o[0]) + (qrow0 + wrow0 + lane) * int64_t(kD));
@@ -981,21 +997,39 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           fph ^= 1u;
           tc_fence_after();
           const float inv = 1.f / l;
-#pragma unroll
-          for (int cc = 0; cc < kD; cc += 32) {
-            float o[32];
-            tmem_ld32(tO + cc, o);
-            tmem_wait_ld();
-            stage_row(wbuf, lane, o, inv, cc, 32);
-          }
-          __syncwarp();
           float* os = static_cast<float*>(c.o[1]);
+          if (kEpiHalf) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              float o[32];
+              tmem_ld32(tO + 32 * hf, o);
+              tmem_wait_ld();
+              stage_row_h(wbuf, lane, o, inv);
+              __syncwarp();
 #pragma unroll 4
-          for (int i = 0; i < 16; ++i) {
-            const int rl = 2 * i + (lane >> 4), ch = lane & 15, rr = wrow0 + rl;
-            if (rr < rows) *reinterpret_cast<float4*>(os + (qrow0 + rr) * int64_t(kD) + 4 * ch) = staged_chunk(wbuf, rl, ch);
+              for (int i = 0; i < 8; ++i) {
+                const int rl = 4 * i + (lane >> 3), ch = lane & 7, rr = wrow0 + rl;
+                if (rr < rows)
+                  *reinterpret_cast<float4*>(os + (qrow0 + rr) * int64_t(kD) + 32 * hf + 4 * ch) = staged_h(wbuf, rl, ch);
+              }
+              __syncwarp();
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < kD; cc += 32) {
+              float o[32];
+              tmem_ld32(tO + cc, o);
+              tmem_wait_ld();
+              stage_row(wbuf, lane, o, inv, cc, 32);
+            }
+            __syncwarp();
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+              const int rl = 2 * i + (lane >> 4), ch = lane & 15, rr = wrow0 + rl;
+              if (rr < rows) *reinterpret_cast<float4*>(os + (qrow0 + rr) * int64_t(kD) + 4 * ch) = staged_chunk(wbuf, rl, ch);
+            }
+            __syncwarp();
           }
-          __syncwarp();
           lse_slc = m + lg2(l);
           m = -1e30f;
           l = 0.f;
@@ -1038,18 +1072,19 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
             }
           }
         }
+        // the max first: it overlaps the wait for P.V(j-1) below
+        // (a tile may hold no key of this row at all under a per-row mask: keep the max finite)
+        const float mx0 = max128(v) * cl2;
+        const float mx = kMask ? fmaxf(mx0, -1e30f) : mx0;
+        const bool bump = fresh || mx > m + kRescale;
+        const float m_new = bump ? mx : m;
+        const float alpha = ex2(m - m_new);           // 1 when the reference does not move
         if (!closed) {   // P.V(j-1) complete: O is up to date and P may be rewritten
           mbar_wait(&S->p_free[wg], fph);
           fph ^= 1u;
           tc_fence_after();
         }
         if (warp == 0) TRACE_SW(2, 12, j);
-        // (a tile may hold no key of this row at all under a per-row mask: keep the max finite)
-        const float mx0 = fmaxf(fmaxf(max32(v), max32(v + 32)), fmaxf(max32(v + 64), max32(v + 96))) * cl2;
-        const float mx = kMask ? fmaxf(mx0, -1e30f) : mx0;
-        const bool bump = fresh || mx > m + kRescale;
-        const float m_new = bump ? mx : m;
-        const float alpha = ex2(m - m_new);           // 1 when the reference does not move
         l *= alpha;
         m = m_new;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1098,79 +1133,141 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         tc_fence_before();
         mbar_arrive(&S->p_full[wg]);
       }
-      // Epilogue (gated sum, Eq. 6). The window output is staged through the warp's shared slot so every
-      // global access is a coalesced row pair (lanes 0-15 / 16-31 take rows 2i / 2i+1, four columns
-      // each); the gated sum's global operands (O_slc written at the branch close, O_cmp, gates,
-      // destination rows) come in two batches of 8 row pairs, the first issued before O is ready.
-      const int ch = lane & 15;
       const float* os_g = static_cast<const float*>(c.o[1]);
       const float* ocm_g = static_cast<const float*>(c.o[0]);
-      float4 e_sl[8], e_cm[8];
-      float e_w[8][3];
-      int e_dst[8];
-      auto epi_load = [&](int bt) {
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) {
-          const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
-          const int64_t grow = qrow0 + rr;
-          if (!c.no_win) e_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 4 * ch);
-          e_cm[ii] = *reinterpret_cast<const float4*>(ocm_g + grow * kD + 4 * ch);
-          e_w[ii][0] = c.gs[grow * 3];
-          e_w[ii][1] = c.gs[grow * 3 + 1];
-          e_w[ii][2] = c.gs[grow * 3 + 2];
-          const int tok = t0 + rr / c.h_s;
-          e_dst[ii] = c.sorted_input ? tok : c.perm[tok];
-        }
-      };
-      epi_load(0);
-      if (warp == 0) TRACE_SW(2, 13, pr);
-      mbar_wait(&S->o_full[wg], oph);
-      oph ^= 1u;
-      if (warp == 0) TRACE_SW(2, 14, pr);
-      tc_fence_after();
-      const float inv = 1.f / l;
-#pragma unroll
-      for (int cc = 0; cc < kD; cc += 32) {
-        float o[32];
-        tmem_ld32(tO + cc, o);
-        tmem_wait_ld();
-        stage_row(wbuf, lane, o, inv, cc, 32);
-      }
-      tc_fence_before();
-      mbar_arrive(&S->o_empty[wg]);
-      if (rvalid) {
-        // window-only: keep the "no keys" sentinel of the selection LSE (api.cu); no-window: the O in
-        // TMEM is the selection branch's (its tiles were the last ones)
-        if (n_slc_tiles > 0 && !c.no_win) c.lse[1][row] = lse_slc;
-        c.lse[c.no_win ? 1 : 2][row] = m + lg2(l);
-      }
-      __syncwarp();
-      if (warp == 0) TRACE_SW(2, 0, pr);
       float* ow = static_cast<float*>(c.o[c.no_win ? 1 : 2]);
+      // gated sum of one staged 4-column chunk of row rr (Eq. 6), O_win (or O_slc under SSA_NO_WINDOW) stored
+      auto combine = [&](int rr, int col, const float4& wn, const float4& sl_in, const float4& cm, const float* w3,
+                         int dst) {
+        const int64_t grow = qrow0 + rr;
+        const float4 sl = c.no_win ? wn : sl_in;
+        const float w0 = w3[0], w1 = w3[1], w2 = c.no_win ? 0.f : w3[2];
+        *reinterpret_cast<float4*>(ow + grow * kD + col) = wn;
+        if (col >= c.Dc) return;             // zero-padded head dims (d = 32) are not output
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + rr % c.h_s) * c.Dc + col;
+        float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
+                               w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w);
+        if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's out (e.g. the shifted-window pass)
+          const uint2 old = *reinterpret_cast<const uint2*>(out);
+          const float2 a = unpack_bf16(old.x), b = unpack_bf16(old.y);
+          y.x += a.x; y.y += a.y; y.z += b.x; y.w += b.y;
+        }
+        *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+      };
+      if (kEpiHalf) {
+        // Epilogue (gated sum, Eq. 6), 32 columns at a time: the window output is staged through the warp's
+        // 4 KB slot and read back four rows per instruction (lanes 8i..8i+7: row 4k+i, four columns each);
+        // the gated sum's global operands (O_slc written at the branch close, O_cmp, gates, destination
+        // rows) come in batches of four row quads, the first issued before O is ready.
+        const int ch = lane & 7;
+        float4 h_sl[4], h_cm[4];
+        float h_w[4][3];
+        int h_dst[4];
+        auto epi_load_h = [&](int hf, int bt) {
 #pragma unroll
-      for (int bt = 0; bt < 2; ++bt) {
-        if (bt == 1) epi_load(1);
-        if (warp == 0) TRACE_SW(2, 2 + 2 * bt, pr);
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) {
-          const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = wrow0 + rl;
-          if (rr < rows) {
+          for (int ii = 0; ii < 4; ++ii) {
+            const int rl = 4 * (bt * 4 + ii) + (lane >> 3), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
             const int64_t grow = qrow0 + rr;
-            const float4 wn = staged_chunk(wbuf, rl, ch), cm = e_cm[ii];
-            const float4 sl = c.no_win ? wn : e_sl[ii];
-            const float w0 = e_w[ii][0], w1 = e_w[ii][1], w2 = c.no_win ? 0.f : e_w[ii][2];
-            *reinterpret_cast<float4*>(ow + grow * kD + 4 * ch) = wn;
-            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) +
-                                 (int64_t(e_dst[ii]) * c.H + g * c.h_s + rr % c.h_s) * c.Dc + 4 * ch;
-            float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
-                                   w0 * cm.z + w1 * sl.z + w2 * wn.z, w0 * cm.w + w1 * sl.w + w2 * wn.w);
-            if (4 * ch >= c.Dc) continue;        // zero-padded head dims (d = 32) are not output
-            if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's out (e.g. the shifted-window pass)
-              const uint2 old = *reinterpret_cast<const uint2*>(out);
-              const float2 a = unpack_bf16(old.x), b = unpack_bf16(old.y);
-              y.x += a.x; y.y += a.y; y.z += b.x; y.w += b.y;
+            if (!c.no_win) h_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 32 * hf + 4 * ch);
+            h_cm[ii] = *reinterpret_cast<const float4*>(ocm_g + grow * kD + 32 * hf + 4 * ch);
+            h_w[ii][0] = c.gs[grow * 3];
+            h_w[ii][1] = c.gs[grow * 3 + 1];
+            h_w[ii][2] = c.gs[grow * 3 + 2];
+            const int tok = t0 + rr / c.h_s;
+            h_dst[ii] = c.sorted_input ? tok : c.perm[tok];
+          }
+        };
+        epi_load_h(0, 0);
+        if (warp == 0) TRACE_SW(2, 13, pr);
+        mbar_wait(&S->o_full[wg], oph);
+        oph ^= 1u;
+        if (warp == 0) TRACE_SW(2, 14, pr);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        if (rvalid) {
+          // window-only: keep the "no keys" sentinel of the selection LSE (api.cu); no-window: the O in
+          // TMEM is the selection branch's (its tiles were the last ones)
+          if (n_slc_tiles > 0 && !c.no_win) c.lse[1][row] = lse_slc;
+          c.lse[c.no_win ? 1 : 2][row] = m + lg2(l);
+        }
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          {
+            float o[32];
+            tmem_ld32(tO + 32 * hf, o);
+            tmem_wait_ld();
+            stage_row_h(wbuf, lane, o, inv);
+          }
+          if (hf == 1) {                 // O fully read: the next pair's P.V may overwrite it
+            tc_fence_before();
+            mbar_arrive(&S->o_empty[wg]);
+          }
+          __syncwarp();
+          if (warp == 0) TRACE_SW(2, 0, pr);
+#pragma unroll
+          for (int bt = 0; bt < 2; ++bt) {
+            if (hf + bt > 0) epi_load_h(hf, bt);
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+              const int rl = 4 * (bt * 4 + ii) + (lane >> 3), rr = wrow0 + rl;
+              if (rr < rows) combine(rr, 32 * hf + 4 * ch, staged_h(wbuf, rl, ch), h_sl[ii], h_cm[ii], h_w[ii], h_dst[ii]);
             }
-            *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+          }
+          __syncwarp();
+        }
+      } else {
+        // Epilogue (gated sum, Eq. 6). The window output is staged through the warp's shared slot so every
+        // global access is a coalesced row pair (lanes 0-15 / 16-31 take rows 2i / 2i+1, four columns
+        // each); the gated sum's global operands (O_slc written at the branch close, O_cmp, gates,
+        // destination rows) come in two batches of 8 row pairs, the first issued before O is ready.
+        const int ch = lane & 15;
+        float4 e_sl[8], e_cm[8];
+        float e_w[8][3];
+        int e_dst[8];
+        auto epi_load = [&](int bt) {
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) {
+            const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
+            const int64_t grow = qrow0 + rr;
+            if (!c.no_win) e_sl[ii] = *reinterpret_cast<const float4*>(os_g + grow * kD + 4 * ch);
+            e_cm[ii] = *reinterpret_cast<const float4*>(ocm_g + grow * kD + 4 * ch);
+            e_w[ii][0] = c.gs[grow * 3];
+            e_w[ii][1] = c.gs[grow * 3 + 1];
+            e_w[ii][2] = c.gs[grow * 3 + 2];
+            const int tok = t0 + rr / c.h_s;
+            e_dst[ii] = c.sorted_input ? tok : c.perm[tok];
+          }
+        };
+        epi_load(0);
+        if (warp == 0) TRACE_SW(2, 13, pr);
+        mbar_wait(&S->o_full[wg], oph);
+        oph ^= 1u;
+        if (warp == 0) TRACE_SW(2, 14, pr);
+        tc_fence_after();
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int cc = 0; cc < kD; cc += 32) {
+          float o[32];
+          tmem_ld32(tO + cc, o);
+          tmem_wait_ld();
+          stage_row(wbuf, lane, o, inv, cc, 32);
+        }
+        tc_fence_before();
+        mbar_arrive(&S->o_empty[wg]);
+        if (rvalid) {
+          if (n_slc_tiles > 0 && !c.no_win) c.lse[1][row] = lse_slc;
+          c.lse[c.no_win ? 1 : 2][row] = m + lg2(l);
+        }
+        __syncwarp();
+        if (warp == 0) TRACE_SW(2, 0, pr);
+#pragma unroll
+        for (int bt = 0; bt < 2; ++bt) {
+          if (bt == 1) epi_load(1);
+          if (warp == 0) TRACE_SW(2, 2 + 2 * bt, pr);
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) {
+            const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = wrow0 + rl;
+            if (rr < rows) combine(rr, 4 * ch, staged_chunk(wbuf, rl, ch), e_sl[ii], e_cm[ii], e_w[ii], e_dst[ii]);
           }
         }
       }
@@ -1332,7 +1429,8 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
   }
   {
     const int nq = cv.n_blk[SSA_LEVEL_Q];
-    const size_t smem = 1024 + 32768 + kStages * 32768 + 65536 + sizeof(SwSmem);
+    const size_t smem = 1024 + 32768 + kStages * 32768 + kEpiBytes + sizeof(SwSmem);
+    static_assert(1024 + 32768 + kStages * 32768 + kEpiBytes + sizeof(SwSmem) <= 232448, "selection/window shared memory");
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ProfScope ps("tc_slc_win_fwd", st);

@@ -9,9 +9,10 @@ import torch
 from paper_2505_17412_b200 import ssa
 from ssa_workload import CONFIGS, config_coords, make_inputs
 
-cfg = CONFIGS["C2"]
-c, grid, batch = config_coords("C2")
-inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed=1)
+CFG = os.environ.get("MQ_CONFIG", "C2")
+cfg = CONFIGS[CFG]
+c, grid, batch = config_coords(CFG)
+inp = make_inputs(c, grid, batch, 16, 2, 64, "bf16", seed={"C2": 1, "C3": 2}.get(CFG, 1))
 t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (inp.q, inp.k, inp.v, inp.gates, inp.dout)]
 cc = torch.from_numpy(c).cuda()
 for m_q in [int(x) for x in (sys.argv[1:] or ['8', '4', '1'])]:
@@ -28,7 +29,7 @@ for m_q in [int(x) for x in (sys.argv[1:] or ['8', '4', '1'])]:
         if i >= 3:
             ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(f"C2 m_q={m_q}: {ts[len(ts) // 2]:.2f} ms fwd+bwd (median of 10; {'tcgen05' if saved.used_tcgen05 else 'SIMT'}), "
+    print(f"{CFG} m_q={m_q}: {ts[len(ts) // 2]:.2f} ms fwd+bwd (median of 10; {'tcgen05' if saved.used_tcgen05 else 'SIMT'}), "
           f"bwd ws {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB peak, N={c.shape[0]}", flush=True)
     ssa.profile_reset()
     ssa.profile_enable(True)
