@@ -230,6 +230,8 @@ double q_rows(const Dims& d) { return d.n_q > 0 ? double(d.N) / d.n_q * (d.H / d
 int vq_group(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
   if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32 || d.h_kv > 8)
     return 0;
+  // one query block's selections must fit a virtual block's key capacity
+  if (int64_t(d.T) * p->info.max_fill[SSA_LEVEL_SLC] > kVqKeyCap) return 0;
   if (cfg->q_end > 0 && (cfg->q_begin > 0 || cfg->q_end < d.n_q)) return 0;
   const double target = env_or("SSA_VQ_ROWS", 256.0);
   const int S = std::min(32, std::max(1, int(target / q_rows(d) + 0.5)));
@@ -251,7 +253,7 @@ VqBwd vq_backward(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg, bool tc
   v.kv = v.S > 0 && q_rows(d) < kv_rows;
   v.dkv = d;
   if (v.kv) {
-    v.dkv.n_q = int(vq_bound(d.n_slc, d.n_q, v.S, d.T));
+    v.dkv.n_q = int(vq_bound(d.n_slc, d.n_q, v.S, d.T, p->info.max_fill[SSA_LEVEL_SLC]));
     v.dkv.T = vq_slots(v.S, d.T);
   }
   v.qbpi = v.kv ? vq_qb_per_item() : tc_qb_per_item(p->info.m[SSA_LEVEL_SLC], p->info.m[SSA_LEVEL_Q]);

@@ -79,7 +79,7 @@ struct Ctx {
   int32_t qb_per_item;            // raw-key KV-outer work item size in query blocks (tc_qb_per_item)
   // query blocks smaller than the selection blocks on tcgen05 (pertoken.cu): the virtual-level context
   // carries the per-token slot masks and, for the KV-outer row masks, the per-query-block selections
-  const unsigned long long* umask;  // [N][h_kv] union-slot mask of every token, null on the plain path
+  const unsigned long long* umask;  // [N][h_kv][2] 128-bit union-slot mask of every token, null on the plain path
   const int32_t* tok_I;             // [n_q][h_kv][tok_T] per-query-block selections
   int32_t tok_T;
   const int32_t* tok_qb;            // token -> query block
@@ -132,7 +132,11 @@ int tok_cmp_hs(int m_q, int h_s);   // h_s when the per-token compression kernel
 size_t tok_cmp_ws_bytes(int n_q, int batch, int h_s, int max_slc_b);
 int vq_qb_per_item();
 bool vq_enabled();
-int64_t vq_bound(int n_slc, int n_q, int S, int T);
+// union capacity of a virtual query block: slots (mask bits) and keys (within the selection / dQ kernels'
+// packed-tile capacity: 28 672 keys + 8-key granule padding of 128 blocks + a window block <= 264 x 128)
+constexpr int kVqSlots = 128;
+constexpr int kVqKeyCap = 28672;
+int64_t vq_bound(int n_slc, int n_q, int S, int T, int max_fill_slc);
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc);
 ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
 // learned.cu

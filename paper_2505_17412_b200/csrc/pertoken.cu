@@ -5,13 +5,13 @@
 // selection / window and dQ / KV-outer kernels would then see one query block's few rows per 128-row
 // tile, so they run on a "virtual" query level instead: each selection block's query blocks are cut
 // into sub-groups of consecutive query blocks (contiguous rows) — greedily, up to S query blocks (S chosen
-// on the host so that a sub-group fills about one 128-row tile) while the union of the sub-group's
-// selections stays within 64 blocks for every kv group; a sub-group's key set is that union, and every row
-// keeps only its own query block's blocks through a 64-bit slot mask (umask[token][g]): the softmax loops
-// set the other granules' logits to -inf (forward, dQ), the KV-outer producer gives the rows of query
-// blocks that did not select the key block an LSE of +inf (p = 0). Same arithmetic per row as the
-// query-block path; only the row / key grouping changes. A sub-group closed by the 64-slot cap holds at
-// least floor(64 / T) query blocks, which bounds the number of sub-groups (vq_bound).
+// on the host so that a sub-group fills a row-tile pair) while the union of the sub-group's selections
+// stays within kVqSlots = 128 blocks and kVqKeyCap keys for every kv group; a sub-group's key set is that
+// union, and every row keeps only its own query block's blocks through a 128-bit slot mask
+// (umask[token][g][2]): the softmax loops set the other granules' logits to -inf (forward, dQ), the
+// KV-outer producer gives the rows of query blocks that did not select the key block an LSE of +inf
+// (p = 0). Same arithmetic per row as the query-block path; only the row / key grouping changes. A
+// sub-group closed by a cap holds at least kmin query blocks (vq_bound), which bounds their number.
 #include <climits>
 #include <cstdlib>
 
@@ -31,23 +31,25 @@ __device__ __forceinline__ void slc_qblocks(const Ctx& c, int B, int* qa, int* q
 
 // Greedy sub-groups of chunk ch (2 S consecutive query blocks) of selection block B (one warp per chunk):
 // walk its query blocks in order, closing the open sub-group before a query block whose selections would
-// push any kv group's union past 64 blocks, or when it holds S query blocks. With qa = the chunk's first
-// query block, per sub-group k (k < count <= its query blocks): first[qa + k] = its first query block,
-// un[((qa + k) * h_kv + g) * 64 + j] = its union for kv group g (order of first appearance, -1 padded);
-// cnt[B * cmax + ch] = count; umask[t][g] = the union slots of token t's own query block's selections (bits
-// stay valid: the union only grows by appending). The open unions live in shared memory; membership of
-// the T candidates (one per lane) is tested against the union held two entries per lane, by ballot.
+// push any kv group's union past kVqSlots blocks or kVqKeyCap keys (the tile capacity of the selection /
+// dQ kernels), or when it holds S query blocks. With qa = the chunk's first query block, per sub-group k
+// (k < count <= its query blocks): first[qa + k] = its first query block, un[((qa + k) * h_kv + g) *
+// kVqSlots + j] = its union for kv group g (order of first appearance, -1 padded); cnt[B * cmax + ch] =
+// count; umask[(t * h_kv + g) * 2 + w] = word w of the union slots of token t's own query block's
+// selections (bits stay valid: the union only grows by appending). The open unions live in shared memory;
+// membership of the T candidates (one per lane) is tested against the union held four entries per lane,
+// by ballot.
 constexpr int kVqWarps = 4;
 constexpr int kVqMaxG = 8;                         // kv groups of the virtual level (vq_group)
 __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cmax, int32_t* __restrict__ cnt,
                                                             int32_t* __restrict__ first, int32_t* __restrict__ un,
                                                             unsigned long long* __restrict__ umask) {
-  extern __shared__ int vq_u[];                    // [warp][g][64]
+  extern __shared__ int vq_u[];                    // [warp][g][kVqSlots]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int w = blockIdx.x * kVqWarps + wid;       // (selection block, chunk of 2 S query blocks)
   const int B = w / cmax, ch = w % cmax;
   if (B >= c.n_blk[SSA_LEVEL_SLC]) return;         // warp-uniform
-  int* u = vq_u + wid * c.h_kv * 64;
+  int* u = vq_u + wid * c.h_kv * kVqSlots;
   int qa, qe;
   slc_qblocks(c, B, &qa, &qe);
   // chunks are walked independently (a sub-group never spans two): the serial walk is at most 2 S long
@@ -58,13 +60,13 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
   }
   qe = min(qe, qa + 2 * S);
   int n_open = 0, size = 0, start = qa;
-  int nu_lane = 0;                                 // lane g < h_kv: union size of kv group g
+  int nu_lane = 0, nk_lane = 0;                    // lane g < h_kv: union size / keys of kv group g
   auto flush = [&](int k) {                        // write the open sub-group's unions as sub-group k
     for (int g = 0; g < c.h_kv; ++g) {
       const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
-      int32_t* o = un + (int64_t(qa + k) * c.h_kv + g) * 64;
-      o[lane] = lane < nu ? u[g * 64 + lane] : -1;
-      o[lane + 32] = lane + 32 < nu ? u[g * 64 + lane + 32] : -1;
+      int32_t* o = un + (int64_t(qa + k) * c.h_kv + g) * kVqSlots;
+#pragma unroll
+      for (int q4 = 0; q4 < kVqSlots / 32; ++q4) o[lane + 32 * q4] = lane + 32 * q4 < nu ? u[g * kVqSlots + lane + 32 * q4] : -1;
     }
   };
   // candidates of the next query block, loaded one query block ahead (lane j < T: block I[q][g][j])
@@ -73,10 +75,11 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
   for (int g = 0; g < kVqMaxG; ++g) nxt[g] = g < c.h_kv && lane < c.T && qa < qe ? c.I[(int64_t(qa) * c.h_kv + g) * c.T + lane] : -1;
   int nxt_t = c.off[SSA_LEVEL_Q][qa];               // token range of the next query block, also one ahead
   for (int q = qa; q < qe; ++q) {
-    int cand[kVqMaxG];
+    int cand[kVqMaxG], ckeys[kVqMaxG];
 #pragma unroll
     for (int g = 0; g < kVqMaxG; ++g) {
       cand[g] = nxt[g];
+      ckeys[g] = cand[g] >= 0 ? c.off[SSA_LEVEL_SLC][cand[g] + 1] - c.off[SSA_LEVEL_SLC][cand[g]] : 0;
       nxt[g] = g < c.h_kv && lane < c.T && q + 1 < qe ? c.I[(int64_t(q + 1) * c.h_kv + g) * c.T + lane] : -1;
     }
     const int tq0 = nxt_t;
@@ -90,15 +93,24 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
       slot[g] = -1;
       if (g >= c.h_kv) continue;
       const int Bj = cand[g];
-      const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
-      const int u0 = lane < nu ? u[g * 64 + lane] : -2, u1 = lane + 32 < nu ? u[g * 64 + lane + 32] : -2;
+      const int nu = __shfl_sync(0xffffffffu, nu_lane, g), nk = __shfl_sync(0xffffffffu, nk_lane, g);
+      int uu[kVqSlots / 32];
+#pragma unroll
+      for (int q4 = 0; q4 < kVqSlots / 32; ++q4) uu[q4] = lane + 32 * q4 < nu ? u[g * kVqSlots + lane + 32 * q4] : -2;
       for (int j = 0; j < c.T; ++j) {
         const int b = __shfl_sync(0xffffffffu, Bj, j);
-        const unsigned h0 = __ballot_sync(0xffffffffu, u0 == b), h1 = __ballot_sync(0xffffffffu, u1 == b);
-        if (lane == j && b >= 0 && (h0 | h1)) slot[g] = h0 ? __ffs(h0) - 1 : 32 + __ffs(h1) - 1;
+        int pos = -1;
+#pragma unroll
+        for (int q4 = kVqSlots / 32 - 1; q4 >= 0; --q4) {
+          const unsigned h = __ballot_sync(0xffffffffu, uu[q4] == b);
+          if (h) pos = 32 * q4 + __ffs(h) - 1;
+        }
+        if (lane == j && b >= 0) slot[g] = pos;
       }
-      const int nnew = __popc(__ballot_sync(0xffffffffu, Bj >= 0 && slot[g] < 0));
-      over |= nu + nnew > 64;
+      const bool is_new = Bj >= 0 && slot[g] < 0;
+      const int nnew = __popc(__ballot_sync(0xffffffffu, is_new));
+      const int knew = __reduce_add_sync(0xffffffffu, is_new ? ckeys[g] : 0);
+      over |= nu + nnew > kVqSlots || nk + knew > kVqKeyCap;
     }
     if (size > 0 && (size == S || over)) {         // close the open sub-group before q
       flush(n_open);
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
       start = q;
       size = 0;
       nu_lane = 0;
+      nk_lane = 0;
 #pragma unroll
       for (int g = 0; g < kVqMaxG; ++g) slot[g] = -1;
     }
@@ -117,17 +130,27 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
       const int Bj = cand[g];
       const int nu = __shfl_sync(0xffffffffu, nu_lane, g);
       int sl = slot[g];
-      const unsigned mk = __ballot_sync(0xffffffffu, Bj >= 0 && sl < 0);
-      if ((mk >> lane) & 1u) {
+      const bool is_new = Bj >= 0 && sl < 0;
+      const unsigned mk = __ballot_sync(0xffffffffu, is_new);
+      const int knew = __reduce_add_sync(0xffffffffu, is_new ? ckeys[g] : 0);
+      if (is_new) {
         sl = nu + __popc(mk & ((1u << lane) - 1u));
-        u[g * 64 + sl] = Bj;
+        u[g * kVqSlots + sl] = Bj;
       }
       __syncwarp();
-      if (lane == g) nu_lane = nu + __popc(mk);
-      const unsigned long long bit = Bj >= 0 && sl >= 0 ? 1ull << sl : 0ull;
-      const unsigned long long m = (unsigned long long)__reduce_or_sync(0xffffffffu, uint32_t(bit >> 32)) << 32 |
-                                   __reduce_or_sync(0xffffffffu, uint32_t(bit));
-      for (int t = tq0 + lane; t < tq1; t += 32) umask[int64_t(t) * c.h_kv + g] = m;
+      if (lane == g) {
+        nu_lane = nu + __popc(mk);
+        nk_lane += knew;
+      }
+      const bool hit = Bj >= 0 && sl >= 0;
+      const uint32_t b0 = hit && sl < 32 ? 1u << sl : 0u, b1 = hit && sl >= 32 && sl < 64 ? 1u << (sl - 32) : 0u;
+      const uint32_t b2 = hit && sl >= 64 && sl < 96 ? 1u << (sl - 64) : 0u, b3 = hit && sl >= 96 ? 1u << (sl - 96) : 0u;
+      const unsigned long long m0 = (unsigned long long)__reduce_or_sync(0xffffffffu, b1) << 32 | __reduce_or_sync(0xffffffffu, b0);
+      const unsigned long long m1 = (unsigned long long)__reduce_or_sync(0xffffffffu, b3) << 32 | __reduce_or_sync(0xffffffffu, b2);
+      for (int t = tq0 + lane; t < tq1; t += 32) {
+        umask[(int64_t(t) * c.h_kv + g) * 2] = m0;
+        umask[(int64_t(t) * c.h_kv + g) * 2 + 1] = m1;
+      }
     }
     ++size;
   }
@@ -174,7 +197,7 @@ __global__ void k_vq_fill(Ctx c, int vT, int S, int cmax, const int32_t* __restr
   qrange[2 * v + 1] = e;
   batch_v[v] = c.q_batch[a];
   for (int g = 0; g < c.h_kv; ++g)
-    for (int j = 0; j < vT; ++j) I_u[(int64_t(v) * c.h_kv + g) * vT + j] = un[(int64_t(qa + k) * c.h_kv + g) * 64 + j];
+    for (int j = 0; j < vT; ++j) I_u[(int64_t(v) * c.h_kv + g) * vT + j] = un[(int64_t(qa + k) * c.h_kv + g) * kVqSlots + j];
 }
 
 }  // namespace
@@ -193,23 +216,29 @@ bool vq_enabled() {
   return !(e && atoi(e) == 0);
 }
 
-int vq_slots(int S, int T) { return S * T < 64 ? S * T : 64; }
-// every sub-group but the last of a selection block holds S query blocks or was closed by the 64-slot cap
-// (then it holds > (64 - T) / T, i.e. >= floor(64 / T), query blocks)
-int64_t vq_bound(int n_slc, int n_q, int S, int T) {
-  const int kmin = S < 64 / T ? S : 64 / T;
-  // + one short sub-group per chunk of 2 S query blocks (chunks: at most n_q / (2 S) + n_slc)
+int vq_slots(int S, int T) { return S * T < kVqSlots ? S * T : kVqSlots; }
+// every sub-group but the last of a chunk holds S query blocks or was closed by a cap: by the slot cap it
+// then holds > (128 - T) / T, i.e. >= floor(128 / T), query blocks; by the key cap (each query block adds
+// at most T * max_fill keys) >= floor(kVqKeyCap / (T * max_fill)); one short sub-group per chunk of 2 S
+int vq_kmin(int S, int T, int max_fill_slc) {
+  int k = S < kVqSlots / T ? S : kVqSlots / T;
+  const int kk = kVqKeyCap / (T * (max_fill_slc > 0 ? max_fill_slc : 1));
+  k = k < kk ? k : kk;
+  return k > 1 ? k : 1;
+}
+int64_t vq_bound(int n_slc, int n_q, int S, int T, int max_fill_slc) {
+  const int kmin = vq_kmin(S, T, max_fill_slc);
   return int64_t(n_slc) * 2 + int64_t(n_q) / (2 * S) + (int64_t(n_q) + kmin - 1) / kmin + 1;
 }
 // chunks of 2 S query blocks per selection block (a selection block holds at most max_fill_slc of them,
 // its most-populated one exactly that many tokens); the (selection block, chunk) grid is n_slc x cmax
 static int vq_cmax(int max_fill_slc, int S) { return (max_fill_slc + 2 * S - 1) / (2 * S); }
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc) {
-  const int64_t bound = vq_bound(n_slc, n_q, S, T);
+  const int64_t bound = vq_bound(n_slc, n_q, S, T, max_fill_slc);
   const int64_t chunks = int64_t(n_slc) * vq_cmax(max_fill_slc, S);
   return size_t(chunks + 2) * 4 * 2 + scan_ws_bytes(chunks + 1) + size_t(bound + 2) * 4 * 5 + size_t(n_q + 1) * 4 +
-         size_t(n_q) * h_kv * 64 * 4 +
-         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 8 + 18 * 256;
+         size_t(n_q) * h_kv * kVqSlots * 4 +
+         size_t(bound) * h_kv * vq_slots(S, T) * 4 + size_t(N) * h_kv * 16 + 18 * 256;
 }
 
 // Build the virtual query level (see the header) with sub-groups of at most S query blocks from the per-query-
@@ -219,23 +248,23 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
   const int vT = vq_slots(S, c.T);
   if (S < 2 || c.T > 32) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
-  const int64_t bound = vq_bound(n_slc, n_q, S, c.T);
+  const int64_t bound = vq_bound(n_slc, n_q, S, c.T, c.max_fill[SSA_LEVEL_SLC]);
   Carve cw(ws, vq_ws_bytes(c.N, c.h_kv, n_slc, n_q, S, c.T, c.max_fill[SSA_LEVEL_SLC]));
   const int cmax = vq_cmax(c.max_fill[SSA_LEVEL_SLC], S);
   const int64_t nw = int64_t(n_slc) * cmax;
   int32_t* cnt = cw.take<int32_t>(nw + 1);
   int32_t* start = cw.take<int32_t>(nw + 1);
   int32_t* first = cw.take<int32_t>(n_q + 1);
-  int32_t* un = cw.take<int32_t>(size_t(n_q) * c.h_kv * 64);
+  int32_t* un = cw.take<int32_t>(size_t(n_q) * c.h_kv * kVqSlots);
   void* sws = cw.take<char>(scan_ws_bytes(nw + 1));
   int32_t* off_v = cw.take<int32_t>(bound + 1);
   int32_t* qrange = cw.take<int32_t>(2 * bound + 2);
   int32_t* batch_v = cw.take<int32_t>(bound + 1);
   int32_t* order_v = cw.take<int32_t>(bound + 1);
   int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
-  unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv);
+  unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv * 2);
   if (n_slc > 0) {
-    k_vq_count<<<nb(nw, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * 64 * 4, st>>>(c, S, cmax, cnt, first, un, umask);
+    k_vq_count<<<nb(nw, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * kVqSlots * 4, st>>>(c, S, cmax, cnt, first, un, umask);
     SSA_LAUNCH_CHECK("k_vq_count");
   }
   ssa_status s = exclusive_scan(cnt, start, nw, start + nw, sws, st);

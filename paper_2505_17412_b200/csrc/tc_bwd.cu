@@ -481,7 +481,8 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         Dv[br] = c.Dd[br][row];
       }
       // small query blocks (virtual level): the selection slots this row's query block selected
-      const unsigned long long rmask = (kMask && rvalid) ? c.umask[int64_t(t0 + r / c.h_s) * c.h_kv + g] : ~0ull;
+      const int64_t mi = (int64_t(t0 + (rvalid ? r : 0) / c.h_s) * c.h_kv + g) * 2;
+      const unsigned long long rm0 = (kMask && rvalid) ? c.umask[mi] : ~0ull, rm1 = (kMask && rvalid) ? c.umask[mi + 1] : ~0ull;
       for (int j = 0; j < n_tiles; ++j) {
         const int br = S->tile_br[j];
         const uint32_t mk0 = S->tile_mask[j][0], mk1 = S->tile_mask[j][1], mk2 = S->tile_mask[j][2];
@@ -493,7 +494,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         if (kMask && br == 1)
           for (int q = S->tile_seg[j]; q < S->tile_seg[j + 1]; ++q) {
             const uint32_t slot = S->seg_slot[q];
-            if (slot < 64u && !((rmask >> slot) & 1ull)) {
+            if (slot < 128u && !(((slot < 64u ? rm0 : rm1) >> (slot & 63u)) & 1ull)) {
               const int dst = S->seg_dst_len[q] >> 8, len = S->seg_dst_len[q] & 0xff;
               umk |= ((1u << (len / 8)) - 1u) << (dst / 8);
             }

@@ -988,7 +988,8 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       float lse_slc = 0.f;
       float m = -1e30f, l = 0.f;
       // small query blocks (virtual level): the selection slots this row's query block selected
-      const unsigned long long rmask = (kMask && rvalid) ? c.umask[int64_t(t0 + r / c.h_s) * c.h_kv + g] : ~0ull;
+      const int64_t mi = (int64_t(t0 + (rvalid ? r : 0) / c.h_s) * c.h_kv + g) * 2;
+      const unsigned long long rm0 = (kMask && rvalid) ? c.umask[mi] : ~0ull, rm1 = (kMask && rvalid) ? c.umask[mi + 1] : ~0ull;
       for (int j = 0; j < n_tiles; ++j) {
         const bool fresh = j == 0 || j == n_slc_tiles;
         const bool closed = j == n_slc_tiles && j > 0;
@@ -1066,7 +1067,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 #pragma unroll
           for (int gr = 0; gr < kTile / 8; ++gr) {
             const uint32_t slot = (gw[gr >> 2] >> (8 * (gr & 3))) & 0xffu;
-            if (slot < 64u && !((rmask >> slot) & 1ull)) {
+            if (slot < 128u && !(((slot < 64u ? rm0 : rm1) >> (slot & 63u)) & 1ull)) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[8 * gr + i] = -INFINITY;
             }
