@@ -216,7 +216,8 @@ int pick_chunks(const Plan* p, int h_kv) {
 // query blocks smaller than the selection blocks on the tcgen05 path run the selection / window, dQ and
 // KV-outer kernels on a virtual query level (pertoken.cu): its block count bound and 64 union slots
 // S = query blocks per sub-group (at most): enough for about SSA_VQ_ROWS (default 256: a row-tile pair, so both
-// softmax warpgroups of the selection / dQ kernels work; measured C2 m_q = 1: 3.0 -> 2.0 ms, 3.0 -> 2.15 ms) query rows at
+// softmax warpgroups of the selection / dQ kernels work; measured C2 m_q = 1: 3.0 -> 2.0 ms, 3.0 -> 2.15 ms; 128, 192,
+// 384, 512 rows all slower at C2 and C3) query rows at
 // the plan's mean tokens per query block, at most 32 (k_vq_count also closes a sub-group before its union of
 // selected blocks would exceed 64); 0 = no virtual level (m_q == m_slc, query blocks
 // that fill a tile on their own, or a query-block range / SSA_LOCAL_ROWS, which the virtual level does
