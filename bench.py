@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import math
 import os
 import subprocess
@@ -315,7 +316,7 @@ def main():
             ncu_name = {"tc_cmp_fwd": "k_tc_cmp_fwd", "tc_slc_win_fwd": "k_tc_slcwin_fwd", "tc_bwd_dq": "k_tc_dq",
                         "tc_bwd_kv": "k_tc_dkdv", "tc_bwd_cmp_kv": "k_tc_dkdv#1"}[dom]   # dkdv: raw launch, then cmp
             for kname, val in tj.items():
-                if kname.endswith(ncu_name):
+                if re.sub(r"<[^<>]*>", "", kname).endswith(ncu_name):   # template arguments dropped
                     traffic = {"dram_bytes_per_launch": val, "source": os.path.relpath(tf, ROOT)}
         if xu_ach / xu_peak >= tc_ach / tc_peak:
             roofline = {"kernel": dom, "bound": "alu", "achieved": round(xu_ach, 4), "peak": round(xu_peak, 4),
