@@ -168,24 +168,28 @@ def _identities(inp, r, h_kv):
     return res
 
 
-@pytest.mark.parametrize("config", ["C3", "C4"])
-def test_fullsize_sampled_parity(config):
+@pytest.mark.parametrize("config,m_q", [("C3", None), ("C4", None), ("C2", 1), ("C3", 1)])
+def test_fullsize_sampled_parity(config, m_q):
+    """m_q = 1: the paper's per-token selection (Alg. 1, I in R^{N x h_kv x T}) at full size, in the launch
+    configuration of bench.py's per_token_m_q1 line (virtual query level, packed KV-outer row tiles):
+    sampled tokens' out / dq / dgates / Eq. 8 scores and sampled selection blocks' dk / dv."""
     from ssa_workload import CONFIGS, config_coords, make_inputs
     cfg = CONFIGS[config]
+    m_q = cfg["m_q"] if m_q is None else m_q
     c, grid, batch = config_coords(config)
     inp = make_inputs(c, grid, batch, cfg["H"], cfg["h_kv"], cfg["d"], "bf16", seed=cfg["seed"])
-    kw = dict(h_kv=cfg["h_kv"], T=cfg["T"], m_cmp=cfg["m_cmp"], m_slc=cfg["m_slc"], m_win=cfg["m_win"],
-              m_q=cfg["m_q"])
+    kw = dict(h_kv=cfg["h_kv"], T=cfg["T"], m_cmp=cfg["m_cmp"], m_slc=cfg["m_slc"], m_win=cfg["m_win"], m_q=m_q)
     r = run_gpu(inp, **kw)
     assert r["saved"].used_tcgen05
-    plan_o = O.block_build(c, grid, batch, cfg["m_cmp"], cfg["m_slc"], cfg["m_win"], cfg["m_q"])
+    plan_o = O.block_build(c, grid, batch, cfg["m_cmp"], cfg["m_slc"], cfg["m_win"], m_q)
     assert np.array_equal(plan_o.perm, r["perm"])
     rng = np.random.Generator(np.random.PCG64(17))
-    blocks = _sample_blocks(plan_o, 6 if config == "C3" else 8, rng)
-    test = f"test_fullsize_sampled_parity[{config}]"
+    blocks = _sample_blocks(plan_o, 6 if config == "C3" else 8, rng) if m_q == cfg["m_q"] else \
+        _sample_blocks(plan_o, 24, rng)
+    test = f"test_fullsize_sampled_parity[{config},m_q={m_q}]"
     errs, n_amb = _check_blocks(inp, kw, r, plan_o, blocks, test)
-    items = [0] if config == "C3" else [0, 3]
-    kv_blocks, sel = _sample_kv_blocks(plan_o, r["I"], cfg["h_kv"], items, 8 if config == "C3" else 4, rng)
+    items = [0] if batch == 1 else [0, 3]
+    kv_blocks, sel = _sample_kv_blocks(plan_o, r["I"], cfg["h_kv"], items, 8 if batch == 1 else 4, rng)
     errs.update(_check_kv_blocks(inp, kw, r, plan_o, kv_blocks, test))
     assert all(v <= 2e-2 for v in errs.values()), errs
     ids = _identities(inp, r, cfg["h_kv"])
