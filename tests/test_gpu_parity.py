@@ -212,6 +212,21 @@ def test_tc_head_layouts(heads):
     _check_all(inp, kw, expect_tc=True)
 
 
+@pytest.mark.parametrize("m_q", [1, 2])
+@pytest.mark.parametrize("heads", [(8, 2), (4, 4), (32, 2)])
+def test_tc_small_query_heads(heads, m_q):
+    """Per-token / small query blocks with other head layouts (h_s = 4, 1, 16 rows per token): tokens that
+    are not a multiple of the 8-row granule leave padded slots in the KV-outer packed row tiles (valid
+    counts < 8, TMA boxes reading the next token's rows, masked by an LSE of +inf), and h_s = 1 puts 128
+    tokens in a row tile of the virtual query level — parity and top-k against the oracle."""
+    from ssa_workload import batch_coords, make_inputs, sphere_shell
+    H, h_kv = heads
+    c = batch_coords([sphere_shell(32, 13.0, 2.0)])
+    inp = make_inputs(c, (32, 32, 32), 1, H, h_kv, 64, "bf16", seed=31)
+    kw = dict(h_kv=h_kv, T=4, m_cmp=4, m_slc=8, m_win=8, m_q=m_q)
+    _check_all(inp, kw, expect_tc=True, test=f"test_tc_small_query_heads[{H},{h_kv},{m_q}]")
+
+
 @pytest.mark.parametrize("T", [4, 32])
 def test_tc_dense_blocks(T):
     """Solid ball (5 616 tokens): a full 8^3 selection block of 512 keys (4 tiles) among blocks of 47-416
