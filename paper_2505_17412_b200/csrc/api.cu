@@ -227,6 +227,12 @@ double env_or(const char* name, double dflt) {
   const double x = e ? atof(e) : 0.0;
   return x > 0.0 ? x : dflt;
 }
+// per-token selection (m_q = 1) on the virtual level: the selection branch as a per-block pass + merge
+// (pertoken.cu) instead of the union-masked tiles; not with the window-only / no-window flags
+bool use_blk(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg, int vq_S) {
+  return vq_S > 0 && p->info.m[SSA_LEVEL_Q] == 1 && blk_enabled() &&
+         !(cfg->flags & (SSA_WINDOW_ONLY | SSA_NO_WINDOW)) && d.h_kv >= 1;
+}
 double q_rows(const Dims& d) { return d.n_q > 0 ? double(d.N) / d.n_q * (d.H / d.h_kv) : 0.0; }
 int vq_group(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg) {
   if (p->info.m[SSA_LEVEL_Q] >= p->info.m[SSA_LEVEL_SLC] || !vq_enabled() || d.n_q <= 0 || d.T > 32 || d.h_kv > 8)
@@ -366,6 +372,7 @@ extern "C" ssa_status ssa_forward_size(ssa_plan plan, const ssa_attn_cfg* cfg, s
   fill_common(&x, p, d, cfg);
   *ws_bytes = cw.used + tc_fwd_ws_bytes(d.N, d.H, d.h_kv, d.D) + learned_fwd_ws_bytes(x) + size_t(d.n_slc + 64) * 4 +
               (vq_group(p, d, cfg) ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq_group(p, d, cfg), d.T, p->info.max_fill[SSA_LEVEL_SLC]) : 0) +
+              (use_blk(p, d, cfg, vq_group(p, d, cfg)) ? blk_ws_bytes(d.N, d.h_kv, d.h_s, d.D, d.n_slc, d.n_q, d.T) + 256 : 0) +
               tok_cmp_ws_bytes(d.n_q, p->info.batch, tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s), d.max_slc_b) + 2048;
   return SSA_OK;
 }
@@ -404,6 +411,7 @@ extern "C" ssa_status ssa_forward(ssa_plan plan, const ssa_attn_cfg* cfg, const 
   x.fetch_mark = cw.take<int32_t>(size_t(d.n_slc) + 1);
   x.vq_S = tc ? vq_group(p, d, cfg) : 0;
   x.vq_ws = x.vq_S ? cw.take<char>(vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, x.vq_S, d.T, p->info.max_fill[SSA_LEVEL_SLC])) : nullptr;
+  x.blk_ws = use_blk(p, d, cfg, x.vq_S) ? cw.take<char>(blk_ws_bytes(d.N, d.h_kv, d.h_s, d.D, d.n_slc, d.n_q, d.T)) : nullptr;
   x.tok_cmp = tc ? tok_cmp_hs(p->info.m[SSA_LEVEL_Q], d.h_s) : 0;
   x.tok_ws = x.tok_cmp ? cw.take<char>(tok_cmp_ws_bytes(d.n_q, p->info.batch, x.tok_cmp, d.max_slc_b)) : nullptr;
   if (lgates) x.gs = saved_gates;

@@ -55,6 +55,7 @@ struct Ctx {
   int64_t row_base;               // SSA_LOCAL_ROWS: first row held by the caller's row tensors (else 0)
   int32_t save_scores;
   int32_t kv_grad_f32;            // dk / dv written as fp32 (SSA_KV_GRAD_FP32)
+  int32_t sel_partial;            // per-block selection pass (pertoken.cu): epilogue writes only O (o[1]) and LSE
   // plan (device)
   const int32_t *perm, *inv_perm, *sorted_coords;
   const int32_t *off[kLevels], *tok_block[kLevels], *bb[kLevels];
@@ -84,6 +85,7 @@ struct Ctx {
   int32_t tok_T;
   const int32_t* tok_qb;            // token -> query block
   void* vq_ws;                      // scratch of the virtual level (forward), null when it is not used
+  void* blk_ws;                     // scratch of the per-block selection pass (forward, m_q = 1), or null
   int32_t vq_S;                     // its sub-group size in query blocks
   // per-token compression (m_q = 1, tc_fwd.cu k_tc_cmp_fwd<h_s>): tok_cmp = h_s when used, else 0
   int32_t tok_cmp;
@@ -139,6 +141,18 @@ constexpr int kVqKeyCap = 28672;
 int64_t vq_bound(int n_slc, int n_q, int S, int T, int max_fill_slc);
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc);
 ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
+// pertoken.cu: per-block selection pass of per-token selection (m_q = 1)
+struct BlkPass {
+  int32_t *off_e, *I_e, *order_e, *off_slc, *inv_off, *inv_list;
+  __nv_bfloat16* q_exp;
+  float *o_exp, *lse_exp;
+  int64_t bound, n_exp;
+};
+bool blk_enabled();
+size_t blk_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T);
+ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b);
+Ctx blk_context(const Ctx& c, const BlkPass& b);
+ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);
 size_t gate_bwd_ws_bytes(int64_t N, int H, int C);

@@ -288,4 +288,216 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   return SSA_OK;
 }
 
+
+// ================================================================================================
+// Per-block selection pass for per-token selection (m_q = 1). The union-based virtual level makes a row
+// attend to its sub-group's union of selected blocks (masked), which with diverse per-token selections is
+// many times the T blocks the row needs. This pass instead attends every (token, selected block) pair
+// exactly once: for every (selection block B, kv group g), the tokens that selected B (the inverse
+// selection CSR, ascending) are laid out contiguously in an "expanded" token space e, their q rows
+// gathered into Q_exp [e][h_s][D]; the selection/window kernel runs on it with the single key block B per
+// virtual query block of <= 32 expanded tokens (no window, epilogue = O and LSE only), and a merge
+// combines each row's T partial results by their LSEs (log2 domain):
+//   LSE = log2 sum_j 2^{LSE_j},  O_slc = sum_j 2^{LSE_j - LSE} O_j
+// which is the softmax over the union of the T blocks' keys (Alg. 1's per-token selection attention).
+// ================================================================================================
+namespace {
+
+constexpr int kBlkChunk = 32;   // expanded tokens per virtual query block (h_s = 8: a row-tile pair)
+
+__device__ __forceinline__ int key_of(const int32_t* __restrict__ inv_off, int nkeys, int64_t e) {
+  int lo = 0, hi = nkeys;         // largest key with inv_off[key] <= e
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (inv_off[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_blk_count(Ctx c, int32_t* __restrict__ cnt) {
+  const int key = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  if (key >= nkeys) return;
+  const int len = c.inv_off[key + 1] - c.inv_off[key];
+  cnt[key] = (len + kBlkChunk - 1) / kBlkChunk;
+}
+
+// virtual query block v: expanded tokens [off_e[v], off_e[v + 1]) of key (B, g), its one block B' = g n_slc + B
+__global__ void k_blk_fill(Ctx c, const int32_t* __restrict__ start, int32_t* __restrict__ off_e, int32_t* __restrict__ I_e,
+                           int32_t* __restrict__ order_e, int bound) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > bound) return;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  const int total = start[nkeys], n_e = c.inv_off[nkeys];
+  if (v < bound) order_e[v] = v;
+  if (v >= total) {
+    off_e[v] = n_e;
+    if (v < bound) I_e[v] = -1;
+    return;
+  }
+  int lo = 0, hi = nkeys;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (start[mid] <= v) lo = mid; else hi = mid;
+  }
+  const int key = lo, B = key / c.h_kv, g = key % c.h_kv;
+  off_e[v] = c.inv_off[key] + (v - start[key]) * kBlkChunk;
+  I_e[v] = g * c.n_blk[SSA_LEVEL_SLC] + B;
+}
+
+// selection-level offsets of the expanded context: block B' = g n_slc + B covers key rows g N + [C_B, C_B+1)
+__global__ void k_blk_slc_off(Ctx c, int32_t* __restrict__ off) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC];
+  if (j > n_slc * c.h_kv) return;
+  off[j] = j == n_slc * c.h_kv ? c.h_kv * c.N : (j / n_slc) * c.N + c.off[SSA_LEVEL_SLC][j % n_slc];
+}
+
+// Q_exp[e] = the h_s q rows (internal layout) of token inv_list[e] in the kv group of e's key; one warp per e
+__global__ void k_blk_gather(Ctx c, __nv_bfloat16* __restrict__ q_exp) {
+  const int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  if (e >= c.inv_off[nkeys]) return;
+  const int key = key_of(c.inv_off, nkeys, e), g = key % c.h_kv;
+  const int t = c.off[SSA_LEVEL_Q][c.inv_list[e]];   // m_q = 1: the query block's one token
+  const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.qs) + (int64_t(g) * c.N + t) * c.h_s * c.D);
+  uint4* dst = reinterpret_cast<uint4*>(q_exp + e * c.h_s * c.D);
+  for (int i = lane; i < c.h_s * c.D / 8; i += 32) dst[i] = src[i];
+}
+
+// per row (token t, group g, head s): combine the T partial results of its selected blocks (one warp per (t, g))
+__global__ void k_blk_merge(Ctx c, const float* __restrict__ o_exp, const float* __restrict__ lse_exp) {
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= int64_t(c.N) * c.h_kv) return;
+  const int t = int(w / c.h_kv), g = int(w % c.h_kv);
+  const int Q = c.tok_block[SSA_LEVEL_Q][t];
+  // lane j < T: the expanded index of (t, j-th selected block), or -1
+  int64_t ej = -1;
+  if (lane < c.T) {
+    const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + lane];
+    if (B >= 0) {
+      const int key = B * c.h_kv + g;
+      int lo = c.inv_off[key], hi = c.inv_off[key + 1];   // ascending query blocks: binary search for Q
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c.inv_list[mid] < Q) lo = mid + 1; else hi = mid;
+      }
+      ej = lo;
+    }
+  }
+  const int64_t row0 = (int64_t(g) * c.N + t) * c.h_s;
+  float* O = static_cast<float*>(c.o[1]);
+  for (int idx = lane * 4; idx < c.h_s * c.D; idx += 128) {
+    const int s = idx / c.D, col = idx % c.D;
+    float M = -INFINITY;
+    for (int j = 0; j < c.T; ++j) {
+      const int64_t e = __shfl_sync(0xffffffffu, ej, j);
+      if (e >= 0) M = fmaxf(M, lse_exp[e * c.h_s + s]);
+    }
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < c.T; ++j) {
+      const int64_t e = __shfl_sync(0xffffffffu, ej, j);
+      if (e < 0) continue;
+      const float wgt = exp2f(lse_exp[e * c.h_s + s] - M);
+      const float4 o = *reinterpret_cast<const float4*>(o_exp + (e * c.h_s + s) * c.D + col);
+      L += wgt;
+      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    *reinterpret_cast<float4*>(O + (row0 + s) * c.D + col) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (col == 0) c.lse[1][row0 + s] = L > 0.f ? M + log2f(L) : __int_as_float(0x7f7f7f7f);
+  }
+}
+
+}  // namespace
+
+bool blk_enabled() {
+  const char* e = getenv("SSA_VQ_BLOCKSEL");
+  return !(e && atoi(e) == 0);
+}
+static int64_t blk_bound(int n_slc, int h_kv, int64_t n_exp) { return int64_t(n_slc) * h_kv + n_exp / kBlkChunk + 1; }
+size_t blk_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T) {
+  const int64_t n_exp = int64_t(n_q) * h_kv * T, nkeys = int64_t(n_slc) * h_kv, bound = blk_bound(n_slc, h_kv, n_exp);
+  (void)N;
+  return inverse_csr_ws_bytes(n_slc, h_kv, n_q) + size_t(nkeys + 2) * 4 * 3 + size_t(n_exp + 1) * 4 +
+         scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 3 + size_t(nkeys + 2) * 4 +
+         size_t(n_exp) * h_s * D * 2 + size_t(n_exp) * h_s * D * 4 + size_t(n_exp) * h_s * 4 + 16 * 256;
+}
+
+ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b) {
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
+  const int64_t n_exp = int64_t(n_q) * c.h_kv * c.T, nkeys = int64_t(n_slc) * c.h_kv;
+  const int64_t bound = blk_bound(n_slc, c.h_kv, n_exp);
+  Carve cw(ws, blk_ws_bytes(c.N, c.h_kv, c.h_s, c.D, n_slc, n_q, c.T));
+  void* inv_ws = cw.take<char>(inverse_csr_ws_bytes(n_slc, c.h_kv, n_q));
+  Ctx ci = c;
+  ci.inv_off = cw.take<int32_t>(nkeys + 2);
+  ci.inv_list = cw.take<int32_t>(n_exp + 1);
+  int32_t* cnt = cw.take<int32_t>(nkeys + 2);
+  int32_t* start = cw.take<int32_t>(nkeys + 2);
+  void* sws = cw.take<char>(scan_ws_bytes(nkeys + 1));
+  b->off_e = cw.take<int32_t>(bound + 2);
+  b->I_e = cw.take<int32_t>(bound + 2);
+  b->order_e = cw.take<int32_t>(bound + 2);
+  b->off_slc = cw.take<int32_t>(nkeys + 2);
+  b->q_exp = cw.take<__nv_bfloat16>(size_t(n_exp) * c.h_s * c.D);
+  b->o_exp = cw.take<float>(size_t(n_exp) * c.h_s * c.D);
+  b->lse_exp = cw.take<float>(size_t(n_exp) * c.h_s);
+  if (!cw.ok()) { set_error("per-block selection: workspace carve"); return SSA_ERR_WORKSPACE; }
+  b->bound = bound;
+  b->n_exp = n_exp;
+  b->inv_off = ci.inv_off;
+  b->inv_list = ci.inv_list;
+  ssa_status s = build_inverse_csr(ci, inv_ws, st);
+  if (s != SSA_OK) return s;
+  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(ci, cnt);
+  SSA_LAUNCH_CHECK("k_blk_count");
+  if ((s = exclusive_scan(cnt, start, nkeys, start + nkeys, sws, st)) != SSA_OK) return s;
+  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(ci, start, b->off_e, b->I_e, b->order_e, int(bound));
+  SSA_LAUNCH_CHECK("k_blk_fill");
+  k_blk_slc_off<<<nb(nkeys + 1, 256), 256, 0, st>>>(ci, b->off_slc);
+  SSA_LAUNCH_CHECK("k_blk_slc_off");
+  k_blk_gather<<<nb(n_exp * 32, 256), 256, 0, st>>>(ci, b->q_exp);
+  SSA_LAUNCH_CHECK("k_blk_gather");
+  return SSA_OK;
+}
+
+// the expanded context the selection kernel runs on (h_kv = 1 view: blocks B' = g n_slc + B over all
+// groups' key rows; no window; epilogue O / LSE only)
+Ctx blk_context(const Ctx& c, const BlkPass& b) {
+  Ctx e = c;
+  e.h_kv = 1;
+  e.N = int32_t(b.n_exp);
+  e.T = 1;
+  e.n_blk[SSA_LEVEL_Q] = int32_t(b.bound);
+  e.n_blk[SSA_LEVEL_SLC] = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  e.off[SSA_LEVEL_Q] = b.off_e;
+  e.off[SSA_LEVEL_SLC] = b.off_slc;
+  e.I = b.I_e;
+  e.q_order = b.order_e;
+  e.q_begin = 0;
+  e.q_end = int32_t(b.bound);
+  e.no_win = 1;
+  e.accumulate = 0;
+  e.sel_partial = 1;
+  e.umask = nullptr;
+  e.o[1] = b.o_exp;
+  e.lse[1] = b.lse_exp;
+  e.qs = b.q_exp;
+  return e;
+}
+
+ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st) {
+  Ctx ci = c;
+  ci.inv_off = b.inv_off;
+  ci.inv_list = b.inv_list;
+  const int64_t warps = int64_t(c.N) * c.h_kv;
+  k_blk_merge<<<nb(warps * 32, 256), 256, 0, st>>>(ci, b.o_exp, b.lse_exp);
+  SSA_LAUNCH_CHECK("k_blk_merge");
+  return SSA_OK;
+}
+
 }  // namespace ssa

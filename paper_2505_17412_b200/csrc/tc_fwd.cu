@@ -979,7 +979,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       const int64_t row = qrow0 + (rvalid ? r : 0);
       const int wrow0 = rt * kTile + (warp & 3) * 32;   // first row of this warp
       float* wbuf = reinterpret_cast<float*>(sEpi + wg * (kEpiBytes / 2) + (warp & 3) * (kEpiBytes / 8));
-      if (wrow0 + lane < rows) {
+      if (wrow0 + lane < rows && !c.sel_partial) {
         // pull this warp's O_cmp rows (HBM) and gates toward L2 now; the epilogue reads them a pair later
         const char* pc = reinterpret_cast<const char*>(static_cast<const float*>(c.o[0]) + (qrow0 + wrow0 + lane) * int64_t(kD));
         asm volatile("prefetch.global.L2 [%0];\n\tprefetch.global.L2 [%1];" :: "l"(pc), "l"(pc + 128));
@@ -1144,6 +1144,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         const float4 sl = c.no_win ? wn : sl_in;
         const float w0 = w3[0], w1 = w3[1], w2 = c.no_win ? 0.f : w3[2];
         *reinterpret_cast<float4*>(ow + grow * kD + col) = wn;
+        if (c.sel_partial) return;           // per-block selection pass: O and LSE only
         if (col >= c.Dc) return;             // zero-padded head dims (d = 32) are not output
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + rr % c.h_s) * c.Dc + col;
         float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
@@ -1165,6 +1166,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         float h_w[4][3];
         int h_dst[4];
         auto epi_load_h = [&](int hf, int bt) {
+          if (c.sel_partial) return;
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
             const int rl = 4 * (bt * 4 + ii) + (lane >> 3), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
@@ -1226,6 +1228,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         float e_w[8][3];
         int e_dst[8];
         auto epi_load = [&](int bt) {
+          if (c.sel_partial) return;
 #pragma unroll
           for (int ii = 0; ii < 8; ++ii) {
             const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
@@ -1434,11 +1437,27 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
     static_assert(1024 + 32768 + kStages * 32768 + kEpiBytes + sizeof(SwSmem) <= 232448, "selection/window shared memory");
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ProfScope ps("tc_slc_win_fwd", st);
     TmapSet4 tk, tv;
     for (int b = 0; b < 4; ++b)
       if (!make_tmap_bf16_2d(&tk.m[b], c.ks, krows, 64u >> b) || !make_tmap_bf16_2d(&tv.m[b], vs16, krows, 64u >> b))
         return SSA_ERR_CUDA;
+    if (c.blk_ws) {
+      // per-token selection: every (token, selected block) pair once (pertoken.cu), partial O / LSE merged
+      // into O_slc / LSE_slc; the virtual level then runs the window branch + gated sum alone
+      ProfScope pb("tc_slc_blk_fwd", st);
+      BlkPass bp;
+      ssa_status s = blk_build(c, c.blk_ws, st, &bp);
+      if (s != SSA_OK) return s;
+      const Ctx ce = blk_context(c, bp);
+      CUtensorMap tmQe;
+      if (!make_tmap_bf16_2d(&tmQe, bp.q_exp, uint64_t(bp.n_exp) * c.h_s, kTile)) return SSA_ERR_CUDA;
+      k_tc_slcwin_fwd<false><<<dim3(unsigned(bp.bound), 1), kSwThreads, smem, st>>>(ce, tmQe, tk, tv);
+      SSA_LAUNCH_CHECK("k_tc_slcwin_fwd(blocks)");
+      if ((s = blk_merge(c, bp, st)) != SSA_OK) return s;
+      SSA_CUDA_TRY(cudaMemsetAsync(cv.I, 0xff, size_t(cv.n_blk[SSA_LEVEL_Q]) * cv.h_kv * cv.T * 4, st));   // no selections
+      cv.umask = nullptr;
+    }
+    ProfScope ps("tc_slc_win_fwd", st);
     if (cv.umask) k_tc_slcwin_fwd<true><<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(cv, tmQ, tk, tv);
     else k_tc_slcwin_fwd<false><<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(cv, tmQ, tk, tv);
     SSA_LAUNCH_CHECK("k_tc_slcwin_fwd");
