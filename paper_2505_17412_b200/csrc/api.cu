@@ -470,7 +470,9 @@ extern "C" ssa_status ssa_backward_size(ssa_plan plan, const ssa_attn_cfg* cfg, 
   const VqBwd vq = vq_backward(p, d, cfg, use_tc_bwd(d, cfg, p));
   carve_inputs(cw, d, &x, true);
   carve_bwd(cw, vq.dkv, p, &x);
-  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q) + (vq.S ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T, p->info.max_fill[SSA_LEVEL_SLC]) : 0);
+  size_t scan = inverse_csr_ws_bytes(d.n_slc, d.h_kv, vq.dkv.n_q) + (vq.S ? vq_ws_bytes(d.N, d.h_kv, d.n_slc, d.n_q, vq.S, d.T, p->info.max_fill[SSA_LEVEL_SLC]) : 0) +
+                (vq.S && use_blk(p, d, cfg, vq.S) && use_tc_bwd(d, cfg, p) && !vq.kv
+                     ? blk_bwd_ws_bytes(d.N, d.h_kv, d.h_s, d.D, d.n_slc, d.n_q, d.T) + 256 : 0);
   if (cfg->learned && cfg->learned->x) scan += gate_bwd_ws_bytes(d.N, d.H, cfg->learned->c);
   if (cfg->learned && cfg->learned->conv_k_w) scan += conv_bwd_ws_bytes(d.N, d.h_kv, p->info.m[SSA_LEVEL_CMP], d.n_cmp, d.D);
   *ws_bytes = cw.used + scan + tc_bwd_ws_bytes(d.N, d.H, d.h_kv, d.D, d.n_slc, vq.dkv.n_q, vq.dkv.T,
@@ -533,6 +535,8 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   // the tcgen05 backward gathers the q / dO rows and computes D_c, dgates in its own row prologue
   if ((s = gather_inputs(x, bf16, st, true, /*rows=*/!tc, true, /*gates=*/!lgates)) != SSA_OK) return s;
   if (!tc && (s = bwd_prologue(x, bf16, st)) != SSA_OK) return s;
+  x.blk_ws = (vq.S && use_blk(p, d, cfg, vq.S) && tc && !vq.kv)
+                 ? cw.take<char>(blk_bwd_ws_bytes(d.N, d.h_kv, d.h_s, d.D, d.n_slc, d.n_q, d.T)) : nullptr;
   Ctx xq = x;                                      // the dQ context (virtual level for small m_q)
   if (vq.S && (s = build_virtual_level(x, vq.S, vq_ws, st, &xq)) != SSA_OK) return s;
   Ctx& xk = vq.kv ? xq : x;                        // the KV-outer context

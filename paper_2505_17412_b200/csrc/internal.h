@@ -56,6 +56,9 @@ struct Ctx {
   int32_t save_scores;
   int32_t kv_grad_f32;            // dk / dv written as fp32 (SSA_KV_GRAD_FP32)
   int32_t sel_partial;            // per-block selection pass (pertoken.cu): epilogue writes only O (o[1]) and LSE
+                                  // (forward), fp32 dQ partials to dq_part (k_tc_dq), no compressed keys
+  float* dq_part;                 // [expanded rows][D] fp32 dQ partials of the per-block pass (sel_partial)
+  const float* dq_extra;          // [rows][D] fp32 added to dq before its bf16 store (per-block selection dQ)
   // plan (device)
   const int32_t *perm, *inv_perm, *sorted_coords;
   const int32_t *off[kLevels], *tok_block[kLevels], *bb[kLevels];
@@ -147,12 +150,19 @@ struct BlkPass {
   __nv_bfloat16* q_exp;
   float *o_exp, *lse_exp;
   int64_t bound, n_exp;
+  int32_t* batch_e;               // zeros (the expanded context has no compressed keys)
+  float* dq_part;                 // backward: fp32 dQ partials per expanded row
 };
 bool blk_enabled();
 size_t blk_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T);
 ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b);
 Ctx blk_context(const Ctx& c, const BlkPass& b);
 ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st);
+// backward (tc_bwd.cu): the selection branch's dQ per block; c = the real-level context with the inverse CSR
+size_t blk_bwd_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T);
+ssa_status blk_bwd_build(const Ctx& c, const __half* q16, const __half* do16, void* ws, cudaStream_t st, BlkPass* b,
+                         Ctx* e, float** dq_extra);
+ssa_status blk_bwd_merge(const Ctx& c, const BlkPass& b, float* dq_extra, cudaStream_t st);
 // learned.cu
 size_t learned_fwd_ws_bytes(const Ctx& c);
 size_t gate_bwd_ws_bytes(int64_t N, int H, int C);

@@ -500,4 +500,152 @@ ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st) {
   return SSA_OK;
 }
 
+
+// ---- backward: the selection branch's dQ per block ----------------------------------------------
+namespace {
+// expanded row operands: fp16 q / dO rows of token inv_list[e] in e's kv group, its selection-branch row
+// stats (LSE, D) and gates; one warp per e
+__global__ void k_blk_gather_bwd(Ctx c, const __half* __restrict__ q16, const __half* __restrict__ do16,
+                                 __half* __restrict__ q_e, __half* __restrict__ do_e, float* __restrict__ lse_e,
+                                 float* __restrict__ D_e, float* __restrict__ gs_e) {
+  const int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  if (e >= c.inv_off[nkeys]) return;
+  const int key = key_of(c.inv_off, nkeys, e), g = key % c.h_kv;
+  const int t = c.off[SSA_LEVEL_Q][c.inv_list[e]];
+  const int64_t r0 = (int64_t(g) * c.N + t) * c.h_s;
+  const uint4* sq = reinterpret_cast<const uint4*>(q16 + r0 * c.D);
+  const uint4* sd = reinterpret_cast<const uint4*>(do16 + r0 * c.D);
+  uint4* dq_ = reinterpret_cast<uint4*>(q_e + e * c.h_s * c.D);
+  uint4* dd_ = reinterpret_cast<uint4*>(do_e + e * c.h_s * c.D);
+  for (int i = lane; i < c.h_s * c.D / 8; i += 32) {
+    dq_[i] = sq[i];
+    dd_[i] = sd[i];
+  }
+  for (int s = lane; s < c.h_s; s += 32) {
+    lse_e[e * c.h_s + s] = c.lse[1][r0 + s];
+    D_e[e * c.h_s + s] = c.Dd[1][r0 + s];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gs_e[(e * c.h_s + s) * 3 + k] = c.gs[(r0 + s) * 3 + k];
+  }
+}
+// dq_extra of row (t, g, s) = sum over its selected blocks j (slot order) of the per-block partials
+__global__ void k_blk_merge_bwd(Ctx c, const float* __restrict__ dq_part, float* __restrict__ dq_extra) {
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= int64_t(c.N) * c.h_kv) return;
+  const int t = int(w / c.h_kv), g = int(w % c.h_kv);
+  const int Q = c.tok_block[SSA_LEVEL_Q][t];
+  int64_t ej = -1;
+  if (lane < c.T) {
+    const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + lane];
+    if (B >= 0) {
+      const int key = B * c.h_kv + g;
+      int lo = c.inv_off[key], hi = c.inv_off[key + 1];
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c.inv_list[mid] < Q) lo = mid + 1; else hi = mid;
+      }
+      ej = lo;
+    }
+  }
+  const int64_t row0 = (int64_t(g) * c.N + t) * c.h_s;
+  for (int idx = lane * 4; idx < c.h_s * c.D; idx += 128) {
+    const int s = idx / c.D, col = idx % c.D;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < c.T; ++j) {
+      const int64_t e = __shfl_sync(0xffffffffu, ej, j);
+      if (e < 0) continue;
+      const float4 x = *reinterpret_cast<const float4*>(dq_part + (e * c.h_s + s) * c.D + col);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    *reinterpret_cast<float4*>(dq_extra + (row0 + s) * c.D + col) = acc;
+  }
+}
+}  // namespace
+
+size_t blk_bwd_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T) {
+  const int64_t n_exp = int64_t(n_q) * h_kv * T, nkeys = int64_t(n_slc) * h_kv, bound = blk_bound(n_slc, h_kv, n_exp);
+  const int64_t re = n_exp * h_s;
+  return size_t(nkeys + 2) * 4 * 3 + scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 4 +
+         size_t(re) * D * 2 * 2 + size_t(re) * 4 * 5 + size_t(re) * D * 4 + size_t(N) * h_kv * h_s * D * 4 + 20 * 256;
+}
+
+ssa_status blk_bwd_build(const Ctx& c, const __half* q16, const __half* do16, void* ws, cudaStream_t st, BlkPass* b,
+                         Ctx* e, float** dq_extra) {
+  const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
+  const int64_t n_exp = int64_t(n_q) * c.h_kv * c.T, nkeys = int64_t(n_slc) * c.h_kv;
+  const int64_t bound = blk_bound(n_slc, c.h_kv, n_exp), re = n_exp * c.h_s;
+  Carve cw(ws, blk_bwd_ws_bytes(c.N, c.h_kv, c.h_s, c.D, n_slc, n_q, c.T));
+  int32_t* cnt = cw.take<int32_t>(nkeys + 2);
+  int32_t* start = cw.take<int32_t>(nkeys + 2);
+  void* sws = cw.take<char>(scan_ws_bytes(nkeys + 1));
+  b->off_e = cw.take<int32_t>(bound + 2);
+  b->I_e = cw.take<int32_t>(bound + 2);
+  b->order_e = cw.take<int32_t>(bound + 2);
+  b->batch_e = cw.take<int32_t>(bound + 2);
+  b->off_slc = cw.take<int32_t>(nkeys + 2);
+  __half* q_e = cw.take<__half>(size_t(re) * c.D);
+  __half* do_e = cw.take<__half>(size_t(re) * c.D);
+  float* lse_e = cw.take<float>(re);
+  float* D_e = cw.take<float>(re);
+  float* gs_e = cw.take<float>(size_t(re) * 3);
+  float* dq_part = cw.take<float>(size_t(re) * c.D);
+  *dq_extra = cw.take<float>(size_t(c.N) * c.h_kv * c.h_s * c.D);
+  if (!cw.ok()) { set_error("per-block selection dQ: workspace carve"); return SSA_ERR_WORKSPACE; }
+  b->bound = bound;
+  b->n_exp = n_exp;
+  b->inv_off = c.inv_off;
+  b->inv_list = c.inv_list;
+  b->q_exp = nullptr;
+  b->o_exp = nullptr;
+  b->lse_exp = lse_e;
+  b->dq_part = dq_part;
+  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(c, cnt);
+  SSA_LAUNCH_CHECK("k_blk_count");
+  ssa_status s = exclusive_scan(cnt, start, nkeys, start + nkeys, sws, st);
+  if (s != SSA_OK) return s;
+  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, start, b->off_e, b->I_e, b->order_e, int(bound));
+  SSA_LAUNCH_CHECK("k_blk_fill");
+  k_blk_slc_off<<<nb(nkeys + 1, 256), 256, 0, st>>>(c, b->off_slc);
+  SSA_LAUNCH_CHECK("k_blk_slc_off");
+  SSA_CUDA_TRY(cudaMemsetAsync(b->batch_e, 0, size_t(bound + 2) * 4, st));
+  k_blk_gather_bwd<<<nb(n_exp * 32, 256), 256, 0, st>>>(c, q16, do16, q_e, do_e, lse_e, D_e, gs_e);
+  SSA_LAUNCH_CHECK("k_blk_gather_bwd");
+  Ctx x = c;
+  x.h_kv = 1;
+  x.N = int32_t(n_exp);
+  x.T = 1;
+  x.n_blk[SSA_LEVEL_Q] = int32_t(bound);
+  x.n_blk[SSA_LEVEL_SLC] = n_slc * c.h_kv;
+  x.off[SSA_LEVEL_Q] = b->off_e;
+  x.off[SSA_LEVEL_SLC] = b->off_slc;
+  x.I = b->I_e;
+  x.q_order = b->order_e;
+  x.q_batch = b->batch_e;
+  x.q_begin = 0;
+  x.q_end = int32_t(bound);
+  x.no_win = 1;
+  x.win_only = 0;
+  x.accumulate = 0;
+  x.sel_partial = 1;
+  x.umask = nullptr;
+  x.dq_extra = nullptr;
+  x.dq_part = dq_part;
+  for (int br = 0; br < 3; ++br) { x.lse[br] = lse_e; x.Dd[br] = D_e; }
+  x.gs = gs_e;
+  x.qs = q_e;        // (the tensor maps of the expanded rows are built from these two)
+  x.dos = do_e;
+  *e = x;
+  return SSA_OK;
+}
+
+ssa_status blk_bwd_merge(const Ctx& c, const BlkPass& b, float* dq_extra, cudaStream_t st) {
+  const int64_t warps = int64_t(c.N) * c.h_kv;
+  k_blk_merge_bwd<<<nb(warps * 32, 256), 256, 0, st>>>(c, b.dq_part, dq_extra);
+  SSA_LAUNCH_CHECK("k_blk_merge_bwd");
+  return SSA_OK;
+}
+
 }  // namespace ssa

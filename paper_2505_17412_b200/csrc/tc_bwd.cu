@@ -274,7 +274,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
         if (hi > lo) mk[w] |= (hi - lo == 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << (lo - 32 * w);
       }
     };
-    for (int x = c0; x < c1 && n < kMaxKT && !c.win_only; x += kKT) {   // (window-only: no compressed keys)
+    for (int x = c0; x < c1 && n < kMaxKT && !c.win_only && !c.sel_partial; x += kKT) {   // (window-only / per-block pass: no compressed keys)
       mk[0] = mk[1] = mk[2] = 0u;
       set_bits(0, min(kKT, c1 - x));
       S->tile_row[n] = g * ncmp + x;
@@ -571,9 +571,16 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&S->dq_empty[wg]);
-      if (rvalid) {
+      if (rvalid && c.sel_partial) {   // per-block selection pass: fp32 partial of this (token, block) row
+        const float osc = c.scale * do_pow2(c.do_amax, true);
+        float* o = c.dq_part + (int64_t(qrow0) + r) * kD;
+#pragma unroll
+        for (int e = 0; e < kD; e += 4)
+          *reinterpret_cast<float4*>(o + e) = make_float4(v[e] * osc, v[e + 1] * osc, v[e + 2] * osc, v[e + 3] * osc);
+      } else if (rvalid) {
         const float osc = c.scale * do_pow2(c.do_amax, true);
         const int tok = t0 + r / c.h_s, hs = r % c.h_s;
+        const float* xtra = c.dq_extra ? c.dq_extra + (int64_t(qrow0) + r) * kD : nullptr;
         const int dst = c.sorted_input ? tok : c.perm[tok];
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.dq) + (int64_t(dst) * c.H + g * c.h_s + hs) * c.Dc;
 #pragma unroll
@@ -581,7 +588,7 @@ k_tc_dq(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const 
           if (e >= c.Dc) break;                  // zero-padded head dims are not output
           float y[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) y[u] = v[e + u] * osc;
+          for (int u = 0; u < 8; ++u) y[u] = v[e + u] * osc + (xtra ? xtra[e + u] : 0.f);
           if (c.accumulate) {   // SSA_ACCUMULATE: add to the caller's dq
             const uint4 old = *reinterpret_cast<const uint4*>(o + e);
             const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
@@ -1418,6 +1425,27 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
     static_assert(1024 + 65536 + kStages * 2 * kKVBytes + 65536 + sizeof(DqSmem) <= 232448, "dQ shared memory");
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_dq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (c.blk_ws) {
+      // per-token selection (pertoken.cu): the selection branch's dQ per (token, selected block) pair on the
+      // expanded rows (ck: the real level, whose inverse CSR lists the tokens selecting every block), summed
+      // per row into dq_extra; the virtual level then runs the compressed keys + window and adds it
+      ProfScope pb("tc_bwd_blk_dq", st);
+      BlkPass bb;
+      Ctx ce;
+      float* dqx = nullptr;
+      ssa_status s = blk_bwd_build(ck, q16, do16, c.blk_ws, st, &bb, &ce, &dqx);
+      if (s != SSA_OK) return s;
+      ce.do_amax = amax;
+      const uint64_t erows = uint64_t(bb.n_exp) * c.h_s;
+      CUtensorMap tmQe, tmDOe;
+      if (!make_tmap_bf16_2d(&tmQe, ce.qs, erows, 128) || !make_tmap_bf16_2d(&tmDOe, ce.dos, erows, 128)) return SSA_ERR_CUDA;
+      k_tc_dq<false><<<dim3(unsigned(bb.bound), 1), kDqThreads, smem, st>>>(ce, tmQe, tmDOe, tmKc, tmVc, tmK, tmV);
+      SSA_LAUNCH_CHECK("k_tc_dq(blocks)");
+      if ((s = blk_bwd_merge(ck, bb, dqx, st)) != SSA_OK) return s;
+      SSA_CUDA_TRY(cudaMemsetAsync(c.I, 0xff, size_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T * 4, st));   // no selections
+      c.umask = nullptr;
+      c.dq_extra = dqx;
+    }
     ProfScope ps("tc_bwd_dq", st);
     if (c.umask) k_tc_dq<true><<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
     else k_tc_dq<false><<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);
