@@ -538,7 +538,7 @@ extern "C" ssa_status ssa_backward(ssa_plan plan, const ssa_attn_cfg* cfg, const
   x.blk_ws = (vq.S && use_blk(p, d, cfg, vq.S) && tc && !vq.kv)
                  ? cw.take<char>(blk_bwd_ws_bytes(d.N, d.h_kv, d.h_s, d.D, d.n_slc, d.n_q, d.T)) : nullptr;
   Ctx xq = x;                                      // the dQ context (virtual level for small m_q)
-  if (vq.S && (s = build_virtual_level(x, vq.S, vq_ws, st, &xq)) != SSA_OK) return s;
+  if (vq.S && (s = build_virtual_level(x, vq.S, vq_ws, st, &xq, /*plain=*/x.blk_ws != nullptr)) != SSA_OK) return s;
   Ctx& xk = vq.kv ? xq : x;                        // the KV-outer context
   if ((s = build_inverse_csr(xk, scan_ws, st)) != SSA_OK) return s;
   if (tc) {

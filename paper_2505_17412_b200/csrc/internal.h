@@ -143,7 +143,8 @@ constexpr int kVqSlots = 128;
 constexpr int kVqKeyCap = 28672;
 int64_t vq_bound(int n_slc, int n_q, int S, int T, int max_fill_slc);
 size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int max_fill_slc);
-ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v);
+// plain: sub-groups of S query blocks with empty selection lists and no slot masks (the per-block pass)
+ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v, bool plain = false);
 // pertoken.cu: per-block selection pass of per-token selection (m_q = 1)
 struct BlkPass {
   int32_t *off_e, *I_e, *order_e, *off_slc, *inv_off, *inv_list;

@@ -161,6 +161,22 @@ __global__ void __launch_bounds__(32 * kVqWarps) k_vq_count(Ctx c, int S, int cm
   }
 }
 
+// plain sub-groups (no unions: the per-block selection pass empties the selection lists): chunk ch of
+// selection block B as sub-groups of S consecutive query blocks
+__global__ void k_vq_count_plain(Ctx c, int S, int cmax, int32_t* __restrict__ cnt, int32_t* __restrict__ first) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  const int B = w / cmax, ch = w % cmax;
+  if (B >= c.n_blk[SSA_LEVEL_SLC]) return;
+  int qa, qe;
+  slc_qblocks(c, B, &qa, &qe);
+  qa += ch * 2 * S;
+  if (qa >= qe) { cnt[w] = 0; return; }
+  qe = min(qe, qa + 2 * S);
+  int k = 0;
+  for (int q = qa; q < qe; q += S) first[qa + k++] = q;
+  cnt[w] = k;
+}
+
 // sub-group v of selection block B covers query blocks [qa_v, qe_v): token offsets off_v, batch item,
 // identity work order; slots past the real count are empty (off = N) so their CTAs do nothing
 __global__ void k_vq_fill(Ctx c, int vT, int S, int cmax, const int32_t* __restrict__ start, const int32_t* __restrict__ first,
@@ -197,7 +213,8 @@ __global__ void k_vq_fill(Ctx c, int vT, int S, int cmax, const int32_t* __restr
   qrange[2 * v + 1] = e;
   batch_v[v] = c.q_batch[a];
   for (int g = 0; g < c.h_kv; ++g)
-    for (int j = 0; j < vT; ++j) I_u[(int64_t(v) * c.h_kv + g) * vT + j] = un[(int64_t(qa + k) * c.h_kv + g) * kVqSlots + j];
+    for (int j = 0; j < vT; ++j)
+      I_u[(int64_t(v) * c.h_kv + g) * vT + j] = un ? un[(int64_t(qa + k) * c.h_kv + g) * kVqSlots + j] : -1;
 }
 
 }  // namespace
@@ -244,7 +261,7 @@ size_t vq_ws_bytes(int64_t N, int h_kv, int n_slc, int n_q, int S, int T, int ma
 // Build the virtual query level (see the header) with sub-groups of at most S query blocks from the per-query-
 // block selections c.I and return in *v the context the selection / window, dQ and KV-outer kernels run
 // with.
-ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v) {
+ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, Ctx* v, bool plain) {
   const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
   const int vT = vq_slots(S, c.T);
   if (S < 2 || c.T > 32) { set_error("virtual query level: bad sub-group size"); return SSA_ERR_UNSUPPORTED; }
@@ -264,12 +281,13 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   int32_t* I_u = cw.take<int32_t>(size_t(bound) * c.h_kv * vT);
   unsigned long long* umask = cw.take<unsigned long long>(size_t(c.N) * c.h_kv * 2);
   if (n_slc > 0) {
-    k_vq_count<<<nb(nw, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * kVqSlots * 4, st>>>(c, S, cmax, cnt, first, un, umask);
+    if (plain) k_vq_count_plain<<<nb(nw, 128), 128, 0, st>>>(c, S, cmax, cnt, first);
+    else k_vq_count<<<nb(nw, kVqWarps), 32 * kVqWarps, size_t(kVqWarps) * c.h_kv * kVqSlots * 4, st>>>(c, S, cmax, cnt, first, un, umask);
     SSA_LAUNCH_CHECK("k_vq_count");
   }
   ssa_status s = exclusive_scan(cnt, start, nw, start + nw, sws, st);
   if (s != SSA_OK) return s;
-  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, vT, S, cmax, start, first, un, I_u, off_v, qrange, batch_v, order_v, int(bound));
+  k_vq_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, vT, S, cmax, start, first, plain ? nullptr : un, I_u, off_v, qrange, batch_v, order_v, int(bound));
   SSA_LAUNCH_CHECK("k_vq_fill");
   *v = c;
   v->tok_I = c.I;            // the per-query-block selections (KV-outer row masks)
@@ -283,7 +301,7 @@ ssa_status build_virtual_level(const Ctx& c, int S, void* ws, cudaStream_t st, C
   v->q_end = int32_t(bound);
   v->I = I_u;
   v->T = vT;
-  v->umask = umask;
+  v->umask = plain ? nullptr : umask;
   v->qb_per_item = vq_qb_per_item();     // KV-outer work items in virtual query blocks (bounds the partial buffers)
   return SSA_OK;
 }

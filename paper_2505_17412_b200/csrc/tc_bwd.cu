@@ -1442,9 +1442,7 @@ ssa_status tc_backward(const Ctx& c_in, const Ctx& ck_in, void* ws, cudaStream_t
       k_tc_dq<false><<<dim3(unsigned(bb.bound), 1), kDqThreads, smem, st>>>(ce, tmQe, tmDOe, tmKc, tmVc, tmK, tmV);
       SSA_LAUNCH_CHECK("k_tc_dq(blocks)");
       if ((s = blk_bwd_merge(ck, bb, dqx, st)) != SSA_OK) return s;
-      SSA_CUDA_TRY(cudaMemsetAsync(c.I, 0xff, size_t(c.n_blk[SSA_LEVEL_Q]) * c.h_kv * c.T * 4, st));   // no selections
-      c.umask = nullptr;
-      c.dq_extra = dqx;
+      c.dq_extra = dqx;   // (c: the plain virtual level, empty selection lists: compressed keys + window)
     }
     ProfScope ps("tc_bwd_dq", st);
     if (c.umask) k_tc_dq<true><<<dim3(c.n_blk[SSA_LEVEL_Q], c.h_kv), kDqThreads, smem, st>>>(c, tmQ, tmDO, tmKc, tmVc, tmK, tmV);

@@ -1428,7 +1428,7 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
   }
   Ctx cv = c;   // query blocks smaller than the selection blocks: the virtual level (pertoken.cu)
   if (c.vq_ws) {
-    ssa_status s = build_virtual_level(c, c.vq_S, c.vq_ws, st, &cv);
+    ssa_status s = build_virtual_level(c, c.vq_S, c.vq_ws, st, &cv, /*plain=*/c.blk_ws != nullptr);
     if (s != SSA_OK) return s;
   }
   {
@@ -1454,8 +1454,7 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
       k_tc_slcwin_fwd<false><<<dim3(unsigned(bp.bound), 1), kSwThreads, smem, st>>>(ce, tmQe, tk, tv);
       SSA_LAUNCH_CHECK("k_tc_slcwin_fwd(blocks)");
       if ((s = blk_merge(c, bp, st)) != SSA_OK) return s;
-      SSA_CUDA_TRY(cudaMemsetAsync(cv.I, 0xff, size_t(cv.n_blk[SSA_LEVEL_Q]) * cv.h_kv * cv.T * 4, st));   // no selections
-      cv.umask = nullptr;
+      // (the plain virtual level has empty selection lists and no slot masks: window + gated sum only)
     }
     ProfScope ps("tc_slc_win_fwd", st);
     if (cv.umask) k_tc_slcwin_fwd<true><<<dim3(nq, c.h_kv), kSwThreads, smem, st>>>(cv, tmQ, tk, tv);
