@@ -595,21 +595,62 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
           row = wrow;
         }
         __syncwarp();
-        for (int it = 0; it < Teff; ++it) {
-          float best = -2.f;
-          int bidx = 0x7fffffff;
-          for (int B = lane; B < ns; B += 32) {
-            const float v = row[B];
-            if (v > best) { best = v; bidx = B; }
-          }
+        if (Teff <= 8) {
+          // one pass: every lane keeps its own top 8 (descending value, ascending index on ties: its
+          // blocks are scanned in ascending order and only a strictly larger value moves ahead), then
+          // Teff rounds of a warp argmax over the lanes' heads (same order), the winner pops its head
+          float tv[8];
+          int ti[8];
 #pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-            if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+          for (int k = 0; k < 8; ++k) { tv[k] = -2.f; ti[k] = 0x7fffffff; }
+          for (int B = lane; B < ns; B += 32) {
+            float v = row[B];
+            int bi = B;
+            if (v > tv[7]) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (v > tv[k]) {
+                  const float fv = tv[k];
+                  const int fi = ti[k];
+                  tv[k] = v; ti[k] = bi;
+                  v = fv; bi = fi;
+                }
+            }
           }
-          if (lane == 0) { wch[it] = bidx; row[bidx] = -1.f; }
+          for (int it = 0; it < Teff; ++it) {
+            float best = tv[0];
+            int bidx = ti[0];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+              if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+            }
+            if ((bidx & 31) == lane && bidx == ti[0]) {   // the owner pops its head
+#pragma unroll
+              for (int k = 0; k < 7; ++k) { tv[k] = tv[k + 1]; ti[k] = ti[k + 1]; }
+              tv[7] = -2.f; ti[7] = 0x7fffffff;
+            }
+            if (lane == 0) wch[it] = bidx;
+          }
           __syncwarp();
+        } else {
+          for (int it = 0; it < Teff; ++it) {
+            float best = -2.f;
+            int bidx = 0x7fffffff;
+            for (int B = lane; B < ns; B += 32) {
+              const float v = row[B];
+              if (v > best) { best = v; bidx = B; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+              if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+            }
+            if (lane == 0) { wch[it] = bidx; row[bidx] = -1.f; }
+            __syncwarp();
+          }
         }
         if (lane == 0)
           for (int i = 1; i < Teff; ++i) {
