@@ -781,7 +781,7 @@ __device__ __forceinline__ float4 staged_h(const float* wbuf, int rl, int ch) {
 
 // kMask: the per-row union-slot masks of small query blocks (pertoken.cu); a separate instantiation so
 // the query-block path carries none of its registers
-template <bool kMask>
+template <bool kMask, bool kPartial = false>
 __global__ void __launch_bounds__(kSwThreads, 1)
 k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant__ const TmapSet4 tmK,
                 __grid_constant__ const TmapSet4 tmV) {
@@ -1020,7 +1020,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
       const int64_t row = qrow0 + (rvalid ? r : 0);
       const int wrow0 = rt * kTile + (warp & 3) * 32;   // first row of this warp
       float* wbuf = reinterpret_cast<float*>(sEpi + wg * (kEpiBytes / 2) + (warp & 3) * (kEpiBytes / 8));
-      if (wrow0 + lane < rows && !c.sel_partial) {
+      if (wrow0 + lane < rows && !kPartial) {
         // pull this warp's O_cmp rows (HBM) and gates toward L2 now; the epilogue reads them a pair later
         const char* pc = reinterpret_cast<const char*>(static_cast<const float*>(c.o[0]) + (qrow0 + wrow0 + lane) * int64_t(kD));
         asm volatile("prefetch.global.L2 [%0];\n\tprefetch.global.L2 [%1];" :: "l"(pc), "l"(pc + 128));
@@ -1185,7 +1185,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         const float4 sl = c.no_win ? wn : sl_in;
         const float w0 = w3[0], w1 = w3[1], w2 = c.no_win ? 0.f : w3[2];
         *reinterpret_cast<float4*>(ow + grow * kD + col) = wn;
-        if (c.sel_partial) return;           // per-block selection pass: O and LSE only
+        if (kPartial) return;           // per-block selection pass: O and LSE only
         if (col >= c.Dc) return;             // zero-padded head dims (d = 32) are not output
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(c.out) + (int64_t(dst) * c.H + g * c.h_s + rr % c.h_s) * c.Dc + col;
         float4 y = make_float4(w0 * cm.x + w1 * sl.x + w2 * wn.x, w0 * cm.y + w1 * sl.y + w2 * wn.y,
@@ -1207,7 +1207,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         float h_w[4][3];
         int h_dst[4];
         auto epi_load_h = [&](int hf, int bt) {
-          if (c.sel_partial) return;
+          if (kPartial) return;
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
             const int rl = 4 * (bt * 4 + ii) + (lane >> 3), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
@@ -1269,7 +1269,7 @@ k_tc_slcwin_fwd(Ctx c, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
         float e_w[8][3];
         int e_dst[8];
         auto epi_load = [&](int bt) {
-          if (c.sel_partial) return;
+          if (kPartial) return;
 #pragma unroll
           for (int ii = 0; ii < 8; ++ii) {
             const int rl = 2 * (bt * 8 + ii) + (lane >> 4), rr = min(wrow0 + rl, rows - 1);   // clamp: valid memory
@@ -1492,7 +1492,8 @@ ssa_status tc_forward(const Ctx& c, void* ws, cudaStream_t st, cudaEvent_t kv_ev
       const Ctx ce = blk_context(c, bp);
       CUtensorMap tmQe;
       if (!make_tmap_bf16_2d(&tmQe, bp.q_exp, uint64_t(bp.n_exp) * c.h_s, kTile)) return SSA_ERR_CUDA;
-      k_tc_slcwin_fwd<false><<<dim3(unsigned(bp.bound), 1), kSwThreads, smem, st>>>(ce, tmQe, tk, tv);
+      SSA_CUDA_TRY(cudaFuncSetAttribute(k_tc_slcwin_fwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_tc_slcwin_fwd<false, true><<<dim3(unsigned(bp.bound), 1), kSwThreads, smem, st>>>(ce, tmQe, tk, tv);
       SSA_LAUNCH_CHECK("k_tc_slcwin_fwd(blocks)");
       if ((s = blk_merge(c, bp, st)) != SSA_OK) return s;
       // (the plain virtual level has empty selection lists and no slot masks: window + gated sum only)
