@@ -228,9 +228,11 @@ double env_or(const char* name, double dflt) {
   return x > 0.0 ? x : dflt;
 }
 // per-token selection (m_q = 1) on the virtual level: the selection branch as a per-block pass + merge
+// (pertoken.cu; it handles any m_q < m_slc, but for m_q = 2 / 4 the union-masked sub-groups measured faster:
+// C2 m_q = 2 7.3 vs 7.7 ms — SSA_VQ_BLOCKSEL=2 forces it, for tests)
 // (pertoken.cu) instead of the union-masked tiles; not with the window-only / no-window flags
 bool use_blk(const Plan* p, const Dims& d, const ssa_attn_cfg* cfg, int vq_S) {
-  return vq_S > 0 && p->info.m[SSA_LEVEL_Q] == 1 && blk_enabled() &&
+  return vq_S > 0 && (p->info.m[SSA_LEVEL_Q] == 1 || blk_forced()) && blk_enabled() &&
          !(cfg->flags & (SSA_WINDOW_ONLY | SSA_NO_WINDOW)) && d.h_kv >= 1;
 }
 double q_rows(const Dims& d) { return d.n_q > 0 ? double(d.N) / d.n_q * (d.H / d.h_kv) : 0.0; }

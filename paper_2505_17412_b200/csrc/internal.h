@@ -153,8 +153,10 @@ struct BlkPass {
   int64_t bound, n_exp;
   int32_t* batch_e;               // zeros (the expanded context has no compressed keys)
   float* dq_part;                 // backward: fp32 dQ partials per expanded row
+  int32_t* etok;                  // [entries + 1] first expanded token of every inverse-CSR entry
 };
 bool blk_enabled();
+bool blk_forced();   // SSA_VQ_BLOCKSEL=2: the per-block pass also for m_q > 1
 size_t blk_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T);
 ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b);
 Ctx blk_context(const Ctx& c, const BlkPass& b);

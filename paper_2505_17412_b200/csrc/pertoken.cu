@@ -332,21 +332,40 @@ __device__ __forceinline__ int key_of(const int32_t* __restrict__ inv_off, int n
   return lo;
 }
 
-__global__ void k_blk_count(Ctx c, int32_t* __restrict__ cnt) {
+// entries of the inverse CSR = (key, query block) pairs; etok = exclusive scan of their token counts (the
+// expanded token space: an entry's tokens are contiguous, each token a row group of h_s rows)
+__global__ void k_blk_entry_tokens(Ctx c, int32_t* __restrict__ cnt, int64_t n_entries_bound) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_entries_bound) return;
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  if (i >= c.inv_off[nkeys]) { cnt[i] = 0; return; }
+  const int Q = c.inv_list[i];
+  cnt[i] = c.off[SSA_LEVEL_Q][Q + 1] - c.off[SSA_LEVEL_Q][Q];
+}
+__device__ __forceinline__ int64_t entry_of(const int32_t* __restrict__ etok, int64_t n_entries, int64_t e) {
+  int64_t lo = 0, hi = n_entries;   // largest entry with etok[entry] <= e (token counts are >= 1)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (etok[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_blk_count(Ctx c, const int32_t* __restrict__ etok, int32_t* __restrict__ cnt) {
   const int key = blockIdx.x * blockDim.x + threadIdx.x;
   const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
   if (key >= nkeys) return;
-  const int len = c.inv_off[key + 1] - c.inv_off[key];
+  const int len = etok[c.inv_off[key + 1]] - etok[c.inv_off[key]];
   cnt[key] = (len + kBlkChunk - 1) / kBlkChunk;
 }
 
 // virtual query block v: expanded tokens [off_e[v], off_e[v + 1]) of key (B, g), its one block B' = g n_slc + B
-__global__ void k_blk_fill(Ctx c, const int32_t* __restrict__ start, int32_t* __restrict__ off_e, int32_t* __restrict__ I_e,
-                           int32_t* __restrict__ order_e, int bound) {
+__global__ void k_blk_fill(Ctx c, const int32_t* __restrict__ etok, const int32_t* __restrict__ start,
+                           int32_t* __restrict__ off_e, int32_t* __restrict__ I_e, int32_t* __restrict__ order_e, int bound) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > bound) return;
   const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
-  const int total = start[nkeys], n_e = c.inv_off[nkeys];
+  const int total = start[nkeys], n_e = etok[c.inv_off[nkeys]];
   if (v < bound) order_e[v] = v;
   if (v >= total) {
     off_e[v] = n_e;
@@ -359,7 +378,7 @@ __global__ void k_blk_fill(Ctx c, const int32_t* __restrict__ start, int32_t* __
     if (start[mid] <= v) lo = mid; else hi = mid;
   }
   const int key = lo, B = key / c.h_kv, g = key % c.h_kv;
-  off_e[v] = c.inv_off[key] + (v - start[key]) * kBlkChunk;
+  off_e[v] = etok[c.inv_off[key]] + (v - start[key]) * kBlkChunk;
   I_e[v] = g * c.n_blk[SSA_LEVEL_SLC] + B;
 }
 
@@ -371,21 +390,42 @@ __global__ void k_blk_slc_off(Ctx c, int32_t* __restrict__ off) {
   off[j] = j == n_slc * c.h_kv ? c.h_kv * c.N : (j / n_slc) * c.N + c.off[SSA_LEVEL_SLC][j % n_slc];
 }
 
-// Q_exp[e] = the h_s q rows (internal layout) of token inv_list[e] in the kv group of e's key; one warp per e
-__global__ void k_blk_gather(Ctx c, __nv_bfloat16* __restrict__ q_exp) {
+// expanded token e -> (kv group, token): entry i holding e, its key and query block
+// (one-token query blocks, m_q = 1: entries and expanded tokens coincide, no search)
+__device__ __forceinline__ void exp_token(const Ctx& c, const int32_t* __restrict__ etok, int64_t e, int* g, int* t) {
+  const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
+  const int64_t i = c.n_blk[SSA_LEVEL_Q] == c.N ? e : entry_of(etok, c.inv_off[nkeys], e);
+  *g = key_of(c.inv_off, nkeys, i) % c.h_kv;
+  const int Q = c.inv_list[i];
+  *t = c.off[SSA_LEVEL_Q][Q] + int(e - etok[i]);
+}
+// position of token t (query block Q) of key (B, g) in the expanded token space (Q is in the key's list)
+__device__ __forceinline__ int64_t exp_index(const Ctx& c, const int32_t* __restrict__ etok, int B, int g, int Q, int t) {
+  const int key = B * c.h_kv + g;
+  int lo = c.inv_off[key], hi = c.inv_off[key + 1];   // ascending query blocks: binary search for Q
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (c.inv_list[mid] < Q) lo = mid + 1; else hi = mid;
+  }
+  return int64_t(etok[lo]) + (t - c.off[SSA_LEVEL_Q][Q]);
+}
+
+// Q_exp[e] = the h_s q rows (internal layout) of expanded token e; one warp per e
+__global__ void k_blk_gather(Ctx c, const int32_t* __restrict__ etok, __nv_bfloat16* __restrict__ q_exp) {
   const int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
-  if (e >= c.inv_off[nkeys]) return;
-  const int key = key_of(c.inv_off, nkeys, e), g = key % c.h_kv;
-  const int t = c.off[SSA_LEVEL_Q][c.inv_list[e]];   // m_q = 1: the query block's one token
+  if (e >= etok[c.inv_off[nkeys]]) return;
+  int g, t;
+  exp_token(c, etok, e, &g, &t);
   const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(c.qs) + (int64_t(g) * c.N + t) * c.h_s * c.D);
   uint4* dst = reinterpret_cast<uint4*>(q_exp + e * c.h_s * c.D);
   for (int i = lane; i < c.h_s * c.D / 8; i += 32) dst[i] = src[i];
 }
 
 // per row (token t, group g, head s): combine the T partial results of its selected blocks (one warp per (t, g))
-__global__ void k_blk_merge(Ctx c, const float* __restrict__ o_exp, const float* __restrict__ lse_exp) {
+__global__ void k_blk_merge(Ctx c, const int32_t* __restrict__ etok, const float* __restrict__ o_exp,
+                            const float* __restrict__ lse_exp) {
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= int64_t(c.N) * c.h_kv) return;
@@ -395,15 +435,7 @@ __global__ void k_blk_merge(Ctx c, const float* __restrict__ o_exp, const float*
   int64_t ej = -1;
   if (lane < c.T) {
     const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + lane];
-    if (B >= 0) {
-      const int key = B * c.h_kv + g;
-      int lo = c.inv_off[key], hi = c.inv_off[key + 1];   // ascending query blocks: binary search for Q
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (c.inv_list[mid] < Q) lo = mid + 1; else hi = mid;
-      }
-      ej = lo;
-    }
+    if (B >= 0) ej = exp_index(c, etok, B, g, Q, t);
   }
   const int64_t row0 = (int64_t(g) * c.N + t) * c.h_s;
   float* O = static_cast<float*>(c.o[1]);
@@ -436,24 +468,39 @@ bool blk_enabled() {
   const char* e = getenv("SSA_VQ_BLOCKSEL");
   return !(e && atoi(e) == 0);
 }
+bool blk_forced() {
+  const char* e = getenv("SSA_VQ_BLOCKSEL");
+  return e && atoi(e) == 2;
+}
 static int64_t blk_bound(int n_slc, int h_kv, int64_t n_exp) { return int64_t(n_slc) * h_kv + n_exp / kBlkChunk + 1; }
+// entries (key, query block) <= n_q h_kv T; expanded tokens <= N h_kv T (a token is in <= T lists per group)
+static size_t blk_entries_bytes(int64_t n_ent) { return size_t(n_ent + 2) * 4 * 2 + scan_ws_bytes(n_ent + 1) + 3 * 256; }
 size_t blk_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T) {
-  const int64_t n_exp = int64_t(n_q) * h_kv * T, nkeys = int64_t(n_slc) * h_kv, bound = blk_bound(n_slc, h_kv, n_exp);
-  (void)N;
-  return inverse_csr_ws_bytes(n_slc, h_kv, n_q) + size_t(nkeys + 2) * 4 * 3 + size_t(n_exp + 1) * 4 +
-         scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 3 + size_t(nkeys + 2) * 4 +
+  const int64_t n_ent = int64_t(n_q) * h_kv * T, n_exp = N * h_kv * T, nkeys = int64_t(n_slc) * h_kv;
+  const int64_t bound = blk_bound(n_slc, h_kv, n_exp);
+  return inverse_csr_ws_bytes(n_slc, h_kv, n_q) + size_t(nkeys + 2) * 4 * 3 + size_t(n_ent + 1) * 4 +
+         blk_entries_bytes(n_ent) + scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 3 + size_t(nkeys + 2) * 4 +
          size_t(n_exp) * h_s * D * 2 + size_t(n_exp) * h_s * D * 4 + size_t(n_exp) * h_s * 4 + 16 * 256;
+}
+// etok over the inverse CSR's entries (exclusive scan of their token counts)
+static ssa_status blk_entries(const Ctx& c, int64_t n_ent, Carve& cw, cudaStream_t st, int32_t** etok) {
+  int32_t* tc = cw.take<int32_t>(n_ent + 2);
+  *etok = cw.take<int32_t>(n_ent + 2);
+  void* ws = cw.take<char>(scan_ws_bytes(n_ent + 1));
+  k_blk_entry_tokens<<<nb(n_ent + 1, 256), 256, 0, st>>>(c, tc, n_ent + 1);
+  SSA_LAUNCH_CHECK("k_blk_entry_tokens");
+  return exclusive_scan(tc, *etok, n_ent + 1, nullptr, ws, st);
 }
 
 ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b) {
   const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
-  const int64_t n_exp = int64_t(n_q) * c.h_kv * c.T, nkeys = int64_t(n_slc) * c.h_kv;
-  const int64_t bound = blk_bound(n_slc, c.h_kv, n_exp);
+  const int64_t n_ent = int64_t(n_q) * c.h_kv * c.T, n_exp = int64_t(c.N) * c.h_kv * c.T;
+  const int64_t nkeys = int64_t(n_slc) * c.h_kv, bound = blk_bound(n_slc, c.h_kv, n_exp);
   Carve cw(ws, blk_ws_bytes(c.N, c.h_kv, c.h_s, c.D, n_slc, n_q, c.T));
   void* inv_ws = cw.take<char>(inverse_csr_ws_bytes(n_slc, c.h_kv, n_q));
   Ctx ci = c;
   ci.inv_off = cw.take<int32_t>(nkeys + 2);
-  ci.inv_list = cw.take<int32_t>(n_exp + 1);
+  ci.inv_list = cw.take<int32_t>(n_ent + 1);
   int32_t* cnt = cw.take<int32_t>(nkeys + 2);
   int32_t* start = cw.take<int32_t>(nkeys + 2);
   void* sws = cw.take<char>(scan_ws_bytes(nkeys + 1));
@@ -464,21 +511,22 @@ ssa_status blk_build(const Ctx& c, void* ws, cudaStream_t st, BlkPass* b) {
   b->q_exp = cw.take<__nv_bfloat16>(size_t(n_exp) * c.h_s * c.D);
   b->o_exp = cw.take<float>(size_t(n_exp) * c.h_s * c.D);
   b->lse_exp = cw.take<float>(size_t(n_exp) * c.h_s);
-  if (!cw.ok()) { set_error("per-block selection: workspace carve"); return SSA_ERR_WORKSPACE; }
   b->bound = bound;
   b->n_exp = n_exp;
   b->inv_off = ci.inv_off;
   b->inv_list = ci.inv_list;
   ssa_status s = build_inverse_csr(ci, inv_ws, st);
   if (s != SSA_OK) return s;
-  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(ci, cnt);
+  if ((s = blk_entries(ci, n_ent, cw, st, &b->etok)) != SSA_OK) return s;
+  if (!cw.ok()) { set_error("per-block selection: workspace carve"); return SSA_ERR_WORKSPACE; }
+  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(ci, b->etok, cnt);
   SSA_LAUNCH_CHECK("k_blk_count");
   if ((s = exclusive_scan(cnt, start, nkeys, start + nkeys, sws, st)) != SSA_OK) return s;
-  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(ci, start, b->off_e, b->I_e, b->order_e, int(bound));
+  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(ci, b->etok, start, b->off_e, b->I_e, b->order_e, int(bound));
   SSA_LAUNCH_CHECK("k_blk_fill");
   k_blk_slc_off<<<nb(nkeys + 1, 256), 256, 0, st>>>(ci, b->off_slc);
   SSA_LAUNCH_CHECK("k_blk_slc_off");
-  k_blk_gather<<<nb(n_exp * 32, 256), 256, 0, st>>>(ci, b->q_exp);
+  k_blk_gather<<<nb(n_exp * 32, 256), 256, 0, st>>>(ci, b->etok, b->q_exp);
   SSA_LAUNCH_CHECK("k_blk_gather");
   return SSA_OK;
 }
@@ -513,7 +561,7 @@ ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st) {
   ci.inv_off = b.inv_off;
   ci.inv_list = b.inv_list;
   const int64_t warps = int64_t(c.N) * c.h_kv;
-  k_blk_merge<<<nb(warps * 32, 256), 256, 0, st>>>(ci, b.o_exp, b.lse_exp);
+  k_blk_merge<<<nb(warps * 32, 256), 256, 0, st>>>(ci, b.etok, b.o_exp, b.lse_exp);
   SSA_LAUNCH_CHECK("k_blk_merge");
   return SSA_OK;
 }
@@ -523,15 +571,15 @@ ssa_status blk_merge(const Ctx& c, const BlkPass& b, cudaStream_t st) {
 namespace {
 // expanded row operands: fp16 q / dO rows of token inv_list[e] in e's kv group, its selection-branch row
 // stats (LSE, D) and gates; one warp per e
-__global__ void k_blk_gather_bwd(Ctx c, const __half* __restrict__ q16, const __half* __restrict__ do16,
-                                 __half* __restrict__ q_e, __half* __restrict__ do_e, float* __restrict__ lse_e,
-                                 float* __restrict__ D_e, float* __restrict__ gs_e) {
+__global__ void k_blk_gather_bwd(Ctx c, const int32_t* __restrict__ etok, const __half* __restrict__ q16,
+                                 const __half* __restrict__ do16, __half* __restrict__ q_e, __half* __restrict__ do_e,
+                                 float* __restrict__ lse_e, float* __restrict__ D_e, float* __restrict__ gs_e) {
   const int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nkeys = c.n_blk[SSA_LEVEL_SLC] * c.h_kv;
-  if (e >= c.inv_off[nkeys]) return;
-  const int key = key_of(c.inv_off, nkeys, e), g = key % c.h_kv;
-  const int t = c.off[SSA_LEVEL_Q][c.inv_list[e]];
+  if (e >= etok[c.inv_off[nkeys]]) return;
+  int g, t;
+  exp_token(c, etok, e, &g, &t);
   const int64_t r0 = (int64_t(g) * c.N + t) * c.h_s;
   const uint4* sq = reinterpret_cast<const uint4*>(q16 + r0 * c.D);
   const uint4* sd = reinterpret_cast<const uint4*>(do16 + r0 * c.D);
@@ -549,7 +597,8 @@ __global__ void k_blk_gather_bwd(Ctx c, const __half* __restrict__ q16, const __
   }
 }
 // dq_extra of row (t, g, s) = sum over its selected blocks j (slot order) of the per-block partials
-__global__ void k_blk_merge_bwd(Ctx c, const float* __restrict__ dq_part, float* __restrict__ dq_extra) {
+__global__ void k_blk_merge_bwd(Ctx c, const int32_t* __restrict__ etok, const float* __restrict__ dq_part,
+                                float* __restrict__ dq_extra) {
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= int64_t(c.N) * c.h_kv) return;
@@ -558,15 +607,7 @@ __global__ void k_blk_merge_bwd(Ctx c, const float* __restrict__ dq_part, float*
   int64_t ej = -1;
   if (lane < c.T) {
     const int B = c.I[(int64_t(Q) * c.h_kv + g) * c.T + lane];
-    if (B >= 0) {
-      const int key = B * c.h_kv + g;
-      int lo = c.inv_off[key], hi = c.inv_off[key + 1];
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (c.inv_list[mid] < Q) lo = mid + 1; else hi = mid;
-      }
-      ej = lo;
-    }
+    if (B >= 0) ej = exp_index(c, etok, B, g, Q, t);
   }
   const int64_t row0 = (int64_t(g) * c.N + t) * c.h_s;
   for (int idx = lane * 4; idx < c.h_s * c.D; idx += 128) {
@@ -584,17 +625,17 @@ __global__ void k_blk_merge_bwd(Ctx c, const float* __restrict__ dq_part, float*
 }  // namespace
 
 size_t blk_bwd_ws_bytes(int64_t N, int h_kv, int h_s, int D, int n_slc, int n_q, int T) {
-  const int64_t n_exp = int64_t(n_q) * h_kv * T, nkeys = int64_t(n_slc) * h_kv, bound = blk_bound(n_slc, h_kv, n_exp);
-  const int64_t re = n_exp * h_s;
-  return size_t(nkeys + 2) * 4 * 3 + scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 4 +
+  const int64_t n_ent = int64_t(n_q) * h_kv * T, n_exp = N * h_kv * T, nkeys = int64_t(n_slc) * h_kv;
+  const int64_t bound = blk_bound(n_slc, h_kv, n_exp), re = n_exp * h_s;
+  return blk_entries_bytes(n_ent) + size_t(nkeys + 2) * 4 * 3 + scan_ws_bytes(nkeys + 1) + size_t(bound + 2) * 4 * 4 +
          size_t(re) * D * 2 * 2 + size_t(re) * 4 * 5 + size_t(re) * D * 4 + size_t(N) * h_kv * h_s * D * 4 + 20 * 256;
 }
 
 ssa_status blk_bwd_build(const Ctx& c, const __half* q16, const __half* do16, void* ws, cudaStream_t st, BlkPass* b,
                          Ctx* e, float** dq_extra) {
   const int n_slc = c.n_blk[SSA_LEVEL_SLC], n_q = c.n_blk[SSA_LEVEL_Q];
-  const int64_t n_exp = int64_t(n_q) * c.h_kv * c.T, nkeys = int64_t(n_slc) * c.h_kv;
-  const int64_t bound = blk_bound(n_slc, c.h_kv, n_exp), re = n_exp * c.h_s;
+  const int64_t n_ent = int64_t(n_q) * c.h_kv * c.T, n_exp = int64_t(c.N) * c.h_kv * c.T;
+  const int64_t nkeys = int64_t(n_slc) * c.h_kv, bound = blk_bound(n_slc, c.h_kv, n_exp), re = n_exp * c.h_s;
   Carve cw(ws, blk_bwd_ws_bytes(c.N, c.h_kv, c.h_s, c.D, n_slc, n_q, c.T));
   int32_t* cnt = cw.take<int32_t>(nkeys + 2);
   int32_t* start = cw.take<int32_t>(nkeys + 2);
@@ -620,16 +661,18 @@ ssa_status blk_bwd_build(const Ctx& c, const __half* q16, const __half* do16, vo
   b->o_exp = nullptr;
   b->lse_exp = lse_e;
   b->dq_part = dq_part;
-  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(c, cnt);
-  SSA_LAUNCH_CHECK("k_blk_count");
-  ssa_status s = exclusive_scan(cnt, start, nkeys, start + nkeys, sws, st);
+  ssa_status s = blk_entries(c, n_ent, cw, st, &b->etok);
   if (s != SSA_OK) return s;
-  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, start, b->off_e, b->I_e, b->order_e, int(bound));
+  if (!cw.ok()) { set_error("per-block selection dQ: workspace carve"); return SSA_ERR_WORKSPACE; }
+  k_blk_count<<<nb(nkeys, 256), 256, 0, st>>>(c, b->etok, cnt);
+  SSA_LAUNCH_CHECK("k_blk_count");
+  if ((s = exclusive_scan(cnt, start, nkeys, start + nkeys, sws, st)) != SSA_OK) return s;
+  k_blk_fill<<<nb(bound + 1, 256), 256, 0, st>>>(c, b->etok, start, b->off_e, b->I_e, b->order_e, int(bound));
   SSA_LAUNCH_CHECK("k_blk_fill");
   k_blk_slc_off<<<nb(nkeys + 1, 256), 256, 0, st>>>(c, b->off_slc);
   SSA_LAUNCH_CHECK("k_blk_slc_off");
   SSA_CUDA_TRY(cudaMemsetAsync(b->batch_e, 0, size_t(bound + 2) * 4, st));
-  k_blk_gather_bwd<<<nb(n_exp * 32, 256), 256, 0, st>>>(c, q16, do16, q_e, do_e, lse_e, D_e, gs_e);
+  k_blk_gather_bwd<<<nb(n_exp * 32, 256), 256, 0, st>>>(c, b->etok, q16, do16, q_e, do_e, lse_e, D_e, gs_e);
   SSA_LAUNCH_CHECK("k_blk_gather_bwd");
   Ctx x = c;
   x.h_kv = 1;
@@ -661,7 +704,7 @@ ssa_status blk_bwd_build(const Ctx& c, const __half* q16, const __half* do16, vo
 
 ssa_status blk_bwd_merge(const Ctx& c, const BlkPass& b, float* dq_extra, cudaStream_t st) {
   const int64_t warps = int64_t(c.N) * c.h_kv;
-  k_blk_merge_bwd<<<nb(warps * 32, 256), 256, 0, st>>>(c, b.dq_part, dq_extra);
+  k_blk_merge_bwd<<<nb(warps * 32, 256), 256, 0, st>>>(c, b.etok, b.dq_part, dq_extra);
   SSA_LAUNCH_CHECK("k_blk_merge_bwd");
   return SSA_OK;
 }

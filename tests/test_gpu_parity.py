@@ -348,6 +348,8 @@ _VQ_MODES = {
     "direct": {"SSA_VQ": "0"},
     "vq_dq": {"SSA_VQ_ROWS": "100000", "SSA_VQ_KV_ROWS": "0.001"},
     "vq_all": {"SSA_VQ_ROWS": "100000", "SSA_VQ_KV_ROWS": "100000", "SSA_VQ_QB_PER_ITEM": "3"},
+    "union": {"SSA_VQ_BLOCKSEL": "0"},       # m_q = 1 through the union-masked sub-groups
+    "blocks": {"SSA_VQ_BLOCKSEL": "2"},      # the per-block selection passes also for m_q = 2, 4
 }
 
 
