@@ -194,6 +194,7 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   constexpr int kGT = kTok > 0 ? kTile / kTok : 1;   // tokens per row tile (per-token mode)
   float* tbuf = reinterpret_cast<float*>(S + 1);     // per-token mode: [2 wg][2 parity][kGT][129] tile sums
   int* tchosen = reinterpret_cast<int*>(tbuf + 4 * kGT * 129);   // [8 warps][64]
+  int* sbeg = tchosen + 8 * 64;   // per-token mode: first compressed key of each selection block (item-relative)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = blockIdx.y;
@@ -247,6 +248,8 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
   if (warp == 9) tmem_alloc<512>(&S->tmem);
   if constexpr (kTok == 0)
     for (int i = tid; i < nk; i += kCmpThreads) { sc_cmp0[i] = 0.f; sc_cmp1[i] = 0.f; }
+  if constexpr (kTok > 0)
+    for (int i = tid; i <= ns; i += kCmpThreads) sbeg[i] = c.slc_cmp_begin[s0 + i] - c0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -528,13 +531,19 @@ k_tc_cmp_fwd(TcArgs a, __grid_constant__ const CUtensorMap tmQ, __grid_constant_
 #pragma unroll
           for (int j = 0; j < kGT; ++j) bw[j * 129 + t] = kvalid ? cs[j] : 0.f;
           named_bar_sync(1 + wg, 128);   // (also orders the previous tile's score updates)
-          while (Bcur + 1 < ns && c.slc_cmp_begin[s0 + Bcur + 1] - c0 <= k0) ++Bcur;
+          {   // the selection block holding key k0: binary search in the staged block starts (blocks non-empty)
+            int hi = ns;
+            while (hi - Bcur > 1) {
+              const int mid = (Bcur + hi) >> 1;
+              if (sbeg[mid] <= k0) Bcur = mid; else hi = mid;
+            }
+          }
           for (int pi = t;; pi += 128) {
             const int B = Bcur + pi / kGT, j = pi % kGT;
             if (B >= ns) break;
-            const int a0 = c.slc_cmp_begin[s0 + B] - c0;
+            const int a0 = sbeg[B];
             if (a0 >= k1) break;
-            const int e0 = c.slc_cmp_begin[s0 + B + 1] - c0;
+            const int e0 = sbeg[B + 1];
             const int lo = max(a0, k0) - k0, hi = min(e0, k1) - k0;
             float sum = 0.f;
             for (int k = lo; k < hi; ++k) sum += bw[j * 129 + k];
@@ -1387,7 +1396,8 @@ static size_t cmp_smem_bytes(const Ctx& c) {
   const size_t base = 1024 + 32768 + kCmpStages * 49152 + sizeof(CmpSmem) + 16;
   if (kTok == 0) return base + (2 * size_t(c.max_cmp_b) + c.max_slc_b) * sizeof(float);
   // tile buffers + chosen lists; at least 120 KB so that one CTA is resident per SM (per-SM scratch slot)
-  return std::max<size_t>(base + (4 * (kTile / std::max(kTok, 1)) * 129 + 8 * 64) * 4, 120 * 1024);
+  return std::max<size_t>(base + (4 * (kTile / std::max(kTok, 1)) * 129 + 8 * 64 + size_t(c.max_slc_b) + 2) * 4,
+                          120 * 1024);
 }
 template <int kTok>
 static ssa_status launch_cmp(const Ctx& c, const TcArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmKh,
