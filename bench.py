@@ -549,7 +549,8 @@ def main():
         torch.cuda.synchronize(dev)
         t_ms = float(np.mean([a.elapsed_time(b) for a, b in tt])) / batch
         tok_ctx = {"impl": "per-token selection m_q = 1 (Alg. 1 granularity), same tokens and heads, tcgen05 "
-                           "(virtual query level for selection/window and dQ, packed KV-outer row tiles)",
+                           "(selection forward and dQ as per-block passes merged by LSE, window / compressed keys "
+                           "on sub-groups of tokens, packed KV-outer row tiles)",
                    "fwd_bwd_ms": round(t_ms, 4), "ratio_vs_query_block_path": round(t_ms / ms_per_step, 2),
                    "path": "tcgen05" if sv.used_tcgen05 else "simt"}
 
