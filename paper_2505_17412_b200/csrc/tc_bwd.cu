@@ -14,6 +14,7 @@
 //             (mode 0): a 1/n_chunk share of the batch item's rows -> per-chunk partials reduced in a
 //             fixed order (deterministic).
 #include <cfloat>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -1318,6 +1319,8 @@ static int64_t kv_tiles_bound(int64_t N, int H, int h_kv, int n_slc, int n_q, in
 }
 
 int tc_qb_per_item(int m_slc, int m_q) {
+  const char* e = getenv("SSA_KV_QBPI");   // A/B knob: raw-key work item size in query blocks
+  if (e && atoi(e) > 0) return atoi(e);
   const int r = m_q > 0 && m_slc % m_q == 0 ? m_slc / m_q : 1;
   return kQBlocksPerItem * r * r * r;
 }
